@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""bench.py -- agent-updates/s of the F.A.S.T. planning + motion hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config plaza] [--impl ours|reference]
+
+A step is one simulation step (plan_phase + move_phase, engine.hpp:143-148) over the whole
+roster; agent-updates = sum over steps of the alive count entering the step.
+`value` is device-timed (CUDA events around fp_run's stepping loop, state resident in HBM);
+`e2e` runs the same steps through the C ABI with host buffers every step (H2D of the roster,
+plan+move, D2H of positions/alive), wall-clocked.  `--impl reference` times the reference's own
+CPU run() (oracle/_ref, all host threads) on the same workload.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "agent-updates/sec (v_m=4, k_S=1.2)"
+UNIT = "agent-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for k, nm in enumerate(names):
+                    if r[2 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def coverage_u(grid, x, y, v, alive):
+    """U: distinct cells within Chebyshev distance v_i of some alive agent."""
+    H, W = grid.height, grid.width
+    mark = np.zeros((H, W), bool)
+    al = alive.astype(bool)
+    xs, ys, vs = x[al].astype(np.int64), y[al].astype(np.int64), v[al].astype(np.int64)
+    vmax = int(vs.max()) if len(vs) else 0
+    for dy in range(-vmax, vmax + 1):
+        for dx in range(-vmax, vmax + 1):
+            sel = np.maximum(abs(dx), abs(dy)) <= vs
+            yy = ys[sel] + dy
+            xx = xs[sel] + dx
+            if grid.boundary == 1:
+                xx %= W
+                ok = (yy >= 0) & (yy < H)
+            else:
+                ok = (yy >= 0) & (yy < H) & (xx >= 0) & (xx < W)
+            mark[yy[ok], xx[ok]] = True
+    return int(mark.sum())
+
+
+def plan_bytes(n_alive, U, mixed_v, drive_x):
+    """Algorithmic bytes of one plan launch (SURVEY 8d B_plan)."""
+    per_cell = 0.25 if drive_x else 8.25
+    return n_alive * (8 + 8 + (1 if mixed_v else 0)) + U * per_cell
+
+
+def build_workload(cfg, seed):
+    from paper_0911_2900_b200 import scenarios
+    return scenarios.build(cfg, seed=seed)
+
+
+def reference_cpu(wl, field, steps, cores):
+    """The reference's own run() (oracle/_ref) on this workload: agent-updates/s."""
+    import oracle as O
+    ro = wl.roster
+    if O.have_reference():
+        st = O.RefState(wl.grid.cells, field, ro.x, ro.y, ro.v_max, ro.alive, wl.grid.boundary,
+                        potential=wl.potential, drive_gradient=wl.drive_gradient)
+        n0 = st.alive_count
+        r = st.run(wl.k_s, wl.seed, steps, cores)
+        n1 = st.alive_count
+        # alive entering each step is between n1 and n0; exits per step are tiny vs N
+        upd = (n0 + n1) / 2.0 * steps
+        return upd / r["wall_time_s"], "reference", cores, r
+    st = O.State(wl.grid.cells, field, ro.x, ro.y, ro.v_max, ro.alive, wl.grid.boundary,
+                 potential=wl.potential, drive_gradient=wl.drive_gradient)
+    upd = 0
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        upd += st.alive_count
+        st.step_once(wl.k_s, wl.seed)
+    return upd / (time.perf_counter() - t0), "port", 1, None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="plaza", choices=["corridor", "room", "ring", "plaza", "obstacles"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config_desc = {"workload": args.config, "seed": args.seed, "k_s": 1.2, "v_max": 4,
+                   "steps_from": 0, "l2": "inputs larger than L2 (field fp64 > 126 MB)"
+                   if args.config in ("plaza", "obstacles") else "L2-resident inputs; no flush"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        wl = build_workload(args.config, args.seed)
+        from paper_0911_2900_b200 import fastped as fp
+        import oracle as O
+        field = O.static_field(wl.grid.cells, wl.grid.boundary)
+        cores = os.cpu_count() or 1
+        vals = []
+        for _ in range(args.warmup if args.warmup < 1 else 1):
+            reference_cpu(wl, field, 1, cores)
+        v, kind, c, _ = reference_cpu(wl, field, max(1, args.steps), cores)
+        config_desc.update(n_agents=int(len(wl.roster)), grid=[wl.grid.width, wl.grid.height])
+        out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+               "warmup": args.warmup, "higher_is_better": True, "impl": "reference", "dtype": "f64",
+               "data": "synthetic", "scaling": "weak", "vs_baseline": None, "config": config_desc,
+               "cpu_baseline": {"value": v, "unit": UNIT, "cores": c, "kind": kind,
+                                "sample": f"{args.steps} steps of {args.config} from step 0"},
+               "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_0911_2900_b200 import fastped as fp
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    wl = build_workload(args.config, args.seed)
+    ro = wl.roster
+    n = len(ro)
+    st = fp.SimState(wl.grid, None, ro, device=local)
+    if wl.potential:
+        st.set_potential(wl.potential, wl.drive_gradient)
+    params = fp.SimParams(k_s=wl.k_s, seed=wl.seed, steps=max(1, args.warmup))
+    # warm-up steps, then reset the roster to the initial state (untimed)
+    if args.warmup > 0:
+        fp.run(st, params)
+    st.set_agents(ro.x, ro.y, ro.alive)
+    st.step = 0
+    c0 = st.counters()
+    U0 = coverage_u(wl.grid, ro.x, ro.y, ro.v_max, ro.alive)
+    params.steps = args.steps
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        rs = fp.run(st, params)
+    torch.cuda.synchronize()
+    c1 = st.counters()
+    x1, y1, a1 = st.agents()
+    U1 = coverage_u(wl.grid, x1, y1, ro.v_max, a1)
+    t = torch.tensor([rs.wall_time_s, rs.agent_updates], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tt = t.clone()
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        wall, updates = float(tm[0]), float(tt[1])
+    else:
+        wall, updates = rs.wall_time_s, rs.agent_updates
+    value = updates / wall
+
+    # e2e: the C ABI with host buffers, every step H2D roster + step + D2H positions/alive
+    e2e_steps = args.e2e_steps or min(args.steps, 50)
+    st2 = fp.SimState(wl.grid, st.field(), ro, device=local)
+    if wl.potential:
+        st2.set_potential(wl.potential, wl.drive_gradient)
+    hx = torch.from_numpy(ro.x.copy()).pin_memory().numpy()
+    hy = torch.from_numpy(ro.y.copy()).pin_memory().numpy()
+    ha = torch.from_numpy(ro.alive.copy()).pin_memory().numpy()
+    upd2 = 0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        st2.set_agents(hx, hy, ha)
+        upd2 += int(ha.sum())
+        fp.step(st2, params)
+        hx, hy, ha = st2.agents()
+    torch.cuda.synchronize()
+    e2e_wall = time.perf_counter() - t0
+    e2e = {"value": upd2 / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": n * 9, "d2h_bytes_per_step": n * 9,
+           "steps": e2e_steps, "path": "fp_update_agents + fp_step + fp_get_agents (C ABI, host arrays)"}
+
+    if rank != 0:
+        return
+    peak, peak_kind = peaks()
+    mixed = bool((ro.v_max != ro.v_max[0]).any()) if n else False
+    U = 0.5 * (U0 + U1)
+    nalive_avg = rs.agent_updates / max(rs.steps, 1)
+    bytes_per_launch = plan_bytes(nalive_avg, U, mixed, wl.potential == fp.DRIVE_X)
+    plan_launch_s = rs.plan_time_s / max(rs.steps, 1)
+    achieved = bytes_per_launch / plan_launch_s / 1e9
+    roof = {"kernel": "plan_exact_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "bytes_per_launch": bytes_per_launch, "U_cells": U, "plan_ms_per_launch": plan_launch_s * 1e3,
+            "plan_share_of_step": rs.plan_time_s / rs.wall_time_s}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        field = st.field()
+        cores = os.cpu_count() or 1
+        # bounded sample: enough steps for ~10-30 s of CPU work
+        est = n * 1.0e-6 / max(min(cores, 16) * 0.55, 1)  # ~1 us/agent-plan on one core
+        sample_steps = int(max(1, min(396, 15.0 / max(est, 1e-6))))
+        v, kind, c, _ = reference_cpu(wl, field, sample_steps, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": c, "kind": kind,
+               "sample": f"{sample_steps} steps of {args.config} from step 0 ({n} agents)"}
+
+    config_desc.update(n_agents=n, grid=[wl.grid.width, wl.grid.height], mixed_v=mixed)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": wall / max(rs.steps, 1) * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_desc, "parallelism": "replicas" if world > 1 else "single",
+           "phases_ms": {"plan": rs.plan_time_s * 1e3, "move": rs.move_time_s * 1e3, "total": rs.wall_time_s * 1e3},
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+           "gpu_launches": int(c1["kernel_launches"] - c0["kernel_launches"]),
+           "motion_rounds_per_step": (c1["motion_rounds"] - c0["motion_rounds"]) / max(rs.steps, 1)}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,159 @@
+/*
+ * fastped_b200.h -- C ABI of the B200-native F.A.S.T. planning + motion engine.
+ *
+ * The reference (/root/reference/proj/include/fastped, header-only C++20) has no FFI, plugin
+ * or operator registry: its boundary is the `namespace fastped` API.  This header is the thin
+ * C layer that API's drop-in replacement (include/fastped_b200/fastped.hpp, C++) and the
+ * Python binding (paper_0911_2900_b200/fastped.py, ctypes) call.  Each entry point names the
+ * reference function it stands in for.
+ *
+ * Conventions
+ *  - Every function returns FP_OK (0) or an FP_E* status; fp_last_error(ctx) (or
+ *    fp_last_error(NULL) for context-free calls) holds a message whose wording follows the
+ *    reference's exception text where one exists (std::invalid_argument -> FP_EINVAL,
+ *    std::runtime_error -> FP_ERUNTIME).
+ *  - All host buffers are caller-owned and copied; nothing is retained after a call returns.
+ *  - A context is single-owner and not thread-safe (SimState's "one controller" rule,
+ *    state.hpp:19-21).  It owns one CUDA device, one stream and all device-resident state.
+ *  - Cells are row-major, index y*width + x (world.hpp:88-91); CellKind bytes 0 Free, 1 Wall,
+ *    2 Exit (world.hpp:18); boundary 0 Closed, 1 PeriodicX (world.hpp:19).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute call fails with
+ *    FP_ECUDA.
+ */
+#ifndef FASTPED_B200_H
+#define FASTPED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP_OK 0
+#define FP_EINVAL 1   /* std::invalid_argument in the reference */
+#define FP_ERUNTIME 2 /* std::runtime_error in the reference */
+#define FP_ECUDA 3    /* CUDA runtime / device failure (no GPU, OOM, kernel fault) */
+#define FP_ENCCL 4    /* reserved for the multi-GPU strip path */
+
+#define FP_CELL_FREE 0
+#define FP_CELL_WALL 1
+#define FP_CELL_EXIT 2
+#define FP_BOUNDARY_CLOSED 0
+#define FP_BOUNDARY_PERIODIC_X 1
+#define FP_POTENTIAL_EXIT_DISTANCE 0 /* Potential::ExitDistance, state.hpp:17 */
+#define FP_POTENTIAL_DRIVE_X 1       /* Potential::DriveX */
+
+typedef struct fp_ctx fp_ctx;
+
+/* Grid(width, height, cell_size, boundary, cells) -- world.hpp:37-63 */
+typedef struct {
+    int32_t width;
+    int32_t height;
+    double cell_size;
+    int32_t boundary;
+} fp_grid_desc;
+
+/* StepStats -- engine.hpp:137-141 */
+typedef struct {
+    int64_t alive;
+    int64_t exited;
+    int64_t displacement_cells;
+} fp_step_stats;
+
+/* RunStats -- engine.hpp:150-158 (times from CUDA events on the context's stream) */
+typedef struct {
+    double wall_time_s;
+    double plan_time_s;
+    double move_time_s;
+    int64_t steps;
+    int64_t exited;
+    int64_t displacement_cells;
+    int64_t alive;
+    int64_t agent_updates; /* sum over steps of the alive count entering the step */
+} fp_run_stats;
+
+/* Engine counters for observability (not in the reference). */
+typedef struct {
+    int64_t kernel_launches;   /* kernels launched on this context so far */
+    int64_t motion_rounds;     /* conflict-resolution rounds executed */
+    int64_t plan_fallbacks;    /* agents re-sampled on the exact fp64 path */
+    int64_t planned_agents;    /* agents planned */
+} fp_counters;
+
+const char* fp_version(void);
+const char* fp_last_error(const fp_ctx* ctx);
+
+/* compute_blocksize(number_of_agents, cores) -- engine.hpp:27-33 (host arithmetic). */
+int fp_compute_blocksize(int64_t number_of_agents, int cores, int32_t* out);
+
+/* Grid validation + device upload; field == NULL computes compute_static_field on the device
+ * (world.hpp:220-266, bit-identical).  `device` is the CUDA ordinal. */
+int fp_create(const fp_grid_desc* grid, const uint8_t* cells, const double* field, int device,
+              fp_ctx** out);
+void fp_destroy(fp_ctx* ctx);
+
+/* compute_static_field(grid) -- world.hpp:220-266, on the device, context-free. */
+int fp_static_field(const fp_grid_desc* grid, const uint8_t* cells, int device, double* out_s);
+/* StaticField::s of a context (fp64, +inf = unreachable). */
+int fp_get_field(const fp_ctx* ctx, double* out_s);
+
+/* make_state(grid, field, roster) -- state.hpp:38-76.  Ids are dense indices; v_max per agent
+ * (1..5); alive may be NULL (all alive).  Validates like make_state (bounds, wall, shared cell)
+ * except that heterogeneous v_max is accepted (the kernels read the per-agent value, as the
+ * reference's planning.hpp:25 / engine.hpp:117 do). */
+int fp_set_agents(fp_ctx* ctx, uint32_t n, const int32_t* x, const int32_t* y,
+                  const int32_t* v_max, const uint8_t* alive, int64_t step);
+/* Re-uploads positions/alive of the current roster (the drop-in's per-call host sync). */
+int fp_update_agents(fp_ctx* ctx, const int32_t* x, const int32_t* y, const uint8_t* alive);
+/* SimState::step */
+int fp_set_step(fp_ctx* ctx, int64_t step);
+int fp_get_step(const fp_ctx* ctx, int64_t* step);
+int fp_get_alive_count(const fp_ctx* ctx, int64_t* alive);
+/* SimState::potential / drive_gradient -- state.hpp:32-33 */
+int fp_set_potential(fp_ctx* ctx, int kind, double drive_gradient);
+/* SimState::desired (scratch between phases); injected by motion-only tests. */
+int fp_set_desired(fp_ctx* ctx, const int32_t* x, const int32_t* y);
+
+/* plan_phase(st, params, sched) -- engine.hpp:71-84: desired cell of every alive agent,
+ * bit-identical to choose_desired_cell (planning.hpp:88-108). */
+int fp_plan(fp_ctx* ctx, double k_s, uint64_t seed);
+/* move_phase(st, params) -- engine.hpp:95-135 (does not advance the step counter).
+ * Exited ids (processing order) are kept for fp_get_exited. */
+int fp_move(fp_ctx* ctx, uint64_t seed, fp_step_stats* out);
+/* step(st, params, sched) -- engine.hpp:143-148. */
+int fp_step(fp_ctx* ctx, double k_s, uint64_t seed, fp_step_stats* out);
+/* run(st, params, sched) -- engine.hpp:161-183: `steps` steps, device-resident, event-timed. */
+int fp_run(fp_ctx* ctx, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out);
+
+/* Dumps (trajectory / occupancy): SimState::agents, desired, occupancy (id or -1). */
+int fp_get_agents(const fp_ctx* ctx, int32_t* x, int32_t* y, uint8_t* alive);
+int fp_get_desired(const fp_ctx* ctx, int32_t* x, int32_t* y);
+int fp_get_occupancy(const fp_ctx* ctx, int32_t* occ);
+/* MoveOutcome::exited of the last fp_move/fp_step (ids in processing order). */
+int fp_get_exited(const fp_ctx* ctx, uint32_t* ids, uint32_t cap, uint32_t* n);
+/* The last step's movement order (alive ids in processing order, engine.hpp:99-111). */
+int fp_get_order(const fp_ctx* ctx, uint32_t* ids, uint32_t cap, uint32_t* n);
+/* state_hash(st) -- state.hpp:80-95. */
+int fp_state_hash(const fp_ctx* ctx, uint64_t* out);
+
+/* Test mode: candidate list of one agent in the reference order (enumerate_candidates,
+ * planning.hpp:23-57), its exact fp64 weights (planning.hpp:93-103), and the choice
+ * probabilities of the production sampling path (fp32). */
+int fp_get_choice(fp_ctx* ctx, uint32_t agent, double k_s, int32_t* cx, int32_t* cy,
+                  double* weights, float* probs, uint32_t cap, uint32_t* n);
+
+/* The movement permutation of positions 0..n-1 for (seed, step) computed by the device
+ * (engine.hpp:99-111 Fisher-Yates), context-free. */
+int fp_movement_order(int64_t n, uint64_t seed, int64_t step, int device, uint32_t* out);
+
+/* spawn_agents(grid, n, v_max, seed) positions -- scenario_io.hpp:47-69 (host, setup). */
+int fp_spawn_agents(int32_t width, int32_t height, const uint8_t* cells, int64_t n,
+                    uint64_t seed, int32_t* x, int32_t* y);
+
+int fp_get_counters(const fp_ctx* ctx, fp_counters* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,611 @@
+// capi.cu -- the C ABI (include/fastped_b200.h): context lifecycle, uploads, the step
+// sequence, dumps.  Host logic mirrors the reference's validation and error wording
+// (state.hpp:38-76, engine.hpp, world.hpp:37-63, scenario_io.hpp:47-69).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+static thread_local std::string g_error;
+
+void fp_set_global_error(const std::string& s) { g_error = s; }
+
+static int fail(fp_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    g_error = msg;
+    return code;
+}
+
+int fp_cuda_fail(fp_ctx* ctx, cudaError_t e, const char* what) {
+    return fail(ctx, FP_ECUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+extern "C" const char* fp_version(void) { return "fastped-b200 0.1 (sm_100a)"; }
+
+extern "C" const char* fp_last_error(const fp_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_error.c_str();
+}
+
+extern "C" int fp_compute_blocksize(int64_t agents, int cores, int32_t* out) {
+    if (cores < 1) return fail(nullptr, FP_EINVAL, "compute_blocksize: cores must be >= 1");
+    if (agents < 0) return fail(nullptr, FP_EINVAL, "compute_blocksize: agent count must be >= 0");
+    const int64_t c = std::min<int64_t>(agents / cores, 32767);
+    *out = (int32_t)std::max<int64_t>(c, 1);
+    return FP_OK;
+}
+
+// ------------------------------------------------------------------------ grid validation
+static int validate_grid(const fp_grid_desc* g, const uint8_t* cells) {
+    if (!g || !cells) return fail(nullptr, FP_EINVAL, "Grid: null descriptor or cells");
+    if (g->width < 1 || g->height < 1) return fail(nullptr, FP_EINVAL, "Grid: width and height must be >= 1");
+    if (!(g->cell_size > 0.0)) return fail(nullptr, FP_EINVAL, "Grid: cell_size must be > 0");
+    if (g->boundary != FP_BOUNDARY_CLOSED && g->boundary != FP_BOUNDARY_PERIODIC_X)
+        return fail(nullptr, FP_EINVAL, "Grid: unknown boundary");
+    if ((int64_t)g->width * g->height >= (int64_t)1 << 32)
+        return fail(nullptr, FP_EINVAL, "Grid: more than 2^32 cells");
+    const int W = g->width, H = g->height;
+    const size_t n = (size_t)W * H;
+    uint8_t mx = 0;
+    for (size_t i = 0; i < n; ++i) mx = cells[i] > mx ? cells[i] : mx;
+    if (mx > FP_CELL_EXIT) return fail(nullptr, FP_EINVAL, "Grid: unknown cell kind");
+    if (g->boundary == FP_BOUNDARY_CLOSED) {
+        auto bad = [&](int x, int y) { return cells[(size_t)y * W + x] == FP_CELL_FREE; };
+        for (int x = 0; x < W; ++x)
+            if (bad(x, 0) || bad(x, H - 1))
+                return fail(nullptr, FP_EINVAL, "Grid: closed boundary requires every border cell to be Wall or Exit");
+        for (int y = 0; y < H; ++y)
+            if (bad(0, y) || bad(W - 1, y))
+                return fail(nullptr, FP_EINVAL, "Grid: closed boundary requires every border cell to be Wall or Exit");
+    } else {
+        for (int x = 0; x < W; ++x)
+            if (cells[x] != FP_CELL_WALL || cells[(size_t)(H - 1) * W + x] != FP_CELL_WALL)
+                return fail(nullptr, FP_EINVAL, "Grid: periodic-x boundary requires solid top and bottom rows");
+    }
+    return FP_OK;
+}
+
+// ------------------------------------------------------------------------ bitplanes
+__global__ void pack_planes_kernel(const uint8_t* cells, int W, int H, int P, uint32_t* wall, uint32_t* ex) {
+    const size_t nw = (size_t)P * H;
+    for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < nw; w += (size_t)gridDim.x * blockDim.x) {
+        const int y = (int)(w / P), x0 = (int)(w % P) * 32;
+        uint32_t bw = 0, be = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int x = x0 + b;
+            if (x >= W) break;
+            const uint8_t k = cells[(size_t)y * W + x];
+            bw |= (uint32_t)(k == FP_CELL_WALL) << b;
+            be |= (uint32_t)(k == FP_CELL_EXIT) << b;
+        }
+        wall[w] = bw;
+        ex[w] = be;
+    }
+}
+
+// occupancy from alive positions + make_state checks (state.hpp:46-70)
+__global__ void build_occ_kernel(const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
+                                 Geo g, uint32_t* occ, unsigned long long* errs) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !alive[i]) return;
+    const int ax = g.wrap(x[i]), ay = y[i];
+    if (ax < 0 || ax >= g.W || ay < 0 || ay >= g.H) {
+        atomicMin(&errs[0], (unsigned long long)i);
+        return;
+    }
+    if (g.is_wall(ax, ay)) {
+        atomicMin(&errs[1], (unsigned long long)i);
+        return;
+    }
+    const uint32_t bit = 1u << (ax & 31);
+    const uint32_t old = atomicOr(&occ[g.word(ax, ay)], bit);
+    if (old & bit) atomicMin(&errs[2], (unsigned long long)i);
+}
+
+__global__ void occ_dump_kernel(const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
+                                Geo g, int32_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !alive[i]) return;
+    out[(size_t)y[i] * g.W + g.wrap(x[i])] = (int32_t)i;
+}
+
+__global__ void u8_from_i32_kernel(const int32_t* in, uint8_t* out, uint32_t n) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (uint8_t)in[i];
+}
+
+static Geo geo_of(const fp_ctx* c) { return Geo{c->W, c->H, c->boundary, c->P, c->d_wall, c->d_exit}; }
+
+static void free_agents(fp_ctx* c) {
+    void* ptrs[] = {c->d_x, c->d_y, c->d_dx, c->d_dy, c->d_v, c->d_alive, c->d_rank, c->d_alive_ids,
+                    c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
+                    c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    c->d_x = c->d_y = c->d_dx = c->d_dy = nullptr;
+    c->d_v = c->d_alive = nullptr;
+    c->d_rank = c->d_alive_ids = c->d_order = c->d_j = c->d_cnt = c->d_off = c->d_cursor = nullptr;
+    c->d_bucket = c->d_succ = c->d_nxt = c->d_V = c->d_pend_a = c->d_pend_b = nullptr;
+    c->d_exits = c->d_exits_sorted = nullptr;
+    c->cap = 0;
+}
+
+static int ensure_agents(fp_ctx* c, uint32_t n) {
+    if (n <= c->cap && c->d_x) return FP_OK;
+    free_agents(c);
+    const size_t m = std::max<uint32_t>(n, 1);
+    FP_CUDA(c, cudaMalloc(&c->d_x, m * 4));
+    FP_CUDA(c, cudaMalloc(&c->d_y, m * 4));
+    FP_CUDA(c, cudaMalloc(&c->d_dx, m * 4));
+    FP_CUDA(c, cudaMalloc(&c->d_dy, m * 4));
+    FP_CUDA(c, cudaMalloc(&c->d_v, m));
+    FP_CUDA(c, cudaMalloc(&c->d_alive, m));
+    uint32_t** u32s[] = {&c->d_rank, &c->d_alive_ids, &c->d_order, &c->d_j, &c->d_cnt, &c->d_off,
+                         &c->d_cursor, &c->d_bucket, &c->d_succ, &c->d_nxt, &c->d_V, &c->d_pend_a,
+                         &c->d_pend_b};
+    for (uint32_t** p : u32s) FP_CUDA(c, cudaMalloc(p, m * 4));
+    FP_CUDA(c, cudaMalloc(&c->d_exits, m * 8));
+    FP_CUDA(c, cudaMalloc(&c->d_exits_sorted, m * 8));
+    c->cap = (uint32_t)m;
+    return FP_OK;
+}
+
+extern "C" int fp_create(const fp_grid_desc* g, const uint8_t* cells, const double* field, int device,
+                         fp_ctx** out) {
+    if (!out) return fail(nullptr, FP_EINVAL, "fp_create: null output");
+    *out = nullptr;
+    if (int rc = validate_grid(g, cells)) return rc;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(nullptr, FP_ECUDA, std::string("fp_create: no CUDA device available (") +
+                                           cudaGetErrorString(e) + "); there is no CPU fallback");
+    if (device < 0 || device >= ndev) return fail(nullptr, FP_EINVAL, "fp_create: bad device ordinal");
+    fp_ctx* c = new fp_ctx();
+    c->device = device;
+    e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        int rc = fp_cuda_fail(c, e, "cudaSetDevice");
+        delete c;
+        return rc;
+    }
+    auto bail = [&](int rc) {
+        g_error = c->err;
+        fp_destroy(c);
+        return rc;
+    };
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaStreamCreate"));
+    c->W = g->width;
+    c->H = g->height;
+    c->boundary = g->boundary;
+    c->cell_size = g->cell_size;
+    c->P = (c->W + 31) / 32;
+    const size_t ncell = (size_t)c->W * c->H;
+    const size_t nwords = (size_t)c->P * c->H;
+    if (cudaMalloc(&c->d_wall, nwords * 4) || cudaMalloc(&c->d_exit, nwords * 4) ||
+        cudaMalloc(&c->d_occ, nwords * 4) || cudaMalloc(&c->d_field, ncell * 8) ||
+        cudaMalloc(&c->d_counters, 16 * sizeof(unsigned long long)) ||
+        cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)))
+        return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaMalloc(grid)"));
+    uint8_t* d_cells = nullptr;
+    if (cudaMalloc(&d_cells, ncell) != cudaSuccess)
+        return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaMalloc(cells)"));
+    cudaMemcpyAsync(d_cells, cells, ncell, cudaMemcpyHostToDevice, c->stream);
+    pack_planes_kernel<<<1184, 256, 0, c->stream>>>(d_cells, c->W, c->H, c->P, c->d_wall, c->d_exit);
+    c->ctr.kernel_launches++;
+    cudaMemsetAsync(c->d_occ, 0, nwords * 4, c->stream);
+    int rc = FP_OK;
+    if (field) {
+        cudaMemcpyAsync(c->d_field, field, ncell * 8, cudaMemcpyHostToDevice, c->stream);
+    } else {
+        rc = fp_field_compute(c, d_cells);
+    }
+    e = cudaStreamSynchronize(c->stream);
+    cudaFree(d_cells);
+    if (rc != FP_OK) return bail(rc);
+    if (e != cudaSuccess) return bail(fp_cuda_fail(c, e, "fp_create"));
+    *out = c;
+    return FP_OK;
+}
+
+extern "C" void fp_destroy(fp_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    free_agents(c);
+    void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_res, c->d_counters, c->d_temp};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (c->h_counters) cudaFreeHost(c->h_counters);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+extern "C" int fp_static_field(const fp_grid_desc* g, const uint8_t* cells, int device, double* out) {
+    fp_ctx* c = nullptr;
+    if (int rc = fp_create(g, cells, nullptr, device, &c)) return rc;
+    int rc = fp_get_field(c, out);
+    fp_destroy(c);
+    return rc;
+}
+
+extern "C" int fp_get_field(const fp_ctx* cc, double* out) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c || !out) return fail(c, FP_EINVAL, "fp_get_field: null argument");
+    cudaSetDevice(c->device);
+    FP_CUDA(c, cudaMemcpyAsync(out, c->d_field, (size_t)c->W * c->H * 8, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const uint8_t* alive) {
+    cudaStream_t s = c->stream;
+    const uint32_t n = c->n;
+    FP_CUDA(c, cudaMemcpyAsync(c->d_x, x, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    FP_CUDA(c, cudaMemcpyAsync(c->d_y, y, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    if (alive)
+        FP_CUDA(c, cudaMemcpyAsync(c->d_alive, alive, n, cudaMemcpyHostToDevice, s));
+    else
+        FP_CUDA(c, cudaMemsetAsync(c->d_alive, 1, n, s));
+    FP_CUDA(c, cudaMemsetAsync(c->d_occ, 0, (size_t)c->P * c->H * 4, s));
+    unsigned long long init[3] = {~0ull, ~0ull, ~0ull};
+    FP_CUDA(c, cudaMemcpyAsync(c->d_counters + 8, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    if (n) {
+        build_occ_kernel<<<fp_blocks(n, 256), 256, 0, s>>>(c->d_x, c->d_y, c->d_alive, n, geo_of(c), c->d_occ,
+                                                            c->d_counters + 8);
+        FP_LAUNCHED(c);
+    }
+    FP_CUDA(c, cudaMemcpyAsync(c->h_counters + 8, c->d_counters + 8, 3 * 8, cudaMemcpyDeviceToHost, s));
+    FP_CUDA(c, cudaStreamSynchronize(s));
+    const unsigned long long* e = c->h_counters + 8;
+    if (e[0] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[0]) + " is out of bounds");
+    if (e[1] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[1]) + " placed on a Wall cell");
+    if (e[2] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[2]) + " shares a cell");
+    int64_t al = 0;
+    if (alive)
+        for (uint32_t i = 0; i < n; ++i) al += alive[i] != 0;
+    else
+        al = n;
+    c->alive = al;
+    return FP_OK;
+}
+
+extern "C" int fp_set_agents(fp_ctx* c, uint32_t n, const int32_t* x, const int32_t* y, const int32_t* v_max,
+                             const uint8_t* alive, int64_t step) {
+    if (!c) return fail(nullptr, FP_EINVAL, "fp_set_agents: null context");
+    if (n && (!x || !y || !v_max)) return fail(c, FP_EINVAL, "fp_set_agents: null roster arrays");
+    for (uint32_t i = 0; i < n; ++i)
+        if (v_max[i] < 1 || v_max[i] > 5) return fail(c, FP_EINVAL, "make_state: v_max must be in [1,5]");
+    cudaSetDevice(c->device);
+    if (int rc = ensure_agents(c, n)) return rc;
+    c->n = n;
+    c->step = step;
+    c->n_order = 0;
+    c->n_exits = 0;
+    if (n) {
+        int32_t* d_tmp = c->d_dx;  // stage v_max as i32, convert to u8
+        FP_CUDA(c, cudaMemcpyAsync(d_tmp, v_max, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
+        u8_from_i32_kernel<<<fp_blocks(n, 256), 256, 0, c->stream>>>(d_tmp, c->d_v, n);
+        FP_LAUNCHED(c);
+    }
+    if (int rc = upload_agents(c, x, y, alive)) return rc;
+    // desired = pos for alive agents (state.hpp:74)
+    FP_CUDA(c, cudaMemcpyAsync(c->d_dx, c->d_x, (size_t)n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    FP_CUDA(c, cudaMemcpyAsync(c->d_dy, c->d_y, (size_t)n * 4, cudaMemcpyDeviceToDevice, c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_update_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const uint8_t* alive) {
+    if (!c) return fail(nullptr, FP_EINVAL, "fp_update_agents: null context");
+    cudaSetDevice(c->device);
+    return upload_agents(c, x, y, alive);
+}
+
+extern "C" int fp_set_step(fp_ctx* c, int64_t step) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    c->step = step;
+    return FP_OK;
+}
+extern "C" int fp_get_step(const fp_ctx* c, int64_t* step) {
+    if (!c || !step) return fail(nullptr, FP_EINVAL, "null argument");
+    *step = c->step;
+    return FP_OK;
+}
+extern "C" int fp_get_alive_count(const fp_ctx* c, int64_t* a) {
+    if (!c || !a) return fail(nullptr, FP_EINVAL, "null argument");
+    *a = c->alive;
+    return FP_OK;
+}
+
+extern "C" int fp_set_potential(fp_ctx* c, int kind, double g) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (kind != FP_POTENTIAL_EXIT_DISTANCE && kind != FP_POTENTIAL_DRIVE_X)
+        return fail(c, FP_EINVAL, "fp_set_potential: unknown potential");
+    c->potential = kind;
+    c->drive_gradient = g;
+    return FP_OK;
+}
+
+extern "C" int fp_set_desired(fp_ctx* c, const int32_t* x, const int32_t* y) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    cudaSetDevice(c->device);
+    FP_CUDA(c, cudaMemcpyAsync(c->d_dx, x, (size_t)c->n * 4, cudaMemcpyHostToDevice, c->stream));
+    FP_CUDA(c, cudaMemcpyAsync(c->d_dy, y, (size_t)c->n * 4, cudaMemcpyHostToDevice, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_plan(fp_ctx* c, double k_s, uint64_t seed) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    cudaSetDevice(c->device);
+    if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+static int move_impl(fp_ctx* c, uint64_t seed, bool collect, fp_step_stats* out) {
+    const int64_t alive0 = c->alive;
+    if (int rc = fp_order_launch(c, seed, c->step)) return rc;
+    if (int rc = fp_motion_launch(c, collect)) return rc;
+    if (out) {
+        out->alive = c->alive;
+        out->exited = alive0 - c->alive;
+        out->displacement_cells = c->last_displacement;
+    }
+    return FP_OK;
+}
+
+extern "C" int fp_move(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    cudaSetDevice(c->device);
+    if (int rc = move_impl(c, seed, true, out)) return rc;
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    cudaSetDevice(c->device);
+    if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
+    if (int rc = move_impl(c, seed, true, out)) return rc;
+    c->step++;
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (steps < 1) return fail(c, FP_EINVAL, "SimParams: steps must be >= 1");
+    cudaSetDevice(c->device);
+    cudaEvent_t ev[3];
+    for (auto& e : ev) FP_CUDA(c, cudaEventCreate(&e));
+    fp_run_stats rs{};
+    float plan_ms = 0, move_ms = 0;
+    cudaEvent_t t0, t1;
+    FP_CUDA(c, cudaEventCreate(&t0));
+    FP_CUDA(c, cudaEventCreate(&t1));
+    FP_CUDA(c, cudaEventRecord(t0, c->stream));
+    for (int s = 0; s < steps; ++s) {
+        rs.agent_updates += c->alive;
+        const int64_t alive0 = c->alive;
+        cudaEventRecord(ev[0], c->stream);
+        if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
+        cudaEventRecord(ev[1], c->stream);
+        if (int rc = move_impl(c, seed, false, nullptr)) return rc;
+        cudaEventRecord(ev[2], c->stream);
+        cudaEventSynchronize(ev[2]);
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        plan_ms += a;
+        move_ms += b;
+        rs.exited += alive0 - c->alive;
+        rs.displacement_cells += c->last_displacement;
+        c->step++;
+        rs.steps++;
+    }
+    FP_CUDA(c, cudaEventRecord(t1, c->stream));
+    FP_CUDA(c, cudaEventSynchronize(t1));
+    float tot = 0;
+    cudaEventElapsedTime(&tot, t0, t1);
+    rs.wall_time_s = tot * 1e-3;
+    rs.plan_time_s = plan_ms * 1e-3;
+    rs.move_time_s = move_ms * 1e-3;
+    rs.alive = c->alive;
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+    if (out) *out = rs;
+    return FP_OK;
+}
+
+extern "C" int fp_get_agents(const fp_ctx* cc, int32_t* x, int32_t* y, uint8_t* alive) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    cudaSetDevice(c->device);
+    const size_t n = c->n;
+    if (x) FP_CUDA(c, cudaMemcpyAsync(x, c->d_x, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (y) FP_CUDA(c, cudaMemcpyAsync(y, c->d_y, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (alive) FP_CUDA(c, cudaMemcpyAsync(alive, c->d_alive, n, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_get_desired(const fp_ctx* cc, int32_t* x, int32_t* y) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    cudaSetDevice(c->device);
+    FP_CUDA(c, cudaMemcpyAsync(x, c->d_dx, (size_t)c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaMemcpyAsync(y, c->d_dy, (size_t)c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_get_occupancy(const fp_ctx* cc, int32_t* occ) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c || !occ) return fail(c, FP_EINVAL, "null argument");
+    cudaSetDevice(c->device);
+    const size_t ncell = (size_t)c->W * c->H;
+    int32_t* d = nullptr;
+    FP_CUDA(c, cudaMalloc(&d, ncell * 4));
+    cudaMemsetAsync(d, 0xFF, ncell * 4, c->stream);
+    if (c->n) {
+        occ_dump_kernel<<<fp_blocks(c->n, 256), 256, 0, c->stream>>>(c->d_x, c->d_y, c->d_alive, c->n, geo_of(c), d);
+        c->ctr.kernel_launches++;
+    }
+    cudaMemcpyAsync(occ, d, ncell * 4, cudaMemcpyDeviceToHost, c->stream);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return fp_cuda_fail(c, e, "fp_get_occupancy");
+    return FP_OK;
+}
+
+extern "C" int fp_get_exited(const fp_ctx* cc, uint32_t* ids, uint32_t cap, uint32_t* n) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c || !n) return fail(c, FP_EINVAL, "null argument");
+    *n = c->n_exits;
+    if (c->n_exits == 0 || !ids) return FP_OK;
+    std::vector<unsigned long long> rec(c->n_exits);
+    cudaSetDevice(c->device);
+    FP_CUDA(c, cudaMemcpyAsync(rec.data(), c->d_exits, rec.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    for (uint32_t i = 0; i < c->n_exits && i < cap; ++i) ids[i] = (uint32_t)(rec[i] & 0xFFFFFFFFull);
+    return FP_OK;
+}
+
+extern "C" int fp_get_order(const fp_ctx* cc, uint32_t* ids, uint32_t cap, uint32_t* n) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c || !n) return fail(c, FP_EINVAL, "null argument");
+    *n = c->n_order;
+    if (!ids || c->n_order == 0) return FP_OK;
+    cudaSetDevice(c->device);
+    FP_CUDA(c, cudaMemcpyAsync(ids, c->d_order, (size_t)std::min(cap, c->n_order) * 4, cudaMemcpyDeviceToHost,
+                               c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_state_hash(const fp_ctx* cc, uint64_t* out) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c || !out) return fail(c, FP_EINVAL, "null argument");
+    std::vector<int32_t> x(c->n), y(c->n);
+    std::vector<uint8_t> a(c->n);
+    if (int rc = fp_get_agents(c, x.data(), y.data(), a.data())) return rc;
+    uint64_t h = 14695981039346656037ULL;  // state.hpp:80-95
+    auto mix = [&h](uint64_t v) {
+        h ^= v;
+        h *= 1099511628211ULL;
+    };
+    mix((uint64_t)c->step);
+    mix((uint64_t)c->alive);
+    for (uint32_t i = 0; i < c->n; ++i) {
+        mix(i);
+        mix((uint32_t)x[i]);
+        mix((uint32_t)y[i]);
+        mix(a[i] ? 1 : 0);
+    }
+    *out = h;
+    return FP_OK;
+}
+
+extern "C" int fp_get_choice(fp_ctx* c, uint32_t agent, double k_s, int32_t* cx, int32_t* cy, double* w,
+                             float* p, uint32_t cap, uint32_t* n) {
+    if (!c || !n) return fail(c, FP_EINVAL, "null argument");
+    if (agent >= c->n) return fail(c, FP_EINVAL, "fp_get_choice: agent out of range");
+    cudaSetDevice(c->device);
+    const size_t M = 128;
+    void* d = nullptr;
+    FP_CUDA(c, cudaMalloc(&d, M * (4 + 4 + 8 + 4) + 16));
+    int32_t* dcx = (int32_t*)d;
+    int32_t* dcy = dcx + M;
+    double* dw = (double*)(dcy + M);
+    float* dp = (float*)(dw + M);
+    uint32_t* dn = (uint32_t*)(dp + M);
+    int rc = fp_choice_launch(c, agent, k_s, dcx, dcy, dw, dp, dn);
+    if (rc == FP_OK) {
+        std::vector<char> h(M * (4 + 4 + 8 + 4) + 16);
+        cudaMemcpyAsync(h.data(), d, h.size(), cudaMemcpyDeviceToHost, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) {
+            rc = fp_cuda_fail(c, e, "fp_get_choice");
+        } else {
+            const int32_t* hx = (const int32_t*)h.data();
+            const int32_t* hy = hx + M;
+            const double* hw = (const double*)(hy + M);
+            const float* hp = (const float*)(hw + M);
+            const uint32_t k = *(const uint32_t*)(hp + M);
+            *n = k;
+            for (uint32_t i = 0; i < k && i < cap; ++i) {
+                if (cx) cx[i] = hx[i];
+                if (cy) cy[i] = hy[i];
+                if (w) w[i] = hw[i];
+                if (p) p[i] = hp[i];
+            }
+        }
+    }
+    cudaFree(d);
+    return rc;
+}
+
+extern "C" int fp_movement_order(int64_t n, uint64_t seed, int64_t step, int device, uint32_t* out) {
+    if (n < 0 || n >= ((int64_t)1 << 32)) return fail(nullptr, FP_EINVAL, "fp_movement_order: bad n");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(nullptr, FP_ECUDA, "fp_movement_order: no CUDA device available");
+    fp_ctx* c = new fp_ctx();
+    c->device = device;
+    cudaSetDevice(device);
+    int rc = FP_OK;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) rc = FP_ECUDA;
+    if (rc == FP_OK) rc = ensure_agents(c, (uint32_t)n);
+    if (rc == FP_OK && n > 0) rc = fp_order_positions(c, (uint32_t)n, seed, step, c->d_order);
+    if (rc == FP_OK && n > 0) {
+        cudaMemcpyAsync(out, c->d_order, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream);
+        cudaError_t e = cudaStreamSynchronize(c->stream);
+        if (e != cudaSuccess) rc = fp_cuda_fail(c, e, "fp_movement_order");
+    }
+    if (rc != FP_OK) g_error = c->err;
+    fp_destroy(c);
+    return rc;
+}
+
+// scenario_io.hpp:47-69 -- host placement (setup, untimed): partial Fisher-Yates over the
+// row-major free-cell list with the kSpawnStream draws.
+extern "C" int fp_spawn_agents(int32_t w, int32_t h, const uint8_t* cells, int64_t n, uint64_t seed,
+                               int32_t* x, int32_t* y) {
+    if (n < 0) return fail(nullptr, FP_EINVAL, "spawn_agents: agent count must be >= 0");
+    if (w < 1 || h < 1 || !cells) return fail(nullptr, FP_EINVAL, "spawn_agents: bad grid");
+    const size_t total = (size_t)w * h;
+    std::vector<uint32_t> fr;
+    fr.reserve(total / 2);
+    for (size_t i = 0; i < total; ++i)
+        if (cells[i] == FP_CELL_FREE) fr.push_back((uint32_t)i);
+    if ((size_t)n > fr.size())
+        return fail(nullptr, FP_ERUNTIME,
+                    "spawn_agents: requested " + std::to_string(n) + " agents but the scenario has only " +
+                        std::to_string(fr.size()) + " free cells");
+    uint64_t draw = 0;
+    const size_t F = fr.size();
+    for (int64_t i = 0; i < n; ++i) {
+        const uint64_t r = fp_rng_u64(seed, FP_SPAWN_STREAM, 0, draw++);
+        const size_t j = (size_t)i + (size_t)(r % (uint64_t)(F - (size_t)i));
+        std::swap(fr[(size_t)i], fr[j]);
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = (int32_t)(fr[(size_t)i] % (uint32_t)w);
+        y[i] = (int32_t)(fr[(size_t)i] / (uint32_t)w);
+    }
+    return FP_OK;
+}
+
+extern "C" int fp_get_counters(const fp_ctx* c, fp_counters* out) {
+    if (!c || !out) return fail(nullptr, FP_EINVAL, "null argument");
+    *out = c->ctr;
+    return FP_OK;
+}
