@@ -176,6 +176,7 @@ int fp_motion_launch(fp_ctx* ctx, bool collect_exits) {
 
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_counters, 0, 6 * sizeof(unsigned long long), s));
     ctx->n_exits = 0;
+    ctx->last_displacement = 0;
     const uint32_t n = ctx->n_order;
     if (n == 0) return FP_OK;
     move_seed_kernel<<<fp_blocks(n, 256), 256, 0, s>>>(a, ctx->d_order, n, ctx->d_pend_a);
