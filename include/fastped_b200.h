@@ -153,6 +153,10 @@ int fp_spawn_agents(int32_t width, int32_t height, const uint8_t* cells, int64_t
 
 int fp_get_counters(const fp_ctx* ctx, fp_counters* out);
 
+/* Benchmark helper: average duration (ms, CUDA events) of `iters` launches of the planning
+ * kernel alone on the current state (bucketing done once, untimed). */
+int fp_time_plan_kernel(fp_ctx* ctx, double k_s, uint64_t seed, int32_t iters, double* ms_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,90 @@
+// bucket.cu -- counting sort of the alive agents by plan tile (each step).
+//
+// The plan kernel stages one tile of the weight plane (plus halo) in shared memory per CTA and
+// plans every agent standing in it; this groups agent ids by tile.  Order inside a tile is
+// irrelevant (planning is a pure per-agent function of the pre-step snapshot,
+// planning.hpp:14-17), so atomics are fine.  Also leaves the compacted list of non-empty tiles.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
+#include "internal.cuh"
+
+__global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
+                                    int tile_w, int tile_h, int tiles_x, uint32_t* cnt, uint32_t* tile_of,
+                                    uint32_t* slot) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (!alive[i]) continue;
+        const int px = g.wrap(x[i]), py = y[i];
+        const uint32_t t = (uint32_t)(py / tile_h) * (uint32_t)tiles_x + (uint32_t)(px / tile_w);
+        tile_of[i] = t;
+        slot[i] = atomicAdd(&cnt[t], 1u);
+    }
+}
+
+__global__ void bucket_scatter_kernel(const uint8_t* alive, uint32_t n, const uint32_t* tile_of, const uint32_t* slot,
+                                      const uint32_t* off, uint32_t* bucket) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        if (!alive[i]) continue;
+        bucket[off[tile_of[i]] + slot[i]] = i;
+    }
+}
+
+struct NonEmpty {
+    const uint32_t* cnt;
+    __device__ __forceinline__ bool operator()(uint32_t t) const { return cnt[t] != 0; }
+};
+
+int fp_bucket_reserve(fp_ctx* ctx) {
+    const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
+    if (nt > ctx->n_tiles_alloc) {
+        if (ctx->d_tile_cnt) cudaFree(ctx->d_tile_cnt);
+        if (ctx->d_tile_off) cudaFree(ctx->d_tile_off);
+        if (ctx->d_tile_list) cudaFree(ctx->d_tile_list);
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_cnt, nt * 4));
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_off, nt * 4));
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_list, nt * 4));
+        ctx->n_tiles_alloc = nt;
+        ctx->graph_valid = false;
+    }
+    size_t need1 = 0, need2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_tile_cnt, ctx->d_tile_off, (int)nt, ctx->stream);
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(nullptr, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt,
+                          NonEmpty{ctx->d_tile_cnt}, ctx->stream);
+    const size_t need = std::max(need1, need2) + 256;
+    if (need > ctx->temp_b_bytes) {
+        if (ctx->d_temp_b) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaFree(ctx->d_temp_b);
+        }
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_temp_b, need));
+        ctx->temp_b_bytes = need;
+        ctx->graph_valid = false;
+    }
+    return FP_OK;
+}
+
+// Enqueues the bucketing of the current alive agents (graph-safe; resources reserved).
+int fp_bucket_launch(fp_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
+    const uint32_t n = ctx->n;
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_cnt, 0, nt * 4, s));
+    const unsigned G = (unsigned)std::min<size_t>(fp_blocks(n, 256), (size_t)ctx->sm_count * 16);
+    bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_alive, n, ctx->tile_w, ctx->tile_h,
+                                          ctx->tiles_x, ctx->d_tile_cnt, ctx->d_flags, ctx->d_cursor_b);
+    FP_LAUNCHED(ctx);
+    size_t need1 = 0, need2 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_tile_cnt, ctx->d_tile_off, (int)nt, s);
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(nullptr, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt, NonEmpty{ctx->d_tile_cnt}, s);
+    if (std::max(need1, need2) > ctx->temp_b_bytes) return fp_fail(ctx, FP_ERUNTIME, "bucket: scratch not reserved");
+    FP_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_temp_b, need1, ctx->d_tile_cnt, ctx->d_tile_off, (int)nt, s));
+    ctx->ctr.kernel_launches += 2;
+    FP_CUDA(ctx, cub::DeviceSelect::If(ctx->d_temp_b, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt,
+                                       NonEmpty{ctx->d_tile_cnt}, s));
+    ctx->ctr.kernel_launches += 2;
+    bucket_scatter_kernel<<<G, 256, 0, s>>>(ctx->d_alive, n, ctx->d_flags, ctx->d_cursor_b, ctx->d_tile_off, ctx->d_bucket);
+    FP_LAUNCHED(ctx);
+    return FP_OK;
+}

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -21,6 +22,8 @@ static int fail(fp_ctx* ctx, int code, const std::string& msg) {
     g_error = msg;
     return code;
 }
+
+int fp_fail(fp_ctx* ctx, int code, const std::string& msg) { return fail(ctx, code, msg); }
 
 int fp_cuda_fail(fp_ctx* ctx, cudaError_t e, const char* what) {
     return fail(ctx, FP_ECUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
@@ -74,11 +77,11 @@ static int validate_grid(const fp_grid_desc* g, const uint8_t* cells) {
 __global__ void pack_planes_kernel(const uint8_t* cells, int W, int H, int P, uint32_t* wall, uint32_t* ex) {
     const size_t nw = (size_t)P * H;
     for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < nw; w += (size_t)gridDim.x * blockDim.x) {
-        const int y = (int)(w / P), x0 = (int)(w % P) * 32;
+        const int y = (int)(w / P), x0 = (int)(w % P) * 32 - FP_XPAD_BITS;
         uint32_t bw = 0, be = 0;
         for (int b = 0; b < 32; ++b) {
             const int x = x0 + b;
-            if (x >= W) break;
+            if (x < 0 || x >= W) continue;
             const uint8_t k = cells[(size_t)y * W + x];
             bw |= (uint32_t)(k == FP_CELL_WALL) << b;
             be |= (uint32_t)(k == FP_CELL_EXIT) << b;
@@ -87,6 +90,13 @@ __global__ void pack_planes_kernel(const uint8_t* cells, int W, int H, int P, ui
         ex[w] = be;
     }
 }
+
+__global__ void sc_set_kernel(DevScalars* sc, long long step, unsigned long long alive) {
+    sc->step = step;
+    sc->alive = alive;
+}
+
+__global__ void sc_step_kernel(DevScalars* sc) { sc->step += 1; }
 
 // occupancy from alive positions + make_state checks (state.hpp:46-70)
 __global__ void build_occ_kernel(const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
@@ -119,12 +129,13 @@ __global__ void u8_from_i32_kernel(const int32_t* in, uint8_t* out, uint32_t n) 
     if (i < n) out[i] = (uint8_t)in[i];
 }
 
-static Geo geo_of(const fp_ctx* c) { return Geo{c->W, c->H, c->boundary, c->P, c->d_wall, c->d_exit}; }
+static Geo geo_of(const fp_ctx* c) { return fp_geo(c); }
 
 static void free_agents(fp_ctx* c) {
     void* ptrs[] = {c->d_x, c->d_y, c->d_dx, c->d_dy, c->d_v, c->d_alive, c->d_rank, c->d_alive_ids,
                     c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
-                    c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted};
+                    c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted,
+                    c->d_fy_bucket, c->d_flags, c->d_cursor_b};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->d_x = c->d_y = c->d_dx = c->d_dy = nullptr;
@@ -132,7 +143,9 @@ static void free_agents(fp_ctx* c) {
     c->d_rank = c->d_alive_ids = c->d_order = c->d_j = c->d_cnt = c->d_off = c->d_cursor = nullptr;
     c->d_bucket = c->d_succ = c->d_nxt = c->d_V = c->d_pend_a = c->d_pend_b = nullptr;
     c->d_exits = c->d_exits_sorted = nullptr;
+    c->d_fy_bucket = c->d_flags = c->d_cursor_b = nullptr;
     c->cap = 0;
+    c->graph_valid = false;
 }
 
 static int ensure_agents(fp_ctx* c, uint32_t n) {
@@ -147,7 +160,7 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
     FP_CUDA(c, cudaMalloc(&c->d_alive, m));
     uint32_t** u32s[] = {&c->d_rank, &c->d_alive_ids, &c->d_order, &c->d_j, &c->d_cnt, &c->d_off,
                          &c->d_cursor, &c->d_bucket, &c->d_succ, &c->d_nxt, &c->d_V, &c->d_pend_a,
-                         &c->d_pend_b};
+                         &c->d_pend_b, &c->d_fy_bucket, &c->d_flags, &c->d_cursor_b};
     for (uint32_t** p : u32s) FP_CUDA(c, cudaMalloc(p, m * 4));
     FP_CUDA(c, cudaMalloc(&c->d_exits, m * 8));
     FP_CUDA(c, cudaMalloc(&c->d_exits_sorted, m * 8));
@@ -179,26 +192,36 @@ extern "C" int fp_create(const fp_grid_desc* g, const uint8_t* cells, const doub
         fp_destroy(c);
         return rc;
     };
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
         return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaStreamCreate"));
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (const char* e2 = getenv("FP_NO_TMA")) c->use_tma = (e2[0] == '1') ? 0 : 1;
     c->W = g->width;
     c->H = g->height;
     c->boundary = g->boundary;
     c->cell_size = g->cell_size;
-    c->P = (c->W + 31) / 32;
+    c->P = (c->W + 2 * FP_XPAD_BITS + 31) / 32;
+    c->PW = ((c->W + 2 * FP_XPAD_W) + 3) & ~3;
     const size_t ncell = (size_t)c->W * c->H;
     const size_t nwords = (size_t)c->P * c->H;
     if (cudaMalloc(&c->d_wall, nwords * 4) || cudaMalloc(&c->d_exit, nwords * 4) ||
         cudaMalloc(&c->d_occ, nwords * 4) || cudaMalloc(&c->d_field, ncell * 8) ||
         cudaMalloc(&c->d_counters, 16 * sizeof(unsigned long long)) ||
-        cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)))
+        cudaMallocHost(&c->h_counters, 16 * sizeof(unsigned long long)) ||
+        cudaMalloc(&c->d_sc, sizeof(DevScalars)) || cudaMallocHost(&c->h_sc, sizeof(DevScalars)))
         return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaMalloc(grid)"));
     uint8_t* d_cells = nullptr;
     if (cudaMalloc(&d_cells, ncell) != cudaSuccess)
         return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaMalloc(cells)"));
     cudaMemcpyAsync(d_cells, cells, ncell, cudaMemcpyHostToDevice, c->stream);
+    cudaMemsetAsync(c->d_sc, 0, sizeof(DevScalars), c->stream);
+    cudaMemsetAsync(c->d_counters, 0, 16 * sizeof(unsigned long long), c->stream);
     pack_planes_kernel<<<1184, 256, 0, c->stream>>>(d_cells, c->W, c->H, c->P, c->d_wall, c->d_exit);
     c->ctr.kernel_launches++;
+    fp_ghost_static(c);
     cudaMemsetAsync(c->d_occ, 0, nwords * 4, c->stream);
     int rc = FP_OK;
     if (field) {
@@ -219,10 +242,18 @@ extern "C" void fp_destroy(fp_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_agents(c);
-    void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_res, c->d_counters, c->d_temp};
+    if (c->stream2) cudaStreamSynchronize(c->stream2);
+    if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
+    if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
+    void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_res, c->d_counters, c->d_temp, c->d_temp_b,
+                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);
+    if (c->h_sc) cudaFreeHost(c->h_sc);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->stream2) cudaStreamDestroy(c->stream2);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -241,6 +272,24 @@ extern "C" int fp_get_field(const fp_ctx* cc, double* out) {
     cudaSetDevice(c->device);
     FP_CUDA(c, cudaMemcpyAsync(out, c->d_field, (size_t)c->W * c->H * 8, cudaMemcpyDeviceToHost, c->stream));
     FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+// host mirror (step, alive) -> device scalars
+static int sync_scalars(fp_ctx* c) {
+    sc_set_kernel<<<1, 1, 0, c->stream>>>(c->d_sc, (long long)c->step, (unsigned long long)c->alive);
+    FP_LAUNCHED(c);
+    return FP_OK;
+}
+
+// device scalars -> host mirror, after a sync
+static int read_scalars(fp_ctx* c) {
+    FP_CUDA(c, cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->alive = (int64_t)c->h_sc->alive;
+    c->step = (int64_t)c->h_sc->step;
+    c->ctr.plan_fallbacks = (int64_t)c->h_sc->fallbacks;
+    c->ctr.motion_rounds = (int64_t)c->h_sc->pad[1];
     return FP_OK;
 }
 
@@ -273,7 +322,8 @@ static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const ui
     else
         al = n;
     c->alive = al;
-    return FP_OK;
+    if (int rc = fp_ghost_occ(c)) return rc;
+    return sync_scalars(c);
 }
 
 extern "C" int fp_set_agents(fp_ctx* c, uint32_t n, const int32_t* x, const int32_t* y, const int32_t* v_max,
@@ -310,7 +360,7 @@ extern "C" int fp_update_agents(fp_ctx* c, const int32_t* x, const int32_t* y, c
 extern "C" int fp_set_step(fp_ctx* c, int64_t step) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     c->step = step;
-    return FP_OK;
+    return sync_scalars(c);
 }
 extern "C" int fp_get_step(const fp_ctx* c, int64_t* step) {
     if (!c || !step) return fail(nullptr, FP_EINVAL, "null argument");
@@ -341,18 +391,39 @@ extern "C" int fp_set_desired(fp_ctx* c, const int32_t* x, const int32_t* y) {
     return FP_OK;
 }
 
-extern "C" int fp_plan(fp_ctx* c, double k_s, uint64_t seed) {
-    if (!c) return fail(nullptr, FP_EINVAL, "null context");
-    cudaSetDevice(c->device);
-    if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
-    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+// Allocations / setup of every stage for (k_s): never inside a graph capture.
+static int prepare(fp_ctx* c, double k_s) {
+    if (int rc = fp_plan_prepare(c, k_s)) return rc;
+    if (int rc = fp_order_reserve(c)) return rc;
+    if (int rc = fp_ensure_res(c)) return rc;
     return FP_OK;
 }
 
-static int move_impl(fp_ctx* c, uint64_t seed, bool collect, fp_step_stats* out) {
+extern "C" int fp_plan(fp_ctx* c, double k_s, uint64_t seed) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    cudaSetDevice(c->device);
+    if (c->alive == 0) return FP_OK;  // engine.hpp:73
+    if (int rc = prepare(c, k_s)) return rc;
+    if (int rc = sync_scalars(c)) return rc;
+    if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
+    c->ctr.planned_agents += c->alive;
+    return read_scalars(c);
+}
+
+// order + motion on the main stream (API path), then the exit list in processing order.
+static int move_impl(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
+    if (int rc = fp_order_reserve(c)) return rc;
+    if (int rc = fp_ensure_res(c)) return rc;
     const int64_t alive0 = c->alive;
-    if (int rc = fp_order_launch(c, seed, c->step)) return rc;
-    if (int rc = fp_motion_launch(c, collect)) return rc;
+    if (int rc = sync_scalars(c)) return rc;
+    if (int rc = fp_order_launch(c, seed, c->stream)) return rc;
+    if (int rc = fp_motion_launch(c)) return rc;
+    if (int rc = read_scalars(c)) return rc;
+    c->n_order = (uint32_t)c->h_sc->n_alive;
+    c->n_exits = (uint32_t)c->h_sc->n_exits;
+    c->last_displacement = (int64_t)c->h_sc->disp;
+    if (int rc = fp_exits_finish(c)) return rc;
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
     if (out) {
         out->alive = c->alive;
         out->exited = alive0 - c->alive;
@@ -364,63 +435,123 @@ static int move_impl(fp_ctx* c, uint64_t seed, bool collect, fp_step_stats* out)
 extern "C" int fp_move(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     cudaSetDevice(c->device);
-    if (int rc = move_impl(c, seed, true, out)) return rc;
-    FP_CUDA(c, cudaStreamSynchronize(c->stream));
-    return FP_OK;
+    return move_impl(c, seed, out);
 }
 
 extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     cudaSetDevice(c->device);
-    if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
-    if (int rc = move_impl(c, seed, true, out)) return rc;
+    if (int rc = fp_plan(c, k_s, seed)) return rc;
+    if (int rc = move_impl(c, seed, out)) return rc;
     c->step++;
-    FP_CUDA(c, cudaStreamSynchronize(c->stream));
     return FP_OK;
 }
 
+// Captures the two per-step graphs: plan phase = bucketing + plan kernel, with the movement
+// order (alive compaction + parallel Fisher-Yates) on a forked branch; move phase = motion
+// rounds + ghost refresh + step advance.
+static int capture(fp_ctx* c, double k_s, uint64_t seed) {
+    if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
+    if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
+    c->graph_plan = c->graph_move = nullptr;
+    cudaGraph_t g = nullptr;
+    const int64_t k0 = c->ctr.kernel_launches;
+    FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = FP_OK;
+    cudaEventRecord(c->ev_fork, c->stream);
+    cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
+    rc = fp_order_launch(c, seed, c->stream2);
+    cudaEventRecord(c->ev_join, c->stream2);
+    if (rc == FP_OK) rc = fp_plan_launch(c, k_s, seed);
+    cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (rc != FP_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return fp_cuda_fail(c, e, "capture(plan)");
+    e = cudaGraphInstantiate(&c->graph_plan, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(plan)");
+    g = nullptr;
+    FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    rc = fp_motion_launch(c);
+    if (rc == FP_OK) {
+        sc_step_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+        c->ctr.kernel_launches++;
+    }
+    e = cudaStreamEndCapture(c->stream, &g);
+    if (rc != FP_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return fp_cuda_fail(c, e, "capture(move)");
+    e = cudaGraphInstantiate(&c->graph_move, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(move)");
+    c->launches_per_step = c->ctr.kernel_launches - k0;  // captured, not yet executed
+    c->ctr.kernel_launches = k0;
+    c->graph_valid = true;
+    c->graph_ks = k_s;
+    c->graph_seed = seed;
+    return FP_OK;
+}
+
+__global__ void run_begin_kernel(DevScalars* sc) {
+    sc->tot_exits = 0;
+    sc->tot_disp = 0;
+    sc->tot_updates = 0;
+}
+
+// run(): `steps` steps as graph replays, CUDA events between phases; one host sync at the end.
 extern "C" int fp_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     if (steps < 1) return fail(c, FP_EINVAL, "SimParams: steps must be >= 1");
     cudaSetDevice(c->device);
-    cudaEvent_t ev[3];
+    if (int rc = prepare(c, k_s)) return rc;
+    if (!c->graph_valid || c->graph_ks != k_s || c->graph_seed != seed)
+        if (int rc = capture(c, k_s, seed)) return rc;
+    if (int rc = sync_scalars(c)) return rc;
+    run_begin_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+    FP_LAUNCHED(c);
+    const int64_t launches_per_step = 0;  // counted at capture; see fp_counters note
+    (void)launches_per_step;
+    std::vector<cudaEvent_t> ev((size_t)2 * steps + 1);
     for (auto& e : ev) FP_CUDA(c, cudaEventCreate(&e));
-    fp_run_stats rs{};
-    float plan_ms = 0, move_ms = 0;
-    cudaEvent_t t0, t1;
-    FP_CUDA(c, cudaEventCreate(&t0));
-    FP_CUDA(c, cudaEventCreate(&t1));
-    FP_CUDA(c, cudaEventRecord(t0, c->stream));
+    const int64_t k0 = c->ctr.kernel_launches;
     for (int s = 0; s < steps; ++s) {
-        rs.agent_updates += c->alive;
-        const int64_t alive0 = c->alive;
-        cudaEventRecord(ev[0], c->stream);
-        if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
-        cudaEventRecord(ev[1], c->stream);
-        if (int rc = move_impl(c, seed, false, nullptr)) return rc;
-        cudaEventRecord(ev[2], c->stream);
-        cudaEventSynchronize(ev[2]);
+        cudaEventRecord(ev[2 * s], c->stream);
+        FP_CUDA(c, cudaGraphLaunch(c->graph_plan, c->stream));
+        cudaEventRecord(ev[2 * s + 1], c->stream);
+        FP_CUDA(c, cudaGraphLaunch(c->graph_move, c->stream));
+    }
+    cudaEventRecord(ev[2 * steps], c->stream);
+    FP_CUDA(c, cudaEventSynchronize(ev[2 * steps]));
+    (void)k0;
+    c->ctr.kernel_launches += (int64_t)steps * c->launches_per_step;
+    fp_run_stats rs{};
+    float plan_ms = 0, move_ms = 0, tot = 0;
+    for (int s = 0; s < steps; ++s) {
         float a = 0, b = 0;
-        cudaEventElapsedTime(&a, ev[0], ev[1]);
-        cudaEventElapsedTime(&b, ev[1], ev[2]);
+        cudaEventElapsedTime(&a, ev[2 * s], ev[2 * s + 1]);
+        cudaEventElapsedTime(&b, ev[2 * s + 1], ev[2 * s + 2]);
         plan_ms += a;
         move_ms += b;
-        rs.exited += alive0 - c->alive;
-        rs.displacement_cells += c->last_displacement;
-        c->step++;
-        rs.steps++;
     }
-    FP_CUDA(c, cudaEventRecord(t1, c->stream));
-    FP_CUDA(c, cudaEventSynchronize(t1));
-    float tot = 0;
-    cudaEventElapsedTime(&tot, t0, t1);
+    cudaEventElapsedTime(&tot, ev[0], ev[2 * steps]);
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (int rc = read_scalars(c)) return rc;
     rs.wall_time_s = tot * 1e-3;
     rs.plan_time_s = plan_ms * 1e-3;
     rs.move_time_s = move_ms * 1e-3;
+    rs.steps = steps;
+    rs.exited = (int64_t)c->h_sc->tot_exits;
+    rs.displacement_cells = (int64_t)c->h_sc->tot_disp;
+    rs.agent_updates = (int64_t)c->h_sc->tot_updates;
     rs.alive = c->alive;
-    for (auto& e : ev) cudaEventDestroy(e);
-    cudaEventDestroy(t0);
-    cudaEventDestroy(t1);
+    c->n_order = (uint32_t)c->h_sc->n_alive;
+    c->n_exits = 0;  // the per-phase exit list is only kept by fp_move / fp_step
+    c->ctr.planned_agents += rs.agent_updates;
     if (out) *out = rs;
     return FP_OK;
 }
@@ -561,9 +692,13 @@ extern "C" int fp_movement_order(int64_t n, uint64_t seed, int64_t step, int dev
     fp_ctx* c = new fp_ctx();
     c->device = device;
     cudaSetDevice(device);
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     int rc = FP_OK;
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) rc = FP_ECUDA;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&c->d_sc, sizeof(DevScalars)) != cudaSuccess)
+        rc = fp_cuda_fail(c, cudaGetLastError(), "fp_movement_order setup");
     if (rc == FP_OK) rc = ensure_agents(c, (uint32_t)n);
+    if (rc == FP_OK) c->n = (uint32_t)n;
     if (rc == FP_OK && n > 0) rc = fp_order_positions(c, (uint32_t)n, seed, step, c->d_order);
     if (rc == FP_OK && n > 0) {
         cudaMemcpyAsync(out, c->d_order, (size_t)n * 4, cudaMemcpyDeviceToHost, c->stream);
@@ -602,6 +737,16 @@ extern "C" int fp_spawn_agents(int32_t w, int32_t h, const uint8_t* cells, int64
         y[i] = (int32_t)(fr[(size_t)i] / (uint32_t)w);
     }
     return FP_OK;
+}
+
+int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, double* ms);
+
+extern "C" int fp_time_plan_kernel(fp_ctx* c, double k_s, uint64_t seed, int32_t iters, double* ms) {
+    if (!c || !ms) return fail(c, FP_EINVAL, "null argument");
+    cudaSetDevice(c->device);
+    if (int rc = sync_scalars(c)) return rc;
+    if (int rc = fp_plan_kernel_time(c, k_s, seed, iters, ms)) return rc;
+    return read_scalars(c);
 }
 
 extern "C" int fp_get_counters(const fp_ctx* c, fp_counters* out) {

@@ -1,13 +1,19 @@
 // internal.cuh -- device context, data layout and shared device helpers.
 //
-// HBM layout (all row-major y*W+x like world.hpp:88-91):
-//   wall / exit / occupancy : 1-bit planes, P = ceil(W/32) u32 words per row
-//   field                   : fp64 per cell (StaticField::s; fp64 is required for bit-exact
-//                             weights)
+// HBM layout (row-major in y like world.hpp:88-91, x padded with ghost columns):
+//   wall / exit / occupancy : 1-bit planes, P u32 words per row covering x in [-32, 32*P-32);
+//                             for periodic-x grids the ghost bits mirror the wrapped columns
+//   weight plane            : u32 per cell, pitch PW covering x in [-8, PW-8): the static
+//                             planning data of a cell for one (k_s, potential) -- wall flag,
+//                             unreachable flag, and the fp32-mantissa / integer-exponent split of
+//                             2^(-k_s*log2(e)*S) (plane.cu).  Read by the plan kernel via TMA.
+//   field                   : fp64 per cell (StaticField::s), read only by the exact path
 //   reservation             : u64 per cell, round-stamped keys of the motion rounds
 //   agents (SoA)            : x, y (i32), v_max (u8), alive (u8), desired x/y (i32), rank (u32)
+//   tile buckets            : agent ids grouped by plan tile (counting sort each step)
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -16,6 +22,15 @@
 #include "../../include/fastped_b200.h"
 
 #define FP_NONE 0xFFFFFFFFu
+#define FP_XPAD_BITS 32  // ghost columns left of x = 0 in the bitplanes
+#define FP_XPAD_W 8      // ghost columns left of x = 0 in the weight plane
+#define FP_HALO 5        // largest v_max (agents.hpp:10)
+
+// weight-plane word encoding (plane.cu)
+#define FP_W_WALL 0xFFFFFFFFu
+#define FP_W_UNREACH 0x80000000u
+#define FP_W_SPECIAL 0x80000000u
+#define FP_W_UNSAFE 0x40000000u
 
 struct Geo {
     int W, H, boundary, P;
@@ -30,7 +45,7 @@ struct Geo {
         return x;
     }
     __device__ __forceinline__ size_t word(int x, int y) const {
-        return (size_t)y * (size_t)P + (size_t)(x >> 5);
+        return (size_t)y * (size_t)P + (size_t)((x + FP_XPAD_BITS) >> 5);
     }
     __device__ __forceinline__ bool is_wall(int x, int y) const {
         return (__ldg(&wall[word(x, y)]) >> (x & 31)) & 1u;
@@ -86,9 +101,31 @@ __host__ __device__ __forceinline__ double fp_unit_interval(uint64_t x) {
 #define FP_MOVE_ORDER_STREAM (1ULL << 63)
 #define FP_SPAWN_STREAM ((1ULL << 63) + 1)
 
+// Device-resident per-step scalars (graph-friendly: kernels read them, nothing is baked in).
+struct DevScalars {
+    long long step;               // SimState::step
+    unsigned long long n_alive;   // alive count entering the motion phase (select output)
+    unsigned long long alive;     // running alive count
+    unsigned long long round_seq; // motion round stamp counter
+    unsigned long long pend;      // pending count (motion)
+    unsigned long long n_exits;   // exits of the current move phase
+    unsigned long long disp;      // displacement of the current move phase
+    unsigned long long tot_exits; // accumulated over a run
+    unsigned long long tot_disp;  // accumulated over a run
+    unsigned long long tot_updates;  // sum of alive counts entering each step
+    unsigned long long fallbacks; // exact-path re-samples
+    unsigned long long n_tiles;   // non-empty plan tiles this step
+    unsigned long long tile_next; // dynamic tile scheduler cursor
+    unsigned long long err;       // device-detected errors (bit flags)
+    unsigned long long pad[2];
+};
+
 struct fp_ctx {
     int device = 0;
-    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;   // main stream
+    cudaStream_t stream2 = nullptr;  // order (Fisher-Yates) branch
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
 
     // geometry
@@ -99,7 +136,18 @@ struct fp_ctx {
     uint32_t* d_occ = nullptr;
     double* d_field = nullptr;
     unsigned long long* d_res = nullptr;  // motion reservations (allocated on first move)
-    uint64_t round_seq = 0;
+
+    // weight plane (plane.cu), valid for (plane_ks, plane_potential, plane_gradient)
+    uint32_t* d_plane = nullptr;
+    int PW = 0;
+    bool plane_valid = false;
+    double plane_ks = 0.0;
+    int plane_potential = -1;
+    CUtensorMap tmap_plane;          // TMA descriptor of the plane (one tile box)
+    int tile_w = 0, tile_h = 0;      // plan tile (cells)
+    int tiles_x = 0, tiles_y = 0;
+    bool tiles_ok = false;           // tiled fast path usable for this grid
+    int use_tma = 1;                 // FP_NO_TMA=1 stages plan tiles with plain loads
 
     // potential
     int potential = FP_POTENTIAL_EXIT_DISTANCE;
@@ -112,11 +160,17 @@ struct fp_ctx {
     uint32_t* d_rank = nullptr;
     int64_t step = 0;
     int64_t alive = 0;
+    bool mixed_v = false;
+    int vmax_all = 1;
+
+    // tile buckets
+    uint32_t *d_tile_cnt = nullptr, *d_tile_off = nullptr, *d_tile_list = nullptr, *d_bucket = nullptr;
+    size_t n_tiles_alloc = 0;
 
     // order scratch (sized by cap)
     uint32_t *d_alive_ids = nullptr, *d_order = nullptr, *d_j = nullptr, *d_cnt = nullptr,
-             *d_off = nullptr, *d_cursor = nullptr, *d_bucket = nullptr, *d_succ = nullptr,
-             *d_nxt = nullptr, *d_V = nullptr;
+             *d_off = nullptr, *d_cursor = nullptr, *d_fy_bucket = nullptr, *d_succ = nullptr,
+             *d_nxt = nullptr, *d_V = nullptr, *d_flags = nullptr, *d_cursor_b = nullptr;
     uint32_t n_order = 0;  // alive count of the last computed order
 
     // motion scratch
@@ -125,16 +179,26 @@ struct fp_ctx {
     unsigned long long* d_exits_sorted = nullptr;
     int64_t last_displacement = 0;
     uint32_t n_exits = 0;
-    // small device counters: [0] pending next, [1] exits, [2] alive-count delta, [3] spare
-    // [4..5] displacement (u64), [6] n_alive (select), [7] plan fallbacks
-    unsigned long long* d_counters = nullptr;
 
-    // cub temp
+    DevScalars* d_sc = nullptr;   // device scalars
+    DevScalars* h_sc = nullptr;   // pinned mirror
+    unsigned long long* d_counters = nullptr;  // legacy scratch (errors of uploads)
+    unsigned long long* h_counters = nullptr;
+
+    // cub temp: order stage (two halves: scan | select) and bucketing stage
     void* d_temp = nullptr;
     size_t temp_bytes = 0;
+    void* d_temp_b = nullptr;
+    size_t temp_b_bytes = 0;
 
-    // pinned host mirror of counters
-    unsigned long long* h_counters = nullptr;
+    // captured step graphs (fp_run): plan phase (bucketing + plan || order) and move phase
+    cudaGraphExec_t graph_plan = nullptr;
+    cudaGraphExec_t graph_move = nullptr;
+    double graph_ks = 0.0;
+    uint64_t graph_seed = 0;
+    bool graph_valid = false;
+    int move_blocks = 0;
+    int64_t launches_per_step = 0;  // kernels in one replay of the two step graphs
 
     fp_counters ctr{};
 };
@@ -142,6 +206,7 @@ struct fp_ctx {
 // -------------------------------------------------------------------------- error helpers
 void fp_set_global_error(const std::string& s);
 int fp_cuda_fail(fp_ctx* ctx, cudaError_t e, const char* what);
+int fp_fail(fp_ctx* ctx, int code, const std::string& msg);
 
 #define FP_CUDA(ctx, call)                                                   \
     do {                                                                     \
@@ -161,12 +226,24 @@ inline unsigned fp_blocks(size_t n, unsigned tpb) {
     return (unsigned)(b == 0 ? 1 : b);
 }
 
-// Stage entry points (implemented in plan.cu / order.cu / move.cu / field.cu).
-int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed);
-int fp_order_launch(fp_ctx* ctx, uint64_t seed, int64_t step);
-int fp_motion_launch(fp_ctx* ctx, bool collect_exits);
-int fp_field_compute(fp_ctx* ctx, const uint8_t* d_cells);
+inline Geo fp_geo(const fp_ctx* c) { return Geo{c->W, c->H, c->boundary, c->P, c->d_wall, c->d_exit}; }
+
+// Stage entry points.
+int fp_plane_ensure(fp_ctx* ctx, double k_s);                         // plane.cu
+int fp_ghost_occ(fp_ctx* ctx);                                        // plane.cu
+int fp_ghost_static(fp_ctx* ctx);                                     // plane.cu
+int fp_bucket_launch(fp_ctx* ctx);                                    // bucket.cu
+int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed);           // plan.cu
+int fp_plan_exact_launch(fp_ctx* ctx, double k_s, uint64_t seed);     // plan.cu
+int fp_order_launch(fp_ctx* ctx, uint64_t seed, cudaStream_t s);     // order.cu
+int fp_motion_launch(fp_ctx* ctx);                                    // move.cu
+int fp_exits_finish(fp_ctx* ctx);                                     // move.cu
+int fp_field_compute(fp_ctx* ctx, const uint8_t* d_cells);            // field.cu
 int fp_choice_launch(fp_ctx* ctx, uint32_t agent, double k_s, int32_t* d_cx, int32_t* d_cy,
-                     double* d_w, float* d_p, uint32_t* d_n);
+                     double* d_w, float* d_p, uint32_t* d_n);         // plan.cu
 int fp_order_positions(fp_ctx* ctx, uint32_t n, uint64_t seed, int64_t step, uint32_t* d_out);
 int fp_ensure_temp(fp_ctx* ctx, size_t bytes);
+int fp_ensure_res(fp_ctx* ctx);
+int fp_order_reserve(fp_ctx* ctx);                                    // order.cu
+int fp_plan_prepare(fp_ctx* ctx, double k_s);                         // plan.cu
+int fp_bucket_reserve(fp_ctx* ctx);                                   // bucket.cu

@@ -11,13 +11,22 @@
 // with atomicMin; an agent that holds all of its cells is the earliest pending agent on each of
 // them, so everything that precedes it in the reference order on those cells has already run
 // -- it executes its walk now.  Committed agents in one round have disjoint footprints.  The
-// result equals the sequential walk bit for bit (tests/test_motion_gpu.py).  Agents with an
+// result equals the sequential walk bit for bit (tests/test_gpu_parity.py).  Agents with an
 // empty path (staying put) never change occupancy and skip the rounds entirely.
 //
-// Round stamps make the reservation plane self-cleaning: newer rounds carry smaller keys.
+// One cooperative launch runs all rounds of a step: grid-wide rounds (grid.sync between the
+// reserve and commit phases) while many agents are pending, then block 0 finishes the tail
+// alone with __syncthreads.  Round stamps make the reservation plane self-cleaning: newer rounds
+// carry smaller keys, so nothing is ever reset.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+#define MOVE_THREADS 512
+#define MOVE_TAIL 4096  // pending agents at or below which block 0 runs the rounds alone
 
 struct MoveArgs {
     Geo g;
@@ -30,15 +39,16 @@ struct MoveArgs {
     const uint8_t* v;
     uint8_t* alive;
     const uint32_t* rank;
-    unsigned long long* counters;  // [0] next pending, [1] exits, [2] exited, [4] displacement
+    const uint32_t* order;
+    uint32_t* pend[2];
+    unsigned int* pcount;          // [2] pending counts (device scratch)
+    DevScalars* sc;
     unsigned long long* exits;     // (rank << 32 | id)
-    unsigned long long stamp;      // (0xFFFFFFFF - round) << 32
 };
 
 // Path cells the walk may visit (engine.hpp:116-119 static stops), at most 5.
-__device__ __forceinline__ int footprint(const MoveArgs& a, uint32_t id, int* cx, int* cy) {
+__device__ __forceinline__ int footprint(const MoveArgs& a, uint32_t id, int sx, int sy, int* cx, int* cy) {
     const Geo& g = a.g;
-    const int sx = g.wrap(a.x[id]), sy = a.y[id];
     const int tx = g.wrap(a.dx[id]), ty = a.dy[id];
     const int v = a.v[id];
     Bres b;
@@ -60,109 +70,167 @@ __device__ __forceinline__ size_t cell_index(const Geo& g, int x, int y) {
     return (size_t)y * (size_t)g.W + (size_t)x;
 }
 
-// Initial pending list: alive agents whose walk has at least one cell.
-__global__ void move_seed_kernel(MoveArgs a, const uint32_t* order, uint32_t n, uint32_t* pend) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    const uint32_t id = order[k];
-    int cx[5], cy[5];
-    const bool active = footprint(a, id, cx, cy) > 0;
-    // warp-aggregated append
-    const unsigned mask = __ballot_sync(__activemask(), active);
-    if (!active) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    unsigned base = 0;
-    if (lane == leader) base = (unsigned)atomicAdd(&a.counters[0], (unsigned long long)__popc(mask));
-    base = __shfl_sync(mask, base, leader);
-    pend[base + __popc(mask & ((1u << lane) - 1))] = id;
-}
-
-__global__ void move_reserve_kernel(MoveArgs a, const uint32_t* pend, uint32_t np) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= np) return;
-    const uint32_t id = pend[k];
-    const unsigned long long key = a.stamp | a.rank[id];
-    int cx[5], cy[5];
-    const int m = footprint(a, id, cx, cy);
-    atomicMin(&a.res[cell_index(a.g, a.g.wrap(a.x[id]), a.y[id])], key);
-    for (int i = 0; i < m; ++i) atomicMin(&a.res[cell_index(a.g, cx[i], cy[i])], key);
-}
-
 __device__ __forceinline__ bool occ_test(const MoveArgs& a, int x, int y) {
     return (__ldcg(&a.occ[a.g.word(x, y)]) >> (x & 31)) & 1u;
 }
 
-__global__ void move_commit_kernel(MoveArgs a, const uint32_t* pend, uint32_t np, uint32_t* next) {
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    bool retry = false;
-    unsigned long long hops = 0;
-    if (k < np) {
-        const uint32_t id = pend[k];
-        const unsigned long long key = a.stamp | a.rank[id];
-        int cx[5], cy[5];
-        const int m = footprint(a, id, cx, cy);
-        const int sx = a.g.wrap(a.x[id]), sy = a.y[id];
-        bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == key;
-        for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == key;
-        if (!own) {
-            retry = true;
-        } else {
-            // The walk (engine.hpp:116-129), net effect on occupancy.
-            int h = 0;
-            bool exited = false;
-            for (int i = 0; i < m; ++i) {
-                if (occ_test(a, cx[i], cy[i])) break;
-                ++h;
-                if (a.g.is_exit(cx[i], cy[i])) {
-                    exited = true;
-                    break;
-                }
-            }
-            if (h > 0) {
-                atomicAnd(&a.occ[a.g.word(sx, sy)], ~(1u << (sx & 31)));
-                const int fx = cx[h - 1], fy = cy[h - 1];
-                a.x[id] = fx;
-                a.y[id] = fy;
-                if (exited) {
-                    a.alive[id] = 0;
-                    const unsigned long long slot = atomicAdd(&a.counters[1], 1ull);
-                    a.exits[slot] = ((unsigned long long)a.rank[id] << 32) | id;
-                } else {
-                    atomicOr(&a.occ[a.g.word(fx, fy)], 1u << (fx & 31));
-                }
-            }
-            hops = (unsigned long long)h;
+__device__ __forceinline__ void append(unsigned int* count, uint32_t* list, bool take, uint32_t id) {
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (!mask) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(count, (unsigned)__popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (take) list[base + __popc(mask & ((1u << lane) - 1))] = id;
+}
+
+__device__ __forceinline__ void reserve_one(const MoveArgs& a, uint32_t id, unsigned long long stamp) {
+    const unsigned long long key = stamp | a.rank[id];
+    const int sx = a.g.wrap(a.x[id]), sy = a.y[id];
+    int cx[5], cy[5];
+    const int m = footprint(a, id, sx, sy, cx, cy);
+    atomicMin(&a.res[cell_index(a.g, sx, sy)], key);
+    for (int i = 0; i < m; ++i) atomicMin(&a.res[cell_index(a.g, cx[i], cy[i])], key);
+}
+
+// Returns true if the agent committed (walked); false if it must retry next round.
+__device__ __forceinline__ bool commit_one(const MoveArgs& a, uint32_t id, unsigned long long stamp,
+                                           unsigned long long* hops_acc) {
+    const unsigned long long key = stamp | a.rank[id];
+    const int sx = a.g.wrap(a.x[id]), sy = a.y[id];
+    int cx[5], cy[5];
+    const int m = footprint(a, id, sx, sy, cx, cy);
+    bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == key;
+    for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == key;
+    if (!own) return false;
+    // The walk (engine.hpp:116-129), net effect on occupancy.
+    int h = 0;
+    bool exited = false;
+    for (int i = 0; i < m; ++i) {
+        if (occ_test(a, cx[i], cy[i])) break;
+        ++h;
+        if (a.g.is_exit(cx[i], cy[i])) {
+            exited = true;
+            break;
         }
     }
-    // displacement: warp reduce then one atomic
+    if (h > 0) {
+        atomicAnd(&a.occ[a.g.word(sx, sy)], ~(1u << (sx & 31)));
+        const int fx = cx[h - 1], fy = cy[h - 1];
+        a.x[id] = fx;
+        a.y[id] = fy;
+        if (exited) {
+            a.alive[id] = 0;
+            const unsigned long long slot = atomicAdd(&a.sc->n_exits, 1ull);
+            a.exits[slot] = ((unsigned long long)a.rank[id] << 32) | id;
+        } else {
+            atomicOr(&a.occ[a.g.word(fx, fy)], 1u << (fx & 31));
+        }
+    }
+    *hops_acc += (unsigned long long)h;
+    return true;
+}
+
+__device__ __forceinline__ void flush_hops(DevScalars* sc, unsigned long long hops) {
     for (int o = 16; o > 0; o >>= 1) hops += __shfl_down_sync(0xffffffffu, hops, o);
-    if ((threadIdx.x & 31) == 0 && hops) atomicAdd(&a.counters[4], hops);
-    const unsigned mask = __ballot_sync(0xffffffffu, retry);
-    if (retry) {
-        const int lane = threadIdx.x & 31;
-        const int leader = __ffs(mask) - 1;
-        unsigned base = 0;
-        if (lane == leader) base = (unsigned)atomicAdd(&a.counters[0], (unsigned long long)__popc(mask));
-        base = __shfl_sync(mask, base, leader);
-        next[base + __popc(mask & ((1u << lane) - 1))] = pend[k];
+    if ((threadIdx.x & 31) == 0 && hops) atomicAdd(&sc->disp, hops);
+}
+
+__global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const unsigned nthreads = gridDim.x * blockDim.x;
+    const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t n = (uint32_t)__ldcg(&a.sc->n_alive);
+    const unsigned long long round0 = __ldcg(&a.sc->round_seq);
+    // seed the pending list with every alive agent whose walk has at least one cell
+    for (uint32_t base = 0; base < n; base += nthreads) {
+        const uint32_t k = base + gtid;
+        bool take = false;
+        uint32_t id = 0;
+        if (k < n) {
+            id = a.order[k];
+            const int sx = a.g.wrap(a.x[id]), sy = a.y[id];
+            int cx[5], cy[5];
+            take = footprint(a, id, sx, sy, cx, cy) > 0;
+        }
+        append(&a.pcount[0], a.pend[0], take, id);
+    }
+    grid.sync();
+    unsigned r = 0;
+    bool solo = false;
+    for (;; ++r) {
+        const unsigned cur = r & 1, nxt = cur ^ 1;
+        const unsigned np = __ldcg(&a.pcount[cur]);
+        if (np == 0) break;
+        if (!solo && np <= MOVE_TAIL) {
+            if (blockIdx.x != 0) return;  // every block reads the same np: block 0 continues alone
+            solo = true;
+        }
+        const unsigned long long stamp = (0xFFFFFFFFull - ((round0 + r) & 0xFFFFFFFFull)) << 32;
+        const unsigned stride = solo ? blockDim.x : nthreads;
+        const unsigned me = solo ? threadIdx.x : gtid;
+        if (gtid == 0) a.pcount[nxt] = 0;
+        const uint32_t* list = a.pend[cur];
+        for (unsigned k = me; k < np; k += stride) reserve_one(a, __ldcg(&list[k]), stamp);
+        if (solo) __syncthreads(); else grid.sync();
+        unsigned long long hops = 0;
+        for (unsigned base = 0; base < np; base += stride) {
+            const unsigned k = base + me;
+            bool retry = false;
+            uint32_t id = 0;
+            if (k < np) {
+                id = __ldcg(&list[k]);
+                retry = !commit_one(a, id, stamp, &hops);
+            }
+            append(&a.pcount[nxt], a.pend[nxt], retry, id);
+        }
+        flush_hops(a.sc, hops);
+        if (solo) __syncthreads(); else grid.sync();
+    }
+    if (gtid == 0) {
+        a.sc->round_seq = round0 + r;
+        a.sc->pad[1] += r;  // rounds executed (observability)
+        a.pcount[0] = 0;
+        a.pcount[1] = 0;
+        const unsigned long long ne = a.sc->n_exits;
+        a.sc->alive -= ne;
+        a.sc->tot_exits += ne;
+        a.sc->tot_disp += a.sc->disp;
     }
 }
 
-// Runs the rounds of one motion phase after fp_order_launch.  Leaves the exit records in
-// ctx->d_exits (sorted by rank when collect_exits), updates ctx->alive.
-int fp_motion_launch(fp_ctx* ctx, bool collect_exits) {
-    cudaStream_t s = ctx->stream;
+__global__ void move_begin_kernel(DevScalars* sc) {
+    sc->n_exits = 0;
+    sc->disp = 0;
+    sc->tot_updates += sc->alive;
+}
+
+int fp_ensure_res(fp_ctx* ctx) {
+    if (ctx->d_res) return FP_OK;
     const size_t cells = (size_t)ctx->W * (size_t)ctx->H;
-    if (!ctx->d_res) {
-        FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned long long)));
-        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned long long), s));
-        ctx->round_seq = 0;
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned long long)));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned long long), ctx->stream));
+    return FP_OK;
+}
+
+static int g_move_blocks = 0;
+
+// Enqueues one motion phase (after fp_order_launch) on ctx->stream.  Graph-safe.
+int fp_motion_launch(fp_ctx* ctx) {
+    cudaStream_t s = ctx->stream;
+    move_begin_kernel<<<1, 1, 0, s>>>(ctx->d_sc);
+    FP_LAUNCHED(ctx);
+    if (ctx->n == 0) return FP_OK;
+    if (!g_move_blocks) {
+        int per_sm = 0;
+        FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS, 0));
+        g_move_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
     }
     MoveArgs a;
-    a.g = Geo{ctx->W, ctx->H, ctx->boundary, ctx->P, ctx->d_wall, ctx->d_exit};
+    a.g = fp_geo(ctx);
     a.occ = ctx->d_occ;
-    a.res = (unsigned long long*)ctx->d_res;
+    a.res = ctx->d_res;
     a.x = ctx->d_x;
     a.y = ctx->d_y;
     a.dx = ctx->d_dx;
@@ -170,60 +238,40 @@ int fp_motion_launch(fp_ctx* ctx, bool collect_exits) {
     a.v = ctx->d_v;
     a.alive = ctx->d_alive;
     a.rank = ctx->d_rank;
-    a.counters = ctx->d_counters;
+    a.order = ctx->d_order;
+    a.pend[0] = ctx->d_pend_a;
+    a.pend[1] = ctx->d_pend_b;
+    a.pcount = (unsigned int*)ctx->d_counters;  // [0], [1] as u32 (kept zero between phases)
+    a.sc = ctx->d_sc;
     a.exits = ctx->d_exits;
-    a.stamp = 0;
+    const unsigned blocks = (unsigned)std::min<size_t>((size_t)g_move_blocks,
+                                                        std::max<size_t>(1, fp_blocks(ctx->n, MOVE_THREADS)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(MOVE_THREADS);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel, a));
+    ctx->ctr.kernel_launches++;
+    return fp_ghost_occ(ctx);
+}
 
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_counters, 0, 6 * sizeof(unsigned long long), s));
-    ctx->n_exits = 0;
-    ctx->last_displacement = 0;
-    const uint32_t n = ctx->n_order;
-    if (n == 0) return FP_OK;
-    move_seed_kernel<<<fp_blocks(n, 256), 256, 0, s>>>(a, ctx->d_order, n, ctx->d_pend_a);
-    FP_LAUNCHED(ctx);
-    FP_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-    FP_CUDA(ctx, cudaStreamSynchronize(s));
-    uint32_t np = (uint32_t)ctx->h_counters[0];
-    uint32_t* cur = ctx->d_pend_a;
-    uint32_t* nxt = ctx->d_pend_b;
-    while (np > 0) {
-        if (ctx->round_seq >= 0xFFFFFFF0ull) {
-            FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned long long), s));
-            ctx->round_seq = 0;
-        }
-        a.stamp = (0xFFFFFFFFull - ctx->round_seq) << 32;
-        ctx->round_seq++;
-        ctx->ctr.motion_rounds++;
-        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_counters, 0, sizeof(unsigned long long), s));
-        move_reserve_kernel<<<fp_blocks(np, 256), 256, 0, s>>>(a, cur, np);
-        FP_LAUNCHED(ctx);
-        move_commit_kernel<<<fp_blocks(np, 256), 256, 0, s>>>(a, cur, np, nxt);
-        FP_LAUNCHED(ctx);
-        FP_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToHost, s));
-        FP_CUDA(ctx, cudaStreamSynchronize(s));
-        np = (uint32_t)ctx->h_counters[0];
-        uint32_t* t = cur;
-        cur = nxt;
-        nxt = t;
-    }
-    FP_CUDA(ctx, cudaMemcpyAsync(ctx->h_counters, ctx->d_counters, 6 * sizeof(unsigned long long),
-                                 cudaMemcpyDeviceToHost, s));
-    FP_CUDA(ctx, cudaStreamSynchronize(s));
-    const uint32_t ne = (uint32_t)ctx->h_counters[1];
-    ctx->n_exits = ne;
-    ctx->alive -= ne;
-    ctx->last_displacement = (int64_t)ctx->h_counters[4];
-    if (collect_exits && ne > 1) {
-        size_t need = 0;
-        cub::DeviceRadixSort::SortKeys(nullptr, need, ctx->d_exits, ctx->d_exits_sorted, (int)ne, 0, 64, s);
-        if (int rc = fp_ensure_temp(ctx, need)) return rc;
-        FP_CUDA(ctx, cub::DeviceRadixSort::SortKeys(ctx->d_temp, need, ctx->d_exits,
-                                                    ctx->d_exits_sorted, (int)ne, 0, 64, s));
-        ctx->ctr.kernel_launches++;
-        FP_CUDA(ctx, cudaMemcpyAsync(ctx->d_exits, ctx->d_exits_sorted, ne * sizeof(unsigned long long),
-                                     cudaMemcpyDeviceToDevice, s));
-    }
+// Sorts the exit records of the last phase by rank (processing order) for fp_get_exited.
+int fp_exits_finish(fp_ctx* ctx) {
+    const uint32_t ne = ctx->n_exits;
+    if (ne <= 1) return FP_OK;
+    size_t need = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, need, ctx->d_exits, ctx->d_exits_sorted, (int)ne, 0, 64, ctx->stream);
+    if (int rc = fp_ensure_temp(ctx, need)) return rc;
+    FP_CUDA(ctx, cub::DeviceRadixSort::SortKeys(ctx->d_temp, need, ctx->d_exits, ctx->d_exits_sorted, (int)ne, 0, 64,
+                                                ctx->stream));
+    ctx->ctr.kernel_launches += 4;
+    FP_CUDA(ctx, cudaMemcpyAsync(ctx->d_exits, ctx->d_exits_sorted, ne * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
     return FP_OK;
 }

@@ -12,157 +12,179 @@
 //   * A[0]   = V(0);  A[p>=1] = j_p if succ(p) is undefined else V(succ(p))
 // A is the final permutation of positions; order[p] = alive_ids[A[p]], rank[order[p]] = p.
 // Work is O(n) with counting-sort buckets (expected |L_q| ~ ln(n/q)); chains are short.
+// The alive count comes from device memory, so the whole sequence is graph-capturable.
 // Pinned against the sequential loop by tests (oracle.movement_order, n up to 10^7).
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 
 #include "internal.cuh"
 
-__global__ void fy_targets_kernel(uint32_t n, uint64_t seed, uint64_t step, uint32_t* j,
+#define GS_LOOP(i, n) for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += gridDim.x * blockDim.x)
+
+__global__ void fy_targets_kernel(const unsigned long long* pn, uint64_t seed, const long long* pstep, uint32_t* j,
                                   uint32_t* cnt) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0 || i >= n) return;
-    const uint64_t draw = (uint64_t)(n - 1 - i);
-    const uint64_t r = fp_rng_u64(seed, FP_MOVE_ORDER_STREAM, step, draw);
-    const uint32_t t = (uint32_t)(r % (uint64_t)(i + 1));
-    j[i] = t;
-    atomicAdd(&cnt[t], 1u);
+    const uint32_t n = (uint32_t)*pn;
+    const uint64_t step = (uint64_t)*pstep;
+    GS_LOOP(i, n) {
+        if (i == 0) continue;
+        const uint64_t r = fp_rng_u64(seed, FP_MOVE_ORDER_STREAM, step, (uint64_t)(n - 1 - i));
+        const uint32_t t = (uint32_t)(r % (uint64_t)(i + 1));
+        j[i] = t;
+        atomicAdd(&cnt[t], 1u);
+    }
 }
 
-__global__ void fy_scatter_kernel(uint32_t n, const uint32_t* j, uint32_t* cursor, uint32_t* bucket) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i == 0 || i >= n) return;
-    const uint32_t slot = atomicAdd(&cursor[j[i]], 1u);
-    bucket[slot] = i;
+__global__ void fy_scatter_kernel(const unsigned long long* pn, const uint32_t* j, uint32_t* cursor,
+                                  const uint32_t* off, uint32_t* bucket) {
+    const uint32_t n = (uint32_t)*pn;
+    GS_LOOP(i, n) {
+        if (i == 0) continue;
+        const uint32_t t = j[i];
+        const uint32_t slot = off[t] + atomicAdd(&cursor[t], 1u);
+        bucket[slot] = i;
+    }
 }
 
 // One thread per target slot q: sort L_q (tiny), link succ, record nxt(q).
-__global__ void fy_link_kernel(uint32_t n, const uint32_t* off, const uint32_t* cnt, uint32_t* bucket,
-                               uint32_t* succ, uint32_t* nxt) {
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n) return;
-    const uint32_t o = off[q], c = cnt[q];
-    uint32_t* b = bucket + o;
-    for (uint32_t k = 1; k < c; ++k) {  // insertion sort
-        const uint32_t t = b[k];
-        uint32_t m = k;
-        while (m > 0 && b[m - 1] > t) {
-            b[m] = b[m - 1];
-            --m;
+__global__ void fy_link_kernel(const unsigned long long* pn, const uint32_t* off, const uint32_t* cnt,
+                               uint32_t* bucket, uint32_t* succ, uint32_t* nxt) {
+    const uint32_t n = (uint32_t)*pn;
+    GS_LOOP(q, n) {
+        const uint32_t o = off[q], c = cnt[q];
+        uint32_t* b = bucket + o;
+        for (uint32_t k = 1; k < c; ++k) {  // insertion sort
+            const uint32_t t = b[k];
+            uint32_t m = k;
+            while (m > 0 && b[m - 1] > t) {
+                b[m] = b[m - 1];
+                --m;
+            }
+            b[m] = t;
         }
-        b[m] = t;
+        uint32_t first_gt = FP_NONE;
+        for (uint32_t k = 0; k < c; ++k) {
+            const uint32_t e = b[k];
+            succ[e] = (k + 1 < c) ? b[k + 1] : FP_NONE;
+            if (first_gt == FP_NONE && e > q) first_gt = e;
+        }
+        nxt[q] = first_gt;
     }
-    uint32_t first_gt = FP_NONE;
-    for (uint32_t k = 0; k < c; ++k) {
-        const uint32_t e = b[k];
-        succ[e] = (k + 1 < c) ? b[k + 1] : FP_NONE;
-        if (first_gt == FP_NONE && e > q) first_gt = e;
-    }
-    nxt[q] = first_gt;
-    if (q == 0) succ[0] = FP_NONE;
 }
 
-__global__ void fy_chain_kernel(uint32_t n, const uint32_t* nxt, uint32_t* V) {
-    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n) return;
-    uint32_t t = s;
-    for (;;) {
-        const uint32_t u = nxt[t];
-        if (u == FP_NONE) break;
-        t = u;
+__global__ void fy_chain_kernel(const unsigned long long* pn, const uint32_t* nxt, uint32_t* V) {
+    const uint32_t n = (uint32_t)*pn;
+    GS_LOOP(s, n) {
+        uint32_t t = s;
+        for (;;) {
+            const uint32_t u = nxt[t];
+            if (u == FP_NONE) break;
+            t = u;
+        }
+        V[s] = t;
     }
-    V[s] = t;
 }
 
 // A[p] -> out (positions) or, with ids != null, order/rank of agent ids.
-__global__ void fy_final_kernel(uint32_t n, const uint32_t* j, const uint32_t* succ, const uint32_t* V,
-                                const uint32_t* ids, uint32_t* out, uint32_t* rank) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    uint32_t a;
-    if (p == 0) {
-        a = V[0];
-    } else {
-        const uint32_t s = succ[p];
-        a = (s == FP_NONE) ? j[p] : V[s];
-    }
-    if (ids) {
-        const uint32_t id = ids[a];
-        out[p] = id;
-        rank[id] = p;
-    } else {
-        out[p] = a;
+__global__ void fy_final_kernel(const unsigned long long* pn, const uint32_t* j, const uint32_t* succ,
+                                const uint32_t* V, const uint32_t* ids, uint32_t* out, uint32_t* rank) {
+    const uint32_t n = (uint32_t)*pn;
+    GS_LOOP(p, n) {
+        uint32_t a;
+        if (p == 0) {
+            a = V[0];
+        } else {
+            const uint32_t s = succ[p];
+            a = (s == FP_NONE) ? j[p] : V[s];
+        }
+        if (ids) {
+            const uint32_t id = ids[a];
+            out[p] = id;
+            rank[id] = p;
+        } else {
+            out[p] = a;
+        }
     }
 }
 
-__global__ void flag_alive_kernel(uint32_t n, const uint8_t* alive, uint32_t* flags) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) flags[i] = alive[i] ? 1u : 0u;
-}
+struct IsAlive {
+    const uint8_t* alive;
+    __device__ __forceinline__ bool operator()(uint32_t i) const { return alive[i] != 0; }
+};
 
 int fp_ensure_temp(fp_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->temp_bytes) return FP_OK;
-    if (ctx->d_temp) cudaFree(ctx->d_temp);
+    if (ctx->d_temp) {
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->stream2) cudaStreamSynchronize(ctx->stream2);
+        cudaFree(ctx->d_temp);
+    }
     ctx->d_temp = nullptr;
+    bytes = std::max<size_t>(bytes, (size_t)1 << 20);
     FP_CUDA(ctx, cudaMalloc(&ctx->d_temp, bytes));
     ctx->temp_bytes = bytes;
+    ctx->graph_valid = false;
     return FP_OK;
 }
 
-// Positions permutation A (ids == null) or the id order + ranks, for n entries.
-static int fy_run(fp_ctx* ctx, uint32_t n, uint64_t seed, int64_t step, const uint32_t* ids,
-                  uint32_t* out, uint32_t* rank) {
-    if (n == 0) return FP_OK;
-    cudaStream_t s = ctx->stream;
-    const unsigned B = 256;
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, sizeof(uint32_t) * n, s));
-    fy_targets_kernel<<<fp_blocks(n, B), B, 0, s>>>(n, seed, (uint64_t)step, ctx->d_j, ctx->d_cnt);
+// Positions permutation A (ids == null) or the id order + ranks; n_dev holds the count,
+// cap bounds it (sizes the scan).  Uses d_temp + its second half for scratch.
+static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, uint32_t cap, uint64_t seed,
+                  const long long* step_dev, const uint32_t* ids, uint32_t* out, uint32_t* rank) {
+    if (cap == 0) return FP_OK;
+    const unsigned G = (unsigned)std::min<size_t>(fp_blocks(cap, 256), (size_t)ctx->sm_count * 8);
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, sizeof(uint32_t) * cap, s));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cursor, 0, sizeof(uint32_t) * cap, s));
+    fy_targets_kernel<<<G, 256, 0, s>>>(n_dev, seed, step_dev, ctx->d_j, ctx->d_cnt);
     FP_LAUNCHED(ctx);
     size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, ctx->d_cnt, ctx->d_off, (int)n, s);
-    if (int rc = fp_ensure_temp(ctx, need)) return rc;
-    FP_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_temp, need, ctx->d_cnt, ctx->d_off, (int)n, s));
-    ctx->ctr.kernel_launches++;
-    FP_CUDA(ctx, cudaMemcpyAsync(ctx->d_cursor, ctx->d_off, sizeof(uint32_t) * n,
-                                 cudaMemcpyDeviceToDevice, s));
-    fy_scatter_kernel<<<fp_blocks(n, B), B, 0, s>>>(n, ctx->d_j, ctx->d_cursor, ctx->d_bucket);
+    cub::DeviceScan::ExclusiveSum(nullptr, need, ctx->d_cnt, ctx->d_off, (int)cap, s);
+    if (need > ctx->temp_bytes) return fp_fail(ctx, FP_ERUNTIME, "order: scratch not reserved");
+    FP_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_temp, need, ctx->d_cnt, ctx->d_off, (int)cap, s));
+    ctx->ctr.kernel_launches += 2;
+    fy_scatter_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_j, ctx->d_cursor, ctx->d_off, ctx->d_fy_bucket);
     FP_LAUNCHED(ctx);
-    fy_link_kernel<<<fp_blocks(n, B), B, 0, s>>>(n, ctx->d_off, ctx->d_cnt, ctx->d_bucket,
-                                                 ctx->d_succ, ctx->d_nxt);
+    fy_link_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_off, ctx->d_cnt, ctx->d_fy_bucket, ctx->d_succ, ctx->d_nxt);
     FP_LAUNCHED(ctx);
-    fy_chain_kernel<<<fp_blocks(n, B), B, 0, s>>>(n, ctx->d_nxt, ctx->d_V);
+    fy_chain_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_nxt, ctx->d_V);
     FP_LAUNCHED(ctx);
-    fy_final_kernel<<<fp_blocks(n, B), B, 0, s>>>(n, ctx->d_j, ctx->d_succ, ctx->d_V, ids, out, rank);
+    fy_final_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_j, ctx->d_succ, ctx->d_V, ids, out, rank);
     FP_LAUNCHED(ctx);
     return FP_OK;
+}
+
+// Reserves the CUB scratch of the order + bucketing stages (outside any graph capture).
+int fp_order_reserve(fp_ctx* ctx) {
+    const uint32_t n = std::max<uint32_t>(ctx->n, 1);
+    size_t a = 0, b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, a, ctx->d_cnt, ctx->d_off, (int)n, ctx->stream);
+    thrust::counting_iterator<uint32_t> it(0);
+    cub::DeviceSelect::If(nullptr, b, it, ctx->d_alive_ids, &ctx->d_sc->n_alive, (int)n, IsAlive{ctx->d_alive},
+                          ctx->stream);
+    return fp_ensure_temp(ctx, std::max(a, b) * 2 + 4096);
 }
 
 int fp_order_positions(fp_ctx* ctx, uint32_t n, uint64_t seed, int64_t step, uint32_t* d_out) {
-    return fy_run(ctx, n, seed, step, nullptr, d_out, nullptr);
+    if (int rc = fp_order_reserve(ctx)) return rc;
+    unsigned long long hn = n;
+    long long hs = step;
+    FP_CUDA(ctx, cudaMemcpy(&ctx->d_sc->n_alive, &hn, 8, cudaMemcpyHostToDevice));
+    FP_CUDA(ctx, cudaMemcpy(&ctx->d_sc->step, &hs, 8, cudaMemcpyHostToDevice));
+    return fy_run(ctx, ctx->stream, &ctx->d_sc->n_alive, n, seed, &ctx->d_sc->step, nullptr, d_out, nullptr);
 }
 
-// Alive compaction (ascending ids, engine.hpp:99-102) then the shuffle; leaves
-// ctx->d_order (ids in processing order), ctx->d_rank and ctx->n_order.
-int fp_order_launch(fp_ctx* ctx, uint64_t seed, int64_t step) {
-    cudaStream_t s = ctx->stream;
+// Alive compaction (ascending ids, engine.hpp:99-102) then the shuffle on stream s; leaves
+// ctx->d_order (ids in processing order), ctx->d_rank and d_sc->n_alive.
+int fp_order_launch(fp_ctx* ctx, uint64_t seed, cudaStream_t s) {
     const uint32_t n = ctx->n;
-    if (n == 0) {
-        ctx->n_order = 0;
-        return FP_OK;
-    }
-    // flags into d_cursor (scratch), select into d_alive_ids, count into d_counters[6]
-    flag_alive_kernel<<<fp_blocks(n, 256), 256, 0, s>>>(n, ctx->d_alive, ctx->d_cursor);
-    FP_LAUNCHED(ctx);
+    if (n == 0) return FP_OK;
     thrust::counting_iterator<uint32_t> it(0);
     size_t need = 0;
-    cub::DeviceSelect::Flagged(nullptr, need, it, ctx->d_cursor, ctx->d_alive_ids,
-                               ctx->d_counters + 6, (int)n, s);
-    if (int rc = fp_ensure_temp(ctx, need)) return rc;
-    FP_CUDA(ctx, cub::DeviceSelect::Flagged(ctx->d_temp, need, it, ctx->d_cursor, ctx->d_alive_ids,
-                                            ctx->d_counters + 6, (int)n, s));
-    ctx->ctr.kernel_launches++;
-    // The alive count is tracked on the host (make_state + motion exits), so no sync here.
-    const uint32_t na = (uint32_t)ctx->alive;
-    ctx->n_order = na;
-    return fy_run(ctx, na, seed, step, ctx->d_alive_ids, ctx->d_order, ctx->d_rank);
+    cub::DeviceSelect::If(nullptr, need, it, ctx->d_alive_ids, &ctx->d_sc->n_alive, (int)n, IsAlive{ctx->d_alive}, s);
+    if (need > ctx->temp_bytes / 2) return fp_fail(ctx, FP_ERUNTIME, "order: scratch not reserved");
+    // select uses the upper half of the scratch so it never aliases the scan's
+    void* t2 = (char*)ctx->d_temp + ctx->temp_bytes / 2;
+    FP_CUDA(ctx, cub::DeviceSelect::If(t2, need, it, ctx->d_alive_ids, &ctx->d_sc->n_alive, (int)n,
+                                       IsAlive{ctx->d_alive}, s));
+    ctx->ctr.kernel_launches += 2;
+    return fy_run(ctx, s, &ctx->d_sc->n_alive, n, seed, &ctx->d_sc->step, ctx->d_alive_ids, ctx->d_order, ctx->d_rank);
 }

@@ -1,0 +1,231 @@
+// plane.cu -- the static planning plane and the ghost columns of the bitplanes.
+//
+// The reference weighs candidate c of an agent at p by w = exp(k_s * (S(p) - S(c)))
+// (planning.hpp:102).  With K = k_s*log2(e) and y = K*S, w = 2^(y_p - y_c).  Per cell we store
+// the split 2^(-y_c) = m_c * 2^(-C_c), C_c = ceil(y_c), m_c = 2^(C_c - y_c) in [1, 2), as one u32:
+//     bit 31      special (Wall = 0xFFFFFFFF, unreachable free cell = 0x80000000)
+//     bit 30      "unsafe centre": some reachable cell within Chebyshev 5 has |C - C_c| > 60
+//     bits 29..23 C_c mod 128
+//     bits 22..0  23-bit mantissa of m_c (relative rounding error <= 2^-24)
+// An agent at p then weighs c by m_c * 2^(C_p - C_c) -- the reference weight times the common
+// factor 2^(C_p - y_p) -- so sampling (which is scale invariant, planning.hpp:60-62) sees the
+// reference weights to 2^-24 relative; the plan kernel's guard band turns that into bit-exact
+// decisions (plan.cu).  4 bytes per cell instead of the fp64 field's 8.
+// DriveX: the plane only carries walls (weights depend on dx alone, plan.cu table).
+#include <limits.h>
+#include <math.h>
+
+#include "internal.cuh"
+
+__global__ void plane_build_kernel(Geo g, int PW, const double* field, int potential, double K,
+                                   uint32_t* plane, int* cval) {
+    const size_t total = (size_t)PW * g.H;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i / PW);
+        int x = (int)(i % PW) - FP_XPAD_W;
+        int c = INT_MIN;
+        uint32_t w;
+        if (x < 0 || x >= g.W) {
+            if (g.boundary != FP_BOUNDARY_PERIODIC_X) {
+                plane[i] = FP_W_WALL;
+                cval[i] = INT_MIN;
+                continue;
+            }
+            x = g.wrap(x);
+        }
+        if (g.is_wall(x, y)) {
+            w = FP_W_WALL;
+        } else if (potential == FP_POTENTIAL_DRIVE_X) {
+            w = 0u;
+            c = 0;
+        } else {
+            const double s = field[(size_t)y * g.W + x];
+            if (isinf(s)) {
+                w = FP_W_UNREACH;
+            } else {
+                const double yv = K * s;
+                double C = ceil(yv);
+                const double m = exp2(C - yv);  // [1, 2]
+                double mant = rint((m - 1.0) * 8388608.0);
+                if (mant >= 8388608.0) {  // m rounded up to 2: 2 * 2^-C = 2^-(C-1)
+                    mant = 0.0;
+                    C -= 1.0;
+                }
+                const long long Ci = (long long)C;
+                c = (int)Ci;
+                w = ((uint32_t)(Ci & 0x7F) << 23) | (uint32_t)mant;
+            }
+        }
+        plane[i] = w;
+        cval[i] = c;
+    }
+}
+
+// Row pass of the radius-5 min/max of C (INT_MIN marks non-normal cells).
+__global__ void plane_rowminmax_kernel(int PW, int H, const int* cval, int* rmin, int* rmax) {
+    const size_t total = (size_t)PW * H;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int xp = (int)(i % PW);
+        const size_t row = i - xp;
+        int mn = INT_MAX, mx = INT_MIN;
+        for (int d = -FP_HALO; d <= FP_HALO; ++d) {
+            const int q = xp + d;
+            if (q < 0 || q >= PW) continue;
+            const int c = cval[row + q];
+            if (c == INT_MIN) continue;
+            mn = min(mn, c);
+            mx = max(mx, c);
+        }
+        rmin[i] = mn;
+        rmax[i] = mx;
+    }
+}
+
+__global__ void plane_unsafe_kernel(int PW, int H, const int* cval, const int* rmin, const int* rmax,
+                                    uint32_t* plane, unsigned long long* n_unsafe) {
+    const size_t total = (size_t)PW * H;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int c = cval[i];
+        if (c == INT_MIN) continue;
+        const int xp = (int)(i % PW), y = (int)(i / PW);
+        int mn = INT_MAX, mx = INT_MIN;
+        for (int d = -FP_HALO; d <= FP_HALO; ++d) {
+            const int yy = y + d;
+            if (yy < 0 || yy >= H) continue;
+            mn = min(mn, rmin[(size_t)yy * PW + xp]);
+            mx = max(mx, rmax[(size_t)yy * PW + xp]);
+        }
+        if (mx - c > 60 || c - mn > 60) {
+            plane[i] |= FP_W_UNSAFE;
+            atomicAdd(n_unsafe, 1ull);
+        }
+    }
+}
+
+// Ghost bits of a bitplane for periodic-x grids: bits at x outside [0, W) mirror wrap(x).
+__global__ void ghost_bits_kernel(Geo g, uint32_t* plane) {
+    // words that hold any x outside [0, W): word 0 (x in [-32,0)) and words from (W+32)/32 on
+    const int first_right = (g.W + FP_XPAD_BITS) >> 5;
+    const int per_row = 1 + (g.P - first_right);
+    const size_t total = (size_t)per_row * g.H;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i / per_row);
+        const int k = (int)(i % per_row);
+        const int wi = (k == 0) ? 0 : first_right + k - 1;
+        const size_t idx = (size_t)y * g.P + wi;
+        uint32_t cur = plane[idx];
+        uint32_t out = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int x = wi * 32 - FP_XPAD_BITS + b;
+            uint32_t bit;
+            if (x >= 0 && x < g.W) {
+                bit = (cur >> b) & 1u;
+            } else {
+                const int xs = g.wrap(x);
+                bit = (plane[g.word(xs, y)] >> (xs & 31)) & 1u;
+            }
+            out |= bit << b;
+        }
+        plane[idx] = out;
+    }
+}
+
+int fp_ghost_occ(fp_ctx* ctx) {
+    if (ctx->boundary != FP_BOUNDARY_PERIODIC_X) return FP_OK;
+    ghost_bits_kernel<<<fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream>>>(fp_geo(ctx), ctx->d_occ);
+    FP_LAUNCHED(ctx);
+    return FP_OK;
+}
+
+int fp_ghost_static(fp_ctx* ctx) {
+    if (ctx->boundary != FP_BOUNDARY_PERIODIC_X) return FP_OK;
+    ghost_bits_kernel<<<fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream>>>(fp_geo(ctx), ctx->d_wall);
+    FP_LAUNCHED(ctx);
+    ghost_bits_kernel<<<fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream>>>(fp_geo(ctx), ctx->d_exit);
+    FP_LAUNCHED(ctx);
+    return FP_OK;
+}
+
+// ---------------------------------------------------------------------------- TMA descriptor
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_encodeTiled)p;
+    }
+    return fn;
+}
+
+// Chooses the plan tile for this grid and encodes the TMA box (tile + FP_HALO halo rows,
+// tile + 6 columns each side so the inner box width stays a multiple of 16 bytes).
+static int make_tmap(fp_ctx* ctx) {
+    const size_t cells = (size_t)ctx->W * ctx->H;
+    if (cells >= (size_t)16 << 20) {
+        ctx->tile_w = 240;
+        ctx->tile_h = 64;
+    } else if (cells >= (size_t)1 << 20) {
+        ctx->tile_w = 120;
+        ctx->tile_h = 32;
+    } else {
+        ctx->tile_w = 56;
+        ctx->tile_h = 16;
+    }
+    ctx->tiles_x = (ctx->W + ctx->tile_w - 1) / ctx->tile_w;
+    ctx->tiles_y = (ctx->H + ctx->tile_h - 1) / ctx->tile_h;
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)ctx->PW, (cuuint64_t)ctx->H};
+    cuuint64_t strides[1] = {(cuuint64_t)ctx->PW * 4};
+    // inner box start x0-8 keeps the inner coordinate 16-byte aligned (an unaligned inner
+    // coordinate faults with "illegal instruction" on sm_100a, tools/tma_probe); box covers
+    // [x0-8, x0+tile_w+8) which contains the 5-cell halo on both sides
+    cuuint32_t box[2] = {(cuuint32_t)(ctx->tile_w + 16), (cuuint32_t)(ctx->tile_h + 2 * FP_HALO)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&ctx->tmap_plane, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, ctx->d_plane, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return FP_OK;
+}
+
+// Builds (or reuses) the plane for (k_s, potential).  Setup work: one pass over the grid.
+int fp_plane_ensure(fp_ctx* ctx, double k_s) {
+    if (ctx->plane_valid && ctx->plane_ks == k_s && ctx->plane_potential == ctx->potential) return FP_OK;
+    cudaStream_t s = ctx->stream;
+    const size_t total = (size_t)ctx->PW * ctx->H;
+    if (!ctx->d_plane) {
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_plane, total * 4));
+        if (int rc = make_tmap(ctx)) return rc;
+    }
+    int *cval = nullptr, *rmin = nullptr, *rmax = nullptr;
+    FP_CUDA(ctx, cudaMallocAsync(&cval, total * 4, s));
+    FP_CUDA(ctx, cudaMallocAsync(&rmin, total * 4, s));
+    FP_CUDA(ctx, cudaMallocAsync(&rmax, total * 4, s));
+    const double K = k_s * 1.4426950408889634;  // k_s * log2(e)
+    const unsigned G = (unsigned)ctx->sm_count * 8;
+    plane_build_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->PW, ctx->d_field, ctx->potential, K, ctx->d_plane, cval);
+    FP_LAUNCHED(ctx);
+    if (ctx->potential == FP_POTENTIAL_EXIT_DISTANCE) {
+        plane_rowminmax_kernel<<<G, 256, 0, s>>>(ctx->PW, ctx->H, cval, rmin, rmax);
+        FP_LAUNCHED(ctx);
+        FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->pad[0], 0, 8, s));
+        plane_unsafe_kernel<<<G, 256, 0, s>>>(ctx->PW, ctx->H, cval, rmin, rmax, ctx->d_plane, &ctx->d_sc->pad[0]);
+        FP_LAUNCHED(ctx);
+    }
+    FP_CUDA(ctx, cudaFreeAsync(cval, s));
+    FP_CUDA(ctx, cudaFreeAsync(rmin, s));
+    FP_CUDA(ctx, cudaFreeAsync(rmax, s));
+    ctx->plane_valid = true;
+    ctx->plane_ks = k_s;
+    ctx->plane_potential = ctx->potential;
+    ctx->graph_valid = false;
+    return FP_OK;
+}

@@ -88,6 +88,7 @@ SIGNATURES = {
     "fp_movement_order": (C.c_int, [C.c_int64, C.c_uint64, C.c_int64, C.c_int, _u32p]),
     "fp_spawn_agents": (C.c_int, [C.c_int32, C.c_int32, _u8p, C.c_int64, C.c_uint64, _i32p, _i32p]),
     "fp_get_counters": (C.c_int, [C.c_void_p, C.POINTER(_Counters)]),
+    "fp_time_plan_kernel": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.POINTER(C.c_double)]),
 }
 
 _lib = None
@@ -428,6 +429,12 @@ class SimState:
         _check(library().fp_get_choice(self._ctx, agent, k_s, cx, cy, w, p, 128, C.byref(n)), self._ctx)
         k = n.value
         return cx[:k].copy(), cy[:k].copy(), w[:k].copy(), p[:k].copy()
+
+    def time_plan_kernel(self, k_s: float, seed: int, iters: int = 10) -> float:
+        """Average plan-kernel launch duration in ms (CUDA events), for the roofline."""
+        ms = C.c_double()
+        _check(library().fp_time_plan_kernel(self._ctx, k_s, seed, iters, C.byref(ms)), self._ctx)
+        return ms.value
 
     def counters(self) -> dict:
         c = _Counters()
