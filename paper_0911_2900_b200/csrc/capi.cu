@@ -135,7 +135,7 @@ static void free_agents(fp_ctx* c) {
     void* ptrs[] = {c->d_x, c->d_y, c->d_dx, c->d_dy, c->d_v, c->d_alive, c->d_rank, c->d_alive_ids,
                     c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
                     c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted,
-                    c->d_fy_bucket, c->d_flags, c->d_cursor_b};
+                    c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->d_x = c->d_y = c->d_dx = c->d_dy = nullptr;
@@ -143,7 +143,7 @@ static void free_agents(fp_ctx* c) {
     c->d_rank = c->d_alive_ids = c->d_order = c->d_j = c->d_cnt = c->d_off = c->d_cursor = nullptr;
     c->d_bucket = c->d_succ = c->d_nxt = c->d_V = c->d_pend_a = c->d_pend_b = nullptr;
     c->d_exits = c->d_exits_sorted = nullptr;
-    c->d_fy_bucket = c->d_flags = c->d_cursor_b = nullptr;
+    c->d_fy_bucket = c->d_flags = c->d_cursor_b = c->d_fallback = nullptr;
     c->cap = 0;
     c->graph_valid = false;
 }
@@ -160,7 +160,7 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
     FP_CUDA(c, cudaMalloc(&c->d_alive, m));
     uint32_t** u32s[] = {&c->d_rank, &c->d_alive_ids, &c->d_order, &c->d_j, &c->d_cnt, &c->d_off,
                          &c->d_cursor, &c->d_bucket, &c->d_succ, &c->d_nxt, &c->d_V, &c->d_pend_a,
-                         &c->d_pend_b, &c->d_fy_bucket, &c->d_flags, &c->d_cursor_b};
+                         &c->d_pend_b, &c->d_fy_bucket, &c->d_flags, &c->d_cursor_b, &c->d_fallback};
     for (uint32_t** p : u32s) FP_CUDA(c, cudaMalloc(p, m * 4));
     FP_CUDA(c, cudaMalloc(&c->d_exits, m * 8));
     FP_CUDA(c, cudaMalloc(&c->d_exits_sorted, m * 8));
@@ -203,7 +203,7 @@ extern "C" int fp_create(const fp_grid_desc* g, const uint8_t* cells, const doub
     c->H = g->height;
     c->boundary = g->boundary;
     c->cell_size = g->cell_size;
-    c->P = (c->W + 2 * FP_XPAD_BITS + 31) / 32;
+    c->P = (((c->W + 2 * FP_XPAD_BITS + 31) / 32) + 3) & ~3;  // 16-byte row pitch (TMA)
     c->PW = ((c->W + 2 * FP_XPAD_W) + 3) & ~3;
     const size_t ncell = (size_t)c->W * c->H;
     const size_t nwords = (size_t)c->P * c->H;
@@ -286,6 +286,12 @@ static int sync_scalars(fp_ctx* c) {
 static int read_scalars(fp_ctx* c) {
     FP_CUDA(c, cudaMemcpyAsync(c->h_sc, c->d_sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
     FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (c->h_sc->err) {
+        const unsigned long long e = c->h_sc->err;
+        cudaMemsetAsync(&c->d_sc->err, 0, 8, c->stream);
+        return fail(c, FP_ECUDA, "device-side scheduler fault (flags " + std::to_string(e) +
+                                     "): a plan/motion wait timed out");
+    }
     c->alive = (int64_t)c->h_sc->alive;
     c->step = (int64_t)c->h_sc->step;
     c->ctr.plan_fallbacks = (int64_t)c->h_sc->fallbacks;

@@ -117,7 +117,9 @@ struct DevScalars {
     unsigned long long n_tiles;   // non-empty plan tiles this step
     unsigned long long tile_next; // dynamic tile scheduler cursor
     unsigned long long err;       // device-detected errors (bit flags)
-    unsigned long long pad[2];
+    unsigned long long pad[2];    // [0] unsafe plane cells, [1] motion rounds executed
+    unsigned long long fb_count;  // agents queued for the exact planning path this step
+    unsigned long long pad2[3];
 };
 
 struct fp_ctx {
@@ -144,6 +146,7 @@ struct fp_ctx {
     double plane_ks = 0.0;
     int plane_potential = -1;
     CUtensorMap tmap_plane;          // TMA descriptor of the plane (one tile box)
+    CUtensorMap tmap_occ;            // TMA descriptor of the occupancy bitplane (16-word box)
     int tile_w = 0, tile_h = 0;      // plan tile (cells)
     int tiles_x = 0, tiles_y = 0;
     bool tiles_ok = false;           // tiled fast path usable for this grid
@@ -175,6 +178,7 @@ struct fp_ctx {
 
     // motion scratch
     uint32_t *d_pend_a = nullptr, *d_pend_b = nullptr;
+    uint32_t* d_fallback = nullptr;  // agents the plan kernel hands to the exact path
     unsigned long long* d_exits = nullptr;  // (rank << 32 | id) records of the last move
     unsigned long long* d_exits_sorted = nullptr;
     int64_t last_displacement = 0;

@@ -235,6 +235,7 @@ struct TileArgs {
     int tile_w, tile_h, tiles_x;
     int use_tma;  // 0: stage the box with coalesced loads (debug / comparison path)
     int boxw, boxh, occw;  // shared-memory strides (words)
+    uint32_t* fallback;    // agents handed to plan_exact_list_kernel
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -250,16 +251,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
+// Bounded wait on an mbarrier phase: false if the phase never completed (error, not a hang).
+__device__ __forceinline__ bool mbar_wait(uint64_t* bar, unsigned parity) {
+    for (int spin = 0; spin < (1 << 22); ++spin) {
+        uint32_t ok;
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return true;
+    }
+    return false;
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int cx, int cy) {
@@ -270,112 +277,127 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
-// Plans one agent from the staged tile; returns false when the exact path must decide.
-__device__ __forceinline__ bool plan_fast(const TileArgs& A, const uint32_t* buf, const uint32_t* occs, int x0, int y0,
-                                          uint32_t id, int px, int py, int v, double u, const double* drive_tab,
-                                          int* ox, int* oy) {
+// Pair of u64 words holding the 121-bit ball wall mask (bit (dy+5)*11 + dx+5).
+struct Mask121 {
+    unsigned long long lo, hi;
+};
+
+// B: frame bit of the row's first cell (a constant once the row loop is unrolled)
+__device__ __forceinline__ void mask_or_row(Mask121& m, uint32_t rowbits, int B) {
+    if (B < 64) m.lo |= (unsigned long long)rowbits << B;
+    if (B + 11 > 64) m.hi |= (B >= 64) ? ((unsigned long long)rowbits << (B - 64)) : ((unsigned long long)rowbits >> (64 - B));
+}
+
+__device__ __forceinline__ bool path_blocked(const Mask121& m, int o) {
+    const unsigned long long plo = ((unsigned long long)c_pathmask[o][1] << 32) | c_pathmask[o][0];
+    const unsigned long long phi = ((unsigned long long)c_pathmask[o][3] << 32) | c_pathmask[o][2];
+    return ((m.lo & plo) | (m.hi & phi)) != 0ull;
+}
+
+// Weight of a reachable plane word in ExitDistance mode as an exact fp64 number:
+// m_c * 2^(C_p - C_c), with (C_p - C_c) recovered mod 128 (|d| <= 60 on safe cells).
+__device__ __forceinline__ double exit_weight(uint32_t w, int cp_biased /* C_p + 64 (+128) */) {
+    const uint32_t t = (uint32_t)(cp_biased - (int)(w >> 23)) & 127u;  // d + 64
+    const int hi = (int)((t << 20) + (959u << 20)) | (int)((w >> 3) & 0xFFFFFu);
+    const int lo = (int)(w << 29);
+    return __hiloint2double(hi, lo);
+}
+
+// Plans one agent from the staged tile (V = its v_max, DRIVE = DriveX potential).  Returns
+// 1 when the fast path decided (result in *ox, *oy), 2 when the exact path must decide.
+//   pass 1  rows centre-out so the line-of-sight test of a cell only needs wall bits of rows
+//           already seen; valid candidates (not Wall/unreachable, not occupied by another agent,
+//           visible) contribute their weight to an fp64 row sum;
+//   pass 2  u*total picks the row; the row is replayed in list order (wrapped-x sorted at a
+//           periodic seam) to find the first cumulative weight > threshold; guard band.
+template <int V, bool DRIVE>
+__device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* buf, const uint32_t* occs, int osh0,
+                                           int x0, int y0, int px, int py, double u, const double* drive_tab,
+                                           int* ox, int* oy) {
+    constexpr int D = 2 * V + 1;
     const PlanCommon& a = A.c;
-    const int X0 = x0 - 8;  // box origin: TMA needs 16-byte aligned inner coordinates
+    const int X0 = x0 - 8;  // box origin (TMA inner coordinates stay 16-byte aligned)
     const int lx = px - X0, ly = py - (y0 - FP_HALO);
-    const uint32_t own = buf[ly * A.boxw + lx];
-    int mode;
-    int Cp = 0;
-    if (a.potential == FP_POTENTIAL_DRIVE_X) {
-        mode = MODE_DRIVE;
-    } else if (own == FP_W_UNREACH) {
-        mode = MODE_ONES;  // planning.hpp:93-95
-    } else {
-        if (own & FP_W_UNSAFE) return false;
-        mode = MODE_EXIT;
-        Cp = (int)((own >> 23) & 0x7Fu);
+    int cpb = 0;
+    if (!DRIVE) {
+        const uint32_t own = buf[ly * A.boxw + lx];
+        if (own & (FP_W_SPECIAL | FP_W_UNSAFE)) return 2;  // "ones" pocket / unsafe centre
+        cpb = (int)((own >> 23) & 0x7Fu) + 64 + 128;
     }
-    const int osh = ((X0 + FP_XPAD_BITS) & 31) + lx - 5;  // bit of dx = -5 in the staged occ row
-    uint32_t wm0 = 0, wm1 = 0, wm2 = 0, wm3 = 0;           // ball wall mask (11x11 frame)
-    double rs[11];
+    const int osh = osh0 + lx - V;  // staged occupancy bit of dx = -V
+    Mask121 wm{0ull, 0ull};
+    double rs[D];  // row sums, indexed by dy + V
 #pragma unroll
-    for (int t = 0; t < 11; ++t) {
-        const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);
-        rs[dy + 5] = 0.0;
-        if (dy < -v || dy > v) continue;
-        const int yy = py + dy;
-        if (yy < 0 || yy >= a.g.H) continue;
-        const uint32_t* row = buf + (ly + dy) * A.boxw + lx;
-        uint32_t wv[11];
+    for (int t = 0; t < D; ++t) {
+        const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);  // centre-out: 0, -1, 1, -2, 2, ...
+        const bool rowok = (unsigned)(py + dy) < (unsigned)a.g.H;
+        const uint32_t* row = buf + (ly + dy) * A.boxw + lx - V;
+        uint32_t wv[D];
+        uint32_t wall = 0u, spec = 0u;
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const int dx = k - 5;
-            wv[k] = (dx >= -v && dx <= v) ? row[dx] : FP_W_WALL;
+        for (int k = 0; k < D; ++k) {
+            wv[k] = row[k];
+            wall |= (uint32_t)(wv[k] == FP_W_WALL) << k;
+            spec |= (wv[k] >> 31) << k;
         }
-#pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const int b = (dy + 5) * 11 + k;
-            const uint32_t bit = (wv[k] == FP_W_WALL && k - 5 >= -v && k - 5 <= v) ? (1u << (b & 31)) : 0u;
-            if ((b >> 5) == 0) wm0 |= bit;
-            else if ((b >> 5) == 1) wm1 |= bit;
-            else if ((b >> 5) == 2) wm2 |= bit;
-            else wm3 |= bit;
-        }
+        if (rowok) mask_or_row(wm, wall, (dy + 5) * 11 + 5 - V);
         const uint32_t* orow = occs + (ly + dy) * A.occw;
-        const uint32_t win = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
-        const bool anywall = (wm0 | wm1 | wm2 | wm3) != 0u;
+        uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
+        if (dy == 0) occ &= ~(1u << V);  // the own cell stays a candidate (planning.hpp:45-46)
+        uint32_t valid = rowok ? (~(spec | occ) & ((1u << D) - 1u)) : 0u;
+        if (wm.lo | wm.hi) {
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+                if (path_blocked(wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
+        }
         double s = 0.0;
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const int dx = k - 5;
-            if (wv[k] == FP_W_WALL) continue;
-            if (((win >> k) & 1u) && !(dx == 0 && dy == 0)) continue;
-            const int o = (dy + 5) * 11 + k;
-            if (anywall && ((wm0 & c_pathmask[o][0]) | (wm1 & c_pathmask[o][1]) | (wm2 & c_pathmask[o][2]) |
-                            (wm3 & c_pathmask[o][3])))
-                continue;
-            s += fast_weight(wv[k], Cp, mode, drive_tab[k]);
+        for (int k = 0; k < D; ++k) {
+            const double w = DRIVE ? drive_tab[k - V + 5] : exit_weight(wv[k], cpb);
+            if ((valid >> k) & 1u) s += w;
         }
-        rs[dy + 5] = s;
+        rs[dy + V] = s;
     }
     double T = 0.0;
 #pragma unroll
-    for (int k = 0; k < 11; ++k) T += rs[k];
+    for (int k = 0; k < D; ++k) T += rs[k];
     const double theta = u * T;
     int rstar = -1;
     double before = 0.0, cum = 0.0;
 #pragma unroll
-    for (int k = 0; k < 11; ++k) {
-        if (rstar < 0 && cum + rs[k] > theta) {
-            rstar = k;
-            before = cum;
-        }
+    for (int k = 0; k < D; ++k) {
+        const bool hit = rstar < 0 && cum + rs[k] > theta;
+        before = hit ? cum : before;
+        rstar = hit ? k : rstar;
         cum += rs[k];
     }
-    if (rstar < 0) return false;
-    // pass 2: replay the crossing row in list order (wrapped-x sorted at a periodic seam)
-    const int dy = rstar - 5;
+    if (rstar < 0) return 2;  // u*total rounded up to total
+    const int dy = rstar - V;
     const uint32_t* row = buf + (ly + dy) * A.boxw + lx;
     const uint32_t* orow = occs + (ly + dy) * A.occw;
-    const uint32_t win = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
-    int a0 = -v, a1 = v, b0 = 0, b1 = -1;
-    if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {
-        if (px + v >= a.g.W) {
-            a0 = a.g.W - px; b0 = -v; b1 = a.g.W - px - 1;
-        } else if (px - v < 0) {
-            a0 = -px; b0 = -v; b1 = -px - 1;
+    uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
+    if (dy == 0) occ &= ~(1u << V);
+    int a0 = -V, a1 = V, b0 = 0, b1 = -1;
+    if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {  // wrapped-x order at the seam (planning.hpp:50-53)
+        if (px + V >= a.g.W) {
+            a0 = a.g.W - px; b0 = -V; b1 = a.g.W - px - 1;
+        } else if (px - V < 0) {
+            a0 = -px; b0 = -V; b1 = -px - 1;
         }
     }
-    const bool anywall = (wm0 | wm1 | wm2 | wm3) != 0u;
+    const bool anywall = (wm.lo | wm.hi) != 0ull;
     double prefix = before, lower = 0.0, upper = 0.0;
     int kx = 0;
     bool found = false;
     for (int seg = 0; seg < 2 && !found; ++seg) {
         const int lo = seg ? b0 : a0, hi = seg ? b1 : a1;
         for (int dx = lo; dx <= hi; ++dx) {
-            const uint32_t wv = row[dx];
-            if (wv == FP_W_WALL) continue;
-            if (((win >> (dx + 5)) & 1u) && !(dx == 0 && dy == 0)) continue;
-            const int o = rstar * 11 + dx + 5;
-            if (anywall && ((wm0 & c_pathmask[o][0]) | (wm1 & c_pathmask[o][1]) | (wm2 & c_pathmask[o][2]) |
-                            (wm3 & c_pathmask[o][3])))
-                continue;
-            const double w = fast_weight(wv, Cp, mode, drive_tab[dx + 5]);
-            const double next = prefix + w;
+            const uint32_t w = row[dx];
+            if (w >> 31) continue;                 // wall / unreachable (weight 0)
+            if ((occ >> (dx + V)) & 1u) continue;  // occupied by another agent
+            if (anywall && path_blocked(wm, (dy + 5) * 11 + dx + 5)) continue;
+            const double wt = DRIVE ? drive_tab[dx + 5] : exit_weight(w, cpb);
+            const double next = prefix + wt;
             if (next > theta) {
                 lower = prefix;
                 upper = next;
@@ -386,33 +408,95 @@ __device__ __forceinline__ bool plan_fast(const TileArgs& A, const uint32_t* buf
             prefix = next;
         }
     }
-    if (!found) return false;
+    if (!found) return 2;
     const double margin = FP_GUARD * T;
-    if (!(upper - theta > margin)) return false;
-    if (!(lower == 0.0 || theta - lower > margin)) return false;
-    *ox = a.g.wrap(px + kx);
+    if (!(upper - theta > margin)) return 2;
+    if (!(lower == 0.0 || theta - lower > margin)) return 2;
+    int cx = px + kx;
+    if (cx < 0) cx += a.g.W;  // periodic seam (|kx| <= 5 < W)
+    else if (cx >= a.g.W) cx -= a.g.W;
+    *ox = cx;
     *oy = py + dy;
-    return true;
+    return 1;
 }
 
-__global__ void __launch_bounds__(256, 1) plan_tile_kernel(const __grid_constant__ CUtensorMap tmap, TileArgs A) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    // TMA destinations need 128-byte alignment: align the dynamic window explicitly
-    unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+template <bool DRIVE>
+__device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint32_t* buf, const uint32_t* occs,
+                                           int osh0, int x0, int y0, int px, int py, double u,
+                                           const double* drive_tab, int* ox, int* oy) {
+    switch (v) {
+        case 1: return plan_fast_t<1, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
+        case 2: return plan_fast_t<2, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
+        case 3: return plan_fast_t<3, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
+        case 4: return plan_fast_t<4, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
+        default: return plan_fast_t<5, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
+    }
+}
+
+#define PLAN_THREADS 512
+
+// Persistent CTA per SM.  Tiles are fetched in pairs of buffer slots (TMA, mbarrier); the
+// agents of fetch i are dealt to threads round-robin starting at thread (i*160) mod 512, one
+// agent per thread.  There is no CTA-wide barrier per tile: a thread finishing its agents of
+// fetch i moves on to fetch i+1; the thread that completes the last agent of fetch i refills
+// that slot with fetch i+2.  Slot metadata is published with a generation number (seqlock).
+__global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                    const __grid_constant__ CUtensorMap tmap_occ,
+                                                                    TileArgs A) {
+    extern __shared__ __align__(128) uint32_t smem_raw[];
+    uint32_t* smem = smem_raw + (((128u - (smem_u32(smem_raw) & 127u)) & 127u) >> 2);
     const int box_words = A.boxw * A.boxh;
-    const int box_bytes = box_words * 4;
-    uint32_t* bufs[2] = {(uint32_t*)smem, (uint32_t*)(smem + ((box_bytes + 127) & ~127))};
-    uint32_t* occs = (uint32_t*)(smem + 2 * ((box_bytes + 127) & ~127));
-    uint64_t* bars = (uint64_t*)(occs + ((A.boxh * A.occw + 31) & ~31));
-    __shared__ int s_tile[2];
+    const int box_stride = (box_words + 31) & ~31;  // words, 128-byte multiple
+    const int occ_words = A.boxh * A.occw;
+    const int occ_stride = (occ_words + 31) & ~31;
+    const unsigned tx_bytes = (unsigned)(box_words + occ_words) * 4u;
+    uint64_t* bars = (uint64_t*)(smem + 2 * box_stride + 2 * occ_stride);
+    // slot metadata is written by one thread and read by others without a CTA barrier: volatile
+    __shared__ volatile int s_tile[2], s_cnt[2], s_off[2], s_x0[2], s_y0[2];
+    __shared__ volatile int s_gen[2];
+    __shared__ int s_done[2];
     __shared__ double s_drive[11];
     const PlanCommon& a = A.c;
     const uint64_t step = (uint64_t)a.sc->step;
-    const unsigned n_tiles = (unsigned)a.sc->n_tiles;
+    const int n_tiles = (int)a.sc->n_tiles;
+    // fetch number i into slot i & 1 (one thread)
+    auto fetch = [&](int i) {
+        const int slot = i & 1;
+        s_gen[slot] = -1;  // seqlock: readers that raced with this refill see a changed generation
+        __threadfence_block();
+        // static deal: fetch i of this CTA is list entry blockIdx.x + i * gridDim.x, so fetch
+        // numbers map monotonically onto the list and an exhausted fetch ends every later one
+        // (refills complete out of order; a shared dynamic cursor would break that)
+        const int t = (int)blockIdx.x + i * (int)gridDim.x;
+        if (t < n_tiles) {
+            const uint32_t tile = A.tile_list[t];
+            const int tx = (int)(tile % (uint32_t)A.tiles_x), ty = (int)(tile / (uint32_t)A.tiles_x);
+            const int x0 = tx * A.tile_w, y0 = ty * A.tile_h;
+            s_tile[slot] = (int)tile;
+            s_cnt[slot] = (int)A.tile_cnt[tile];
+            s_off[slot] = (int)A.tile_off[tile];
+            s_x0[slot] = x0;
+            s_y0[slot] = y0;
+            s_done[slot] = 0;
+            if (A.use_tma) {
+                const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&bars[slot], tx_bytes);
+                tma_load_2d(smem + slot * box_stride, &tmap, &bars[slot], x0 - 8 + FP_XPAD_W, y0 - FP_HALO);
+                tma_load_2d(smem + 2 * box_stride + slot * occ_stride, &tmap_occ, &bars[slot], gws, y0 - FP_HALO);
+            }
+        } else {
+            s_tile[slot] = -1;
+        }
+        __threadfence_block();
+        s_gen[slot] = i;
+    };
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_gen[0] = -1;
+        s_gen[1] = -1;
     }
     if (threadIdx.x < 11) {
         s_drive[threadIdx.x] = (a.potential == FP_POTENTIAL_DRIVE_X)
@@ -420,81 +504,152 @@ __global__ void __launch_bounds__(256, 1) plan_tile_kernel(const __grid_constant
                                    : 0.0;
     }
     __syncthreads();
-    unsigned parity[2] = {0u, 0u};
     if (threadIdx.x == 0) {
-        const int t = (int)atomicAdd(&a.sc->tile_next, 1ull);
-        s_tile[0] = t;
-        if (t < (int)n_tiles && A.use_tma) {
-            const uint32_t tid = A.tile_list[t];
-            const int tx = (int)(tid % (uint32_t)A.tiles_x), ty = (int)(tid / (uint32_t)A.tiles_x);
-            mbar_expect_tx(&bars[0], (unsigned)box_bytes);
-            tma_load_2d(bufs[0], &tmap, &bars[0], tx * A.tile_w - 8 + FP_XPAD_W, ty * A.tile_h - FP_HALO);
-        }
+        fetch(0);
+        fetch(1);
     }
-    __syncthreads();
-    int cur = s_tile[0];
-    int b = 0;
-    while (cur < (int)n_tiles) {
-        if (threadIdx.x == 0) {
-            const int t = (int)atomicAdd(&a.sc->tile_next, 1ull);
-            s_tile[(b ^ 1)] = t;
-            if (t < (int)n_tiles && A.use_tma) {
-                const uint32_t tid = A.tile_list[t];
-                const int tx = (int)(tid % (uint32_t)A.tiles_x), ty = (int)(tid / (uint32_t)A.tiles_x);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&bars[b ^ 1], (unsigned)box_bytes);
-                tma_load_2d(bufs[b ^ 1], &tmap, &bars[b ^ 1], tx * A.tile_w - 8 + FP_XPAD_W, ty * A.tile_h - FP_HALO);
+    for (int i = 0;; ++i) {
+        const int slot = i & 1;
+        // bounded wait: a scheduling bug must surface as an error flag, never as a hung GPU
+        // (-1 while a refill is being published; a generation past i means fetch i already
+        // completed without this thread -- it had no agent there -- and the slot moved on)
+        int gen;
+        for (long long spin = 0; (gen = s_gen[slot]) < i; ++spin) {
+            __nanosleep(64);
+            if (spin > (1ll << 24)) {
+                atomicOr(&a.sc->err, 1ull);
+                return;
             }
         }
-        const uint32_t tile = A.tile_list[cur];
-        const int tx = (int)(tile % (uint32_t)A.tiles_x), ty = (int)(tile / (uint32_t)A.tiles_x);
-        const int x0 = tx * A.tile_w, y0 = ty * A.tile_h;
-        // stage the occupancy words of the window (rows y0-5 .. y0+tile_h+4)
-        {
-            const int gw0 = (x0 - 8 + FP_XPAD_BITS) >> 5;
-            const int total = A.boxh * A.occw;
-            for (int k = threadIdx.x; k < total; k += blockDim.x) {
-                const int r = k / A.occw, wcol = k % A.occw;
-                const int yy = y0 - FP_HALO + r;
-                const int gw = gw0 + wcol;
-                uint32_t val = 0u;
-                if (yy >= 0 && yy < a.g.H && gw < a.g.P) val = a.occ[(size_t)yy * a.g.P + gw];
-                occs[k] = val;
-            }
-        }
+        if (gen > i) continue;
+        const int tile = s_tile[slot];
+        if (tile < 0) break;
+        const int cnt = s_cnt[slot], off = s_off[slot], x0 = s_x0[slot], y0 = s_y0[slot];
+        __threadfence_block();
+        if (s_gen[slot] != i) continue;  // fetch i already completed without this thread's help
+        int k = ((int)threadIdx.x - i * 160) & (PLAN_THREADS - 1);
+        if (k >= cnt) continue;  // no agent of this fetch for this thread
+        uint32_t* buf = smem + slot * box_stride;
+        uint32_t* occs = smem + 2 * box_stride + slot * occ_stride;
+        const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
+        const int osh0 = x0 - 8 + FP_XPAD_BITS - gws * 32;  // staged-occupancy bit of box column 0
         if (A.use_tma) {
-            mbar_wait(&bars[b], parity[b]);
-            parity[b] ^= 1u;
-        } else {
-            uint32_t* dst = bufs[b];
-            const int total = A.boxw * A.boxh;
+            if (!mbar_wait(&bars[slot], (unsigned)(i >> 1) & 1u)) {
+                atomicOr(&a.sc->err, 2ull);
+                return;
+            }
+        } else if (true) {
+            // comparison path: each thread fills what it reads (slow; debugging only)
             const int gx0 = x0 - 8 + FP_XPAD_W, gy0 = y0 - FP_HALO;
-            for (int k = threadIdx.x; k < total; k += blockDim.x) {
-                const int r = k / A.boxw, cidx = k % A.boxw;
+            for (int e = 0; e < box_words; ++e) {
+                const int r = e / A.boxw, cidx = e % A.boxw;
                 const int gy = gy0 + r, gx = gx0 + cidx;
-                dst[k] = (gy >= 0 && gy < a.g.H && gx < A.PW) ? A.plane[(size_t)gy * A.PW + gx] : 0u;
+                buf[e] = (gy >= 0 && gy < a.g.H && gx < A.PW) ? A.plane[(size_t)gy * A.PW + gx] : 0u;
+            }
+            for (int e = 0; e < occ_words; ++e) {
+                const int r = e / A.occw, wcol = e % A.occw;
+                const int gy = gy0 + r, gw = gws + wcol;
+                occs[e] = (gy >= 0 && gy < a.g.H && gw < a.g.P) ? a.occ[(size_t)gy * a.g.P + gw] : 0u;
             }
         }
-        __syncthreads();
-        const uint32_t* buf = bufs[b];
-        const uint32_t off = A.tile_off[tile], cnt = A.tile_cnt[tile];
-        for (uint32_t k = threadIdx.x; k < cnt; k += blockDim.x) {
+        int mine = 0;
+        for (; k < cnt; k += PLAN_THREADS) {
             const uint32_t id = A.bucket[off + k];
             const int px = a.g.wrap(a.x[id]), py = a.y[id];
             const int v = a.v[id];
             const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
-            int cx, cy;
-            if (!plan_fast(A, buf, occs, x0, y0, id, px, py, v, u, s_drive, &cx, &cy)) {
-                choose_exact(a, id, step, &cx, &cy);
-                atomicAdd(&a.sc->fallbacks, 1ull);
+            int cx = 0, cy = 0;
+            const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
+                               ? plan_fast_v<true>(v, A, buf, occs, osh0, x0, y0, px, py, u, s_drive, &cx, &cy)
+                               : plan_fast_v<false>(v, A, buf, occs, osh0, x0, y0, px, py, u, s_drive, &cx, &cy);
+            if (st == 1) {
+                a.dx[id] = cx;
+                a.dy[id] = cy;
+            } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
+                A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = id;
             }
-            a.dx[id] = cx;
-            a.dy[id] = cy;
+            ++mine;
         }
-        __syncthreads();
-        cur = s_tile[b ^ 1];
-        b ^= 1;
+        if (atomicAdd(&s_done[slot], mine) + mine == cnt) fetch(i + 2);  // last agent of fetch i
     }
+}
+
+// The exact path for the agents the tiled kernel could not decide: one warp per agent.  Lanes
+// own candidate slots of the ball in list order (row-major, wrapped-x sorted at the seam),
+// test them against the global bitplanes (walls, occupancy, Bresenham line of sight) and compute
+// the exact weights (restated glibc exp); lane 0 then folds the weights serially in list order
+// (sample_index, planning.hpp:63-73).  Narrow periodic grids (2v+1 > W-?) use choose_exact.
+#define EXACT_WARPS 4
+__global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanCommon a, const uint32_t* list) {
+    __shared__ double s_w[EXACT_WARPS][121];
+    __shared__ int s_c[EXACT_WARPS][121];
+    const unsigned n = (unsigned)a.sc->fb_count;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t step = (uint64_t)a.sc->step;
+    for (unsigned e = blockIdx.x * EXACT_WARPS + warp; e < n; e += gridDim.x * EXACT_WARPS) {
+        const uint32_t id = list[e];
+        const int px = a.g.wrap(a.x[id]), py = a.y[id], v = a.v[id];
+        const int D = 2 * v + 1;
+        if (a.g.boundary == FP_BOUNDARY_PERIODIC_X && D >= a.g.W) {
+            if (lane == 0) {
+                int cx, cy;
+                choose_exact(a, id, step, &cx, &cy);
+                a.dx[id] = cx;
+                a.dy[id] = cy;
+            }
+            continue;
+        }
+        // list-order column -> dx (wrapped-x sort at the periodic seam, planning.hpp:50-53)
+        int a0 = -v, na = D, b0 = 0;
+        if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {
+            if (px + v >= a.g.W) {
+                a0 = a.g.W - px; na = v - a0 + 1; b0 = -v;
+            } else if (px - v < 0) {
+                a0 = -px; na = v - a0 + 1; b0 = -v;
+            }
+        }
+        const ExactWeight wf = make_weight(a, px, py);
+        for (int k = lane; k < D * D; k += 32) {
+            const int r = k / D, c = k % D;
+            const int y = py - v + r;
+            const int dx = c < na ? a0 + c : b0 + (c - na);
+            int x = px + dx;
+            bool ok = y >= 0 && y < a.g.H;
+            if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) x = a.g.wrap(x);
+            else ok = ok && x >= 0 && x < a.g.W;
+            ok = ok && !a.g.is_wall(x, y);
+            ok = ok && !(occ_bit(a.occ, a.g, x, y) && !(x == px && y == py));
+            ok = ok && los(a.g, px, py, x, y);
+            s_w[warp][k] = ok ? wf(x, y) : -1.0;
+            s_c[warp][k] = ok ? (y * a.g.W + x) : -1;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            double total = 0.0;
+            int last = -1;
+            for (int k = 0; k < D * D; ++k)
+                if (s_c[warp][k] >= 0) {
+                    total = FPX_ADD(total, s_w[warp][k]);
+                    last = k;
+                }
+            const double threshold = FPX_MUL(fp_unit_interval(fp_rng_u64(a.seed, id, step, 0)), total);
+            double cum = 0.0;
+            int pick = last;
+            for (int k = 0; k < D * D; ++k)
+                if (s_c[warp][k] >= 0) {
+                    cum = FPX_ADD(cum, s_w[warp][k]);
+                    if (cum > threshold) {
+                        pick = k;
+                        break;
+                    }
+                }
+            const int cell = s_c[warp][pick];
+            a.dx[id] = cell % a.g.W;
+            a.dy[id] = cell / a.g.W;
+        }
+        __syncwarp();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.sc->fallbacks += n;
 }
 
 // Test mode (fp_get_choice): candidates in list order, exact weights and the production
@@ -568,9 +723,30 @@ int fp_plan_exact_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
 static void tile_geometry(const fp_ctx* ctx, TileArgs& A, size_t& smem) {
     A.boxw = ctx->tile_w + 16;
     A.boxh = ctx->tile_h + 2 * FP_HALO;
-    A.occw = (A.boxw + 31) / 32 + 2;
-    const int box_bytes = A.boxw * A.boxh * 4;
-    smem = 2 * (size_t)((box_bytes + 127) & ~127) + (size_t)((A.boxh * A.occw + 31) & ~31) * 4 + 256;
+    A.occw = 16;  // TMA box of the occupancy plane: 16 words (512 bits) from a 16-byte aligned word
+    const size_t box_stride = ((size_t)A.boxw * A.boxh + 31) & ~(size_t)31;
+    const size_t occ_stride = ((size_t)A.boxh * A.occw + 31) & ~(size_t)31;
+    smem = (2 * box_stride + 2 * occ_stride) * 4 + 16 /* barriers */ + 128 /* alignment slack */;
+}
+
+static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& smem, unsigned& grid) {
+    TileArgs A;
+    A.c = make_common(ctx, k_s, seed);
+    A.PW = ctx->PW;
+    A.plane = ctx->d_plane;
+    A.use_tma = ctx->use_tma;
+    A.bucket = ctx->d_bucket;
+    A.tile_off = ctx->d_tile_off;
+    A.tile_cnt = ctx->d_tile_cnt;
+    A.tile_list = ctx->d_tile_list;
+    A.tile_w = ctx->tile_w;
+    A.tile_h = ctx->tile_h;
+    A.tiles_x = ctx->tiles_x;
+    A.fallback = ctx->d_fallback;
+    tile_geometry(ctx, A, smem);
+    const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
+    grid = (unsigned)std::min<size_t>((size_t)ctx->sm_count, nt);
+    return A;
 }
 
 // Everything the planning phase allocates or builds, done outside any graph capture.
@@ -590,32 +766,28 @@ int fp_plan_prepare(fp_ctx* ctx, double k_s) {
     return FP_OK;
 }
 
-// Enqueues the whole planning phase (bucketing + tiled kernel) on ctx->stream.  Graph-safe:
-// the step, tile count and cursors live in device memory; fp_plan_prepare ran before.
+static int launch_tile(fp_ctx* ctx, const TileArgs& A, size_t smem, unsigned grid) {
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
+    plan_tile_kernel<<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ, A);
+    FP_LAUNCHED(ctx);
+    return FP_OK;
+}
+
+// Enqueues the whole planning phase (bucketing + tiled kernel + exact-path pass) on
+// ctx->stream.  Graph-safe: the step, tile count, cursors and the fallback count live in device
+// memory; fp_plan_prepare ran before.
 int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     if (ctx->n == 0) return FP_OK;
     if (!tiled_ok(ctx)) return fp_plan_exact_launch(ctx, k_s, seed);
     if (!ctx->plane_valid || ctx->plane_ks != k_s || ctx->plane_potential != ctx->potential)
         return fp_fail(ctx, FP_ERUNTIME, "plan: weight plane not prepared for this k_s");
     if (int rc = fp_bucket_launch(ctx)) return rc;
-    TileArgs A;
-    A.c = make_common(ctx, k_s, seed);
-    A.PW = ctx->PW;
-    A.plane = ctx->d_plane;
-    A.use_tma = ctx->use_tma;
-    A.bucket = ctx->d_bucket;
-    A.tile_off = ctx->d_tile_off;
-    A.tile_cnt = ctx->d_tile_cnt;
-    A.tile_list = ctx->d_tile_list;
-    A.tile_w = ctx->tile_w;
-    A.tile_h = ctx->tile_h;
-    A.tiles_x = ctx->tiles_x;
     size_t smem;
-    tile_geometry(ctx, A, smem);
-    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
-    const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
-    const unsigned grid = (unsigned)std::min<size_t>((size_t)ctx->sm_count, nt);
-    plan_tile_kernel<<<grid, 256, smem, ctx->stream>>>(ctx->tmap_plane, A);
+    unsigned grid;
+    const TileArgs A = make_tile_args(ctx, k_s, seed, smem, grid);
+    if (int rc = launch_tile(ctx, A, smem, grid)) return rc;
+    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -629,30 +801,18 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
         return FP_OK;
     }
     if (int rc = fp_bucket_launch(ctx)) return rc;
-    TileArgs A;
-    A.c = make_common(ctx, k_s, seed);
-    A.PW = ctx->PW;
-    A.plane = ctx->d_plane;
-    A.use_tma = ctx->use_tma;
-    A.bucket = ctx->d_bucket;
-    A.tile_off = ctx->d_tile_off;
-    A.tile_cnt = ctx->d_tile_cnt;
-    A.tile_list = ctx->d_tile_list;
-    A.tile_w = ctx->tile_w;
-    A.tile_h = ctx->tile_h;
-    A.tiles_x = ctx->tiles_x;
     size_t smem;
-    tile_geometry(ctx, A, smem);
-    const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
-    const unsigned grid = (unsigned)std::min<size_t>((size_t)ctx->sm_count, nt);
+    unsigned grid;
+    const TileArgs A = make_tile_args(ctx, k_s, seed, smem, grid);
     cudaEvent_t e0, e1;
     FP_CUDA(ctx, cudaEventCreate(&e0));
     FP_CUDA(ctx, cudaEventCreate(&e1));
     double total = 0.0;
     for (int i = 0; i < iters; ++i) {
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
+        FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
         cudaEventRecord(e0, ctx->stream);
-        plan_tile_kernel<<<grid, 256, smem, ctx->stream>>>(ctx->tmap_plane, A);
+        plan_tile_kernel<<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ, A);
         FP_LAUNCHED(ctx);
         cudaEventRecord(e1, ctx->stream);
         FP_CUDA(ctx, cudaEventSynchronize(e1));
@@ -660,6 +820,9 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
         cudaEventElapsedTime(&t, e0, e1);
         total += t;
     }
+    // leave the state planned (the fallbacks of the last launch decided exactly)
+    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback);
+    FP_LAUNCHED(ctx);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *ms = total / std::max(iters, 1);

@@ -193,6 +193,15 @@ static int make_tmap(fp_ctx* ctx) {
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    // occupancy bitplane: a 16-word (512-bit) box from a 16-byte aligned word covers the
+    // 5-cell halo window of any tile (tile_w + 16 <= 256 columns, <= 127 bits of misalignment)
+    cuuint64_t odims[2] = {(cuuint64_t)ctx->P, (cuuint64_t)ctx->H};
+    cuuint64_t ostr[1] = {(cuuint64_t)ctx->P * 4};
+    cuuint32_t obox[2] = {16u, (cuuint32_t)(ctx->tile_h + 2 * FP_HALO)};
+    r = enc(&ctx->tmap_occ, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, ctx->d_occ, odims, ostr, obox, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled(occ) failed (" + std::to_string((int)r) + ")");
     return FP_OK;
 }
 
