@@ -135,7 +135,7 @@ static void free_agents(fp_ctx* c) {
     void* ptrs[] = {c->d_x, c->d_y, c->d_dx, c->d_dy, c->d_v, c->d_alive, c->d_rank, c->d_alive_ids,
                     c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
                     c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted,
-                    c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback};
+                    c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback, c->d_rec_a, c->d_rec_b};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->d_x = c->d_y = c->d_dx = c->d_dy = nullptr;
@@ -144,6 +144,7 @@ static void free_agents(fp_ctx* c) {
     c->d_bucket = c->d_succ = c->d_nxt = c->d_V = c->d_pend_a = c->d_pend_b = nullptr;
     c->d_exits = c->d_exits_sorted = nullptr;
     c->d_fy_bucket = c->d_flags = c->d_cursor_b = c->d_fallback = nullptr;
+    c->d_rec_a = c->d_rec_b = nullptr;
     c->cap = 0;
     c->graph_valid = false;
 }
@@ -164,6 +165,8 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
     for (uint32_t** p : u32s) FP_CUDA(c, cudaMalloc(p, m * 4));
     FP_CUDA(c, cudaMalloc(&c->d_exits, m * 8));
     FP_CUDA(c, cudaMalloc(&c->d_exits_sorted, m * 8));
+    FP_CUDA(c, cudaMalloc(&c->d_rec_a, m * sizeof(uint4)));
+    FP_CUDA(c, cudaMalloc(&c->d_rec_b, m * sizeof(uint4)));
     c->cap = (uint32_t)m;
     return FP_OK;
 }
@@ -328,6 +331,7 @@ static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const ui
     else
         al = n;
     c->alive = al;
+    c->bucket_fresh = false;
     if (int rc = fp_ghost_occ(c)) return rc;
     return sync_scalars(c);
 }
@@ -423,7 +427,8 @@ static int move_impl(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
     const int64_t alive0 = c->alive;
     if (int rc = sync_scalars(c)) return rc;
     if (int rc = fp_order_launch(c, seed, c->stream)) return rc;
-    if (int rc = fp_motion_launch(c)) return rc;
+    if (int rc = fp_motion_launch(c, c->bucket_fresh)) return rc;
+    c->bucket_fresh = false;
     if (int rc = read_scalars(c)) return rc;
     c->n_order = (uint32_t)c->h_sc->n_alive;
     c->n_exits = (uint32_t)c->h_sc->n_exits;
@@ -481,7 +486,8 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(plan)");
     g = nullptr;
     FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    rc = fp_motion_launch(c);
+    rc = fp_motion_launch(c, c->bucket_fresh);  // the plan graph re-buckets every step
+    c->bucket_fresh = false;
     if (rc == FP_OK) {
         sc_step_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
         c->ctr.kernel_launches++;

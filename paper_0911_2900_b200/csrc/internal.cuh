@@ -179,6 +179,8 @@ struct fp_ctx {
     // motion scratch
     uint32_t *d_pend_a = nullptr, *d_pend_b = nullptr;
     uint32_t* d_fallback = nullptr;  // agents the plan kernel hands to the exact path
+    uint4 *d_rec_a = nullptr, *d_rec_b = nullptr;  // motion pending records (move.cu)
+    bool bucket_fresh = false;  // plan-tile buckets match the current positions
     unsigned long long* d_exits = nullptr;  // (rank << 32 | id) records of the last move
     unsigned long long* d_exits_sorted = nullptr;
     int64_t last_displacement = 0;
@@ -240,7 +242,7 @@ int fp_bucket_launch(fp_ctx* ctx);                                    // bucket.
 int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed);           // plan.cu
 int fp_plan_exact_launch(fp_ctx* ctx, double k_s, uint64_t seed);     // plan.cu
 int fp_order_launch(fp_ctx* ctx, uint64_t seed, cudaStream_t s);     // order.cu
-int fp_motion_launch(fp_ctx* ctx);                                    // move.cu
+int fp_motion_launch(fp_ctx* ctx, bool spatial);                      // move.cu
 int fp_exits_finish(fp_ctx* ctx);                                     // move.cu
 int fp_field_compute(fp_ctx* ctx, const uint8_t* d_cells);            // field.cu
 int fp_choice_launch(fp_ctx* ctx, uint32_t agent, double k_s, int32_t* d_cx, int32_t* d_cy,

@@ -14,10 +14,13 @@
 // result equals the sequential walk bit for bit (tests/test_gpu_parity.py).  Agents with an
 // empty path (staying put) never change occupancy and skip the rounds entirely.
 //
-// One cooperative launch runs all rounds of a step: grid-wide rounds (grid.sync between the
-// reserve and commit phases) while many agents are pending, then block 0 finishes the tail
-// alone with __syncthreads.  Round stamps make the reservation plane self-cleaning: newer rounds
-// carry smaller keys, so nothing is ever reset.
+// Data path: a seed pass walks the alive agents in plan-tile order (spatial locality for the
+// reservation, occupancy and bitplane traffic), resolves each walk's static stops once, and
+// writes a 16-byte pending record {id, rank, x|m|exit, y|offset}; the rounds then touch only
+// the records, the reservation plane and the occupancy bits -- the path cells come from a
+// per-offset Bresenham table.  One cooperative launch runs all rounds of a step: grid-wide
+// rounds (grid.sync between reserve and commit) while many agents are pending, then block 0
+// finishes the tail alone.  Round stamps make the reservation plane self-cleaning.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -27,6 +30,31 @@ namespace cg = cooperative_groups;
 
 #define MOVE_THREADS 512
 #define MOVE_TAIL 4096  // pending agents at or below which block 0 runs the rounds alone
+
+// Bresenham cells (dx, dy) of the segment from (0,0) to each offset of the 11x11 frame,
+// index (dy+5)*11 + dx+5, in walk order (world.hpp:143-167); host-built, copied per launch to
+// shared memory.
+__constant__ signed char c_bpath[121][5][2];
+static bool g_bpath_ready[64] = {false};
+
+static void host_bpath(signed char out[121][5][2]) {
+    for (int ty = -5; ty <= 5; ++ty)
+        for (int tx = -5; tx <= 5; ++tx) {
+            signed char(*p)[2] = out[(ty + 5) * 11 + tx + 5];
+            for (int j = 0; j < 5; ++j) p[j][0] = p[j][1] = 0;
+            const int adx = abs(tx), sx = 0 < tx ? 1 : -1;
+            const int ady = -abs(ty), sy = 0 < ty ? 1 : -1;
+            int err = adx + ady, x = 0, y = 0, j = 0;
+            while (!(x == tx && y == ty)) {
+                const int e2 = 2 * err;
+                if (e2 >= ady) { err += ady; x += sx; }
+                if (e2 <= adx) { err += adx; y += sy; }
+                p[j][0] = (signed char)x;
+                p[j][1] = (signed char)y;
+                ++j;
+            }
+        }
+}
 
 struct MoveArgs {
     Geo g;
@@ -39,31 +67,82 @@ struct MoveArgs {
     const uint8_t* v;
     uint8_t* alive;
     const uint32_t* rank;
-    const uint32_t* order;
-    uint32_t* pend[2];
-    unsigned int* pcount;          // [2] pending counts (device scratch)
+    const uint32_t* seed_list;     // alive ids (plan-tile order when fresh, else movement order)
+    uint4* rec[2];                 // pending records, ping-pong
+    unsigned int* pcount;          // [2] pending counts (device scratch, zero between phases)
     DevScalars* sc;
     unsigned long long* exits;     // (rank << 32 | id)
 };
 
-// Path cells the walk may visit (engine.hpp:116-119 static stops), at most 5.
-__device__ __forceinline__ int footprint(const MoveArgs& a, uint32_t id, int sx, int sy, int* cx, int* cy) {
+// Pending record: x = id, y = rank, z = px | m << 28 | exit_at_end << 31,
+// w = py | o << 24 | generic << 31  (o: frame offset of the walk's target; generic: the target is
+// farther than 5 cells and the path is re-derived from the agent arrays).
+#define REC_GENERIC 0x80000000u
+
+// Static walk of agent `id` (engine.hpp:116-119): first <= v_max Bresenham cells, cut before a
+// Wall, ending at an Exit.  Returns the record; m = 0 means the agent does not move at all.
+__device__ __forceinline__ uint4 make_record(const MoveArgs& a, uint32_t id, const signed char (*bp)[5][2]) {
     const Geo& g = a.g;
+    const int sx = g.wrap(a.x[id]), sy = a.y[id];
     const int tx = g.wrap(a.dx[id]), ty = a.dy[id];
     const int v = a.v[id];
-    Bres b;
-    b.init(g, sx, sy, tx, ty);
-    int k = 0;
-    while (!b.done() && k < v) {
-        b.next();
-        const int x = g.wrap(b.x), y = b.y;
-        if (g.is_wall(x, y)) break;
-        cx[k] = x;
-        cy[k] = y;
-        ++k;
-        if (g.is_exit(x, y)) break;
+    const int ddx = g.segment_dx(sx, tx), ddy = ty - sy;
+    int m = 0;
+    bool ex = false;
+    uint32_t w;
+    if (abs(ddx) <= 5 && abs(ddy) <= 5) {
+        const int o = (ddy + 5) * 11 + ddx + 5;
+        const int len = min(max(abs(ddx), abs(ddy)), v);
+        for (int j = 0; j < len; ++j) {
+            const int x = g.wrap(sx + bp[o][j][0]), y = sy + bp[o][j][1];
+            if (g.is_wall(x, y)) break;
+            ++m;
+            if (g.is_exit(x, y)) {
+                ex = true;
+                break;
+            }
+        }
+        w = (uint32_t)sy | ((uint32_t)o << 24);
+    } else {
+        Bres b;
+        b.init(g, sx, sy, tx, ty);
+        while (!b.done() && m < v) {
+            b.next();
+            const int x = g.wrap(b.x), y = b.y;
+            if (g.is_wall(x, y)) break;
+            ++m;
+            if (g.is_exit(x, y)) {
+                ex = true;
+                break;
+            }
+        }
+        w = (uint32_t)sy | REC_GENERIC;
     }
-    return k;
+    return make_uint4(id, a.rank[id], (uint32_t)sx | ((uint32_t)m << 28) | (ex ? 0x80000000u : 0u), w);
+}
+
+// The footprint path cells of a record (at most 5).
+__device__ __forceinline__ int record_path(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2], int* cx,
+                                           int* cy) {
+    const Geo& g = a.g;
+    const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
+    const int m = (int)((r.z >> 28) & 7u);
+    if (!(r.w & REC_GENERIC)) {
+        const int o = (int)((r.w >> 24) & 0x7Fu);
+        for (int j = 0; j < m; ++j) {
+            cx[j] = g.wrap(sx + bp[o][j][0]);
+            cy[j] = sy + bp[o][j][1];
+        }
+    } else {
+        Bres b;
+        b.init(g, sx, sy, g.wrap(a.dx[r.x]), a.dy[r.x]);
+        for (int j = 0; j < m; ++j) {
+            b.next();
+            cx[j] = g.wrap(b.x);
+            cy[j] = b.y;
+        }
+    }
+    return m;
 }
 
 __device__ __forceinline__ size_t cell_index(const Geo& g, int x, int y) {
@@ -74,7 +153,7 @@ __device__ __forceinline__ bool occ_test(const MoveArgs& a, int x, int y) {
     return (__ldcg(&a.occ[a.g.word(x, y)]) >> (x & 31)) & 1u;
 }
 
-__device__ __forceinline__ void append(unsigned int* count, uint32_t* list, bool take, uint32_t id) {
+__device__ __forceinline__ void append(unsigned int* count, uint4* list, bool take, const uint4& rec) {
     const unsigned mask = __ballot_sync(0xffffffffu, take);
     if (!mask) return;
     const int lane = threadIdx.x & 31;
@@ -82,40 +161,37 @@ __device__ __forceinline__ void append(unsigned int* count, uint32_t* list, bool
     unsigned base = 0;
     if (lane == leader) base = atomicAdd(count, (unsigned)__popc(mask));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (take) list[base + __popc(mask & ((1u << lane) - 1))] = id;
+    if (take) list[base + __popc(mask & ((1u << lane) - 1))] = rec;
 }
 
-__device__ __forceinline__ void reserve_one(const MoveArgs& a, uint32_t id, unsigned long long stamp) {
-    const unsigned long long key = stamp | a.rank[id];
-    const int sx = a.g.wrap(a.x[id]), sy = a.y[id];
+__device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, unsigned long long stamp,
+                                            const signed char (*bp)[5][2]) {
+    const unsigned long long key = stamp | r.y;
     int cx[5], cy[5];
-    const int m = footprint(a, id, sx, sy, cx, cy);
-    atomicMin(&a.res[cell_index(a.g, sx, sy)], key);
+    const int m = record_path(a, r, bp, cx, cy);
+    atomicMin(&a.res[cell_index(a.g, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu))], key);
     for (int i = 0; i < m; ++i) atomicMin(&a.res[cell_index(a.g, cx[i], cy[i])], key);
 }
 
 // Returns true if the agent committed (walked); false if it must retry next round.
-__device__ __forceinline__ bool commit_one(const MoveArgs& a, uint32_t id, unsigned long long stamp,
-                                           unsigned long long* hops_acc) {
-    const unsigned long long key = stamp | a.rank[id];
-    const int sx = a.g.wrap(a.x[id]), sy = a.y[id];
+__device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, unsigned long long stamp,
+                                           const signed char (*bp)[5][2], unsigned long long* hops_acc) {
+    const unsigned long long key = stamp | r.y;
+    const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
     int cx[5], cy[5];
-    const int m = footprint(a, id, sx, sy, cx, cy);
+    const int m = record_path(a, r, bp, cx, cy);
     bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == key;
     for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == key;
     if (!own) return false;
     // The walk (engine.hpp:116-129), net effect on occupancy.
     int h = 0;
-    bool exited = false;
     for (int i = 0; i < m; ++i) {
         if (occ_test(a, cx[i], cy[i])) break;
         ++h;
-        if (a.g.is_exit(cx[i], cy[i])) {
-            exited = true;
-            break;
-        }
     }
+    const bool exited = (h == m) && (r.z & 0x80000000u);
     if (h > 0) {
+        const uint32_t id = r.x;
         atomicAnd(&a.occ[a.g.word(sx, sy)], ~(1u << (sx & 31)));
         const int fx = cx[h - 1], fy = cy[h - 1];
         a.x[id] = fx;
@@ -123,7 +199,7 @@ __device__ __forceinline__ bool commit_one(const MoveArgs& a, uint32_t id, unsig
         if (exited) {
             a.alive[id] = 0;
             const unsigned long long slot = atomicAdd(&a.sc->n_exits, 1ull);
-            a.exits[slot] = ((unsigned long long)a.rank[id] << 32) | id;
+            a.exits[slot] = ((unsigned long long)r.y << 32) | id;
         } else {
             atomicOr(&a.occ[a.g.word(fx, fy)], 1u << (fx & 31));
         }
@@ -139,22 +215,23 @@ __device__ __forceinline__ void flush_hops(DevScalars* sc, unsigned long long ho
 
 __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     cg::grid_group grid = cg::this_grid();
+    __shared__ signed char s_bp[121][5][2];
+    for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
+    __syncthreads();
     const unsigned nthreads = gridDim.x * blockDim.x;
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = (uint32_t)__ldcg(&a.sc->n_alive);
     const unsigned long long round0 = __ldcg(&a.sc->round_seq);
-    // seed the pending list with every alive agent whose walk has at least one cell
+    // seed: every alive agent whose walk has at least one cell, as a pending record
     for (uint32_t base = 0; base < n; base += nthreads) {
         const uint32_t k = base + gtid;
+        uint4 rec = make_uint4(0, 0, 0, 0);
         bool take = false;
-        uint32_t id = 0;
         if (k < n) {
-            id = a.order[k];
-            const int sx = a.g.wrap(a.x[id]), sy = a.y[id];
-            int cx[5], cy[5];
-            take = footprint(a, id, sx, sy, cx, cy) > 0;
+            rec = make_record(a, a.seed_list[k], s_bp);
+            take = (rec.z >> 28) & 7u;
         }
-        append(&a.pcount[0], a.pend[0], take, id);
+        append(&a.pcount[0], a.rec[0], take, rec);
     }
     grid.sync();
     unsigned r = 0;
@@ -171,19 +248,19 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         const unsigned stride = solo ? blockDim.x : nthreads;
         const unsigned me = solo ? threadIdx.x : gtid;
         if (gtid == 0) a.pcount[nxt] = 0;
-        const uint32_t* list = a.pend[cur];
-        for (unsigned k = me; k < np; k += stride) reserve_one(a, __ldcg(&list[k]), stamp);
+        const uint4* list = a.rec[cur];
+        for (unsigned k = me; k < np; k += stride) reserve_one(a, __ldcg(&list[k]), stamp, s_bp);
         if (solo) __syncthreads(); else grid.sync();
         unsigned long long hops = 0;
         for (unsigned base = 0; base < np; base += stride) {
             const unsigned k = base + me;
             bool retry = false;
-            uint32_t id = 0;
+            uint4 rec = make_uint4(0, 0, 0, 0);
             if (k < np) {
-                id = __ldcg(&list[k]);
-                retry = !commit_one(a, id, stamp, &hops);
+                rec = __ldcg(&list[k]);
+                retry = !commit_one(a, rec, stamp, s_bp, &hops);
             }
-            append(&a.pcount[nxt], a.pend[nxt], retry, id);
+            append(&a.pcount[nxt], a.rec[nxt], retry, rec);
         }
         flush_hops(a.sc, hops);
         if (solo) __syncthreads(); else grid.sync();
@@ -207,6 +284,12 @@ __global__ void move_begin_kernel(DevScalars* sc) {
 }
 
 int fp_ensure_res(fp_ctx* ctx) {
+    if (ctx->device < 64 && !g_bpath_ready[ctx->device]) {
+        signed char bp[121][5][2];
+        host_bpath(bp);
+        FP_CUDA(ctx, cudaMemcpyToSymbol(c_bpath, bp, sizeof(bp)));
+        g_bpath_ready[ctx->device] = true;
+    }
     if (ctx->d_res) return FP_OK;
     const size_t cells = (size_t)ctx->W * (size_t)ctx->H;
     FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned long long)));
@@ -217,7 +300,8 @@ int fp_ensure_res(fp_ctx* ctx) {
 static int g_move_blocks = 0;
 
 // Enqueues one motion phase (after fp_order_launch) on ctx->stream.  Graph-safe.
-int fp_motion_launch(fp_ctx* ctx) {
+// `spatial`: the plan-tile buckets are current (seed in spatial order); else movement order.
+int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     cudaStream_t s = ctx->stream;
     move_begin_kernel<<<1, 1, 0, s>>>(ctx->d_sc);
     FP_LAUNCHED(ctx);
@@ -238,9 +322,9 @@ int fp_motion_launch(fp_ctx* ctx) {
     a.v = ctx->d_v;
     a.alive = ctx->d_alive;
     a.rank = ctx->d_rank;
-    a.order = ctx->d_order;
-    a.pend[0] = ctx->d_pend_a;
-    a.pend[1] = ctx->d_pend_b;
+    a.seed_list = spatial ? ctx->d_bucket : ctx->d_order;
+    a.rec[0] = ctx->d_rec_a;
+    a.rec[1] = ctx->d_rec_b;
     a.pcount = (unsigned int*)ctx->d_counters;  // [0], [1] as u32 (kept zero between phases)
     a.sc = ctx->d_sc;
     a.exits = ctx->d_exits;

@@ -783,6 +783,7 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     if (!ctx->plane_valid || ctx->plane_ks != k_s || ctx->plane_potential != ctx->potential)
         return fp_fail(ctx, FP_ERUNTIME, "plan: weight plane not prepared for this k_s");
     if (int rc = fp_bucket_launch(ctx)) return rc;
+    ctx->bucket_fresh = true;  // the motion seed pass walks agents in this (spatial) order
     size_t smem;
     unsigned grid;
     const TileArgs A = make_tile_args(ctx, k_s, seed, smem, grid);
