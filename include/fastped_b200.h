@@ -79,6 +79,10 @@ typedef struct {
     int64_t motion_rounds;     /* conflict-resolution rounds executed */
     int64_t plan_fallbacks;    /* agents re-sampled on the exact fp64 path */
     int64_t planned_agents;    /* agents planned */
+    int64_t motion_seed_ns;    /* last motion phase: seed pass (device globaltimer) */
+    int64_t motion_grid_ns;    /*   grid-wide rounds */
+    int64_t motion_tail_ns;    /*   single-CTA tail rounds */
+    int64_t motion_grid_rounds;/*   rounds run grid-wide in the last phase */
 } fp_counters;
 
 const char* fp_version(void);

@@ -299,6 +299,13 @@ static int read_scalars(fp_ctx* c) {
     c->step = (int64_t)c->h_sc->step;
     c->ctr.plan_fallbacks = (int64_t)c->h_sc->fallbacks;
     c->ctr.motion_rounds = (int64_t)c->h_sc->pad[1];
+    const unsigned long long* tm = c->h_sc->t_motion;
+    if (tm[3] >= tm[2] && tm[2] >= tm[1] && tm[1] >= tm[0] && tm[0]) {
+        c->ctr.motion_seed_ns = (int64_t)(tm[1] - tm[0]);
+        c->ctr.motion_grid_ns = (int64_t)(tm[2] - tm[1]);
+        c->ctr.motion_tail_ns = (int64_t)(tm[3] - tm[2]);
+    }
+    c->ctr.motion_grid_rounds = (int64_t)c->h_sc->grid_rounds;
     return FP_OK;
 }
 

@@ -119,6 +119,8 @@ struct DevScalars {
     unsigned long long err;       // device-detected errors (bit flags)
     unsigned long long pad[2];    // [0] unsafe plane cells, [1] motion rounds executed
     unsigned long long fb_count;  // agents queued for the exact planning path this step
+    unsigned long long t_motion[4];  // globaltimer: motion start, seed done, grid rounds done, end
+    unsigned long long grid_rounds;  // rounds of the last motion phase run grid-wide
     unsigned long long pad2[3];
 };
 
@@ -137,7 +139,7 @@ struct fp_ctx {
     uint32_t* d_exit = nullptr;
     uint32_t* d_occ = nullptr;
     double* d_field = nullptr;
-    unsigned long long* d_res = nullptr;  // motion reservations (allocated on first move)
+    unsigned int* d_res = nullptr;  // motion reservations: rank of the reserving agent (move.cu)
 
     // weight plane (plane.cu), valid for (plane_ks, plane_potential, plane_gradient)
     uint32_t* d_plane = nullptr;

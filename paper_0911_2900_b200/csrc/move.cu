@@ -7,12 +7,15 @@
 // Parallel form (deterministic reservations): an agent's footprint is its start cell plus the
 // path cells it could visit (capped at v_max, cut before a Wall, ending at an Exit).  Only
 // agents with overlapping footprints can influence each other, and only through those cells.
-// Each round, every pending agent writes its key (round stamp, rank) into its footprint cells
-// with atomicMin; an agent that holds all of its cells is the earliest pending agent on each of
-// them, so everything that precedes it in the reference order on those cells has already run
-// -- it executes its walk now.  Committed agents in one round have disjoint footprints.  The
-// result equals the sequential walk bit for bit (tests/test_gpu_parity.py).  Agents with an
-// empty path (staying put) never change occupancy and skip the rounds entirely.
+// Each round, every pending agent writes its rank into its footprint cells with atomicMin; an
+// agent that holds all of its cells is the earliest pending agent on each of them, so
+// everything that precedes it in the reference order on those cells has already run -- it
+// executes its walk now and clears its cells back to "free".  Committed agents in one round
+// have disjoint footprints.  Keys left behind by agents still pending are harmless (they are
+// re-asserted with the same priority next round), so the reservation plane (u32 per cell) needs
+// neither round stamps nor resets and is all-free again when the phase ends.  The result equals
+// the sequential walk bit for bit (tests/test_gpu_parity.py).  Agents with an empty path (staying
+// put) never change occupancy and skip the rounds entirely.
 //
 // Data path: a seed pass walks the alive agents in plan-tile order (spatial locality for the
 // reservation, occupancy and bitplane traffic), resolves each walk's static stops once, and
@@ -20,7 +23,7 @@
 // the records, the reservation plane and the occupancy bits -- the path cells come from a
 // per-offset Bresenham table.  One cooperative launch runs all rounds of a step: grid-wide
 // rounds (grid.sync between reserve and commit) while many agents are pending, then block 0
-// finishes the tail alone.  Round stamps make the reservation plane self-cleaning.
+// finishes the tail alone.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -59,7 +62,7 @@ static void host_bpath(signed char out[121][5][2]) {
 struct MoveArgs {
     Geo g;
     uint32_t* occ;
-    unsigned long long* res;
+    unsigned int* res;
     int32_t* x;
     int32_t* y;
     const int32_t* dx;
@@ -145,6 +148,12 @@ __device__ __forceinline__ int record_path(const MoveArgs& a, const uint4& r, co
     return m;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ size_t cell_index(const Geo& g, int x, int y) {
     return (size_t)y * (size_t)g.W + (size_t)x;
 }
@@ -164,9 +173,8 @@ __device__ __forceinline__ void append(unsigned int* count, uint4* list, bool ta
     if (take) list[base + __popc(mask & ((1u << lane) - 1))] = rec;
 }
 
-__device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, unsigned long long stamp,
-                                            const signed char (*bp)[5][2]) {
-    const unsigned long long key = stamp | r.y;
+__device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2]) {
+    const unsigned int key = r.y;
     int cx[5], cy[5];
     const int m = record_path(a, r, bp, cx, cy);
     atomicMin(&a.res[cell_index(a.g, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu))], key);
@@ -174,15 +182,18 @@ __device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, u
 }
 
 // Returns true if the agent committed (walked); false if it must retry next round.
-__device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, unsigned long long stamp,
-                                           const signed char (*bp)[5][2], unsigned long long* hops_acc) {
-    const unsigned long long key = stamp | r.y;
+__device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
+                                           unsigned long long* hops_acc) {
+    const unsigned int key = r.y;
     const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
     int cx[5], cy[5];
     const int m = record_path(a, r, bp, cx, cy);
     bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == key;
     for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == key;
     if (!own) return false;
+    // release the footprint: losers of this round read it after their own failed check only
+    a.res[cell_index(a.g, sx, sy)] = 0xFFFFFFFFu;
+    for (int i = 0; i < m; ++i) a.res[cell_index(a.g, cx[i], cy[i])] = 0xFFFFFFFFu;
     // The walk (engine.hpp:116-129), net effect on occupancy.
     int h = 0;
     for (int i = 0; i < m; ++i) {
@@ -221,7 +232,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     const unsigned nthreads = gridDim.x * blockDim.x;
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = (uint32_t)__ldcg(&a.sc->n_alive);
-    const unsigned long long round0 = __ldcg(&a.sc->round_seq);
+    if (gtid == 0) a.sc->t_motion[0] = globaltimer();
     // seed: every alive agent whose walk has at least one cell, as a pending record
     for (uint32_t base = 0; base < n; base += nthreads) {
         const uint32_t k = base + gtid;
@@ -234,6 +245,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         append(&a.pcount[0], a.rec[0], take, rec);
     }
     grid.sync();
+    if (gtid == 0) a.sc->t_motion[1] = globaltimer();
     unsigned r = 0;
     bool solo = false;
     for (;; ++r) {
@@ -243,13 +255,16 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         if (!solo && np <= MOVE_TAIL) {
             if (blockIdx.x != 0) return;  // every block reads the same np: block 0 continues alone
             solo = true;
+            if (threadIdx.x == 0) {
+                a.sc->t_motion[2] = globaltimer();
+                a.sc->grid_rounds = r;
+            }
         }
-        const unsigned long long stamp = (0xFFFFFFFFull - ((round0 + r) & 0xFFFFFFFFull)) << 32;
         const unsigned stride = solo ? blockDim.x : nthreads;
         const unsigned me = solo ? threadIdx.x : gtid;
         if (gtid == 0) a.pcount[nxt] = 0;
         const uint4* list = a.rec[cur];
-        for (unsigned k = me; k < np; k += stride) reserve_one(a, __ldcg(&list[k]), stamp, s_bp);
+        for (unsigned k = me; k < np; k += stride) reserve_one(a, __ldcg(&list[k]), s_bp);
         if (solo) __syncthreads(); else grid.sync();
         unsigned long long hops = 0;
         for (unsigned base = 0; base < np; base += stride) {
@@ -258,7 +273,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
             uint4 rec = make_uint4(0, 0, 0, 0);
             if (k < np) {
                 rec = __ldcg(&list[k]);
-                retry = !commit_one(a, rec, stamp, s_bp, &hops);
+                retry = !commit_one(a, rec, s_bp, &hops);
             }
             append(&a.pcount[nxt], a.rec[nxt], retry, rec);
         }
@@ -266,7 +281,12 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         if (solo) __syncthreads(); else grid.sync();
     }
     if (gtid == 0) {
-        a.sc->round_seq = round0 + r;
+        const unsigned long long t = globaltimer();
+        if (!solo) {
+            a.sc->t_motion[2] = t;
+            a.sc->grid_rounds = r;
+        }
+        a.sc->t_motion[3] = t;
         a.sc->pad[1] += r;  // rounds executed (observability)
         a.pcount[0] = 0;
         a.pcount[1] = 0;
@@ -292,8 +312,8 @@ int fp_ensure_res(fp_ctx* ctx) {
     }
     if (ctx->d_res) return FP_OK;
     const size_t cells = (size_t)ctx->W * (size_t)ctx->H;
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned long long)));
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned long long), ctx->stream));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned int)));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned int), ctx->stream));
     return FP_OK;
 }
 

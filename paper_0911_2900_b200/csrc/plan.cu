@@ -523,10 +523,12 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         }
         if (gen > i) continue;
         const int tile = s_tile[slot];
-        if (tile < 0) break;
         const int cnt = s_cnt[slot], off = s_off[slot], x0 = s_x0[slot], y0 = s_y0[slot];
         __threadfence_block();
+        // validate the snapshot before acting on any of it (including the end-of-list marker:
+        // a refill racing with these reads may already have written tile = -1 for fetch i+2)
         if (s_gen[slot] != i) continue;  // fetch i already completed without this thread's help
+        if (tile < 0) break;
         int k = ((int)threadIdx.x - i * 160) & (PLAN_THREADS - 1);
         if (k >= cnt) continue;  // no agent of this fetch for this thread
         uint32_t* buf = smem + slot * box_stride;
@@ -570,7 +572,14 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
             }
             ++mine;
         }
-        if (atomicAdd(&s_done[slot], mine) + mine == cnt) fetch(i + 2);  // last agent of fetch i
+        // release: this thread's reads of the slot happen before its count lands (without the
+        // fence the compiler may sink shared loads below the relaxed atomic and the refill
+        // TMA would overwrite data still being read); the last finisher acquires, then refills
+        __threadfence_block();
+        if (atomicAdd(&s_done[slot], mine) + mine == cnt) {  // last agent of fetch i
+            __threadfence_block();
+            fetch(i + 2);
+        }
     }
 }
 

@@ -256,3 +256,50 @@ def test_config2_room_steps():
             orc.step_once(1.2, wl.seed)
         assert_same_state(dev, orc, f"v={v}")
         assert fp.state_hash(dev) == orc.hash()
+
+
+def test_plan_repeatable_under_load():
+    """Race detector for the tiled plan kernel's slot pipeline: the dense ring (many tiles per
+    CTA, > 512 agents in a tile) planned repeatedly must give identical desired cells, equal to
+    the oracle's."""
+    from paper_0911_2900_b200 import scenarios
+    wl = scenarios.ring()
+    ro = wl.roster
+    dev, orc = pair(wl.grid.cells, ro.x, ro.y, ro.v_max, wl.grid.boundary, wl.potential, wl.drive_gradient)
+    orc.plan(wl.k_s, wl.seed)
+    for _ in range(8):
+        fp.plan_phase(dev, fp.SimParams(k_s=wl.k_s, seed=wl.seed))
+        dx, dy = dev.desired()
+        assert (dx == orc.dx).all() and (dy == orc.dy).all()
+
+
+def test_plaza_sampled_plan_and_invariants():
+    """Config 4 at full size (1e8 cells, 1e6 agents): planned cells of a sample of agents equal
+    the oracle's choose_desired_cell; after motion the state is consistent (occupancy <-> positions),
+    conservation holds and nobody moved farther than v_max."""
+    import ctypes as C
+    from paper_0911_2900_b200 import scenarios
+    wl = scenarios.plaza()
+    ro = wl.roster
+    dev = fp.SimState(wl.grid, None, ro)
+    field = dev.field()
+    fp.plan_phase(dev, fp.SimParams(seed=wl.seed))
+    dx, dy = dev.desired()
+    # oracle on a sample: build a small oracle state view over the full grid
+    orc = O.State(wl.grid.cells, field, ro.x, ro.y, ro.v_max)
+    rng = np.random.default_rng(5)
+    for i in rng.choice(len(ro.x), 2000, replace=False):
+        ox, oy = C.c_int32(), C.c_int32()
+        O.lib().orc_choose_desired.argtypes = [C.POINTER(O.OrcState), C.c_int32, C.c_double, C.c_uint64,
+                                               C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        O.lib().orc_choose_desired(C.byref(orc.s), int(i), 1.2, wl.seed, C.byref(ox), C.byref(oy))
+        assert (dx[i], dy[i]) == (ox.value, oy.value), i
+    x0, y0, _ = dev.agents()
+    mv = fp.move_phase(dev, fp.SimParams(seed=wl.seed))
+    x1, y1, a1 = dev.agents()
+    al = a1.astype(bool)
+    assert np.maximum(np.abs(x1 - x0), np.abs(y1 - y0))[al].max() <= 4
+    assert dev.alive + len(mv.exited) == len(ro.x)
+    occ = dev.occupancy()
+    assert (occ[y1[al], x1[al]] == np.nonzero(al)[0]).all()
+    assert (occ >= 0).sum() == al.sum()

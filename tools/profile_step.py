@@ -28,3 +28,4 @@ if args.mode == "plan":
 else:
     r = fp.run(st, p)
     print("run", r)
+print("counters", st.counters())
