@@ -140,6 +140,7 @@ struct fp_ctx {
     uint32_t* d_occ = nullptr;
     double* d_field = nullptr;
     unsigned int* d_res = nullptr;  // motion reservations: rank of the reserving agent (move.cu)
+    uint32_t *d_p1 = nullptr, *d_p2 = nullptr;  // motion contention bitplanes (move.cu)
 
     // weight plane (plane.cu), valid for (plane_ks, plane_potential, plane_gradient)
     uint32_t* d_plane = nullptr;

@@ -75,6 +75,8 @@ struct MoveArgs {
     unsigned int* pcount;          // [2] pending counts (device scratch, zero between phases)
     DevScalars* sc;
     unsigned long long* exits;     // (rank << 32 | id)
+    uint32_t* p1;                  // contention bitplanes (touched once / twice+), zero between phases
+    uint32_t* p2;
 };
 
 // Pending record: x = id, y = rank, z = px | m << 28 | exit_at_end << 31,
@@ -181,20 +183,10 @@ __device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, c
     for (int i = 0; i < m; ++i) atomicMin(&a.res[cell_index(a.g, cx[i], cy[i])], key);
 }
 
-// Returns true if the agent committed (walked); false if it must retry next round.
-__device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
+// The walk (engine.hpp:116-129) of an agent that owns its footprint, net effect on occupancy.
+__device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, const int* cx, const int* cy, int m,
                                            unsigned long long* hops_acc) {
-    const unsigned int key = r.y;
     const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
-    int cx[5], cy[5];
-    const int m = record_path(a, r, bp, cx, cy);
-    bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == key;
-    for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == key;
-    if (!own) return false;
-    // release the footprint: losers of this round read it after their own failed check only
-    a.res[cell_index(a.g, sx, sy)] = 0xFFFFFFFFu;
-    for (int i = 0; i < m; ++i) a.res[cell_index(a.g, cx[i], cy[i])] = 0xFFFFFFFFu;
-    // The walk (engine.hpp:116-129), net effect on occupancy.
     int h = 0;
     for (int i = 0; i < m; ++i) {
         if (occ_test(a, cx[i], cy[i])) break;
@@ -216,6 +208,41 @@ __device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, co
         }
     }
     *hops_acc += (unsigned long long)h;
+}
+
+// Footprint marking: P1 = touched by some mover, P2 = touched by two or more movers.
+__device__ __forceinline__ void mark_cell(const MoveArgs& a, int x, int y) {
+    const size_t w = a.g.word(x, y);
+    const uint32_t bit = 1u << (x & 31);
+    if (atomicOr(&a.p1[w], bit) & bit) atomicOr(&a.p2[w], bit);
+}
+
+__device__ __forceinline__ void clear_cell(const MoveArgs& a, int x, int y, bool both) {
+    const size_t w = a.g.word(x, y);
+    const uint32_t nbit = ~(1u << (x & 31));
+    atomicAnd(&a.p1[w], nbit);
+    if (both) atomicAnd(&a.p2[w], nbit);
+}
+
+// Returns true if the agent committed (walked); false if it must retry next round.
+__device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
+                                           unsigned long long* hops_acc) {
+    const unsigned int key = r.y;
+    const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
+    int cx[5], cy[5];
+    const int m = record_path(a, r, bp, cx, cy);
+    bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == key;
+    for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == key;
+    if (!own) return false;
+    // release the footprint: losers of this round read it after their own failed check only;
+    // the contention bits go back to zero for the next phase
+    a.res[cell_index(a.g, sx, sy)] = 0xFFFFFFFFu;
+    clear_cell(a, sx, sy, true);
+    for (int i = 0; i < m; ++i) {
+        a.res[cell_index(a.g, cx[i], cy[i])] = 0xFFFFFFFFu;
+        clear_cell(a, cx[i], cy[i], true);
+    }
+    walk_owned(a, r, cx, cy, m, hops_acc);
     return true;
 }
 
@@ -233,7 +260,8 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = (uint32_t)__ldcg(&a.sc->n_alive);
     if (gtid == 0) a.sc->t_motion[0] = globaltimer();
-    // seed: every alive agent whose walk has at least one cell, as a pending record
+    // seed: every alive agent whose walk has at least one cell, as a pending record; its
+    // footprint is marked in the contention bitplanes
     for (uint32_t base = 0; base < n; base += nthreads) {
         const uint32_t k = base + gtid;
         uint4 rec = make_uint4(0, 0, 0, 0);
@@ -241,15 +269,49 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         if (k < n) {
             rec = make_record(a, a.seed_list[k], s_bp);
             take = (rec.z >> 28) & 7u;
+            if (take) {
+                int cx[5], cy[5];
+                const int m = record_path(a, rec, s_bp, cx, cy);
+                mark_cell(a, (int)(rec.z & 0x0FFFFFFFu), (int)(rec.w & 0x00FFFFFFu));
+                for (int i = 0; i < m; ++i) mark_cell(a, cx[i], cy[i]);
+            }
         }
         append(&a.pcount[0], a.rec[0], take, rec);
+    }
+    grid.sync();
+    // movers whose footprint no other mover touches walk now, in any order (nothing they read
+    // or write is touched by anyone else); the rest go to the reservation rounds
+    {
+        const unsigned np0 = __ldcg(&a.pcount[0]);
+        unsigned long long hops = 0;
+        for (unsigned base = 0; base < np0; base += nthreads) {
+            const unsigned k = base + gtid;
+            bool contended = false;
+            uint4 rec = make_uint4(0, 0, 0, 0);
+            if (k < np0) {
+                rec = __ldcg(&a.rec[0][k]);
+                int cx[5], cy[5];
+                const int m = record_path(a, rec, s_bp, cx, cy);
+                const int sx = (int)(rec.z & 0x0FFFFFFFu), sy = (int)(rec.w & 0x00FFFFFFu);
+                contended = (__ldcg(&a.p2[a.g.word(sx, sy)]) >> (sx & 31)) & 1u;
+                for (int i = 0; i < m && !contended; ++i)
+                    contended = (__ldcg(&a.p2[a.g.word(cx[i], cy[i])]) >> (cx[i] & 31)) & 1u;
+                if (!contended) {
+                    walk_owned(a, rec, cx, cy, m, &hops);
+                    clear_cell(a, sx, sy, false);
+                    for (int i = 0; i < m; ++i) clear_cell(a, cx[i], cy[i], false);
+                }
+            }
+            append(&a.pcount[1], a.rec[1], contended, rec);
+        }
+        flush_hops(a.sc, hops);
     }
     grid.sync();
     if (gtid == 0) a.sc->t_motion[1] = globaltimer();
     unsigned r = 0;
     bool solo = false;
     for (;; ++r) {
-        const unsigned cur = r & 1, nxt = cur ^ 1;
+        const unsigned cur = (r + 1) & 1, nxt = cur ^ 1;
         const unsigned np = __ldcg(&a.pcount[cur]);
         if (np == 0) break;
         if (!solo && np <= MOVE_TAIL) {
@@ -311,6 +373,11 @@ int fp_ensure_res(fp_ctx* ctx) {
         g_bpath_ready[ctx->device] = true;
     }
     if (ctx->d_res) return FP_OK;
+    const size_t nwords = (size_t)ctx->P * ctx->H;
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_p1, nwords * 4));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_p2, nwords * 4));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
     const size_t cells = (size_t)ctx->W * (size_t)ctx->H;
     FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned int)));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned int), ctx->stream));
@@ -348,6 +415,8 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.pcount = (unsigned int*)ctx->d_counters;  // [0], [1] as u32 (kept zero between phases)
     a.sc = ctx->d_sc;
     a.exits = ctx->d_exits;
+    a.p1 = ctx->d_p1;
+    a.p2 = ctx->d_p2;
     const unsigned blocks = (unsigned)std::min<size_t>((size_t)g_move_blocks,
                                                         std::max<size_t>(1, fp_blocks(ctx->n, MOVE_THREADS)));
     cudaLaunchConfig_t cfg = {};
