@@ -135,7 +135,8 @@ static void free_agents(fp_ctx* c) {
     void* ptrs[] = {c->d_x, c->d_y, c->d_dx, c->d_dy, c->d_v, c->d_alive, c->d_rank, c->d_alive_ids,
                     c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
                     c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted,
-                    c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback, c->d_rec_a, c->d_rec_b};
+                    c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback, c->d_rec_a, c->d_rec_b,
+                    c->d_rec0};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->d_x = c->d_y = c->d_dx = c->d_dy = nullptr;
@@ -143,8 +144,10 @@ static void free_agents(fp_ctx* c) {
     c->d_rank = c->d_alive_ids = c->d_order = c->d_j = c->d_cnt = c->d_off = c->d_cursor = nullptr;
     c->d_bucket = c->d_succ = c->d_nxt = c->d_V = c->d_pend_a = c->d_pend_b = nullptr;
     c->d_exits = c->d_exits_sorted = nullptr;
-    c->d_fy_bucket = c->d_flags = c->d_cursor_b = c->d_fallback = nullptr;
-    c->d_rec_a = c->d_rec_b = nullptr;
+    c->d_fy_bucket = c->d_flags = c->d_cursor_b = nullptr;
+    c->d_fallback = nullptr;
+    c->d_rec_a = c->d_rec_b = c->d_rec0 = nullptr;
+    c->rec_fresh = false;
     c->cap = 0;
     c->graph_valid = false;
 }
@@ -161,12 +164,14 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
     FP_CUDA(c, cudaMalloc(&c->d_alive, m));
     uint32_t** u32s[] = {&c->d_rank, &c->d_alive_ids, &c->d_order, &c->d_j, &c->d_cnt, &c->d_off,
                          &c->d_cursor, &c->d_bucket, &c->d_succ, &c->d_nxt, &c->d_V, &c->d_pend_a,
-                         &c->d_pend_b, &c->d_fy_bucket, &c->d_flags, &c->d_cursor_b, &c->d_fallback};
+                         &c->d_pend_b, &c->d_fy_bucket, &c->d_flags, &c->d_cursor_b};
     for (uint32_t** p : u32s) FP_CUDA(c, cudaMalloc(p, m * 4));
     FP_CUDA(c, cudaMalloc(&c->d_exits, m * 8));
     FP_CUDA(c, cudaMalloc(&c->d_exits_sorted, m * 8));
     FP_CUDA(c, cudaMalloc(&c->d_rec_a, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_rec_b, m * sizeof(uint4)));
+    FP_CUDA(c, cudaMalloc(&c->d_rec0, m * sizeof(uint4)));
+    FP_CUDA(c, cudaMalloc(&c->d_fallback, m * sizeof(uint2)));
     c->cap = (uint32_t)m;
     return FP_OK;
 }
@@ -339,6 +344,7 @@ static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const ui
         al = n;
     c->alive = al;
     c->bucket_fresh = false;
+    c->rec_fresh = false;
     if (int rc = fp_ghost_occ(c)) return rc;
     return sync_scalars(c);
 }
@@ -404,6 +410,7 @@ extern "C" int fp_set_desired(fp_ctx* c, const int32_t* x, const int32_t* y) {
     cudaSetDevice(c->device);
     FP_CUDA(c, cudaMemcpyAsync(c->d_dx, x, (size_t)c->n * 4, cudaMemcpyHostToDevice, c->stream));
     FP_CUDA(c, cudaMemcpyAsync(c->d_dy, y, (size_t)c->n * 4, cudaMemcpyHostToDevice, c->stream));
+    c->rec_fresh = false;  // the plan's walk records no longer describe the desired cells
     FP_CUDA(c, cudaStreamSynchronize(c->stream));
     return FP_OK;
 }

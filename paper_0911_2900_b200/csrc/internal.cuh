@@ -181,9 +181,12 @@ struct fp_ctx {
 
     // motion scratch
     uint32_t *d_pend_a = nullptr, *d_pend_b = nullptr;
-    uint32_t* d_fallback = nullptr;  // agents the plan kernel hands to the exact path
+    uint2* d_fallback = nullptr;  // (id, bucket position) the plan kernel hands to the exact path
     uint4 *d_rec_a = nullptr, *d_rec_b = nullptr;  // motion pending records (move.cu)
+    uint4* d_rec0 = nullptr;    // walk records in plan-tile order, emitted by the plan phase
     bool bucket_fresh = false;  // plan-tile buckets match the current positions
+    bool rec_fresh = false;     // d_rec0 + contention marks match the current desired cells
+    bool marks_dirty = false;   // contention bitplanes hold marks no motion phase consumed
     unsigned long long* d_exits = nullptr;  // (rank << 32 | id) records of the last move
     unsigned long long* d_exits_sorted = nullptr;
     int64_t last_displacement = 0;

@@ -1,0 +1,115 @@
+// motion_rec.cuh -- the motion phase's per-agent record and contention marks, shared by the plan
+// kernel (which emits them right after choosing the desired cell, in plan-tile order) and the
+// motion kernel (which consumes them, or builds them itself when the plan did not).
+//
+// A walk (engine.hpp:116-119) of agent id from its cell toward its desired cell visits at most
+// v_max Bresenham cells, stops before a Wall and ends at an Exit; everything else that can stop
+// it is occupancy.  Record (16 bytes):
+//     x = id,  y = rank (filled by the motion phase),
+//     z = px | m << 28 | exit_at_end << 31      (m = static walk length, 0..5)
+//     w = py | o << 24 | generic << 31          (o = (dy+5)*11 + dx+5 of the target offset;
+//                                                generic: target farther than 5 cells, the path
+//                                                is re-derived from the agent arrays)
+// Contention marks: P1 = cell in some mover's footprint, P2 = in two or more.
+#pragma once
+
+#include "internal.cuh"
+
+#define REC_GENERIC 0x80000000u
+
+// Bresenham cells of the segment (0,0) -> each offset of the 11x11 frame, in walk order.
+static inline void host_bpath(signed char out[121][5][2]) {
+    for (int ty = -5; ty <= 5; ++ty)
+        for (int tx = -5; tx <= 5; ++tx) {
+            signed char(*p)[2] = out[(ty + 5) * 11 + tx + 5];
+            for (int j = 0; j < 5; ++j) p[j][0] = p[j][1] = 0;
+            const int adx = abs(tx), sx = 0 < tx ? 1 : -1;
+            const int ady = -abs(ty), sy = 0 < ty ? 1 : -1;
+            int err = adx + ady, x = 0, y = 0, j = 0;
+            while (!(x == tx && y == ty)) {
+                const int e2 = 2 * err;
+                if (e2 >= ady) { err += ady; x += sx; }
+                if (e2 <= adx) { err += adx; y += sy; }
+                p[j][0] = (signed char)x;
+                p[j][1] = (signed char)y;
+                ++j;
+            }
+        }
+}
+
+// Record of a walk from (sx, sy) to (tx, ty) (both wrapped), cap v.
+__device__ __forceinline__ uint4 record_of(const Geo& g, uint32_t id, int sx, int sy, int tx, int ty, int v,
+                                           const signed char (*bp)[5][2]) {
+    const int ddx = g.segment_dx(sx, tx), ddy = ty - sy;
+    int m = 0;
+    bool ex = false;
+    uint32_t w;
+    if (abs(ddx) <= 5 && abs(ddy) <= 5) {
+        const int o = (ddy + 5) * 11 + ddx + 5;
+        const int len = min(max(abs(ddx), abs(ddy)), v);
+        for (int j = 0; j < len; ++j) {
+            const int x = g.wrap(sx + bp[o][j][0]), y = sy + bp[o][j][1];
+            if (g.is_wall(x, y)) break;
+            ++m;
+            if (g.is_exit(x, y)) {
+                ex = true;
+                break;
+            }
+        }
+        w = (uint32_t)sy | ((uint32_t)o << 24);
+    } else {
+        Bres b;
+        b.init(g, sx, sy, tx, ty);
+        while (!b.done() && m < v) {
+            b.next();
+            const int x = g.wrap(b.x), y = b.y;
+            if (g.is_wall(x, y)) break;
+            ++m;
+            if (g.is_exit(x, y)) {
+                ex = true;
+                break;
+            }
+        }
+        w = (uint32_t)sy | REC_GENERIC;
+    }
+    return make_uint4(id, 0u, (uint32_t)sx | ((uint32_t)m << 28) | (ex ? 0x80000000u : 0u), w);
+}
+
+// Footprint path cells of a record (at most 5); generic records re-walk toward (gtx, gty).
+__device__ __forceinline__ int record_cells(const Geo& g, const uint4& r, const signed char (*bp)[5][2], int gtx,
+                                            int gty, int* cx, int* cy) {
+    const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
+    const int m = (int)((r.z >> 28) & 7u);
+    if (!(r.w & REC_GENERIC)) {
+        const int o = (int)((r.w >> 24) & 0x7Fu);
+        for (int j = 0; j < m; ++j) {
+            cx[j] = g.wrap(sx + bp[o][j][0]);
+            cy[j] = sy + bp[o][j][1];
+        }
+    } else {
+        Bres b;
+        b.init(g, sx, sy, gtx, gty);
+        for (int j = 0; j < m; ++j) {
+            b.next();
+            cx[j] = g.wrap(b.x);
+            cy[j] = b.y;
+        }
+    }
+    return m;
+}
+
+__device__ __forceinline__ void mark_cell(uint32_t* p1, uint32_t* p2, const Geo& g, int x, int y) {
+    const size_t w = g.word(x, y);
+    const uint32_t bit = 1u << (x & 31);
+    if (atomicOr(&p1[w], bit) & bit) atomicOr(&p2[w], bit);
+}
+
+// Marks the footprint (start + path) of a record with m > 0.
+__device__ __forceinline__ void mark_record(uint32_t* p1, uint32_t* p2, const Geo& g, const uint4& r,
+                                            const signed char (*bp)[5][2], int gtx, int gty) {
+    int cx[5], cy[5];
+    const int m = record_cells(g, r, bp, gtx, gty, cx, cy);
+    if (m == 0) return;
+    mark_cell(p1, p2, g, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu));
+    for (int i = 0; i < m; ++i) mark_cell(p1, p2, g, cx[i], cy[i]);
+}

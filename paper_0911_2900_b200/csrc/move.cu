@@ -4,60 +4,35 @@
 // each walks the Bresenham segment to its desired cell, at most v_max hops, stopping before a
 // Wall or an occupied cell; an Exit removes it.  Later agents see earlier agents' final cells.
 //
-// Parallel form (deterministic reservations): an agent's footprint is its start cell plus the
-// path cells it could visit (capped at v_max, cut before a Wall, ending at an Exit).  Only
-// agents with overlapping footprints can influence each other, and only through those cells.
-// Each round, every pending agent writes its rank into its footprint cells with atomicMin; an
-// agent that holds all of its cells is the earliest pending agent on each of them, so
-// everything that precedes it in the reference order on those cells has already run -- it
-// executes its walk now and clears its cells back to "free".  Committed agents in one round
-// have disjoint footprints.  Keys left behind by agents still pending are harmless (they are
-// re-asserted with the same priority next round), so the reservation plane (u32 per cell) needs
-// neither round stamps nor resets and is all-free again when the phase ends.  The result equals
-// the sequential walk bit for bit (tests/test_gpu_parity.py).  Agents with an empty path (staying
-// put) never change occupancy and skip the rounds entirely.
+// Parallel form.  An agent's footprint is its start cell plus the path cells it could visit
+// (motion_rec.cuh).  Only agents with overlapping footprints can influence each other, and only
+// through those cells.
+//   1. Contention marks (P1/P2 bitplanes) over every mover's footprint -- emitted by the plan
+//      kernel together with the records, or built here when the plan did not.
+//   2. A mover none of whose cells is marked twice walks immediately: nobody else reads or
+//      writes its cells, so its position in the order is irrelevant.
+//   3. The rest resolve in deterministic-reservation rounds: every pending agent writes its rank
+//      into its footprint cells with atomicMin; an agent that holds all of its cells is the
+//      earliest pending agent on each of them, so everything that precedes it in the reference
+//      order on those cells has already run -- it walks now and clears its cells.  Keys left by
+//      agents still pending are re-asserted with the same priority next round, so the u32
+//      reservation plane needs no stamps or resets and ends every phase all-free.
+// The result equals the sequential walk bit for bit (tests/test_gpu_parity.py).
 //
-// Data path: a seed pass walks the alive agents in plan-tile order (spatial locality for the
-// reservation, occupancy and bitplane traffic), resolves each walk's static stops once, and
-// writes a 16-byte pending record {id, rank, x|m|exit, y|offset}; the rounds then touch only
-// the records, the reservation plane and the occupancy bits -- the path cells come from a
-// per-offset Bresenham table.  One cooperative launch runs all rounds of a step: grid-wide
-// rounds (grid.sync between reserve and commit) while many agents are pending, then block 0
-// finishes the tail alone.
+// One cooperative launch runs a whole phase: grid-wide stages (grid.sync between them) while
+// many agents are pending, then block 0 finishes the tail alone with __syncthreads.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
-#include "internal.cuh"
+#include "motion_rec.cuh"
 
 namespace cg = cooperative_groups;
 
 #define MOVE_THREADS 512
 #define MOVE_TAIL 4096  // pending agents at or below which block 0 runs the rounds alone
 
-// Bresenham cells (dx, dy) of the segment from (0,0) to each offset of the 11x11 frame,
-// index (dy+5)*11 + dx+5, in walk order (world.hpp:143-167); host-built, copied per launch to
-// shared memory.
 __constant__ signed char c_bpath[121][5][2];
 static bool g_bpath_ready[64] = {false};
-
-static void host_bpath(signed char out[121][5][2]) {
-    for (int ty = -5; ty <= 5; ++ty)
-        for (int tx = -5; tx <= 5; ++tx) {
-            signed char(*p)[2] = out[(ty + 5) * 11 + tx + 5];
-            for (int j = 0; j < 5; ++j) p[j][0] = p[j][1] = 0;
-            const int adx = abs(tx), sx = 0 < tx ? 1 : -1;
-            const int ady = -abs(ty), sy = 0 < ty ? 1 : -1;
-            int err = adx + ady, x = 0, y = 0, j = 0;
-            while (!(x == tx && y == ty)) {
-                const int e2 = 2 * err;
-                if (e2 >= ady) { err += ady; x += sx; }
-                if (e2 <= adx) { err += adx; y += sy; }
-                p[j][0] = (signed char)x;
-                p[j][1] = (signed char)y;
-                ++j;
-            }
-        }
-}
 
 struct MoveArgs {
     Geo g;
@@ -70,85 +45,16 @@ struct MoveArgs {
     const uint8_t* v;
     uint8_t* alive;
     const uint32_t* rank;
-    const uint32_t* seed_list;     // alive ids (plan-tile order when fresh, else movement order)
+    const uint32_t* seed_list;     // mode B: alive ids to build records from
+    const uint4* rec0;             // mode A: records emitted by the plan kernel (n_alive of them)
+    int premade;                   // 1: mode A, 0: mode B
     uint4* rec[2];                 // pending records, ping-pong
     unsigned int* pcount;          // [2] pending counts (device scratch, zero between phases)
     DevScalars* sc;
     unsigned long long* exits;     // (rank << 32 | id)
-    uint32_t* p1;                  // contention bitplanes (touched once / twice+), zero between phases
+    uint32_t* p1;                  // contention bitplanes, zero between phases
     uint32_t* p2;
 };
-
-// Pending record: x = id, y = rank, z = px | m << 28 | exit_at_end << 31,
-// w = py | o << 24 | generic << 31  (o: frame offset of the walk's target; generic: the target is
-// farther than 5 cells and the path is re-derived from the agent arrays).
-#define REC_GENERIC 0x80000000u
-
-// Static walk of agent `id` (engine.hpp:116-119): first <= v_max Bresenham cells, cut before a
-// Wall, ending at an Exit.  Returns the record; m = 0 means the agent does not move at all.
-__device__ __forceinline__ uint4 make_record(const MoveArgs& a, uint32_t id, const signed char (*bp)[5][2]) {
-    const Geo& g = a.g;
-    const int sx = g.wrap(a.x[id]), sy = a.y[id];
-    const int tx = g.wrap(a.dx[id]), ty = a.dy[id];
-    const int v = a.v[id];
-    const int ddx = g.segment_dx(sx, tx), ddy = ty - sy;
-    int m = 0;
-    bool ex = false;
-    uint32_t w;
-    if (abs(ddx) <= 5 && abs(ddy) <= 5) {
-        const int o = (ddy + 5) * 11 + ddx + 5;
-        const int len = min(max(abs(ddx), abs(ddy)), v);
-        for (int j = 0; j < len; ++j) {
-            const int x = g.wrap(sx + bp[o][j][0]), y = sy + bp[o][j][1];
-            if (g.is_wall(x, y)) break;
-            ++m;
-            if (g.is_exit(x, y)) {
-                ex = true;
-                break;
-            }
-        }
-        w = (uint32_t)sy | ((uint32_t)o << 24);
-    } else {
-        Bres b;
-        b.init(g, sx, sy, tx, ty);
-        while (!b.done() && m < v) {
-            b.next();
-            const int x = g.wrap(b.x), y = b.y;
-            if (g.is_wall(x, y)) break;
-            ++m;
-            if (g.is_exit(x, y)) {
-                ex = true;
-                break;
-            }
-        }
-        w = (uint32_t)sy | REC_GENERIC;
-    }
-    return make_uint4(id, a.rank[id], (uint32_t)sx | ((uint32_t)m << 28) | (ex ? 0x80000000u : 0u), w);
-}
-
-// The footprint path cells of a record (at most 5).
-__device__ __forceinline__ int record_path(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2], int* cx,
-                                           int* cy) {
-    const Geo& g = a.g;
-    const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
-    const int m = (int)((r.z >> 28) & 7u);
-    if (!(r.w & REC_GENERIC)) {
-        const int o = (int)((r.w >> 24) & 0x7Fu);
-        for (int j = 0; j < m; ++j) {
-            cx[j] = g.wrap(sx + bp[o][j][0]);
-            cy[j] = sy + bp[o][j][1];
-        }
-    } else {
-        Bres b;
-        b.init(g, sx, sy, g.wrap(a.dx[r.x]), a.dy[r.x]);
-        for (int j = 0; j < m; ++j) {
-            b.next();
-            cx[j] = g.wrap(b.x);
-            cy[j] = b.y;
-        }
-    }
-    return m;
-}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -164,6 +70,16 @@ __device__ __forceinline__ bool occ_test(const MoveArgs& a, int x, int y) {
     return (__ldcg(&a.occ[a.g.word(x, y)]) >> (x & 31)) & 1u;
 }
 
+__device__ __forceinline__ int path_of(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2], int* cx,
+                                       int* cy) {
+    int gtx = 0, gty = 0;
+    if (r.w & REC_GENERIC) {
+        gtx = a.g.wrap(a.dx[r.x]);
+        gty = a.dy[r.x];
+    }
+    return record_cells(a.g, r, bp, gtx, gty, cx, cy);
+}
+
 __device__ __forceinline__ void append(unsigned int* count, uint4* list, bool take, const uint4& rec) {
     const unsigned mask = __ballot_sync(0xffffffffu, take);
     if (!mask) return;
@@ -175,12 +91,11 @@ __device__ __forceinline__ void append(unsigned int* count, uint4* list, bool ta
     if (take) list[base + __popc(mask & ((1u << lane) - 1))] = rec;
 }
 
-__device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2]) {
-    const unsigned int key = r.y;
-    int cx[5], cy[5];
-    const int m = record_path(a, r, bp, cx, cy);
-    atomicMin(&a.res[cell_index(a.g, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu))], key);
-    for (int i = 0; i < m; ++i) atomicMin(&a.res[cell_index(a.g, cx[i], cy[i])], key);
+__device__ __forceinline__ void clear_cell(const MoveArgs& a, int x, int y, bool both) {
+    const size_t w = a.g.word(x, y);
+    const uint32_t nbit = ~(1u << (x & 31));
+    atomicAnd(&a.p1[w], nbit);
+    if (both) atomicAnd(&a.p2[w], nbit);
 }
 
 // The walk (engine.hpp:116-129) of an agent that owns its footprint, net effect on occupancy.
@@ -202,7 +117,8 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
         if (exited) {
             a.alive[id] = 0;
             const unsigned long long slot = atomicAdd(&a.sc->n_exits, 1ull);
-            a.exits[slot] = ((unsigned long long)r.y << 32) | id;
+            // processing order = rank (uncontended walkers never loaded theirs into the record)
+            a.exits[slot] = ((unsigned long long)a.rank[id] << 32) | id;
         } else {
             atomicOr(&a.occ[a.g.word(fx, fy)], 1u << (fx & 31));
         }
@@ -210,32 +126,24 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
     *hops_acc += (unsigned long long)h;
 }
 
-// Footprint marking: P1 = touched by some mover, P2 = touched by two or more movers.
-__device__ __forceinline__ void mark_cell(const MoveArgs& a, int x, int y) {
-    const size_t w = a.g.word(x, y);
-    const uint32_t bit = 1u << (x & 31);
-    if (atomicOr(&a.p1[w], bit) & bit) atomicOr(&a.p2[w], bit);
-}
-
-__device__ __forceinline__ void clear_cell(const MoveArgs& a, int x, int y, bool both) {
-    const size_t w = a.g.word(x, y);
-    const uint32_t nbit = ~(1u << (x & 31));
-    atomicAnd(&a.p1[w], nbit);
-    if (both) atomicAnd(&a.p2[w], nbit);
+__device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2]) {
+    int cx[5], cy[5];
+    const int m = path_of(a, r, bp, cx, cy);
+    atomicMin(&a.res[cell_index(a.g, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu))], r.y);
+    for (int i = 0; i < m; ++i) atomicMin(&a.res[cell_index(a.g, cx[i], cy[i])], r.y);
 }
 
 // Returns true if the agent committed (walked); false if it must retry next round.
 __device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
                                            unsigned long long* hops_acc) {
-    const unsigned int key = r.y;
     const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
     int cx[5], cy[5];
-    const int m = record_path(a, r, bp, cx, cy);
-    bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == key;
-    for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == key;
+    const int m = path_of(a, r, bp, cx, cy);
+    bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == r.y;
+    for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == r.y;
     if (!own) return false;
-    // release the footprint: losers of this round read it after their own failed check only;
-    // the contention bits go back to zero for the next phase
+    // release the footprint (losers of this round read it after their own failed check only)
+    // and its contention bits (zero again for the next phase)
     a.res[cell_index(a.g, sx, sy)] = 0xFFFFFFFFu;
     clear_cell(a, sx, sy, true);
     for (int i = 0; i < m; ++i) {
@@ -251,6 +159,25 @@ __device__ __forceinline__ void flush_hops(DevScalars* sc, unsigned long long ho
     if ((threadIdx.x & 31) == 0 && hops) atomicAdd(&sc->disp, hops);
 }
 
+// Step 2 for one record: walk now if uncontended, else hand it (with its rank) to the rounds.
+__device__ __forceinline__ bool classify(const MoveArgs& a, uint4& rec, const signed char (*bp)[5][2],
+                                         unsigned long long* hops) {
+    int cx[5], cy[5];
+    const int m = path_of(a, rec, bp, cx, cy);
+    const int sx = (int)(rec.z & 0x0FFFFFFFu), sy = (int)(rec.w & 0x00FFFFFFu);
+    bool contended = (__ldcg(&a.p2[a.g.word(sx, sy)]) >> (sx & 31)) & 1u;
+    for (int i = 0; i < m && !contended; ++i)
+        contended = (__ldcg(&a.p2[a.g.word(cx[i], cy[i])]) >> (cx[i] & 31)) & 1u;
+    if (!contended) {
+        walk_owned(a, rec, cx, cy, m, hops);
+        clear_cell(a, sx, sy, false);
+        for (int i = 0; i < m; ++i) clear_cell(a, cx[i], cy[i], false);
+        return false;
+    }
+    rec.y = a.rank[rec.x];
+    return true;
+}
+
 __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ signed char s_bp[121][5][2];
@@ -260,47 +187,51 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = (uint32_t)__ldcg(&a.sc->n_alive);
     if (gtid == 0) a.sc->t_motion[0] = globaltimer();
-    // seed: every alive agent whose walk has at least one cell, as a pending record; its
-    // footprint is marked in the contention bitplanes
-    for (uint32_t base = 0; base < n; base += nthreads) {
-        const uint32_t k = base + gtid;
-        uint4 rec = make_uint4(0, 0, 0, 0);
-        bool take = false;
-        if (k < n) {
-            rec = make_record(a, a.seed_list[k], s_bp);
-            take = (rec.z >> 28) & 7u;
-            if (take) {
-                int cx[5], cy[5];
-                const int m = record_path(a, rec, s_bp, cx, cy);
-                mark_cell(a, (int)(rec.z & 0x0FFFFFFFu), (int)(rec.w & 0x00FFFFFFu));
-                for (int i = 0; i < m; ++i) mark_cell(a, cx[i], cy[i]);
+    const uint4* cand = a.rec0;
+    unsigned ncand = n;
+    if (!a.premade) {
+        // step 1 here: records of every mover, footprints marked
+        for (uint32_t base = 0; base < n; base += nthreads) {
+            const uint32_t k = base + gtid;
+            uint4 rec = make_uint4(0, 0, 0, 0);
+            bool take = false;
+            if (k < n) {
+                const uint32_t id = a.seed_list[k];
+                const int tx = a.g.wrap(a.dx[id]), ty = a.dy[id];
+                rec = record_of(a.g, id, a.g.wrap(a.x[id]), a.y[id], tx, ty, a.v[id], s_bp);
+                take = (rec.z >> 28) & 7u;
+                if (take) mark_record(a.p1, a.p2, a.g, rec, s_bp, tx, ty);
+            }
+            append(&a.pcount[0], a.rec[0], take, rec);
+        }
+        grid.sync();
+        cand = a.rec[0];
+        ncand = __ldcg(&a.pcount[0]);
+    } else {
+        // step 1 over the plan's records (coalesced, plan-tile order)
+        for (uint32_t k = gtid; k < n; k += nthreads) {
+            const uint4 rec = __ldcg(&a.rec0[k]);
+            if ((rec.z >> 28) & 7u) {
+                int gtx = 0, gty = 0;
+                if (rec.w & REC_GENERIC) {
+                    gtx = a.g.wrap(a.dx[rec.x]);
+                    gty = a.dy[rec.x];
+                }
+                mark_record(a.p1, a.p2, a.g, rec, s_bp, gtx, gty);
             }
         }
-        append(&a.pcount[0], a.rec[0], take, rec);
+        grid.sync();
     }
-    grid.sync();
-    // movers whose footprint no other mover touches walk now, in any order (nothing they read
-    // or write is touched by anyone else); the rest go to the reservation rounds
+    // step 2
     {
-        const unsigned np0 = __ldcg(&a.pcount[0]);
         unsigned long long hops = 0;
-        for (unsigned base = 0; base < np0; base += nthreads) {
+        for (unsigned base = 0; base < ncand; base += nthreads) {
             const unsigned k = base + gtid;
             bool contended = false;
             uint4 rec = make_uint4(0, 0, 0, 0);
-            if (k < np0) {
-                rec = __ldcg(&a.rec[0][k]);
-                int cx[5], cy[5];
-                const int m = record_path(a, rec, s_bp, cx, cy);
-                const int sx = (int)(rec.z & 0x0FFFFFFFu), sy = (int)(rec.w & 0x00FFFFFFu);
-                contended = (__ldcg(&a.p2[a.g.word(sx, sy)]) >> (sx & 31)) & 1u;
-                for (int i = 0; i < m && !contended; ++i)
-                    contended = (__ldcg(&a.p2[a.g.word(cx[i], cy[i])]) >> (cx[i] & 31)) & 1u;
-                if (!contended) {
-                    walk_owned(a, rec, cx, cy, m, &hops);
-                    clear_cell(a, sx, sy, false);
-                    for (int i = 0; i < m; ++i) clear_cell(a, cx[i], cy[i], false);
-                }
+            if (k < ncand) {
+                rec = __ldcg(&cand[k]);
+                if ((rec.z >> 28) & 7u) contended = classify(a, rec, s_bp, &hops);
             }
             append(&a.pcount[1], a.rec[1], contended, rec);
         }
@@ -308,6 +239,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     }
     grid.sync();
     if (gtid == 0) a.sc->t_motion[1] = globaltimer();
+    // step 3
     unsigned r = 0;
     bool solo = false;
     for (;; ++r) {
@@ -381,18 +313,26 @@ int fp_ensure_res(fp_ctx* ctx) {
     const size_t cells = (size_t)ctx->W * (size_t)ctx->H;
     FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned int)));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned int), ctx->stream));
+    ctx->marks_dirty = false;
     return FP_OK;
 }
 
 static int g_move_blocks = 0;
 
 // Enqueues one motion phase (after fp_order_launch) on ctx->stream.  Graph-safe.
-// `spatial`: the plan-tile buckets are current (seed in spatial order); else movement order.
+// Mode A (ctx->rec_fresh): the plan kernel emitted records + marks for the current state.
+// Mode B: records are built here from the plan-tile buckets when current, else the order list.
 int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     cudaStream_t s = ctx->stream;
     move_begin_kernel<<<1, 1, 0, s>>>(ctx->d_sc);
     FP_LAUNCHED(ctx);
     if (ctx->n == 0) return FP_OK;
+    const bool premade = ctx->rec_fresh;
+    if (!premade && ctx->marks_dirty) {  // marks of records that were never consumed
+        const size_t nwords = (size_t)ctx->P * ctx->H;
+        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, s));
+        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, s));
+    }
     if (!g_move_blocks) {
         int per_sm = 0;
         FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS, 0));
@@ -410,6 +350,8 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.alive = ctx->d_alive;
     a.rank = ctx->d_rank;
     a.seed_list = spatial ? ctx->d_bucket : ctx->d_order;
+    a.rec0 = ctx->d_rec0;
+    a.premade = premade ? 1 : 0;
     a.rec[0] = ctx->d_rec_a;
     a.rec[1] = ctx->d_rec_b;
     a.pcount = (unsigned int*)ctx->d_counters;  // [0], [1] as u32 (kept zero between phases)
@@ -431,6 +373,8 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     cfg.numAttrs = 1;
     FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel, a));
     ctx->ctr.kernel_launches++;
+    ctx->rec_fresh = false;
+    ctx->marks_dirty = false;
     return fp_ghost_occ(ctx);
 }
 

@@ -28,8 +28,12 @@
 
 #include "fp_exp.h"
 #include "internal.cuh"
+#include "motion_rec.cuh"
 
 #define FP_GUARD 1.5e-7
+
+// Walk records (motion_rec.cuh): the plan emits them for the motion phase.
+__constant__ signed char c_bpath_p[121][5][2];
 
 // Bresenham path masks over the 11x11 offset frame (bit (dy+5)*11 + dx+5): the cells strictly
 // between (0,0) and (dx,dy) on the segment (world.hpp:143-167).
@@ -61,6 +65,9 @@ static int ensure_pathmasks(fp_ctx* ctx) {
     uint32_t pm[121][4];
     host_pathmasks(pm);
     FP_CUDA(ctx, cudaMemcpyToSymbol(c_pathmask, pm, sizeof(pm)));
+    signed char bp[121][5][2];
+    host_bpath(bp);
+    FP_CUDA(ctx, cudaMemcpyToSymbol(c_bpath_p, bp, sizeof(bp)));
     if (ctx->device < 64) g_pathmask_ready[ctx->device] = true;
     return FP_OK;
 }
@@ -235,7 +242,11 @@ struct TileArgs {
     int tile_w, tile_h, tiles_x;
     int use_tma;  // 0: stage the box with coalesced loads (debug / comparison path)
     int boxw, boxh, occw;  // shared-memory strides (words)
-    uint32_t* fallback;    // agents handed to plan_exact_list_kernel
+    uint2* fallback;       // (id, bucket position) handed to plan_exact_list_kernel
+    uint4* rec0;           // walk records in bucket order (motion_rec.cuh), when emit
+    uint32_t* p1;          // contention marks
+    uint32_t* p2;
+    int emit;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -456,6 +467,8 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     __shared__ volatile int s_gen[2];
     __shared__ int s_done[2];
     __shared__ double s_drive[11];
+    __shared__ signed char s_bp[121][5][2];
+    for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath_p[0][0][0])[k];
     const PlanCommon& a = A.c;
     const uint64_t step = (uint64_t)a.sc->step;
     const int n_tiles = (int)a.sc->n_tiles;
@@ -567,8 +580,9 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
             if (st == 1) {
                 a.dx[id] = cx;
                 a.dy[id] = cy;
+                if (A.emit) A.rec0[off + k] = record_of(a.g, id, px, py, cx, cy, v, s_bp);  // motion's walk record
             } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
-                A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = id;
+                A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, (uint32_t)(off + k));
             }
             ++mine;
         }
@@ -589,14 +603,29 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
 // the exact weights (restated glibc exp); lane 0 then folds the weights serially in list order
 // (sample_index, planning.hpp:63-73).  Narrow periodic grids (2v+1 > W-?) use choose_exact.
 #define EXACT_WARPS 4
-__global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanCommon a, const uint32_t* list) {
+struct EmitArgs {
+    uint4* rec0;
+    uint32_t* p1;
+    uint32_t* p2;
+    int emit;
+};
+
+__device__ __forceinline__ void emit_record(const PlanCommon& a, const EmitArgs& E, uint32_t id, uint32_t pos, int px,
+                                            int py, int cx, int cy, int v) {
+    if (!E.emit) return;
+    E.rec0[pos] = record_of(a.g, id, px, py, cx, cy, v, c_bpath_p);
+}
+
+__global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanCommon a, const uint2* list,
+                                                                           EmitArgs E) {
     __shared__ double s_w[EXACT_WARPS][121];
     __shared__ int s_c[EXACT_WARPS][121];
     const unsigned n = (unsigned)a.sc->fb_count;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t step = (uint64_t)a.sc->step;
     for (unsigned e = blockIdx.x * EXACT_WARPS + warp; e < n; e += gridDim.x * EXACT_WARPS) {
-        const uint32_t id = list[e];
+        const uint2 ent = list[e];
+        const uint32_t id = ent.x;
         const int px = a.g.wrap(a.x[id]), py = a.y[id], v = a.v[id];
         const int D = 2 * v + 1;
         if (a.g.boundary == FP_BOUNDARY_PERIODIC_X && D >= a.g.W) {
@@ -605,6 +634,7 @@ __global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanC
                 choose_exact(a, id, step, &cx, &cy);
                 a.dx[id] = cx;
                 a.dy[id] = cy;
+                emit_record(a, E, id, ent.y, px, py, cx, cy, v);
             }
             continue;
         }
@@ -653,8 +683,10 @@ __global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanC
                     }
                 }
             const int cell = s_c[warp][pick];
-            a.dx[id] = cell % a.g.W;
-            a.dy[id] = cell / a.g.W;
+            const int cx = cell % a.g.W, cy = cell / a.g.W;
+            a.dx[id] = cx;
+            a.dy[id] = cy;
+            emit_record(a, E, id, ent.y, px, py, cx, cy, v);
         }
         __syncwarp();
     }
@@ -752,11 +784,17 @@ static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& s
     A.tile_h = ctx->tile_h;
     A.tiles_x = ctx->tiles_x;
     A.fallback = ctx->d_fallback;
+    A.rec0 = ctx->d_rec0;
+    A.p1 = ctx->d_p1;
+    A.p2 = ctx->d_p2;
+    A.emit = 1;
     tile_geometry(ctx, A, smem);
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
     grid = (unsigned)std::min<size_t>((size_t)ctx->sm_count, nt);
     return A;
 }
+
+static EmitArgs emit_args(const TileArgs& A) { return EmitArgs{A.rec0, A.p1, A.p2, A.emit}; }
 
 // Everything the planning phase allocates or builds, done outside any graph capture.
 int fp_plan_prepare(fp_ctx* ctx, double k_s) {
@@ -764,6 +802,7 @@ int fp_plan_prepare(fp_ctx* ctx, double k_s) {
     if (!tiled_ok(ctx)) return FP_OK;
     if (int rc = fp_plane_ensure(ctx, k_s)) return rc;
     if (int rc = fp_bucket_reserve(ctx)) return rc;
+    if (int rc = fp_ensure_res(ctx)) return rc;  // contention bitplanes the plan marks
     TileArgs A;
     size_t smem;
     tile_geometry(ctx, A, smem);
@@ -793,11 +832,13 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
         return fp_fail(ctx, FP_ERUNTIME, "plan: weight plane not prepared for this k_s");
     if (int rc = fp_bucket_launch(ctx)) return rc;
     ctx->bucket_fresh = true;  // the motion seed pass walks agents in this (spatial) order
+    ctx->rec_fresh = true;     // walk records + contention marks emitted below
+    ctx->marks_dirty = true;
     size_t smem;
     unsigned grid;
     const TileArgs A = make_tile_args(ctx, k_s, seed, smem, grid);
     if (int rc = launch_tile(ctx, A, smem, grid)) return rc;
-    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback);
+    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(A));
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -830,8 +871,11 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
         cudaEventElapsedTime(&t, e0, e1);
         total += t;
     }
+    // repeated launches marked the footprints many times: the next motion rebuilds its records
+    ctx->rec_fresh = false;
+    ctx->marks_dirty = true;
     // leave the state planned (the fallbacks of the last launch decided exactly)
-    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback);
+    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(A));
     FP_LAUNCHED(ctx);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
