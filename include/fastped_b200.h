@@ -83,6 +83,9 @@ typedef struct {
     int64_t motion_grid_ns;    /*   grid-wide rounds */
     int64_t motion_tail_ns;    /*   single-CTA tail rounds */
     int64_t motion_grid_rounds;/*   rounds run grid-wide in the last phase */
+    int64_t motion_mark_ns;    /*   of the seed pass: contention marking */
+    int64_t motion_contended;  /*   movers whose footprint overlapped another's */
+    int64_t motion_prep_ns;    /*   of the grid rounds: interning the contended footprints */
 } fp_counters;
 
 const char* fp_version(void);

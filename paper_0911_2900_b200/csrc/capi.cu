@@ -136,9 +136,10 @@ static void free_agents(fp_ctx* c) {
                     c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
                     c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted,
                     c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback, c->d_rec_a, c->d_rec_b,
-                    c->d_rec0};
+                    c->d_rec0, c->d_hkey, c->d_hres0, c->d_hres1, c->d_cslot};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    c->d_hkey = c->d_hres0 = c->d_hres1 = c->d_cslot = nullptr;
     c->d_x = c->d_y = c->d_dx = c->d_dy = nullptr;
     c->d_v = c->d_alive = nullptr;
     c->d_rank = c->d_alive_ids = c->d_order = c->d_j = c->d_cnt = c->d_off = c->d_cursor = nullptr;
@@ -172,7 +173,17 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
     FP_CUDA(c, cudaMalloc(&c->d_rec_b, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_rec0, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_fallback, m * sizeof(uint2)));
+    // motion hash: 2^hash_lg >= 12 m slots (six cells per agent at load factor <= 1/2)
+    c->hash_lg = 6;
+    while ((1ull << c->hash_lg) < 12ull * m) ++c->hash_lg;
+    const size_t hs = (size_t)1 << c->hash_lg;
+    for (uint32_t** p : {&c->d_hkey, &c->d_hres0, &c->d_hres1}) {
+        FP_CUDA(c, cudaMalloc(p, hs * 4));
+        FP_CUDA(c, cudaMemsetAsync(*p, 0xFF, hs * 4, c->stream));
+    }
+    FP_CUDA(c, cudaMalloc(&c->d_cslot, m * 6 * 4));
     c->cap = (uint32_t)m;
+    c->graph_valid = false;
     return FP_OK;
 }
 
@@ -253,7 +264,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->stream2) cudaStreamSynchronize(c->stream2);
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
-    void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_res, c->d_counters, c->d_temp, c->d_temp_b,
+    void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_counters, c->d_temp, c->d_temp_b,
                     c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sc, c->d_p1, c->d_p2};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -309,6 +320,13 @@ static int read_scalars(fp_ctx* c) {
         c->ctr.motion_seed_ns = (int64_t)(tm[1] - tm[0]);
         c->ctr.motion_grid_ns = (int64_t)(tm[2] - tm[1]);
         c->ctr.motion_tail_ns = (int64_t)(tm[3] - tm[2]);
+        const unsigned long long tk = c->h_sc->t_marked;
+        c->ctr.motion_mark_ns = tk >= tm[0] && tk <= tm[1] ? (int64_t)(tk - tm[0]) : 0;
+    }
+    c->ctr.motion_contended = (int64_t)c->h_sc->contended;
+    {
+        const unsigned long long tp = c->h_sc->t_prep;
+        c->ctr.motion_prep_ns = tp >= tm[1] && tp <= tm[2] ? (int64_t)(tp - tm[1]) : 0;
     }
     c->ctr.motion_grid_rounds = (int64_t)c->h_sc->grid_rounds;
     return FP_OK;

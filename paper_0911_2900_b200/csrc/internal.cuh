@@ -8,7 +8,8 @@
 //                             unreachable flag, and the fp32-mantissa / integer-exponent split of
 //                             2^(-k_s*log2(e)*S) (plane.cu).  Read by the plan kernel via TMA.
 //   field                   : fp64 per cell (StaticField::s), read only by the exact path
-//   reservation             : u64 per cell, round-stamped keys of the motion rounds
+//   motion scratch          : P1/P2 contention bitplanes (like occupancy); a cell -> slot hash
+//                             with two u32 reservation planes sized to the contended agents
 //   agents (SoA)            : x, y (i32), v_max (u8), alive (u8), desired x/y (i32), rank (u32)
 //   tile buckets            : agent ids grouped by plan tile (counting sort each step)
 #pragma once
@@ -121,7 +122,9 @@ struct DevScalars {
     unsigned long long fb_count;  // agents queued for the exact planning path this step
     unsigned long long t_motion[4];  // globaltimer: motion start, seed done, grid rounds done, end
     unsigned long long grid_rounds;  // rounds of the last motion phase run grid-wide
-    unsigned long long pad2[3];
+    unsigned long long t_marked;     // globaltimer: contention marks complete
+    unsigned long long contended;    // movers handed to the reservation rounds, last phase
+    unsigned long long t_prep;       // globaltimer: reservation hash built
 };
 
 struct fp_ctx {
@@ -139,7 +142,6 @@ struct fp_ctx {
     uint32_t* d_exit = nullptr;
     uint32_t* d_occ = nullptr;
     double* d_field = nullptr;
-    unsigned int* d_res = nullptr;  // motion reservations: rank of the reserving agent (move.cu)
     uint32_t *d_p1 = nullptr, *d_p2 = nullptr;  // motion contention bitplanes (move.cu)
 
     // weight plane (plane.cu), valid for (plane_ks, plane_potential, plane_gradient)
@@ -184,6 +186,10 @@ struct fp_ctx {
     uint2* d_fallback = nullptr;  // (id, bucket position) the plan kernel hands to the exact path
     uint4 *d_rec_a = nullptr, *d_rec_b = nullptr;  // motion pending records (move.cu)
     uint4* d_rec0 = nullptr;    // walk records in plan-tile order, emitted by the plan phase
+    // motion reservation rounds (move.cu): cell -> slot hash and two reservation planes over the
+    // slots (2^hash_lg each, H_EMPTY between phases), 6 slots per contended agent
+    uint32_t *d_hkey = nullptr, *d_hres0 = nullptr, *d_hres1 = nullptr, *d_cslot = nullptr;
+    int hash_lg = 0;
     bool bucket_fresh = false;  // plan-tile buckets match the current positions
     bool rec_fresh = false;     // d_rec0 + contention marks match the current desired cells
     bool marks_dirty = false;   // contention bitplanes hold marks no motion phase consumed

@@ -80,36 +80,47 @@ __device__ __forceinline__ int record_cells(const Geo& g, const uint4& r, const 
                                             int gty, int* cx, int* cy) {
     const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
     const int m = (int)((r.z >> 28) & 7u);
+    // fixed-trip predicated loops keep cx/cy in registers (callers index them the same way)
     if (!(r.w & REC_GENERIC)) {
         const int o = (int)((r.w >> 24) & 0x7Fu);
-        for (int j = 0; j < m; ++j) {
-            cx[j] = g.wrap(sx + bp[o][j][0]);
-            cy[j] = sy + bp[o][j][1];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            if (j < m) {
+                cx[j] = g.wrap(sx + bp[o][j][0]);
+                cy[j] = sy + bp[o][j][1];
+            }
         }
     } else {
         Bres b;
         b.init(g, sx, sy, gtx, gty);
-        for (int j = 0; j < m; ++j) {
-            b.next();
-            cx[j] = g.wrap(b.x);
-            cy[j] = b.y;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            if (j < m) {
+                b.next();
+                cx[j] = g.wrap(b.x);
+                cy[j] = b.y;
+            }
         }
     }
     return m;
 }
 
-__device__ __forceinline__ void mark_cell(uint32_t* p1, uint32_t* p2, const Geo& g, int x, int y) {
-    const size_t w = g.word(x, y);
-    const uint32_t bit = 1u << (x & 31);
-    if (atomicOr(&p1[w], bit) & bit) atomicOr(&p2[w], bit);
-}
-
-// Marks the footprint (start + path) of a record with m > 0.
+// Marks the footprint (start + path) of a record with m > 0: all P1 fetch-ORs in flight at once,
+// then the P2 marks (fire-and-forget) for cells some other footprint already held.
 __device__ __forceinline__ void mark_record(uint32_t* p1, uint32_t* p2, const Geo& g, const uint4& r,
                                             const signed char (*bp)[5][2], int gtx, int gty) {
-    int cx[5], cy[5];
-    const int m = record_cells(g, r, bp, gtx, gty, cx, cy);
+    int cx[6], cy[6];
+    const int m = record_cells(g, r, bp, gtx, gty, cx + 1, cy + 1);
     if (m == 0) return;
-    mark_cell(p1, p2, g, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu));
-    for (int i = 0; i < m; ++i) mark_cell(p1, p2, g, cx[i], cy[i]);
+    cx[0] = (int)(r.z & 0x0FFFFFFFu);
+    cy[0] = (int)(r.w & 0x00FFFFFFu);
+    uint32_t old[6];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+        if (i <= m) old[i] = atomicOr(&p1[g.word(cx[i], cy[i])], 1u << (cx[i] & 31));
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        const uint32_t bit = 1u << (cx[i] & 31);
+        if (i <= m && (old[i] & bit)) atomicOr(&p2[g.word(cx[i], cy[i])], bit);
+    }
 }

@@ -16,11 +16,13 @@
 //      earliest pending agent on each of them, so everything that precedes it in the reference
 //      order on those cells has already run -- it walks now and clears its cells.  Keys left by
 //      agents still pending are re-asserted with the same priority next round, so the u32
-//      reservation plane needs no stamps or resets and ends every phase all-free.
+//      reservation plane needs no stamps; the tail resets the keys of the agents it takes over,
+//      so the plane ends every phase all-free.
 // The result equals the sequential walk bit for bit (tests/test_gpu_parity.py).
 //
 // One cooperative launch runs a whole phase: grid-wide stages (grid.sync between them) while
-// many agents are pending, then block 0 finishes the tail alone with __syncthreads.
+// many agents are pending, then block 0 finishes the last TAIL_MAX alone in shared memory
+// while the other blocks zero the contention bitplanes for the next phase.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
@@ -29,7 +31,6 @@
 namespace cg = cooperative_groups;
 
 #define MOVE_THREADS 512
-#define MOVE_TAIL 4096  // pending agents at or below which block 0 runs the rounds alone
 
 __constant__ signed char c_bpath[121][5][2];
 static bool g_bpath_ready[64] = {false};
@@ -37,7 +38,6 @@ static bool g_bpath_ready[64] = {false};
 struct MoveArgs {
     Geo g;
     uint32_t* occ;
-    unsigned int* res;
     int32_t* x;
     int32_t* y;
     const int32_t* dx;
@@ -49,11 +49,23 @@ struct MoveArgs {
     const uint4* rec0;             // mode A: records emitted by the plan kernel (n_alive of them)
     int premade;                   // 1: mode A, 0: mode B
     uint4* rec[2];                 // pending records, ping-pong
-    unsigned int* pcount;          // [2] pending counts (device scratch, zero between phases)
+    unsigned int* pcount;          // [0..1] pending counts, [2..3] seed tile cursors (zero between phases)
     DevScalars* sc;
     unsigned long long* exits;     // (rank << 32 | id)
     uint32_t* p1;                  // contention bitplanes, zero between phases
     uint32_t* p2;
+    // plan tiles (mode A): rec0[tile_off[t] + k], k < tile_cnt[t], for t in tile_list
+    const uint32_t* tile_list;
+    const uint32_t* tile_off;
+    const uint32_t* tile_cnt;
+    int tile_w, tile_h, tiles_x;
+    // reservation rounds: contended records crec (= rec[1]), their hash slots, ping-pong lists
+    const uint4* crec;
+    unsigned int* cslot;           // 6 per contended agent
+    unsigned* plist[2];            // contended indices (carved from rec[0], free after step 2)
+    unsigned int* hkey;            // cell -> slot hash keys, H_EMPTY between phases
+    unsigned int* hres[2];         // reservation planes over the slots, H_EMPTY between phases
+    int hash_lg_max;
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -62,8 +74,21 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
-__device__ __forceinline__ size_t cell_index(const Geo& g, int x, int y) {
-    return (size_t)y * (size_t)g.W + (size_t)x;
+// One L2 load per CTA, broadcast through shared memory: a word every thread of the grid reads
+// right after a barrier would otherwise queue thousands of warp requests at one L2 slice.
+__device__ __forceinline__ unsigned long long cta_load(const unsigned long long* p) {
+    __shared__ unsigned long long s_v;
+    __syncthreads();  // earlier readers are done with s_v
+    if (threadIdx.x == 0) s_v = __ldcg(p);
+    __syncthreads();
+    return s_v;
+}
+__device__ __forceinline__ unsigned cta_load(const unsigned* p) {
+    __shared__ unsigned s_u;
+    __syncthreads();
+    if (threadIdx.x == 0) s_u = __ldcg(p);
+    __syncthreads();
+    return s_u;
 }
 
 __device__ __forceinline__ bool occ_test(const MoveArgs& a, int x, int y) {
@@ -80,38 +105,72 @@ __device__ __forceinline__ int path_of(const MoveArgs& a, const uint4& r, const 
     return record_cells(a.g, r, bp, gtx, gty, cx, cy);
 }
 
-__device__ __forceinline__ void append(unsigned int* count, uint4* list, bool take, const uint4& rec) {
-    const unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (!mask) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(mask) - 1;
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(count, (unsigned)__popc(mask));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (take) list[base + __popc(mask & ((1u << lane) - 1))] = rec;
+__device__ __forceinline__ void bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__device__ __forceinline__ void clear_cell(const MoveArgs& a, int x, int y, bool both) {
-    const size_t w = a.g.word(x, y);
-    const uint32_t nbit = ~(1u << (x & 31));
-    atomicAnd(&a.p1[w], nbit);
-    if (both) atomicAnd(&a.p2[w], nbit);
+// A thread group that synchronises on one hardware barrier: the whole CTA (barrier 0) or one
+// of the seed workers.  s[0] collects the group's append count, s[1] receives its list base,
+// s64 the group's displacement sum -- so each append or flush costs one global atomic per group
+// (per-warp atomics on one counter serialise thousands of requests at a single L2 slice).
+struct Group {
+    int bar, n;
+    bool leader;
+    unsigned* s;
+    unsigned long long* s64;
+    __device__ __forceinline__ void sync() const { bar_sync(bar, n); }
+};
+
+// Appends v to list when take.  Every thread of the group calls it.
+template <typename T>
+__device__ __forceinline__ void append(const Group& G, unsigned int* count, T* list, bool take, const T& v) {
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    const int lane = threadIdx.x & 31;
+    unsigned wo = 0;
+    if (lane == 0 && mask) wo = atomicAdd(&G.s[0], (unsigned)__popc(mask));
+    wo = __shfl_sync(0xffffffffu, wo, 0);
+    G.sync();
+    if (G.leader) {
+        const unsigned c = G.s[0];
+        G.s[1] = c ? atomicAdd(count, c) : 0u;
+        G.s[0] = 0;
+    }
+    G.sync();
+    if (take) list[G.s[1] + wo + __popc(mask & ((1u << lane) - 1))] = v;
+}
+
+// cx[j], cy[j] for a run-time j without spilling the arrays to local memory.
+__device__ __forceinline__ void pick(const int* cx, const int* cy, int j, int& x, int& y) {
+    x = cx[0];
+    y = cy[0];
+#pragma unroll
+    for (int i = 1; i < 5; ++i)
+        if (i == j) {
+            x = cx[i];
+            y = cy[i];
+        }
+}
+
+// Occupancy of the path cells, all loads in flight together.
+__device__ __forceinline__ void load_blocked(const MoveArgs& a, const int* cx, const int* cy, int m, bool* blocked) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) blocked[i] = i < m && occ_test(a, cx[i], cy[i]);
 }
 
 // The walk (engine.hpp:116-129) of an agent that owns its footprint, net effect on occupancy.
-__device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, const int* cx, const int* cy, int m,
-                                           unsigned long long* hops_acc) {
+__device__ __forceinline__ void walk_apply(const MoveArgs& a, const uint4& r, const int* cx, const int* cy, int m,
+                                           const bool* blocked, unsigned long long* hops_acc) {
     const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
     int h = 0;
-    for (int i = 0; i < m; ++i) {
-        if (occ_test(a, cx[i], cy[i])) break;
-        ++h;
-    }
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+        if (i < m && h == i && !blocked[i]) h = i + 1;
     const bool exited = (h == m) && (r.z & 0x80000000u);
     if (h > 0) {
         const uint32_t id = r.x;
         atomicAnd(&a.occ[a.g.word(sx, sy)], ~(1u << (sx & 31)));
-        const int fx = cx[h - 1], fy = cy[h - 1];
+        int fx, fy;
+        pick(cx, cy, h - 1, fx, fy);
         a.x[id] = fx;
         a.y[id] = fy;
         if (exited) {
@@ -126,37 +185,420 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
     *hops_acc += (unsigned long long)h;
 }
 
-__device__ __forceinline__ void reserve_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2]) {
-    int cx[5], cy[5];
-    const int m = path_of(a, r, bp, cx, cy);
-    atomicMin(&a.res[cell_index(a.g, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu))], r.y);
-    for (int i = 0; i < m; ++i) atomicMin(&a.res[cell_index(a.g, cx[i], cy[i])], r.y);
-}
-
-// Returns true if the agent committed (walked); false if it must retry next round.
-__device__ __forceinline__ bool commit_one(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
+__device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, const int* cx, const int* cy, int m,
                                            unsigned long long* hops_acc) {
-    const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
-    int cx[5], cy[5];
-    const int m = path_of(a, r, bp, cx, cy);
-    bool own = __ldcg(&a.res[cell_index(a.g, sx, sy)]) == r.y;
-    for (int i = 0; i < m && own; ++i) own = __ldcg(&a.res[cell_index(a.g, cx[i], cy[i])]) == r.y;
-    if (!own) return false;
-    // release the footprint (losers of this round read it after their own failed check only)
-    // and its contention bits (zero again for the next phase)
-    a.res[cell_index(a.g, sx, sy)] = 0xFFFFFFFFu;
-    clear_cell(a, sx, sy, true);
-    for (int i = 0; i < m; ++i) {
-        a.res[cell_index(a.g, cx[i], cy[i])] = 0xFFFFFFFFu;
-        clear_cell(a, cx[i], cy[i], true);
-    }
-    walk_owned(a, r, cx, cy, m, hops_acc);
-    return true;
+    bool blocked[5];
+    load_blocked(a, cx, cy, m, blocked);
+    walk_apply(a, r, cx, cy, m, blocked, hops_acc);
 }
 
-__device__ __forceinline__ void flush_hops(DevScalars* sc, unsigned long long hops) {
+// ------------------------------------------------------------------ grid-wide reservation rounds
+// The contended agents' footprint cells are interned in an open-addressing hash (cell -> slot)
+// sized to twice their cell count, so the reservation planes hres[0..1] stay L2-resident.  Round
+// r checks plane r&1: a holder of all its slots walks and frees them; a loser frees the slots it
+// holds and re-reserves in the other plane at once, so each round needs one grid barrier.
+#define H_EMPTY 0xFFFFFFFFu
+
+__host__ __device__ __forceinline__ int hash_log2(unsigned contended, int lg_max) {
+    int lg = 6;
+    const unsigned long long want = 12ull * contended;  // <= 6 cells each: load factor <= 1/2
+    while (lg < lg_max && (1ull << lg) < want) ++lg;
+    return lg;
+}
+
+// Interns contended agent ci's footprint and makes its first reservation (plane 0).
+__device__ __forceinline__ void round_prep(const MoveArgs& a, int lg, unsigned ci, const signed char (*bp)[5][2]) {
+    const uint4 r = __ldcg(&a.crec[ci]);
+    int cx[6], cy[6];
+    const int m = path_of(a, r, bp, cx + 1, cy + 1);
+    cx[0] = (int)(r.z & 0x0FFFFFFFu);
+    cy[0] = (int)(r.w & 0x00FFFFFFu);
+    // first probes of all six cells in flight together; collisions continue linearly
+    const unsigned mask = (1u << lg) - 1u;
+    unsigned cell[6], h[6], old[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        if (j > m) continue;
+        cell[j] = (unsigned)cy[j] * (unsigned)a.g.W + (unsigned)cx[j];
+        h[j] = (cell[j] * 0x9E3779B1u) >> (32 - lg);
+        old[j] = atomicCAS(&a.hkey[h[j]], H_EMPTY, cell[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        if (j > m) continue;
+        while (old[j] != H_EMPTY && old[j] != cell[j]) {
+            h[j] = (h[j] + 1) & mask;
+            old[j] = atomicCAS(&a.hkey[h[j]], H_EMPTY, cell[j]);
+        }
+        a.cslot[(size_t)ci * 6 + j] = h[j];
+        atomicMin(&a.hres[0][h[j]], r.y);
+    }
+    a.plist[0][ci] = ci;
+}
+
+// One round for contended agent ci on plane p; returns true if it must retry.
+__device__ __forceinline__ bool round_step(const MoveArgs& a, int p, unsigned ci, const signed char (*bp)[5][2],
+                                           unsigned long long* hops) {
+    const uint4 r = __ldcg(&a.crec[ci]);
+    const int m = (int)((r.z >> 28) & 7u);
+    unsigned s[6];
+    bool mine[6];
+    bool own = true;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        if (j > m) continue;
+        s[j] = __ldcg(&a.cslot[(size_t)ci * 6 + j]);
+        mine[j] = __ldcg(&a.hres[p][s[j]]) == r.y;
+        own &= mine[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        if (j > m) continue;
+        if (mine[j]) a.hres[p][s[j]] = H_EMPTY;             // release (holders only write their own)
+        if (!own) atomicMin(&a.hres[p ^ 1][s[j]], r.y);      // reserve for the next round
+    }
+    if (!own) return true;
+    int cx[5], cy[5];
+    path_of(a, r, bp, cx, cy);
+    walk_owned(a, r, cx, cy, m, hops);
+    return false;
+}
+
+// Resets the hash (keys and both planes) over its first 2^lg slots.
+__device__ void clear_hash(const MoveArgs& a, int lg, unsigned part, unsigned parts) {
+    const size_t n4 = ((size_t)1 << lg) / 4;
+    const uint4 e = make_uint4(H_EMPTY, H_EMPTY, H_EMPTY, H_EMPTY);
+    uint4* k = reinterpret_cast<uint4*>(a.hkey);
+    uint4* r0 = reinterpret_cast<uint4*>(a.hres[0]);
+    uint4* r1 = reinterpret_cast<uint4*>(a.hres[1]);
+    for (size_t i = (size_t)part * blockDim.x + threadIdx.x; i < n4; i += (size_t)parts * blockDim.x) {
+        k[i] = e;
+        r0[i] = e;
+        r1[i] = e;
+    }
+}
+
+// Adds the group's hop counts to the phase displacement.  Every thread of the group calls it.
+__device__ __forceinline__ void flush_hops(const Group& G, DevScalars* sc, unsigned long long hops) {
     for (int o = 16; o > 0; o >>= 1) hops += __shfl_down_sync(0xffffffffu, hops, o);
-    if ((threadIdx.x & 31) == 0 && hops) atomicAdd(&sc->disp, hops);
+    if ((threadIdx.x & 31) == 0 && hops) atomicAdd(G.s64, hops);
+    G.sync();
+    if (G.leader) {
+        if (*G.s64) atomicAdd(&sc->disp, *G.s64);
+        *G.s64 = 0;
+    }
+    G.sync();
+}
+
+// ------------------------------------------------------------------ shared-memory tail rounds
+// Once few agents are pending, block 0 resolves them alone: their footprint cells go into a
+// shared-memory hash (cell -> reservation, occupancy), the rounds run entirely in shared memory
+// with __syncthreads between phases, and the final occupancy is written back once.
+#define TAIL_MAX 1024
+#define TAIL_SLOTS 8192
+#define TAIL_EMPTY 0xFFFFFFFFu
+
+struct TailSmem {
+    uint4 rec[TAIL_MAX];
+    unsigned short slot[TAIL_MAX][6];
+    unsigned short list[2][TAIL_MAX];
+    unsigned int key[TAIL_SLOTS];
+    unsigned int res[TAIL_SLOTS];
+    unsigned char occ[TAIL_SLOTS];
+    unsigned int count[2];
+};
+
+__device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y) {
+    const unsigned cell = (unsigned)y * (unsigned)a.g.W + (unsigned)x;
+    unsigned h = (cell * 2654435761u) >> (32 - 13);
+    for (;;) {
+        const unsigned old = atomicCAS(&T.key[h], TAIL_EMPTY, cell);
+        if (old == TAIL_EMPTY) {  // new entry: its occupancy as of the tail's start
+            T.occ[h] = (unsigned char)((__ldcg(&a.occ[a.g.word(x, y)]) >> (x & 31)) & 1u);
+            return h;
+        }
+        if (old == cell) return h;
+        h = (h + 1) & (TAIL_SLOTS - 1);
+    }
+}
+
+// Pending records: crec[list[t]] (or crec[t] when list is null), t < np <= TAIL_MAX.
+__device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, const unsigned* list, unsigned np,
+                          const signed char (*bp)[5][2], unsigned long long* hops) {
+    for (unsigned k = threadIdx.x; k < TAIL_SLOTS; k += blockDim.x) {
+        T.key[k] = TAIL_EMPTY;
+        T.res[k] = 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    for (unsigned t = threadIdx.x; t < np; t += blockDim.x) {
+        const uint4 r = __ldcg(&crec[list ? __ldcg(&list[t]) : t]);
+        T.rec[t] = r;
+        T.list[0][t] = (unsigned short)t;
+        int cx[5], cy[5];
+        const int m = path_of(a, r, bp, cx, cy);
+        T.slot[t][0] = (unsigned short)tail_insert(T, a, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu));
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+            if (i < m) T.slot[t][1 + i] = (unsigned short)tail_insert(T, a, cx[i], cy[i]);
+    }
+    if (threadIdx.x == 0) {
+        T.count[0] = np;
+        T.count[1] = 0;
+    }
+    __syncthreads();
+    unsigned cur = 0, rounds = 0;
+    for (;;) {
+        const unsigned n = T.count[cur];
+        if (n == 0) break;
+        ++rounds;
+        const unsigned nxt = cur ^ 1;
+        for (unsigned k = threadIdx.x; k < n; k += blockDim.x) {
+            const unsigned t = T.list[cur][k];
+            const uint4 r = T.rec[t];
+            const int m = (int)((r.z >> 28) & 7u);
+            for (int i = 0; i <= m; ++i) atomicMin(&T.res[T.slot[t][i]], r.y);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) T.count[cur] = 0;  // read by everyone before the barrier above
+        for (unsigned k = threadIdx.x; k < n; k += blockDim.x) {
+            const unsigned t = T.list[cur][k];
+            const uint4 r = T.rec[t];
+            const int m = (int)((r.z >> 28) & 7u);
+            bool own = true;
+            for (int i = 0; i <= m && own; ++i) own = T.res[T.slot[t][i]] == r.y;
+            if (!own) {
+                T.list[nxt][atomicAdd(&T.count[nxt], 1u)] = (unsigned short)t;
+                continue;
+            }
+            for (int i = 0; i <= m; ++i) T.res[T.slot[t][i]] = 0xFFFFFFFFu;
+            int h = 0;  // the walk (engine.hpp:116-129) against the shared occupancy
+            while (h < m && !T.occ[T.slot[t][1 + h]]) ++h;
+            if (h > 0) {
+                const bool exited = (h == m) && (r.z & 0x80000000u);
+                T.occ[T.slot[t][0]] = 0;
+                int cx[5], cy[5];
+                path_of(a, r, bp, cx, cy);
+                const uint32_t id = r.x;
+                int fx, fy;
+                pick(cx, cy, h - 1, fx, fy);
+                a.x[id] = fx;
+                a.y[id] = fy;
+                if (exited) {
+                    a.alive[id] = 0;
+                    const unsigned long long s = atomicAdd(&a.sc->n_exits, 1ull);
+                    a.exits[s] = ((unsigned long long)r.y << 32) | id;
+                } else {
+                    T.occ[T.slot[t][h]] = 1;
+                }
+            }
+            *hops += (unsigned long long)h;
+        }
+        __syncthreads();
+        cur = nxt;
+    }
+    // write the final occupancy of every touched cell back to the bitplane
+    for (unsigned s = threadIdx.x; s < TAIL_SLOTS; s += blockDim.x) {
+        const unsigned cell = T.key[s];
+        if (cell == TAIL_EMPTY) continue;
+        const int x = (int)(cell % (unsigned)a.g.W), y = (int)(cell / (unsigned)a.g.W);
+        const uint32_t bit = 1u << (x & 31);
+        if (T.occ[s]) atomicOr(&a.occ[a.g.word(x, y)], bit);
+        else atomicAnd(&a.occ[a.g.word(x, y)], ~bit);
+    }
+    if (threadIdx.x == 0) a.sc->pad[1] += rounds;
+}
+
+// Zeroes the contention bitplanes (dead after step 2) so the next phase starts from all-clear.
+__device__ void zero_marks(const MoveArgs& a, unsigned part, unsigned parts) {
+    const size_t nwords = (size_t)a.g.P * (size_t)a.g.H;  // P is a multiple of 4
+    uint4* p1 = reinterpret_cast<uint4*>(a.p1);
+    uint4* p2 = reinterpret_cast<uint4*>(a.p2);
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (size_t k = (size_t)part * blockDim.x + threadIdx.x; k < nwords / 4; k += (size_t)parts * blockDim.x) {
+        p1[k] = z;
+        p2[k] = z;
+    }
+}
+
+// ------------------------------------------------------------------ tiled seed (mode A)
+// The plan left the records grouped by plan tile, and a footprint never leaves its tile by more
+// than 5 cells.  So each tile's marks are gathered in a shared-memory window (tile + 5-cell
+// halo) first and merged into the global bitplanes a word at a time, row-contiguous; the
+// classification then stages the window of P2 and occupancy the same way.  Each CTA runs
+// SEED_GROUPS independent 128-thread workers (named barriers), one tile each at a time.
+#define SEED_GROUP 128
+#define SEED_GROUPS (MOVE_THREADS / SEED_GROUP)
+
+struct SeedWin {
+    int wx0, ys, ww, wh;  // first word column (padded plane), first row, words per row, rows
+    float inv_ww;         // row of window word w = (int)((w + 0.5f) * inv_ww)  (w < 2^12)
+};
+
+__device__ __forceinline__ void group_sync() {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / SEED_GROUP)), "r"(SEED_GROUP) : "memory");
+}
+
+__host__ __device__ __forceinline__ int seed_ww(int tile_w) { return (tile_w + 10 + 31) / 32 + 1; }
+
+__device__ __forceinline__ SeedWin seed_window(const MoveArgs& a, uint32_t t) {
+    SeedWin s;
+    const int x0 = (int)(t % (uint32_t)a.tiles_x) * a.tile_w, y0 = (int)(t / (uint32_t)a.tiles_x) * a.tile_h;
+    s.wx0 = (x0 - 5 + FP_XPAD_BITS) >> 5;
+    s.ys = y0 - 5;
+    s.ww = seed_ww(a.tile_w);
+    s.wh = a.tile_h + 10;
+    s.inv_ww = 1.0f / (float)s.ww;
+    return s;
+}
+
+// Local word index of cell (x, y) in the window, or -1 when it lies outside (periodic seam).
+__device__ __forceinline__ int seed_local(const SeedWin& s, int x, int y) {
+    const int wi = ((x + FP_XPAD_BITS) >> 5) - s.wx0, yi = y - s.ys;
+    return (wi >= 0 && wi < s.ww && yi >= 0 && yi < s.wh) ? yi * s.ww + wi : -1;
+}
+
+// Global word of window word w, or -1 for rows outside the grid.
+__device__ __forceinline__ long long seed_global(const MoveArgs& a, const SeedWin& s, int w) {
+    const int yi = (int)(((float)w + 0.5f) * s.inv_ww);
+    const int y = s.ys + yi;
+    if (y < 0 || y >= a.g.H) return -1;
+    return (long long)y * a.g.P + (s.wx0 + w - yi * s.ww);
+}
+
+// Next tile for this worker group (dynamic: tiles differ a lot in agent count).
+__device__ __forceinline__ uint32_t seed_next(unsigned int* cursor, unsigned int* slot) {
+    if (threadIdx.x % SEED_GROUP == 0) *slot = atomicAdd(cursor, 1u);
+    group_sync();
+    const uint32_t e = *slot;
+    group_sync();  // everyone has read it before the next fetch overwrites it
+    return e;
+}
+
+__device__ __forceinline__ void record_footprint(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
+                                                 int* cx, int* cy, int& m) {
+    m = path_of(a, r, bp, cx + 1, cy + 1);
+    cx[0] = (int)(r.z & 0x0FFFFFFFu);
+    cy[0] = (int)(r.w & 0x00FFFFFFu);
+}
+
+// S1: every footprint of the group's tiles marked in P1/P2.
+__device__ void seed_mark(const MoveArgs& a, uint32_t* win, unsigned int* slot, const signed char (*bp)[5][2]) {
+    const unsigned lt = threadIdx.x % SEED_GROUP;
+    const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
+    for (;;) {
+        const uint32_t e = seed_next(&a.pcount[2], slot);
+        if (e >= nt) break;
+        const uint32_t t = a.tile_list[e];
+        const SeedWin s = seed_window(a, t);
+        const int nw = s.ww * s.wh;
+        uint32_t* L1 = win;
+        uint32_t* L2 = win + nw;
+        for (int w = lt; w < 2 * nw; w += SEED_GROUP) win[w] = 0;
+        group_sync();
+        const uint32_t off = a.tile_off[t], cnt = a.tile_cnt[t];
+        for (uint32_t k = lt; k < cnt; k += SEED_GROUP) {
+            const uint4 r = __ldcg(&a.rec0[off + k]);
+            if (!((r.z >> 28) & 7u)) continue;
+            int cx[6], cy[6], m;
+            record_footprint(a, r, bp, cx, cy, m);
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                if (i > m) continue;
+                const uint32_t bit = 1u << (cx[i] & 31);
+                const int w = seed_local(s, cx[i], cy[i]);
+                if (w >= 0) {
+                    if (atomicOr(&L1[w], bit) & bit) atomicOr(&L2[w], bit);
+                } else {
+                    const size_t gw = a.g.word(cx[i], cy[i]);
+                    if (atomicOr(&a.p1[gw], bit) & bit) atomicOr(&a.p2[gw], bit);
+                }
+            }
+        }
+        group_sync();
+        // merge: four words per thread in flight at once, then the P2 updates fire-and-forget
+        for (int w0 = lt; w0 < nw; w0 += 4 * SEED_GROUP) {
+            uint32_t l1[4], old[4];
+            long long gw[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int w = w0 + j * SEED_GROUP;
+                l1[j] = w < nw ? L1[w] : 0u;  // marks only land on rows inside the grid
+                gw[j] = l1[j] ? seed_global(a, s, w) : -1;
+                old[j] = l1[j] ? atomicOr(&a.p1[gw[j]], l1[j]) : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!l1[j]) continue;
+                const uint32_t d = L2[w0 + j * SEED_GROUP] | (old[j] & l1[j]);
+                if (d) atomicOr(&a.p2[gw[j]], d);
+            }
+        }
+        group_sync();
+    }
+}
+
+// S2: uncontended movers walk now; the rest go to the rounds (list rec[1]) with their rank.
+__device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, unsigned int* slot,
+                              const signed char (*bp)[5][2],
+                              unsigned long long* hops) {
+    const unsigned lt = threadIdx.x % SEED_GROUP;
+    const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
+    for (;;) {
+        const uint32_t e = seed_next(&a.pcount[3], slot);
+        if (e >= nt) break;
+        const uint32_t t = a.tile_list[e];
+        const SeedWin s = seed_window(a, t);
+        const int nw = s.ww * s.wh;
+        uint32_t* C2 = win;       // P2 window
+        uint32_t* CO = win + nw;  // occupancy window
+#pragma unroll 4
+        for (int w = lt; w < nw; w += SEED_GROUP) {
+            uint32_t v2 = 0, vo = 0;
+            const long long gw = seed_global(a, s, w);
+            if (gw >= 0) {
+                v2 = __ldcg(&a.p2[gw]);
+                vo = __ldcg(&a.occ[gw]);
+            }
+            C2[w] = v2;
+            CO[w] = vo;
+        }
+        group_sync();
+        const uint32_t off = a.tile_off[t], cnt = a.tile_cnt[t];
+        for (uint32_t base = 0; base < cnt; base += SEED_GROUP) {
+            const uint32_t k = base + lt;
+            bool contended = false;
+            uint4 r = make_uint4(0, 0, 0, 0);
+            if (k < cnt) {
+                r = __ldcg(&a.rec0[off + k]);
+                if ((r.z >> 28) & 7u) {
+                    int cx[6], cy[6], m;
+                    record_footprint(a, r, bp, cx, cy, m);
+                    bool blocked[5];
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        if (i > m) continue;
+                        const int sh = cx[i] & 31;
+                        const int w = seed_local(s, cx[i], cy[i]);
+                        uint32_t v2, vo;
+                        if (w >= 0) {
+                            v2 = C2[w];
+                            vo = CO[w];
+                        } else {
+                            const size_t gw = a.g.word(cx[i], cy[i]);
+                            v2 = __ldcg(&a.p2[gw]);
+                            vo = __ldcg(&a.occ[gw]);
+                        }
+                        contended |= (v2 >> sh) & 1u;
+                        if (i > 0) blocked[i - 1] = (vo >> sh) & 1u;
+                    }
+                    if (!contended) walk_apply(a, r, cx + 1, cy + 1, m, blocked, hops);
+                    else r.y = a.rank[r.x];
+                }
+            }
+            append(G, &a.pcount[1], a.rec[1], contended, r);
+        }
+        group_sync();
+    }
 }
 
 // Step 2 for one record: walk now if uncontended, else hand it (with its rank) to the rounds.
@@ -165,13 +607,16 @@ __device__ __forceinline__ bool classify(const MoveArgs& a, uint4& rec, const si
     int cx[5], cy[5];
     const int m = path_of(a, rec, bp, cx, cy);
     const int sx = (int)(rec.z & 0x0FFFFFFFu), sy = (int)(rec.w & 0x00FFFFFFu);
+    // the P2 loads and the (speculative) occupancy loads all in flight at once: if the footprint
+    // is uncontended nobody else touches its cells this phase, so the occupancy read is final
     bool contended = (__ldcg(&a.p2[a.g.word(sx, sy)]) >> (sx & 31)) & 1u;
-    for (int i = 0; i < m && !contended; ++i)
-        contended = (__ldcg(&a.p2[a.g.word(cx[i], cy[i])]) >> (cx[i] & 31)) & 1u;
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+        if (i < m) contended |= (__ldcg(&a.p2[a.g.word(cx[i], cy[i])]) >> (cx[i] & 31)) & 1u;
+    bool blocked[5];
+    load_blocked(a, cx, cy, m, blocked);
     if (!contended) {
-        walk_owned(a, rec, cx, cy, m, hops);
-        clear_cell(a, sx, sy, false);
-        for (int i = 0; i < m; ++i) clear_cell(a, cx[i], cy[i], false);
+        walk_apply(a, rec, cx, cy, m, blocked, hops);
         return false;
     }
     rec.y = a.rank[rec.x];
@@ -181,11 +626,20 @@ __device__ __forceinline__ bool classify(const MoveArgs& a, uint4& rec, const si
 __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ signed char s_bp[121][5][2];
+    extern __shared__ __align__(16) unsigned char s_dyn[];  // TailSmem (block 0's tail) / seed windows
+    __shared__ unsigned int s_slot[SEED_GROUPS];
+    __shared__ unsigned int s_app[2 + 2 * SEED_GROUPS];
+    __shared__ unsigned long long s_hops[1 + SEED_GROUPS];
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
+    if (threadIdx.x < 2 + 2 * SEED_GROUPS) s_app[threadIdx.x] = 0;
+    if (threadIdx.x < 1 + SEED_GROUPS) s_hops[threadIdx.x] = 0;
     __syncthreads();
+    const Group B{0, (int)blockDim.x, threadIdx.x == 0, &s_app[0], &s_hops[0]};
+    const unsigned sg = threadIdx.x / SEED_GROUP;
+    const Group Gs{1 + (int)sg, SEED_GROUP, threadIdx.x % SEED_GROUP == 0, &s_app[2 + 2 * sg], &s_hops[1 + sg]};
     const unsigned nthreads = gridDim.x * blockDim.x;
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t n = (uint32_t)__ldcg(&a.sc->n_alive);
+    const uint32_t n = (uint32_t)cta_load(&a.sc->n_alive);
     if (gtid == 0) a.sc->t_motion[0] = globaltimer();
     const uint4* cand = a.rec0;
     unsigned ncand = n;
@@ -202,26 +656,25 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
                 take = (rec.z >> 28) & 7u;
                 if (take) mark_record(a.p1, a.p2, a.g, rec, s_bp, tx, ty);
             }
-            append(&a.pcount[0], a.rec[0], take, rec);
+            append(B, &a.pcount[0], a.rec[0], take, rec);
         }
         grid.sync();
         cand = a.rec[0];
-        ncand = __ldcg(&a.pcount[0]);
+        ncand = cta_load(&a.pcount[0]);
     } else {
-        // step 1 over the plan's records (coalesced, plan-tile order)
-        for (uint32_t k = gtid; k < n; k += nthreads) {
-            const uint4 rec = __ldcg(&a.rec0[k]);
-            if ((rec.z >> 28) & 7u) {
-                int gtx = 0, gty = 0;
-                if (rec.w & REC_GENERIC) {
-                    gtx = a.g.wrap(a.dx[rec.x]);
-                    gty = a.dy[rec.x];
-                }
-                mark_record(a.p1, a.p2, a.g, rec, s_bp, gtx, gty);
-            }
-        }
+        // steps 1 and 2 tile by tile over the plan's records
+        const int nwmax = seed_ww(a.tile_w) * (a.tile_h + 10);
+        uint32_t* win = reinterpret_cast<uint32_t*>(s_dyn) + (threadIdx.x / SEED_GROUP) * 2 * nwmax;
+        unsigned int* slot = &s_slot[threadIdx.x / SEED_GROUP];
+        seed_mark(a, win, slot, s_bp);
         grid.sync();
+        if (gtid == 0) a.sc->t_marked = globaltimer();
+        unsigned long long hops = 0;
+        seed_classify(a, Gs, win, slot, s_bp, &hops);
+        flush_hops(B, a.sc, hops);
+        ncand = 0;  // step 2 done
     }
+    if (!a.premade && gtid == 0) a.sc->t_marked = globaltimer();
     // step 2
     {
         unsigned long long hops = 0;
@@ -233,57 +686,76 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
                 rec = __ldcg(&cand[k]);
                 if ((rec.z >> 28) & 7u) contended = classify(a, rec, s_bp, &hops);
             }
-            append(&a.pcount[1], a.rec[1], contended, rec);
+            append(B, &a.pcount[1], a.rec[1], contended, rec);
         }
-        flush_hops(a.sc, hops);
+        flush_hops(B, a.sc, hops);
     }
     grid.sync();
-    if (gtid == 0) a.sc->t_motion[1] = globaltimer();
-    // step 3
+    if (gtid == 0) {
+        a.sc->t_motion[1] = globaltimer();
+        a.sc->contended = __ldcg(&a.pcount[1]);
+    }
+    // step 3: grid-wide rounds while many are pending, then block 0 alone in shared memory while
+    // the other blocks zero the contention bitplanes and the hash (dead from here on)
+    const unsigned nc = cta_load(&a.pcount[1]);
+    const bool hashed = nc > TAIL_MAX;
+    const int lg = hash_log2(nc, a.hash_lg_max);
     unsigned r = 0;
-    bool solo = false;
-    for (;; ++r) {
-        const unsigned cur = (r + 1) & 1, nxt = cur ^ 1;
-        const unsigned np = __ldcg(&a.pcount[cur]);
-        if (np == 0) break;
-        if (!solo && np <= MOVE_TAIL) {
-            if (blockIdx.x != 0) return;  // every block reads the same np: block 0 continues alone
-            solo = true;
-            if (threadIdx.x == 0) {
-                a.sc->t_motion[2] = globaltimer();
-                a.sc->grid_rounds = r;
-            }
+    const unsigned* list = nullptr;  // null: the tail takes crec[0, np) directly
+    unsigned np = nc;
+    if (hashed) {
+        for (unsigned ci = gtid; ci < nc; ci += nthreads) round_prep(a, lg, ci, s_bp);
+        if (gtid == 0) {
+            a.pcount[4] = nc;  // round r reads count 4 + r%3, appends to the next, zeroes the third
+            a.pcount[5] = 0;
+            a.pcount[6] = 0;
         }
-        const unsigned stride = solo ? blockDim.x : nthreads;
-        const unsigned me = solo ? threadIdx.x : gtid;
-        if (gtid == 0) a.pcount[nxt] = 0;
-        const uint4* list = a.rec[cur];
-        for (unsigned k = me; k < np; k += stride) reserve_one(a, __ldcg(&list[k]), s_bp);
-        if (solo) __syncthreads(); else grid.sync();
+        grid.sync();
+        if (gtid == 0) a.sc->t_prep = globaltimer();
+        for (;; ++r) {
+            np = cta_load(&a.pcount[4 + r % 3]);
+            list = a.plist[r & 1];
+            if (np <= TAIL_MAX) break;  // every block reads the same np
+            if (gtid == 0) a.pcount[4 + (r + 2) % 3] = 0;
+            unsigned* next = a.plist[(r + 1) & 1];
+            unsigned int* ncount = &a.pcount[4 + (r + 1) % 3];
+            unsigned long long hops = 0;
+            for (unsigned base = 0; base < np; base += nthreads) {
+                const unsigned k = base + gtid;
+                unsigned ci = 0;
+                bool retry = false;
+                if (k < np) {
+                    ci = __ldcg(&list[k]);
+                    retry = round_step(a, (int)(r & 1), ci, s_bp, &hops);
+                }
+                append(B, ncount, next, retry, ci);
+            }
+            flush_hops(B, a.sc, hops);
+            grid.sync();
+        }
+    }
+    if (gridDim.x > 1 && blockIdx.x != 0) {
+        zero_marks(a, blockIdx.x - 1, gridDim.x - 1);
+        if (hashed) clear_hash(a, lg, blockIdx.x - 1, gridDim.x - 1);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        a.sc->t_motion[2] = globaltimer();
+        a.sc->grid_rounds = r;
+    }
+    if (np) {
         unsigned long long hops = 0;
-        for (unsigned base = 0; base < np; base += stride) {
-            const unsigned k = base + me;
-            bool retry = false;
-            uint4 rec = make_uint4(0, 0, 0, 0);
-            if (k < np) {
-                rec = __ldcg(&list[k]);
-                retry = !commit_one(a, rec, s_bp, &hops);
-            }
-            append(&a.pcount[nxt], a.rec[nxt], retry, rec);
-        }
-        flush_hops(a.sc, hops);
-        if (solo) __syncthreads(); else grid.sync();
+        tail_smem(a, *reinterpret_cast<TailSmem*>(s_dyn), a.crec, list, np, s_bp, &hops);
+        flush_hops(B, a.sc, hops);
+    }
+    if (gridDim.x == 1) {
+        zero_marks(a, 0, 1);
+        if (hashed) clear_hash(a, lg, 0, 1);
     }
     if (gtid == 0) {
-        const unsigned long long t = globaltimer();
-        if (!solo) {
-            a.sc->t_motion[2] = t;
-            a.sc->grid_rounds = r;
-        }
-        a.sc->t_motion[3] = t;
-        a.sc->pad[1] += r;  // rounds executed (observability)
-        a.pcount[0] = 0;
-        a.pcount[1] = 0;
+        a.sc->t_motion[3] = globaltimer();
+        a.sc->pad[1] += r;  // grid rounds executed (observability; the tail adds its own)
+        for (int k = 0; k < 7; ++k) a.pcount[k] = 0;  // list counts, seed cursors
         const unsigned long long ne = a.sc->n_exits;
         a.sc->alive -= ne;
         a.sc->tot_exits += ne;
@@ -304,15 +776,12 @@ int fp_ensure_res(fp_ctx* ctx) {
         FP_CUDA(ctx, cudaMemcpyToSymbol(c_bpath, bp, sizeof(bp)));
         g_bpath_ready[ctx->device] = true;
     }
-    if (ctx->d_res) return FP_OK;
+    if (ctx->d_p1) return FP_OK;
     const size_t nwords = (size_t)ctx->P * ctx->H;
     FP_CUDA(ctx, cudaMalloc(&ctx->d_p1, nwords * 4));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_p2, nwords * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
-    const size_t cells = (size_t)ctx->W * (size_t)ctx->H;
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_res, cells * sizeof(unsigned int)));
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_res, 0xFF, cells * sizeof(unsigned int), ctx->stream));
     ctx->marks_dirty = false;
     return FP_OK;
 }
@@ -334,14 +803,16 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
         FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, s));
     }
     if (!g_move_blocks) {
+        FP_CUDA(ctx, cudaFuncSetAttribute(move_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)sizeof(TailSmem)));
         int per_sm = 0;
-        FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS, 0));
+        FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS,
+                                                                   sizeof(TailSmem)));
         g_move_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
     }
     MoveArgs a;
     a.g = fp_geo(ctx);
     a.occ = ctx->d_occ;
-    a.res = ctx->d_res;
     a.x = ctx->d_x;
     a.y = ctx->d_y;
     a.dx = ctx->d_dx;
@@ -359,12 +830,28 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.exits = ctx->d_exits;
     a.p1 = ctx->d_p1;
     a.p2 = ctx->d_p2;
+    a.tile_list = ctx->d_tile_list;
+    a.tile_off = ctx->d_tile_off;
+    a.tile_cnt = ctx->d_tile_cnt;
+    a.tile_w = ctx->tile_w;
+    a.tile_h = ctx->tile_h;
+    a.tiles_x = ctx->tiles_x;
+    a.crec = ctx->d_rec_b;
+    a.cslot = ctx->d_cslot;
+    a.plist[0] = reinterpret_cast<unsigned*>(ctx->d_rec_a);  // 16 B per agent: two u32 lists
+    a.plist[1] = reinterpret_cast<unsigned*>(ctx->d_rec_a) + ctx->cap;
+    a.hkey = ctx->d_hkey;
+    a.hres[0] = ctx->d_hres0;
+    a.hres[1] = ctx->d_hres1;
+    a.hash_lg_max = ctx->hash_lg;
+    if (premade && (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4 > sizeof(TailSmem))
+        return fp_fail(ctx, FP_ERUNTIME, "motion: seed window exceeds shared memory");
     const unsigned blocks = (unsigned)std::min<size_t>((size_t)g_move_blocks,
                                                         std::max<size_t>(1, fp_blocks(ctx->n, MOVE_THREADS)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(MOVE_THREADS);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = sizeof(TailSmem);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;

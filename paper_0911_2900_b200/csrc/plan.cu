@@ -831,6 +831,11 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     if (!ctx->plane_valid || ctx->plane_ks != k_s || ctx->plane_potential != ctx->potential)
         return fp_fail(ctx, FP_ERUNTIME, "plan: weight plane not prepared for this k_s");
     if (int rc = fp_bucket_launch(ctx)) return rc;
+    if (ctx->marks_dirty) {  // marks of an earlier plan no motion phase consumed
+        const size_t nwords = (size_t)ctx->P * ctx->H;
+        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
+        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
+    }
     ctx->bucket_fresh = true;  // the motion seed pass walks agents in this (spatial) order
     ctx->rec_fresh = true;     // walk records + contention marks emitted below
     ctx->marks_dirty = true;

@@ -50,7 +50,9 @@ class _Counters(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("motion_rounds", C.c_int64),
                 ("plan_fallbacks", C.c_int64), ("planned_agents", C.c_int64),
                 ("motion_seed_ns", C.c_int64), ("motion_grid_ns", C.c_int64),
-                ("motion_tail_ns", C.c_int64), ("motion_grid_rounds", C.c_int64)]
+                ("motion_tail_ns", C.c_int64), ("motion_grid_rounds", C.c_int64),
+                ("motion_mark_ns", C.c_int64), ("motion_contended", C.c_int64),
+                ("motion_prep_ns", C.c_int64)]
 
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")

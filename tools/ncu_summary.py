@@ -41,3 +41,26 @@ if len(srows) > 2:
     print("  top stalled SASS (samples, executed, avg threads, instr):")
     for k, r in sorted(enumerate(data), key=lambda t: -int(t[1][iS] or 0))[:ntop]:
         print(f"   #{k:5d} {r[iS]:>6} {r[iE]:>9} {r[iA]:>3}  {r[1][:70]}")
+# per CUDA source line: samples attributed to the SASS under each line (cuda,sass view)
+mix = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                     capture_output=True, text=True).stdout
+agg, fname, line, hdr = {}, "", "", None
+for r in csv.reader(io.StringIO(mix)):
+    if not r:
+        continue
+    if r[0] == "File Path":
+        fname = r[1].split("/")[-1]
+        continue
+    if r[0] == "Line No":
+        hdr = r
+        continue
+    if hdr is None or len(r) < 5:
+        continue
+    if r[0]:
+        line = (fname, int(r[0]), r[1].strip()[:60])
+    elif r[4] not in ("-", ""):
+        agg[line] = agg.get(line, 0) + int(r[4])
+tot = sum(agg.values()) or 1
+print("  top source lines (stall samples %):")
+for (f, ln, txt), s in sorted(agg.items(), key=lambda t: -t[1])[:ntop]:
+    print(f"   {100*s/tot:5.1f}%  {f}:{ln}  {txt}")
