@@ -53,7 +53,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -123,34 +123,70 @@ def build_workload(cfg, seed):
     return scenarios.build(cfg, seed=seed)
 
 
-def reference_cpu(wl, field, steps, cores):
-    """The reference's own run() (oracle/_ref) on this workload: agent-updates/s."""
+def reference_cpu(wl, field, max_steps, cores, budget_s):
+    """The reference's own run() (oracle/_ref, unmodified headers) on this workload, from step 0:
+    one calibration step, then as many more (<= max_steps - 1) as fit in ~budget_s seconds.
+    Returns (agent-updates/s over all timed steps, kind, cores, steps, seconds)."""
     import oracle as O
     ro = wl.roster
     if O.have_reference():
         st = O.RefState(wl.grid.cells, field, ro.x, ro.y, ro.v_max, ro.alive, wl.grid.boundary,
                         potential=wl.potential, drive_gradient=wl.drive_gradient)
+        upd, secs, steps = 0.0, 0.0, 0
         n0 = st.alive_count
-        r = st.run(wl.k_s, wl.seed, steps, cores)
-        n1 = st.alive_count
-        # alive entering each step is between n1 and n0; exits per step are tiny vs N
-        upd = (n0 + n1) / 2.0 * steps
-        return upd / r["wall_time_s"], "reference", cores, r
+        r = st.run(wl.k_s, wl.seed, 1, cores)
+        upd, secs, steps = float(n0), r["wall_time_s"], 1
+        more = int(min(max_steps - 1, max(0.0, budget_s - secs) / max(secs, 1e-9)))
+        if more > 0:
+            n0 = st.alive_count
+            r = st.run(wl.k_s, wl.seed, more, cores)
+            n1 = st.alive_count
+            # alive entering each step lies between n1 and n0 (exits per step << N)
+            upd += (n0 + n1) / 2.0 * more
+            secs += r["wall_time_s"]
+            steps += more
+        return upd / secs, "reference", cores, steps, secs
     st = O.State(wl.grid.cells, field, ro.x, ro.y, ro.v_max, ro.alive, wl.grid.boundary,
                  potential=wl.potential, drive_gradient=wl.drive_gradient)
-    upd = 0
+    upd, steps = 0, 0
     t0 = time.perf_counter()
-    for _ in range(steps):
+    while steps < max_steps and (steps == 0 or time.perf_counter() - t0 < budget_s):
         upd += st.alive_count
         st.step_once(wl.k_s, wl.seed)
-    return upd / (time.perf_counter() - t0), "port", 1, None
+        steps += 1
+    secs = time.perf_counter() - t0
+    return upd / secs, "port", 1, steps, secs
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def plan_traffic(workload):
+    """DRAM bytes per plan-kernel launch from the committed `ncu --set full` summary (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "plan_kernel_ncu.json")) as f:
+            p = json.load(f)
+        if p.get("workload") == workload:
+            return float(p["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=396)  # the reference's run length (SURVEY 8d)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of reference CPU work")
     ap.add_argument("--config", default="plaza", choices=["corridor", "room", "ring", "plaza", "obstacles"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=1)
@@ -173,16 +209,16 @@ def main():
         import oracle as O
         field = O.static_field(wl.grid.cells, wl.grid.boundary)
         cores = os.cpu_count() or 1
-        vals = []
-        for _ in range(args.warmup if args.warmup < 1 else 1):
-            reference_cpu(wl, field, 1, cores)
-        v, kind, c, _ = reference_cpu(wl, field, max(1, args.steps), cores)
+        # each "step" of this arm is the reference's own step; the run is bounded to ~60 s of work
+        v, kind, c, steps_done, secs = reference_cpu(wl, field, max(1, args.steps), cores, 60.0)
         config_desc.update(n_agents=int(len(wl.roster)), grid=[wl.grid.width, wl.grid.height])
-        out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-               "warmup": args.warmup, "higher_is_better": True, "impl": "reference", "dtype": "f64",
-               "data": "synthetic", "scaling": "weak", "vs_baseline": None, "config": config_desc,
-               "cpu_baseline": {"value": v, "unit": UNIT, "cores": c, "kind": kind,
-                                "sample": f"{args.steps} steps of {args.config} from step 0"},
+        sample = (f"{steps_done} of the {args.steps} steps of {args.config} from step 0 "
+                  f"({secs:.1f} s, reference run() with ScheduleParams{{cores={c}}}, {cpu_model()})")
+        out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps_done,
+               "warmup": 0, "ms_per_step": secs / steps_done * 1e3, "higher_is_better": True,
+               "impl": "reference", "dtype": "f64", "data": "synthetic", "scaling": "weak",
+               "vs_baseline": None, "config": config_desc,
+               "cpu_baseline": {"value": v, "unit": UNIT, "cores": c, "kind": kind, "sample": sample},
                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return
@@ -232,7 +268,7 @@ def main():
     value = updates / wall
 
     # e2e: the C ABI with host buffers, every step H2D roster + step + D2H positions/alive
-    e2e_steps = args.e2e_steps or min(args.steps, 50)
+    e2e_steps = args.e2e_steps or args.steps
     st2 = fp.SimState(wl.grid, st.field(), ro, device=local)
     if wl.potential:
         st2.set_potential(wl.potential, wl.drive_gradient)
@@ -262,7 +298,7 @@ def main():
     plan_launch_s = kernel_ms * 1e-3
     achieved = bytes_per_launch / plan_launch_s / 1e9
     roof = {"kernel": "plan_tile_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
-            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": plan_traffic(args.config),
             "bytes_per_launch": bytes_per_launch, "U_cells": U, "plan_ms_per_launch": plan_launch_s * 1e3,
             "plan_share_of_step": plan_launch_s * rs.steps / rs.wall_time_s,
             "layout_bytes_per_launch": nalive_avg * (8 + 8 + (1 if mixed else 0)) + wl.grid.width * wl.grid.height * 4.25,
@@ -270,15 +306,22 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline:
-        import oracle as O
         field = st.field()
         cores = os.cpu_count() or 1
-        # bounded sample: enough steps for ~10-30 s of CPU work
-        est = n * 1.0e-6 / max(min(cores, 16) * 0.55, 1)  # ~1 us/agent-plan on one core
-        sample_steps = int(max(1, min(396, 15.0 / max(est, 1e-6))))
-        v, kind, c, _ = reference_cpu(wl, field, sample_steps, cores)
+        # bounded sample: one calibration step, then steps up to ~cpu_budget seconds of CPU work
+        v, kind, c, steps_done, secs = reference_cpu(wl, field, args.steps, cores, args.cpu_budget)
         cpu = {"value": v, "unit": UNIT, "cores": c, "kind": kind,
-               "sample": f"{sample_steps} steps of {args.config} from step 0 ({n} agents)"}
+               "sample": f"first {steps_done} of {args.steps} steps of {args.config} ({n} agents), {secs:.1f} s, "
+                         f"reference run() on {c} threads, {cpu_model()}"}
+
+    # real-time capacity (bench.hpp:165-226 rule, 1 step = 1 simulated s): the agent count whose
+    # 396 steps take 396 s, extrapolated linearly from this run and capped at the free cells
+    free_cells = int((wl.grid.cells == 0).sum())
+    sec_per_step = wall / max(rs.steps, 1)
+    cap_est = nalive_avg * world / max(sec_per_step, 1e-12)
+    capacity = {"value": int(min(cap_est, free_cells)), "capped": bool(cap_est >= free_cells),
+                "extrapolated_from_n": int(n), "free_cells": free_cells,
+                "method": "linear in N from this run's ms_per_step; geometry fixed"}
 
     config_desc.update(n_agents=n, grid=[wl.grid.width, wl.grid.height], mixed_v=mixed)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -287,6 +330,7 @@ def main():
            "config": config_desc, "parallelism": "replicas" if world > 1 else "single",
            "phases_ms": {"plan": rs.plan_time_s * 1e3, "move": rs.move_time_s * 1e3, "total": rs.wall_time_s * 1e3},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+           "realtime_capacity": capacity,
            "gpu_launches": int(c1["kernel_launches"] - c0["kernel_launches"]),
            "motion_rounds_per_step": (c1["motion_rounds"] - c0["motion_rounds"]) / max(rs.steps, 1),
            "plan_fallbacks_per_step": (c1["plan_fallbacks"] - c0["plan_fallbacks"]) / max(rs.steps, 1)}

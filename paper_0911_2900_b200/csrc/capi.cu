@@ -52,6 +52,8 @@ static int validate_grid(const fp_grid_desc* g, const uint8_t* cells) {
         return fail(nullptr, FP_EINVAL, "Grid: unknown boundary");
     if ((int64_t)g->width * g->height >= (int64_t)1 << 32)
         return fail(nullptr, FP_EINVAL, "Grid: more than 2^32 cells");
+    if (g->width >= (1 << 27) || g->height >= (1 << 24))  // motion record fields (motion_rec.cuh)
+        return fail(nullptr, FP_EINVAL, "Grid: width must be < 2^27 and height < 2^24");
     const int W = g->width, H = g->height;
     const size_t n = (size_t)W * H;
     uint8_t mx = 0;
@@ -136,10 +138,11 @@ static void free_agents(fp_ctx* c) {
                     c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
                     c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted,
                     c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback, c->d_rec_a, c->d_rec_b,
-                    c->d_rec0, c->d_hkey, c->d_hres0, c->d_hres1, c->d_cslot};
+                    c->d_rec0, c->d_entry};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    c->d_hkey = c->d_hres0 = c->d_hres1 = c->d_cslot = nullptr;
+    c->d_entry = nullptr;
+    c->bk_agent_cap = 0;
     c->d_x = c->d_y = c->d_dx = c->d_dy = nullptr;
     c->d_v = c->d_alive = nullptr;
     c->d_rank = c->d_alive_ids = c->d_order = c->d_j = c->d_cnt = c->d_off = c->d_cursor = nullptr;
@@ -173,15 +176,6 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
     FP_CUDA(c, cudaMalloc(&c->d_rec_b, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_rec0, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_fallback, m * sizeof(uint2)));
-    // motion hash: 2^hash_lg >= 12 m slots (six cells per agent at load factor <= 1/2)
-    c->hash_lg = 6;
-    while ((1ull << c->hash_lg) < 12ull * m) ++c->hash_lg;
-    const size_t hs = (size_t)1 << c->hash_lg;
-    for (uint32_t** p : {&c->d_hkey, &c->d_hres0, &c->d_hres1}) {
-        FP_CUDA(c, cudaMalloc(p, hs * 4));
-        FP_CUDA(c, cudaMemsetAsync(*p, 0xFF, hs * 4, c->stream));
-    }
-    FP_CUDA(c, cudaMalloc(&c->d_cslot, m * 6 * 4));
     c->cap = (uint32_t)m;
     c->graph_valid = false;
     return FP_OK;
@@ -265,7 +259,8 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
     void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_counters, c->d_temp, c->d_temp_b,
-                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sc, c->d_p1, c->d_p2};
+                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sc, c->d_p1, c->d_p2,
+                    c->d_bkt, c->d_pool_owner};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -797,4 +792,23 @@ extern "C" int fp_get_counters(const fp_ctx* c, fp_counters* out) {
     if (!c || !out) return fail(nullptr, FP_EINVAL, "null argument");
     *out = c->ctr;
     return FP_OK;
+}
+
+// Diagnostics (not in the header): per grid round of the last motion phase, the globaltimer at
+// its start (relative to the end of the seed pass) and the pending count.  Returns the count.
+extern "C" int fp_debug_rounds(fp_ctx* c, int64_t* t_ns, int64_t* pending, int64_t* checks, int64_t* chk_max,
+                               int64_t* p1_max, int cap) {
+    if (!c) return -1;
+    DevScalars h;
+    if (cudaMemcpy(&h, c->d_sc, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    const int n = (int)std::min<unsigned long long>(h.grid_rounds + 1, (unsigned long long)std::min(cap, 64));
+    for (int r = 0; r < n; ++r) {
+        t_ns[r] = (int64_t)(h.t_round[r] - h.t_motion[1]);
+        pending[r] = (int64_t)h.n_round[r];
+        checks[r] = (int64_t)h.chk_cnt[r];
+        chk_max[r] = (int64_t)h.chk_max[r];
+        p1_max[r] = (int64_t)h.p1_max[r];
+    }
+    if (cap >= 64) chk_max[63] = (int64_t)h.chk_max[63];  // largest bucket of the phase
+    return n;
 }

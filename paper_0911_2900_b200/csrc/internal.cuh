@@ -8,8 +8,8 @@
 //                             unreachable flag, and the fp32-mantissa / integer-exponent split of
 //                             2^(-k_s*log2(e)*S) (plane.cu).  Read by the plan kernel via TMA.
 //   field                   : fp64 per cell (StaticField::s), read only by the exact path
-//   motion scratch          : P1/P2 contention bitplanes (like occupancy); a cell -> slot hash
-//                             with two u32 reservation planes sized to the contended agents
+//   motion scratch          : P1/P2 contention bitplanes (like occupancy); a 32-byte rank
+//                             bucket per cell (+ overflow pool) for the reservation rounds
 //   agents (SoA)            : x, y (i32), v_max (u8), alive (u8), desired x/y (i32), rank (u32)
 //   tile buckets            : agent ids grouped by plan tile (counting sort each step)
 #pragma once
@@ -124,7 +124,12 @@ struct DevScalars {
     unsigned long long grid_rounds;  // rounds of the last motion phase run grid-wide
     unsigned long long t_marked;     // globaltimer: contention marks complete
     unsigned long long contended;    // movers handed to the reservation rounds, last phase
-    unsigned long long t_prep;       // globaltimer: reservation hash built
+    unsigned long long t_prep;       // globaltimer: reservation buckets built
+    unsigned long long t_round[64];  // globaltimer at the start of grid round r (r < 64)
+    unsigned long long n_round[64];  // pending agents entering grid round r
+    unsigned long long chk_max[64];  // diagnostics: longest full check of round r (SM clocks)
+    unsigned long long chk_cnt[64];  //   full checks in round r
+    unsigned long long p1_max[64];   //   longest pass-1 loop of a thread in round r (SM clocks)
 };
 
 struct fp_ctx {
@@ -186,10 +191,11 @@ struct fp_ctx {
     uint2* d_fallback = nullptr;  // (id, bucket position) the plan kernel hands to the exact path
     uint4 *d_rec_a = nullptr, *d_rec_b = nullptr;  // motion pending records (move.cu)
     uint4* d_rec0 = nullptr;    // walk records in plan-tile order, emitted by the plan phase
-    // motion reservation rounds (move.cu): cell -> slot hash and two reservation planes over the
-    // slots (2^hash_lg each, H_EMPTY between phases), 6 slots per contended agent
-    uint32_t *d_hkey = nullptr, *d_hres0 = nullptr, *d_hres1 = nullptr, *d_cslot = nullptr;
-    int hash_lg = 0;
+    // motion reservation rounds (move.cu): rank buckets (8-word chunk per cell + overflow pool,
+    // all-empty between phases) and per-agent entries
+    uint32_t *d_bkt = nullptr, *d_pool_owner = nullptr;
+    uint32_t* d_entry = nullptr;
+    unsigned bk_pool_cap = 0, bk_agent_cap = 0;
     bool bucket_fresh = false;  // plan-tile buckets match the current positions
     bool rec_fresh = false;     // d_rec0 + contention marks match the current desired cells
     bool marks_dirty = false;   // contention bitplanes hold marks no motion phase consumed

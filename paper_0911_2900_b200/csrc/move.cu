@@ -61,11 +61,16 @@ struct MoveArgs {
     int tile_w, tile_h, tiles_x;
     // reservation rounds: contended records crec (= rec[1]), their hash slots, ping-pong lists
     const uint4* crec;
-    unsigned int* cslot;           // 6 per contended agent
-    unsigned* plist[2];            // contended indices (carved from rec[0], free after step 2)
-    unsigned int* hkey;            // cell -> slot hash keys, H_EMPTY between phases
-    unsigned int* hres[2];         // reservation planes over the slots, H_EMPTY between phases
-    int hash_lg_max;
+    uint32_t* bkt;                 // rank buckets: 8-word chunks, base chunk of a cell = cell index,
+                                   // then pool_cap overflow chunks; all-empty between phases
+    unsigned base_words;           // 8 * base chunks (W, H padded to 64, 32); pool chunks follow
+    unsigned bk_bw;                // 64-cell block columns
+    unsigned pool_cap;
+    unsigned* pool_n;              // overflow chunks taken this phase
+    unsigned* pool_owner;          // chunk that links to each taken pool chunk
+    unsigned* entry;               // 6 per contended agent: word index of its bucket entries
+    // contended-index pending lists (ping-pong), carved from rec[0] (free after step 2)
+    uint2* alist[2];               // (contended index, entry of the blocker it waits on)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -160,7 +165,7 @@ __device__ __forceinline__ void load_blocked(const MoveArgs& a, const int* cx, c
 // The walk (engine.hpp:116-129) of an agent that owns its footprint, net effect on occupancy.
 __device__ __forceinline__ void walk_apply(const MoveArgs& a, const uint4& r, const int* cx, const int* cy, int m,
                                            const bool* blocked, unsigned long long* hops_acc) {
-    const int sx = (int)(r.z & 0x0FFFFFFFu), sy = (int)(r.w & 0x00FFFFFFu);
+    const int sx = rec_x(r), sy = rec_y(r);
     int h = 0;
 #pragma unroll
     for (int i = 0; i < 5; ++i)
@@ -193,88 +198,200 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
 }
 
 // ------------------------------------------------------------------ grid-wide reservation rounds
-// The contended agents' footprint cells are interned in an open-addressing hash (cell -> slot)
-// sized to twice their cell count, so the reservation planes hres[0..1] stay L2-resident.  Round
-// r checks plane r&1: a holder of all its slots walks and frees them; a loser frees the slots it
-// holds and re-reserves in the other plane at once, so each round needs one grid barrier.
-#define H_EMPTY 0xFFFFFFFFu
+// Every contended agent enters its rank into the bucket of each footprint cell.  A bucket is a
+// chain of chunks addressed by word index into one array: the cell's base chunk (8 words = one
+// 32-byte sector: entry count, 6 entries, link) then, when crowded, 64-word overflow chunks
+// from a pool (count, 62 entries, link).  An agent is the earliest pending agent on a cell iff
+// its rank is the bucket minimum; holding all of its cells it walks (everything before it in
+// the reference order on those cells has run) and clears its entries.  A blocked agent
+// watches the entry of one blocker (the latest-ranked) and re-checks only once that entry is
+// cleared, so a waiting agent costs one load per round.  Entries are never reused within a
+// phase, so "entry still holds the rank" == "still pending".
+#define BK_EMPTY 0xFFFFFFFFu
+#define BK_NIL 0xFFFFFFFFu
+#define BK_NOWATCH 0xFFFFFFFFu
 
-__host__ __device__ __forceinline__ int hash_log2(unsigned contended, int lg_max) {
-    int lg = 6;
-    const unsigned long long want = 12ull * contended;  // <= 6 cells each: load factor <= 1/2
-    while (lg < lg_max && (1ull << lg) < want) ++lg;
-    return lg;
+__device__ __forceinline__ bool bk_pool(const MoveArgs& a, unsigned c) { return c >= a.base_words; }
+__device__ __forceinline__ unsigned bk_cap(const MoveArgs& a, unsigned c) { return bk_pool(a, c) ? 62u : 6u; }
+__device__ __forceinline__ unsigned bk_link(const MoveArgs& a, unsigned c) { return c + (bk_pool(a, c) ? 63u : 7u); }
+// first word of the chunk holding entry word e
+__device__ __forceinline__ unsigned bk_start(const MoveArgs& a, unsigned e) {
+    return bk_pool(a, e) ? a.base_words + ((e - a.base_words) & ~63u) : (e & ~7u);
 }
 
-// Interns contended agent ci's footprint and makes its first reservation (plane 0).
-__device__ __forceinline__ void round_prep(const MoveArgs& a, int lg, unsigned ci, const signed char (*bp)[5][2]) {
-    const uint4 r = __ldcg(&a.crec[ci]);
-    int cx[6], cy[6];
-    const int m = path_of(a, r, bp, cx + 1, cy + 1);
-    cx[0] = (int)(r.z & 0x0FFFFFFFu);
-    cy[0] = (int)(r.w & 0x00FFFFFFu);
-    // first probes of all six cells in flight together; collisions continue linearly
-    const unsigned mask = (1u << lg) - 1u;
-    unsigned cell[6], h[6], old[6];
+// Base chunk (word index) of cell (x, y): 64x32-cell blocks stored contiguously (64 KB of
+// buckets each), so the buckets of neighbouring agents share DRAM pages and L2 lines.
+__device__ __forceinline__ unsigned cell_of(const MoveArgs& a, int x, int y) {
+    return (((((unsigned)y >> 5) * a.bk_bw + ((unsigned)x >> 6)) << 11) | (((unsigned)y & 31u) << 6) |
+            ((unsigned)x & 63u))
+           << 3;
+}
+
+// Footprint cells of a record: [0] start, [1..mf] path (motion_rec.cuh); returns mf.
+__device__ __forceinline__ int footprint(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
+                                         unsigned* cell) {
+    int cx[5], cy[5];
+    path_of(a, r, bp, cx, cy);
+    const int m = rec_mf(r);
+    cell[0] = cell_of(a, rec_x(r), rec_y(r));
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        if (j > m) continue;
-        cell[j] = (unsigned)cy[j] * (unsigned)a.g.W + (unsigned)cx[j];
-        h[j] = (cell[j] * 0x9E3779B1u) >> (32 - lg);
-        old[j] = atomicCAS(&a.hkey[h[j]], H_EMPTY, cell[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        if (j > m) continue;
-        while (old[j] != H_EMPTY && old[j] != cell[j]) {
-            h[j] = (h[j] + 1) & mask;
-            old[j] = atomicCAS(&a.hkey[h[j]], H_EMPTY, cell[j]);
+    for (int j = 0; j < 5; ++j)
+        if (j < m) cell[j + 1] = cell_of(a, cx[j], cy[j]);
+    return m;
+}
+
+// The overflow chunk linked from chunk c, linking a fresh one from the pool if there is none
+// (BK_NIL when the pool is exhausted).
+__device__ unsigned bk_next(const MoveArgs& a, unsigned c) {
+    unsigned* link = &a.bkt[bk_link(a, c)];
+    const unsigned nx = __ldcg(link);
+    if (nx != BK_NIL) return nx;
+    const unsigned q = atomicAdd(a.pool_n, 1u);
+    if (q >= a.pool_cap) return BK_NIL;
+    const unsigned fresh = a.base_words + q * 64u;  // pool chunks are all-empty between phases
+    const unsigned old = atomicCAS(link, BK_NIL, fresh);
+    a.pool_owner[q] = old == BK_NIL ? c : BK_NIL;  // a lost race leaves the chunk unused
+    return old == BK_NIL ? fresh : old;
+}
+
+// Enters `rank` into the bucket chain starting at chunk `c`; returns the entry's word index, or
+// BK_NIL when the overflow pool is exhausted.  Word 0 of a chunk counts its taken entries
+// (all-ones = none, so the all-ones reset state needs no separate zeroing): the atomicAdd hands
+// out entries without retries; the last word links the next chunk.
+__device__ unsigned bk_insert(const MoveArgs& a, unsigned c, unsigned rank) {
+    for (;;) {
+        const unsigned k = atomicAdd(&a.bkt[c], 1u) + 1u;  // 0-based slot
+        if (k < bk_cap(a, c)) {
+            a.bkt[c + 1 + k] = rank;
+            return c + 1 + k;
         }
-        a.cslot[(size_t)ci * 6 + j] = h[j];
-        atomicMin(&a.hres[0][h[j]], r.y);
+        c = bk_next(a, c);
+        if (c == BK_NIL) return BK_NIL;
     }
-    a.plist[0][ci] = ci;
 }
 
-// One round for contended agent ci on plane p; returns true if it must retry.
-__device__ __forceinline__ bool round_step(const MoveArgs& a, int p, unsigned ci, const signed char (*bp)[5][2],
-                                           unsigned long long* hops) {
+// Minimum pending rank in the bucket chain at chunk `c` and the word holding it.  Base chunks
+// are one 32-byte sector; overflow chunks (62 entries, 256 bytes) are read with all their loads
+// in flight, so even the most crowded cell is at most a couple of dependent hops.
+__device__ __forceinline__ unsigned bk_min(const MoveArgs& a, unsigned c, unsigned& at) {
+    unsigned mn = BK_EMPTY;
+    at = BK_NIL;
+    do {
+        const uint4* p = reinterpret_cast<const uint4*>(a.bkt + c);
+        unsigned nx;
+        if (c < a.base_words) {
+            const uint4 lo = __ldcg(p), hi = __ldcg(p + 1);
+            const unsigned e[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int k = 1; k < 7; ++k)
+                if (e[k] < mn) {
+                    mn = e[k];
+                    at = c + k;
+                }
+            nx = e[7];
+        } else {
+            uint4 q[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) q[i] = __ldcg(p + i);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const unsigned e[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int w = 4 * i + k;
+                    if (w >= 1 && w <= 62 && e[k] < mn) {
+                        mn = e[k];
+                        at = c + w;
+                    }
+                }
+            }
+            nx = q[15].w;
+        }
+        c = nx;
+    } while (c != BK_NIL);
+    return mn;
+}
+
+// Round-0 entry of contended agent ci: the six first-chunk counters taken in parallel, the rare
+// overflows chained afterwards.
+__device__ __forceinline__ void bk_prep(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2]) {
     const uint4 r = __ldcg(&a.crec[ci]);
-    const int m = (int)((r.z >> 28) & 7u);
-    unsigned s[6];
-    bool mine[6];
+    unsigned cell[6], k[6];
+    const int m = footprint(a, r, bp, cell);
+#pragma unroll
+    for (int j = 0; j < 6; ++j)
+        if (j <= m) k[j] = atomicAdd(&a.bkt[cell[j]], 1u) + 1u;
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        if (j > m) continue;
+        unsigned e;
+        if (k[j] < 6) {
+            e = cell[j] + 1 + k[j];
+            a.bkt[e] = r.y;
+        } else {
+            const unsigned nx = bk_next(a, cell[j]);
+            e = nx == BK_NIL ? BK_NIL : bk_insert(a, nx, r.y);
+        }
+        if (e == BK_NIL) atomicOr(&a.sc->err, 8ull);  // pool exhausted (sized for the worst case)
+        a.entry[(size_t)ci * 6 + j] = e;
+    }
+}
+
+// Full check of pending agent ci (its watched blocker, if any, has walked).  Holding every cell
+// it walks and clears its entries right after the walk (release fence between), so a later
+// agent that sees them cleared may walk in the same round: its acquire fence orders its
+// occupancy reads after this walk.  Otherwise returns the entry of the latest-ranked blocker.
+__device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2],
+                                         unsigned long long* hops, unsigned* watch) {
+    const uint4 r = __ldcg(&a.crec[ci]);
+    unsigned cell[6];
+    const int m = footprint(a, r, bp, cell);
+    unsigned best = 0, best_at = BK_NIL;
     bool own = true;
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         if (j > m) continue;
-        s[j] = __ldcg(&a.cslot[(size_t)ci * 6 + j]);
-        mine[j] = __ldcg(&a.hres[p][s[j]]) == r.y;
-        own &= mine[j];
+        unsigned at;
+        const unsigned mn = bk_min(a, cell[j], at);
+        if (mn != r.y) {
+            own = false;
+            if (best_at == BK_NIL || mn > best) {
+                best = mn;
+                best_at = at;
+            }
+        }
     }
+    if (!own) {
+        *watch = best_at;
+        return false;
+    }
+    __threadfence();  // acquire: the walks of the earlier agents on these cells are visible
+    int cx[5], cy[5];
+    const int mw = path_of(a, r, bp, cx, cy);  // the walk covers the whole path (m >= mf)
+    walk_owned(a, r, cx, cy, mw, hops);
+    __threadfence();  // release: this walk before the cleared entries
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         if (j > m) continue;
-        if (mine[j]) a.hres[p][s[j]] = H_EMPTY;             // release (holders only write their own)
-        if (!own) atomicMin(&a.hres[p ^ 1][s[j]], r.y);      // reserve for the next round
+        const unsigned e = __ldcg(&a.entry[(size_t)ci * 6 + j]);
+        if (e == BK_NIL) continue;
+        a.bkt[e] = BK_EMPTY;
+        a.bkt[bk_start(a, e)] = BK_EMPTY;  // the chunk's entry counter (no insertions during the rounds)
     }
-    if (!own) return true;
-    int cx[5], cy[5];
-    path_of(a, r, bp, cx, cy);
-    walk_owned(a, r, cx, cy, m, hops);
-    return false;
+    return true;
 }
 
-// Resets the hash (keys and both planes) over its first 2^lg slots.
-__device__ void clear_hash(const MoveArgs& a, int lg, unsigned part, unsigned parts) {
-    const size_t n4 = ((size_t)1 << lg) / 4;
-    const uint4 e = make_uint4(H_EMPTY, H_EMPTY, H_EMPTY, H_EMPTY);
-    uint4* k = reinterpret_cast<uint4*>(a.hkey);
-    uint4* r0 = reinterpret_cast<uint4*>(a.hres[0]);
-    uint4* r1 = reinterpret_cast<uint4*>(a.hres[1]);
-    for (size_t i = (size_t)part * blockDim.x + threadIdx.x; i < n4; i += (size_t)parts * blockDim.x) {
-        k[i] = e;
-        r0[i] = e;
-        r1[i] = e;
+// End of phase: every used pool chunk back to empty and unlinked (all-ones, 16 threads per
+// chunk).
+__device__ void bk_reset_pool(const MoveArgs& a, unsigned used, unsigned part, unsigned parts) {
+    const uint4 ones = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
+    for (unsigned i = part * blockDim.x + threadIdx.x; i < used * 16u; i += parts * blockDim.x) {
+        const unsigned q = i >> 4;
+        reinterpret_cast<uint4*>(a.bkt + a.base_words + q * 64u)[i & 15u] = ones;
+        if ((i & 15u) == 0) {
+            const unsigned owner = a.pool_owner[q];
+            if (owner != BK_NIL) a.bkt[bk_link(a, owner)] = BK_NIL;
+        }
     }
 }
 
@@ -308,6 +425,11 @@ struct TailSmem {
     unsigned int count[2];
 };
 
+// Round queues in the same dynamic buffer (see the rounds in move_rounds_kernel).
+#define QP_CAP 8192
+#define QC_CAP 8192
+static_assert(QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) <= sizeof(TailSmem), "round queues");
+
 __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y) {
     const unsigned cell = (unsigned)y * (unsigned)a.g.W + (unsigned)x;
     unsigned h = (cell * 2654435761u) >> (32 - 13);
@@ -315,6 +437,12 @@ __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, 
         const unsigned old = atomicCAS(&T.key[h], TAIL_EMPTY, cell);
         if (old == TAIL_EMPTY) {  // new entry: its occupancy as of the tail's start
             T.occ[h] = (unsigned char)((__ldcg(&a.occ[a.g.word(x, y)]) >> (x & 31)) & 1u);
+            // only tail agents (and walkers whose release is in flight) still have entries in
+            // this cell's base chunk: empty it for the next phase (overflow chunks are reset
+            // by the other blocks)
+            uint32_t* b = a.bkt + cell_of(a, x, y);
+            reinterpret_cast<uint4*>(b)[0] = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
+            b[4] = b[5] = b[6] = BK_EMPTY;
             return h;
         }
         if (old == cell) return h;
@@ -323,7 +451,7 @@ __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, 
 }
 
 // Pending records: crec[list[t]] (or crec[t] when list is null), t < np <= TAIL_MAX.
-__device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, const unsigned* list, unsigned np,
+__device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, const uint2* list, unsigned np,
                           const signed char (*bp)[5][2], unsigned long long* hops) {
     for (unsigned k = threadIdx.x; k < TAIL_SLOTS; k += blockDim.x) {
         T.key[k] = TAIL_EMPTY;
@@ -331,12 +459,13 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
     }
     __syncthreads();
     for (unsigned t = threadIdx.x; t < np; t += blockDim.x) {
-        const uint4 r = __ldcg(&crec[list ? __ldcg(&list[t]) : t]);
+        const uint4 r = __ldcg(&crec[list ? __ldcg(&list[t].x) : t]);
         T.rec[t] = r;
         T.list[0][t] = (unsigned short)t;
         int cx[5], cy[5];
-        const int m = path_of(a, r, bp, cx, cy);
-        T.slot[t][0] = (unsigned short)tail_insert(T, a, (int)(r.z & 0x0FFFFFFFu), (int)(r.w & 0x00FFFFFFu));
+        path_of(a, r, bp, cx, cy);
+        const int m = rec_mf(r);  // footprint cells only (a free exit ending the walk has no slot)
+        T.slot[t][0] = (unsigned short)tail_insert(T, a, rec_x(r), rec_y(r));
 #pragma unroll
         for (int i = 0; i < 5; ++i)
             if (i < m) T.slot[t][1 + i] = (unsigned short)tail_insert(T, a, cx[i], cy[i]);
@@ -355,7 +484,7 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
         for (unsigned k = threadIdx.x; k < n; k += blockDim.x) {
             const unsigned t = T.list[cur][k];
             const uint4 r = T.rec[t];
-            const int m = (int)((r.z >> 28) & 7u);
+            const int m = rec_mf(r);
             for (int i = 0; i <= m; ++i) atomicMin(&T.res[T.slot[t][i]], r.y);
         }
         __syncthreads();
@@ -363,16 +492,17 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
         for (unsigned k = threadIdx.x; k < n; k += blockDim.x) {
             const unsigned t = T.list[cur][k];
             const uint4 r = T.rec[t];
-            const int m = (int)((r.z >> 28) & 7u);
+            const int mf = rec_mf(r), m = rec_m(r);
             bool own = true;
-            for (int i = 0; i <= m && own; ++i) own = T.res[T.slot[t][i]] == r.y;
+            for (int i = 0; i <= mf && own; ++i) own = T.res[T.slot[t][i]] == r.y;
             if (!own) {
                 T.list[nxt][atomicAdd(&T.count[nxt], 1u)] = (unsigned short)t;
                 continue;
             }
-            for (int i = 0; i <= m; ++i) T.res[T.slot[t][i]] = 0xFFFFFFFFu;
+            for (int i = 0; i <= mf; ++i) T.res[T.slot[t][i]] = 0xFFFFFFFFu;
             int h = 0;  // the walk (engine.hpp:116-129) against the shared occupancy
-            while (h < m && !T.occ[T.slot[t][1 + h]]) ++h;
+            while (h < mf && !T.occ[T.slot[t][1 + h]]) ++h;
+            if (h == mf) h = m;  // a free exit ending the walk never blocks
             if (h > 0) {
                 const bool exited = (h == m) && (r.z & 0x80000000u);
                 T.occ[T.slot[t][0]] = 0;
@@ -474,11 +604,13 @@ __device__ __forceinline__ uint32_t seed_next(unsigned int* cursor, unsigned int
     return e;
 }
 
+// Start cell [0] and path cells [1..m]; the footprint is [0..mf] (motion_rec.cuh).
 __device__ __forceinline__ void record_footprint(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
-                                                 int* cx, int* cy, int& m) {
+                                                 int* cx, int* cy, int& m, int& mf) {
     m = path_of(a, r, bp, cx + 1, cy + 1);
-    cx[0] = (int)(r.z & 0x0FFFFFFFu);
-    cy[0] = (int)(r.w & 0x00FFFFFFu);
+    mf = rec_mf(r);
+    cx[0] = rec_x(r);
+    cy[0] = rec_y(r);
 }
 
 // S1: every footprint of the group's tiles marked in P1/P2.
@@ -498,12 +630,12 @@ __device__ void seed_mark(const MoveArgs& a, uint32_t* win, unsigned int* slot, 
         const uint32_t off = a.tile_off[t], cnt = a.tile_cnt[t];
         for (uint32_t k = lt; k < cnt; k += SEED_GROUP) {
             const uint4 r = __ldcg(&a.rec0[off + k]);
-            if (!((r.z >> 28) & 7u)) continue;
-            int cx[6], cy[6], m;
-            record_footprint(a, r, bp, cx, cy, m);
+            if (!rec_m(r)) continue;
+            int cx[6], cy[6], m, mf;
+            record_footprint(a, r, bp, cx, cy, m, mf);
 #pragma unroll
             for (int i = 0; i < 6; ++i) {
-                if (i > m) continue;
+                if (i > mf) continue;
                 const uint32_t bit = 1u << (cx[i] & 31);
                 const int w = seed_local(s, cx[i], cy[i]);
                 if (w >= 0) {
@@ -570,9 +702,9 @@ __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, 
             uint4 r = make_uint4(0, 0, 0, 0);
             if (k < cnt) {
                 r = __ldcg(&a.rec0[off + k]);
-                if ((r.z >> 28) & 7u) {
-                    int cx[6], cy[6], m;
-                    record_footprint(a, r, bp, cx, cy, m);
+                if (rec_m(r)) {
+                    int cx[6], cy[6], m, mf;
+                    record_footprint(a, r, bp, cx, cy, m, mf);
                     bool blocked[5];
 #pragma unroll
                     for (int i = 0; i < 6; ++i) {
@@ -588,7 +720,7 @@ __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, 
                             v2 = __ldcg(&a.p2[gw]);
                             vo = __ldcg(&a.occ[gw]);
                         }
-                        contended |= (v2 >> sh) & 1u;
+                        if (i <= mf) contended |= (v2 >> sh) & 1u;
                         if (i > 0) blocked[i - 1] = (vo >> sh) & 1u;
                     }
                     if (!contended) walk_apply(a, r, cx + 1, cy + 1, m, blocked, hops);
@@ -605,14 +737,14 @@ __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, 
 __device__ __forceinline__ bool classify(const MoveArgs& a, uint4& rec, const signed char (*bp)[5][2],
                                          unsigned long long* hops) {
     int cx[5], cy[5];
-    const int m = path_of(a, rec, bp, cx, cy);
-    const int sx = (int)(rec.z & 0x0FFFFFFFu), sy = (int)(rec.w & 0x00FFFFFFu);
+    const int m = path_of(a, rec, bp, cx, cy), mf = rec_mf(rec);
+    const int sx = rec_x(rec), sy = rec_y(rec);
     // the P2 loads and the (speculative) occupancy loads all in flight at once: if the footprint
     // is uncontended nobody else touches its cells this phase, so the occupancy read is final
     bool contended = (__ldcg(&a.p2[a.g.word(sx, sy)]) >> (sx & 31)) & 1u;
 #pragma unroll
     for (int i = 0; i < 5; ++i)
-        if (i < m) contended |= (__ldcg(&a.p2[a.g.word(cx[i], cy[i])]) >> (cx[i] & 31)) & 1u;
+        if (i < mf) contended |= (__ldcg(&a.p2[a.g.word(cx[i], cy[i])]) >> (cx[i] & 31)) & 1u;
     bool blocked[5];
     load_blocked(a, cx, cy, m, blocked);
     if (!contended) {
@@ -630,7 +762,9 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     __shared__ unsigned int s_slot[SEED_GROUPS];
     __shared__ unsigned int s_app[2 + 2 * SEED_GROUPS];
     __shared__ unsigned long long s_hops[1 + SEED_GROUPS];
+    __shared__ unsigned int s_q[3];  // round queue counts and the flush base
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
+    if (threadIdx.x < 3) s_q[threadIdx.x] = 0;
     if (threadIdx.x < 2 + 2 * SEED_GROUPS) s_app[threadIdx.x] = 0;
     if (threadIdx.x < 1 + SEED_GROUPS) s_hops[threadIdx.x] = 0;
     __syncthreads();
@@ -652,8 +786,8 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
             if (k < n) {
                 const uint32_t id = a.seed_list[k];
                 const int tx = a.g.wrap(a.dx[id]), ty = a.dy[id];
-                rec = record_of(a.g, id, a.g.wrap(a.x[id]), a.y[id], tx, ty, a.v[id], s_bp);
-                take = (rec.z >> 28) & 7u;
+                rec = record_of(a.g, a.occ, id, a.g.wrap(a.x[id]), a.y[id], tx, ty, a.v[id], s_bp);
+                take = rec_m(rec) > 0;
                 if (take) mark_record(a.p1, a.p2, a.g, rec, s_bp, tx, ty);
             }
             append(B, &a.pcount[0], a.rec[0], take, rec);
@@ -684,7 +818,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
             uint4 rec = make_uint4(0, 0, 0, 0);
             if (k < ncand) {
                 rec = __ldcg(&cand[k]);
-                if ((rec.z >> 28) & 7u) contended = classify(a, rec, s_bp, &hops);
+                if (rec_m(rec)) contended = classify(a, rec, s_bp, &hops);
             }
             append(B, &a.pcount[1], a.rec[1], contended, rec);
         }
@@ -695,48 +829,104 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         a.sc->t_motion[1] = globaltimer();
         a.sc->contended = __ldcg(&a.pcount[1]);
     }
-    // step 3: grid-wide rounds while many are pending, then block 0 alone in shared memory while
-    // the other blocks zero the contention bitplanes and the hash (dead from here on)
+    // step 3: bucket rounds while many are pending, then block 0 alone in shared memory while
+    // the other blocks clean up (contention bitplanes, overflow chunks)
     const unsigned nc = cta_load(&a.pcount[1]);
-    const bool hashed = nc > TAIL_MAX;
-    const int lg = hash_log2(nc, a.hash_lg_max);
-    unsigned r = 0;
-    const unsigned* list = nullptr;  // null: the tail takes crec[0, np) directly
+    const bool rounds = nc > TAIL_MAX;
+    unsigned r = 0, pool_used = 0;
+    const uint2* list = nullptr;  // null: the tail takes crec[0, np) directly
     unsigned np = nc;
-    if (hashed) {
-        for (unsigned ci = gtid; ci < nc; ci += nthreads) round_prep(a, lg, ci, s_bp);
+    if (rounds) {
+        for (unsigned ci = gtid; ci < nc; ci += nthreads) {
+            bk_prep(a, ci, s_bp);
+            a.alist[0][ci] = make_uint2(ci, BK_NOWATCH);
+        }
         if (gtid == 0) {
-            a.pcount[4] = nc;  // round r reads count 4 + r%3, appends to the next, zeroes the third
-            a.pcount[5] = 0;
-            a.pcount[6] = 0;
+            // pending counts rotate over pcount[4..6]: round r reads its own, fills the next and
+            // zeroes the one last read in round r-1
+            a.pcount[4] = nc;
+            a.pcount[5] = a.pcount[6] = 0;
         }
         grid.sync();
         if (gtid == 0) a.sc->t_prep = globaltimer();
+        pool_used = min(cta_load(a.pool_n), a.pool_cap);
+        // Per round and CTA, in the (now free) dynamic shared memory: a queue of agents whose
+        // watched blocker has walked (full check) and a queue of still-pending (agent, watch)
+        // pairs flushed to the next list with one global atomic.
+        uint2* qp = reinterpret_cast<uint2*>(s_dyn);
+        unsigned* qc = reinterpret_cast<unsigned*>(s_dyn + QP_CAP * sizeof(uint2));
+        unsigned* qpn = &s_q[0];
+        unsigned* qcn = &s_q[1];
         for (;; ++r) {
             np = cta_load(&a.pcount[4 + r % 3]);
-            list = a.plist[r & 1];
+            list = a.alist[r & 1];
+            if (gtid == 0 && r < 64) {
+                a.sc->t_round[r] = globaltimer();
+                a.sc->n_round[r] = np;
+            }
             if (np <= TAIL_MAX) break;  // every block reads the same np
             if (gtid == 0) a.pcount[4 + (r + 2) % 3] = 0;
-            unsigned* next = a.plist[(r + 1) & 1];
+            uint2* next = a.alist[(r + 1) & 1];
             unsigned int* ncount = &a.pcount[4 + (r + 1) % 3];
-            unsigned long long hops = 0;
-            for (unsigned base = 0; base < np; base += nthreads) {
-                const unsigned k = base + gtid;
-                unsigned ci = 0;
-                bool retry = false;
-                if (k < np) {
-                    ci = __ldcg(&list[k]);
-                    retry = round_step(a, (int)(r & 1), ci, s_bp, &hops);
+            // pass 1: watch tests, four list entries per thread in flight
+            const long long c_p1 = clock64();
+            for (unsigned base = gtid; base < np; base += 4 * nthreads) {
+                uint2 e[4];
+                unsigned v[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const unsigned k = base + i * nthreads;
+                    e[i] = k < np ? __ldcg(&list[k]) : make_uint2(BK_NIL, BK_NOWATCH);
                 }
-                append(B, ncount, next, retry, ci);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) v[i] = e[i].y != BK_NOWATCH ? __ldcg(&a.bkt[e[i].y]) : BK_EMPTY;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (e[i].x == BK_NIL) continue;
+                    if (v[i] != BK_EMPTY) {  // blocker still pending: carry over as is
+                        const unsigned s = atomicAdd(qpn, 1u);
+                        if (s < QP_CAP) qp[s] = e[i];
+                        else next[atomicAdd(ncount, 1u)] = e[i];
+                    } else {
+                        const unsigned s = atomicAdd(qcn, 1u);
+                        if (s < QC_CAP) qc[s] = e[i].x;
+                        else next[atomicAdd(ncount, 1u)] = make_uint2(e[i].x, BK_NOWATCH);  // checked next round
+                    }
+                }
             }
-            flush_hops(B, a.sc, hops);
+            __syncthreads();
+            const long long c_p2 = clock64();
+            if (threadIdx.x == 0 && r < 64) atomicMax(&a.sc->p1_max[r], (unsigned long long)(c_p2 - c_p1));
+            // pass 2: full checks of this CTA's woken agents
+            unsigned long long hops = 0;
+            const unsigned nchk = min(*qcn, (unsigned)QC_CAP);
+            if (threadIdx.x == 0 && r < 64 && nchk) atomicAdd(&a.sc->chk_cnt[r], (unsigned long long)nchk);
+            for (unsigned i = threadIdx.x; i < nchk; i += blockDim.x) {
+                const unsigned ci = qc[i];
+                unsigned w;
+                if (!bk_check(a, ci, s_bp, &hops, &w)) {
+                    const unsigned s = atomicAdd(qpn, 1u);
+                    if (s < QP_CAP) qp[s] = make_uint2(ci, w);
+                    else next[atomicAdd(ncount, 1u)] = make_uint2(ci, w);
+                }
+            }
+            flush_hops(B, a.sc, hops);  // (its barriers also complete the queue)
+            if (threadIdx.x == 0 && r < 64) atomicMax(&a.sc->chk_max[r], (unsigned long long)(clock64() - c_p2));
+            const unsigned nq = min(*qpn, (unsigned)QP_CAP);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                s_q[2] = nq ? atomicAdd(ncount, nq) : 0u;
+                *qpn = 0;
+                *qcn = 0;
+            }
+            __syncthreads();
+            for (unsigned i = threadIdx.x; i < nq; i += blockDim.x) next[s_q[2] + i] = qp[i];
             grid.sync();
         }
     }
     if (gridDim.x > 1 && blockIdx.x != 0) {
         zero_marks(a, blockIdx.x - 1, gridDim.x - 1);
-        if (hashed) clear_hash(a, lg, blockIdx.x - 1, gridDim.x - 1);
+        if (rounds) bk_reset_pool(a, pool_used, blockIdx.x - 1, gridDim.x - 1);
         return;
     }
     if (threadIdx.x == 0) {
@@ -750,12 +940,13 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     }
     if (gridDim.x == 1) {
         zero_marks(a, 0, 1);
-        if (hashed) clear_hash(a, lg, 0, 1);
+        if (rounds) bk_reset_pool(a, pool_used, 0, 1);
     }
     if (gtid == 0) {
         a.sc->t_motion[3] = globaltimer();
         a.sc->pad[1] += r;  // grid rounds executed (observability; the tail adds its own)
-        for (int k = 0; k < 7; ++k) a.pcount[k] = 0;  // list counts, seed cursors
+        for (int k = 0; k < 10; ++k) a.pcount[k] = 0;  // list counts, seed cursors
+        *a.pool_n = 0;
         const unsigned long long ne = a.sc->n_exits;
         a.sc->alive -= ne;
         a.sc->tot_exits += ne;
@@ -764,10 +955,14 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
 }
 
 __global__ void move_begin_kernel(DevScalars* sc) {
+    for (int r = threadIdx.x; r < 64; r += blockDim.x) sc->chk_max[r] = sc->chk_cnt[r] = sc->p1_max[r] = 0;
+    if (threadIdx.x) return;
     sc->n_exits = 0;
     sc->disp = 0;
     sc->tot_updates += sc->alive;
 }
+
+static int ensure_buckets(fp_ctx* ctx);
 
 int fp_ensure_res(fp_ctx* ctx) {
     if (ctx->device < 64 && !g_bpath_ready[ctx->device]) {
@@ -776,26 +971,51 @@ int fp_ensure_res(fp_ctx* ctx) {
         FP_CUDA(ctx, cudaMemcpyToSymbol(c_bpath, bp, sizeof(bp)));
         g_bpath_ready[ctx->device] = true;
     }
-    if (ctx->d_p1) return FP_OK;
-    const size_t nwords = (size_t)ctx->P * ctx->H;
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_p1, nwords * 4));
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_p2, nwords * 4));
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
-    ctx->marks_dirty = false;
-    return FP_OK;
+    if (!ctx->d_p1) {
+        const size_t nwords = (size_t)ctx->P * ctx->H;
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_p1, nwords * 4));
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_p2, nwords * 4));
+        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
+        FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
+        ctx->marks_dirty = false;
+    }
+    return ensure_buckets(ctx);  // before any graph capture: allocation is not capturable
 }
 
 static int g_move_blocks = 0;
+
+// Rank buckets (one 32-byte chunk per cell plus 256-byte overflow chunks, enough for every cell
+// to overflow: six entries per agent, seven to overflow a cell) and the per-agent round state;
+// all-empty between phases.
+static int ensure_buckets(fp_ctx* ctx) {
+    const size_t cells = (size_t)((ctx->W + 63) / 64 * 64) * (size_t)((ctx->H + 31) / 32 * 32);  // cell_of
+    const size_t pool = (size_t)ctx->cap * 6 / 7 + 64;
+    if (ctx->d_bkt && ctx->bk_pool_cap >= pool && ctx->bk_agent_cap >= ctx->cap) return FP_OK;
+    const size_t words = cells * 8 + pool * 64;
+    if (words >= 0xFFFFFFFFull)
+        return fp_fail(ctx, FP_ERUNTIME, "motion: grid too large for 32-bit bucket word indices");
+    cudaStreamSynchronize(ctx->stream);
+    for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_pool_owner, (void*)ctx->d_entry})
+        if (p) cudaFree(p);
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_bkt, words * 4));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0xFF, words * 4, ctx->stream));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_owner, pool * 4));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * 6 * 4));
+    ctx->bk_pool_cap = (unsigned)pool;
+    ctx->bk_agent_cap = ctx->cap;
+    ctx->graph_valid = false;
+    return FP_OK;
+}
 
 // Enqueues one motion phase (after fp_order_launch) on ctx->stream.  Graph-safe.
 // Mode A (ctx->rec_fresh): the plan kernel emitted records + marks for the current state.
 // Mode B: records are built here from the plan-tile buckets when current, else the order list.
 int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     cudaStream_t s = ctx->stream;
-    move_begin_kernel<<<1, 1, 0, s>>>(ctx->d_sc);
+    move_begin_kernel<<<1, 64, 0, s>>>(ctx->d_sc);
     FP_LAUNCHED(ctx);
     if (ctx->n == 0) return FP_OK;
+    if (int rc = ensure_buckets(ctx)) return rc;
     const bool premade = ctx->rec_fresh;
     if (!premade && ctx->marks_dirty) {  // marks of records that were never consumed
         const size_t nwords = (size_t)ctx->P * ctx->H;
@@ -837,13 +1057,16 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.tile_h = ctx->tile_h;
     a.tiles_x = ctx->tiles_x;
     a.crec = ctx->d_rec_b;
-    a.cslot = ctx->d_cslot;
-    a.plist[0] = reinterpret_cast<unsigned*>(ctx->d_rec_a);  // 16 B per agent: two u32 lists
-    a.plist[1] = reinterpret_cast<unsigned*>(ctx->d_rec_a) + ctx->cap;
-    a.hkey = ctx->d_hkey;
-    a.hres[0] = ctx->d_hres0;
-    a.hres[1] = ctx->d_hres1;
-    a.hash_lg_max = ctx->hash_lg;
+    a.bkt = ctx->d_bkt;
+    a.bk_bw = (unsigned)((ctx->W + 63) / 64);
+    a.base_words = (unsigned)((size_t)a.bk_bw * 64 * (size_t)((ctx->H + 31) / 32 * 32) * 8);
+    a.pool_cap = ctx->bk_pool_cap;
+    a.pool_n = a.pcount + 10;
+    a.pool_owner = ctx->d_pool_owner;
+    a.entry = ctx->d_entry;
+    uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
+    a.alist[0] = lists;
+    a.alist[1] = lists + ctx->cap;
     if (premade && (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4 > sizeof(TailSmem))
         return fp_fail(ctx, FP_ERUNTIME, "motion: seed window exceeds shared memory");
     const unsigned blocks = (unsigned)std::min<size_t>((size_t)g_move_blocks,

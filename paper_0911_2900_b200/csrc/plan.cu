@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
             if (st == 1) {
                 a.dx[id] = cx;
                 a.dy[id] = cy;
-                if (A.emit) A.rec0[off + k] = record_of(a.g, id, px, py, cx, cy, v, s_bp);  // motion's walk record
+                if (A.emit) A.rec0[off + k] = record_of(a.g, a.occ, id, px, py, cx, cy, v, s_bp);  // motion's walk record
             } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
                 A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, (uint32_t)(off + k));
             }
@@ -613,7 +613,7 @@ struct EmitArgs {
 __device__ __forceinline__ void emit_record(const PlanCommon& a, const EmitArgs& E, uint32_t id, uint32_t pos, int px,
                                             int py, int cx, int cy, int v) {
     if (!E.emit) return;
-    E.rec0[pos] = record_of(a.g, id, px, py, cx, cy, v, c_bpath_p);
+    E.rec0[pos] = record_of(a.g, a.occ, id, px, py, cx, cy, v, c_bpath_p);
 }
 
 __global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanCommon a, const uint2* list,
