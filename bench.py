@@ -249,7 +249,9 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
+        torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects these launches
         rs = fp.run(st, params)
+        torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     c1 = st.counters()
     x1, y1, a1 = st.agents()

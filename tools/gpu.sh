@@ -4,5 +4,5 @@
 set -e
 cd "$(dirname "$0")/.."
 python -c "import __graft_entry__ as g; g.build()" > /tmp/gpu_build.log 2>&1 || { tail -20 /tmp/gpu_build.log; echo BUILD FAILED; exit 1; }
-rm -rf gpurun_out/*
+mkdir -p gpurun_out
 timeout $(( $1 + 600 )) /usr/local/graft/bin/gpurun --timeout "$1" -- "mkdir -p gpurun_out; $2"
