@@ -258,15 +258,8 @@ def main():
     # the plan kernel alone, timed with CUDA events on its stream, on the end-of-run state
     kernel_ms = st.time_plan_kernel(wl.k_s, wl.seed, 20)
     U1 = coverage_u(wl.grid, x1, y1, ro.v_max, a1)
-    t = torch.tensor([rs.wall_time_s, rs.agent_updates], dtype=torch.float64, device="cuda")
-    if world > 1:
-        tt = t.clone()
-        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
-        tm = t.clone()
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-        wall, updates = float(tm[0]), float(tt[1])
-    else:
-        wall, updates = rs.wall_time_s, rs.agent_updates
+    from paper_0911_2900_b200.dist import aggregate
+    wall, updates = aggregate(rs.wall_time_s, rs.agent_updates)  # max time, summed updates over ranks
     value = updates / wall
 
     # e2e: the C ABI with host buffers, every step H2D roster + step + D2H positions/alive
