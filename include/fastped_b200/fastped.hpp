@@ -259,9 +259,22 @@ inline SimState make_state(std::shared_ptr<const Grid> grid, std::shared_ptr<con
     return st;
 }
 
-inline std::uint64_t state_hash(const SimState& st) {  // state.hpp:80-95
-    std::uint64_t h = 0;
-    detail::check(fp_state_hash(st.ctx.get(), &h), st.ctx.get());
+// state_hash (state.hpp:80-95) of the host fields, which are the state between calls (the
+// caller may have edited them, e.g. ++st.step after move_phase, as the reference's tests do).
+inline std::uint64_t state_hash(const SimState& st) {
+    std::uint64_t h = 14695981039346656037ULL;  // FNV-1a 64 over step, alive, (id, x, y, alive)*
+    auto mix = [&h](std::uint64_t v) {
+        h ^= v;
+        h *= 1099511628211ULL;
+    };
+    mix(static_cast<std::uint64_t>(st.step));
+    mix(static_cast<std::uint64_t>(st.alive));
+    for (const Agent& a : st.agents) {
+        mix(a.id);
+        mix(static_cast<std::uint32_t>(a.pos.x));
+        mix(static_cast<std::uint32_t>(a.pos.y));
+        mix(a.alive ? 1u : 0u);
+    }
     return h;
 }
 
