@@ -277,7 +277,7 @@ def main():
         st2.set_agents(hx, hy, ha)
         upd2 += int(ha.sum())
         fp.step(st2, params)
-        hx, hy, ha = st2.agents()
+        st2.agents(out=(hx, hy, ha))  # D2H into the same pinned buffers: next step's input
     torch.cuda.synchronize()
     e2e_wall = time.perf_counter() - t0
     e2e = {"value": upd2 / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": n * 9, "d2h_bytes_per_step": n * 9,

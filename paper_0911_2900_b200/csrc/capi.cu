@@ -104,7 +104,10 @@ __global__ void sc_step_kernel(DevScalars* sc) { sc->step += 1; }
 __global__ void build_occ_kernel(const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
                                  Geo g, uint32_t* occ, unsigned long long* errs) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n || !alive[i]) return;
+    const bool live = i < n && alive[i];
+    const unsigned cnt = __popc(__ballot_sync(0xffffffffu, live));  // alive count -> errs[3]
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&errs[3], (unsigned long long)cnt);
+    if (!live) return;
     const int ax = g.wrap(x[i]), ay = y[i];
     if (ax < 0 || ax >= g.W || ay < 0 || ay >= g.H) {
         atomicMin(&errs[0], (unsigned long long)i);
@@ -337,25 +340,21 @@ static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const ui
     else
         FP_CUDA(c, cudaMemsetAsync(c->d_alive, 1, n, s));
     FP_CUDA(c, cudaMemsetAsync(c->d_occ, 0, (size_t)c->P * c->H * 4, s));
-    unsigned long long init[3] = {~0ull, ~0ull, ~0ull};
-    FP_CUDA(c, cudaMemcpyAsync(c->d_counters + 8, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    // [0..2] first failing agent per make_state check (state.hpp:46-70), [3] alive count
+    FP_CUDA(c, cudaMemsetAsync(c->d_counters + 8, 0xFF, 3 * 8, s));
+    FP_CUDA(c, cudaMemsetAsync(c->d_counters + 11, 0, 8, s));
     if (n) {
         build_occ_kernel<<<fp_blocks(n, 256), 256, 0, s>>>(c->d_x, c->d_y, c->d_alive, n, geo_of(c), c->d_occ,
                                                             c->d_counters + 8);
         FP_LAUNCHED(c);
     }
-    FP_CUDA(c, cudaMemcpyAsync(c->h_counters + 8, c->d_counters + 8, 3 * 8, cudaMemcpyDeviceToHost, s));
+    FP_CUDA(c, cudaMemcpyAsync(c->h_counters + 8, c->d_counters + 8, 4 * 8, cudaMemcpyDeviceToHost, s));
     FP_CUDA(c, cudaStreamSynchronize(s));
     const unsigned long long* e = c->h_counters + 8;
     if (e[0] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[0]) + " is out of bounds");
     if (e[1] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[1]) + " placed on a Wall cell");
     if (e[2] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[2]) + " shares a cell");
-    int64_t al = 0;
-    if (alive)
-        for (uint32_t i = 0; i < n; ++i) al += alive[i] != 0;
-    else
-        al = n;
-    c->alive = al;
+    c->alive = (int64_t)e[3];
     c->bucket_fresh = false;
     c->rec_fresh = false;
     if (int rc = fp_ghost_occ(c)) return rc;
@@ -476,12 +475,40 @@ extern "C" int fp_move(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
     return move_impl(c, seed, out);
 }
 
+static int capture(fp_ctx* c, double k_s, uint64_t seed);
+
+// step(): one replay of the run() graphs (plan with the order on a forked stream, then motion and
+// the step advance), one host sync, then the exit list in processing order.
 extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     cudaSetDevice(c->device);
-    if (int rc = fp_plan(c, k_s, seed)) return rc;
-    if (int rc = move_impl(c, seed, out)) return rc;
-    c->step++;
+    if (c->alive == 0 || c->n == 0) {  // engine.hpp:73: nothing to plan or move
+        c->n_order = 0;
+        c->n_exits = 0;
+        c->last_displacement = 0;
+        c->step++;
+        if (out) *out = fp_step_stats{c->alive, 0, 0};
+        return sync_scalars(c);
+    }
+    if (int rc = prepare(c, k_s)) return rc;
+    if (!c->graph_valid || c->graph_ks != k_s || c->graph_seed != seed)
+        if (int rc = capture(c, k_s, seed)) return rc;
+    const int64_t alive0 = c->alive;
+    if (int rc = sync_scalars(c)) return rc;
+    FP_CUDA(c, cudaGraphLaunch(c->graph_plan, c->stream));
+    FP_CUDA(c, cudaGraphLaunch(c->graph_move, c->stream));
+    c->ctr.kernel_launches += c->launches_per_step;
+    if (int rc = read_scalars(c)) return rc;
+    c->ctr.planned_agents += alive0;
+    c->n_order = (uint32_t)c->h_sc->n_alive;
+    c->n_exits = (uint32_t)c->h_sc->n_exits;
+    c->last_displacement = (int64_t)c->h_sc->disp;
+    if (int rc = fp_exits_finish(c)) return rc;
+    if (out) {
+        out->alive = c->alive;
+        out->exited = alive0 - c->alive;
+        out->displacement_cells = c->last_displacement;
+    }
     return FP_OK;
 }
 

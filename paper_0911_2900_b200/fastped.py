@@ -383,11 +383,19 @@ class SimState:
         return v.value
 
     # -- dumps
-    def agents(self):
-        n = max(self.n, 1)
-        x = np.empty(n, np.int32)
-        y = np.empty(n, np.int32)
-        a = np.empty(n, np.uint8)
+    def agents(self, out=None):
+        """(x, y, alive) of every agent; `out` = three caller-owned (e.g. pinned) arrays to fill."""
+        if out is None:
+            n = max(self.n, 1)
+            x = np.empty(n, np.int32)
+            y = np.empty(n, np.int32)
+            a = np.empty(n, np.uint8)
+        else:
+            x, y, a = out
+            if not (x.dtype == np.int32 and y.dtype == np.int32 and a.dtype == np.uint8 and len(x) >= self.n
+                    and len(y) >= self.n and len(a) >= self.n and x.flags.c_contiguous and y.flags.c_contiguous
+                    and a.flags.c_contiguous):
+                raise ValueError("agents(out=...): need contiguous int32, int32, uint8 arrays of n elements")
         _check(library().fp_get_agents(self._ctx, x.ctypes.data, y.ctypes.data, a.ctypes.data), self._ctx)
         return x[: self.n], y[: self.n], a[: self.n]
 
