@@ -21,6 +21,7 @@ import subprocess
 import sys
 import threading
 import time
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -216,7 +217,7 @@ def main():
                   f"({secs:.1f} s, reference run() with ScheduleParams{{cores={c}}}, {cpu_model()})")
         out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps_done,
                "warmup": 0, "ms_per_step": secs / steps_done * 1e3, "higher_is_better": True,
-               "impl": "reference", "dtype": "f64", "data": "synthetic", "scaling": "weak",
+               "impl": "reference", "dtype": "f64", "data": "synthetic", "scaling": "strong",
                "vs_baseline": None, "config": config_desc,
                "cpu_baseline": {"value": v, "unit": UNIT, "cores": c, "kind": kind, "sample": sample},
                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -228,7 +229,11 @@ def main():
     from paper_0911_2900_b200 import fastped as fp
 
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("FASTPED_DIST_BACKEND") == "gloo":  # functional check of the N>1 path on one GPU
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     wl = build_workload(args.config, args.seed)
     ro = wl.roster
@@ -237,9 +242,25 @@ def main():
     if wl.potential:
         st.set_potential(wl.potential, wl.drive_gradient)
     params = fp.SimParams(k_s=wl.k_s, seed=wl.seed, steps=max(1, args.warmup))
+    from paper_0911_2900_b200.dist import StripStepper, aggregate
+    stepper = StripStepper(st) if world > 1 else None  # x-strip planning + replicated motion
+
+    def strip_run(steps):
+        """`steps` decomposed steps, device-timed (CUDA events; every engine call is synchronous)."""
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        upd = 0
+        ev0.record()
+        for _ in range(steps):
+            upd += st.alive
+            stepper.step(params)
+        ev1.record()
+        ev1.synchronize()
+        return SimpleNamespace(wall_time_s=ev0.elapsed_time(ev1) * 1e-3, agent_updates=upd, steps=steps,
+                               plan_time_s=None, move_time_s=None)
+
     # warm-up steps, then reset the roster to the initial state (untimed)
     if args.warmup > 0:
-        fp.run(st, params)
+        fp.run(st, params) if stepper is None else strip_run(args.warmup)
     st.set_agents(ro.x, ro.y, ro.alive)
     st.step = 0
     # the plan kernel alone (CUDA events on its stream) on the start state; again on the end
@@ -253,7 +274,7 @@ def main():
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects these launches
-        rs = fp.run(st, params)
+        rs = fp.run(st, params) if stepper is None else strip_run(args.steps)
         torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     c1 = st.counters()
@@ -261,8 +282,9 @@ def main():
     kernel_ms1 = st.time_plan_kernel(wl.k_s, wl.seed, 20)
     kernel_ms = 0.5 * (kernel_ms0 + kernel_ms1)
     U1 = coverage_u(wl.grid, x1, y1, ro.v_max, a1)
-    from paper_0911_2900_b200.dist import aggregate
-    wall, updates = aggregate(rs.wall_time_s, rs.agent_updates)  # max time, summed updates over ranks
+    # max time over ranks; the agent updates are the one simulation's (identical on every rank)
+    wall, updates = aggregate(rs.wall_time_s, rs.agent_updates)
+    updates /= world
     value = updates / wall
 
     # e2e: the C ABI with host buffers, every step H2D roster + step + D2H positions/alive
@@ -276,13 +298,15 @@ def main():
     upd2 = 0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    stepper2 = StripStepper(st2) if world > 1 else None
     for _ in range(e2e_steps):
         st2.set_agents(hx, hy, ha)
         upd2 += int(ha.sum())
-        fp.step(st2, params)
+        fp.step(st2, params) if stepper2 is None else stepper2.step(params)
         st2.agents(out=(hx, hy, ha))  # D2H into the same pinned buffers: next step's input
     torch.cuda.synchronize()
     e2e_wall = time.perf_counter() - t0
+    e2e_wall, _ = aggregate(e2e_wall, 0.0)  # slowest rank
     e2e = {"value": upd2 / e2e_wall, "unit": UNIT, "h2d_bytes_per_step": n * 9, "d2h_bytes_per_step": n * 9,
            "steps": e2e_steps, "path": "fp_update_agents + fp_step + fp_get_agents (C ABI, host arrays)"}
 
@@ -325,9 +349,11 @@ def main():
     config_desc.update(n_agents=n, grid=[wl.grid.width, wl.grid.height], mixed_v=mixed)
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": wall / max(rs.steps, 1) * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": config_desc, "parallelism": "replicas" if world > 1 else "single",
-           "phases_ms": {"plan": rs.plan_time_s * 1e3, "move": rs.move_time_s * 1e3, "total": rs.wall_time_s * 1e3},
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_desc,
+           "parallelism": f"x-strips{world} plan + NCCL all-reduce + replicated motion" if world > 1 else "single",
+           "phases_ms": ({"plan": rs.plan_time_s * 1e3, "move": rs.move_time_s * 1e3, "total": rs.wall_time_s * 1e3}
+                         if stepper is None else {"total": rs.wall_time_s * 1e3}),
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
            "realtime_capacity": capacity,
            "gpu_launches": int(c1["kernel_launches"] - c0["kernel_launches"]),

@@ -125,6 +125,14 @@ int fp_set_desired(fp_ctx* ctx, const int32_t* x, const int32_t* y);
 /* plan_phase(st, params, sched) -- engine.hpp:71-84: desired cell of every alive agent,
  * bit-identical to choose_desired_cell (planning.hpp:88-108). */
 int fp_plan(fp_ctx* ctx, double k_s, uint64_t seed);
+/* Multi-GPU x-strip decomposition of plan_phase: plans only
+ * the alive agents whose x lies in [x_lo, x_hi) and sets the desired cell of every other alive
+ * agent to (0, 0), so that a SUM all-reduce of the desired arrays over ranks whose strips tile
+ * the grid yields plan_phase's result bit for bit.  fp_desired_device exposes the two device
+ * arrays (int32[n] each, on the context's device) for that in-place collective; the motion
+ * (fp_move) then runs on every rank on identical inputs. */
+int fp_plan_strip(fp_ctx* ctx, double k_s, uint64_t seed, int32_t x_lo, int32_t x_hi);
+int fp_desired_device(fp_ctx* ctx, void** dx, void** dy);
 /* move_phase(st, params) -- engine.hpp:95-135 (does not advance the step counter).
  * Exited ids (processing order) are kept for fp_get_exited. */
 int fp_move(fp_ctx* ctx, uint64_t seed, fp_step_stats* out);

@@ -9,12 +9,20 @@
 
 #include "internal.cuh"
 
+// Agents outside the planned x strip [strip_lo, strip_hi) (multi-GPU decomposition, DESIGN.md
+// §6) are not bucketed and get desired = (0, 0), so a sum over the ranks' strips is the plan.
 __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
                                     int tile_w, int tile_h, int tiles_x, uint32_t* cnt, uint32_t* tile_of,
-                                    uint32_t* slot) {
+                                    uint32_t* slot, int strip_lo, int strip_hi, int32_t* dx, int32_t* dy) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         if (!alive[i]) continue;
         const int px = g.wrap(x[i]), py = y[i];
+        if (px < strip_lo || px >= strip_hi) {
+            tile_of[i] = FP_NONE;
+            dx[i] = 0;
+            dy[i] = 0;
+            continue;
+        }
         const uint32_t t = (uint32_t)(py / tile_h) * (uint32_t)tiles_x + (uint32_t)(px / tile_w);
         tile_of[i] = t;
         slot[i] = atomicAdd(&cnt[t], 1u);
@@ -24,7 +32,7 @@ __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, c
 __global__ void bucket_scatter_kernel(const uint8_t* alive, uint32_t n, const uint32_t* tile_of, const uint32_t* slot,
                                       const uint32_t* off, uint32_t* bucket) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (!alive[i]) continue;
+        if (!alive[i] || tile_of[i] == FP_NONE) continue;
         bucket[off[tile_of[i]] + slot[i]] = i;
     }
 }
@@ -72,7 +80,8 @@ int fp_bucket_launch(fp_ctx* ctx) {
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_cnt, 0, nt * 4, s));
     const unsigned G = (unsigned)std::min<size_t>(fp_blocks(n, 256), (size_t)ctx->sm_count * 16);
     bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_alive, n, ctx->tile_w, ctx->tile_h,
-                                          ctx->tiles_x, ctx->d_tile_cnt, ctx->d_flags, ctx->d_cursor_b);
+                                          ctx->tiles_x, ctx->d_tile_cnt, ctx->d_flags, ctx->d_cursor_b, ctx->strip_lo,
+                                          ctx->strip_hi, ctx->d_dx, ctx->d_dy);
     FP_LAUNCHED(ctx);
     size_t need1 = 0, need2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_tile_cnt, ctx->d_tile_off, (int)nt, s);

@@ -446,6 +446,29 @@ extern "C" int fp_plan(fp_ctx* c, double k_s, uint64_t seed) {
     return read_scalars(c);
 }
 
+extern "C" int fp_plan_strip(fp_ctx* c, double k_s, uint64_t seed, int32_t x_lo, int32_t x_hi) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (x_lo < 0 || x_hi > c->W || x_lo >= x_hi)
+        return fail(c, FP_EINVAL, "fp_plan_strip: need 0 <= x_lo < x_hi <= width");
+    c->strip_lo = x_lo;
+    c->strip_hi = x_hi;
+    const int rc = fp_plan(c, k_s, seed);
+    c->strip_lo = 0;
+    c->strip_hi = 0x7FFFFFFF;
+    // the desired cells will be completed by the other ranks: the plan's walk records and tile
+    // buckets cover this strip only, so the motion builds its own from the order list
+    c->rec_fresh = false;
+    c->bucket_fresh = false;
+    return rc;
+}
+
+extern "C" int fp_desired_device(fp_ctx* c, void** dx, void** dy) {
+    if (!c || !dx || !dy) return fail(c, FP_EINVAL, "null argument");
+    *dx = c->d_dx;
+    *dy = c->d_dy;
+    return FP_OK;
+}
+
 // order + motion on the main stream (API path), then the exit list in processing order.
 static int move_impl(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
     if (int rc = fp_order_reserve(c)) return rc;

@@ -158,6 +158,7 @@ struct fp_ctx {
     CUtensorMap tmap_plane;          // TMA descriptor of the plane (one tile box)
     CUtensorMap tmap_occ;            // TMA descriptor of the occupancy bitplane (16-word box)
     int tile_w = 0, tile_h = 0;      // plan tile (cells)
+    int strip_lo = 0, strip_hi = 0x7FFFFFFF;  // x range planned (fp_plan_strip; full otherwise)
     int tiles_x = 0, tiles_y = 0;
     bool tiles_ok = false;           // tiled fast path usable for this grid
     int use_tma = 1;                 // FP_NO_TMA=1 stages plan tiles with plain loads

@@ -88,6 +88,7 @@ struct PlanCommon {
     double k_s;
     uint64_t seed;
     DevScalars* sc;
+    int strip_lo, strip_hi;  // planned x range (full grid unless fp_plan_strip)
 };
 
 __device__ __forceinline__ bool occ_bit(const uint32_t* occ, const Geo& g, int x, int y) {
@@ -205,6 +206,12 @@ __device__ __noinline__ void choose_exact(const PlanCommon& a, uint32_t i, uint6
 __global__ void plan_exact_kernel(PlanCommon a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n || !a.alive[i]) return;
+    const int px = a.g.wrap(a.x[i]);
+    if (px < a.strip_lo || px >= a.strip_hi) {  // another rank's strip (bucket.cu)
+        a.dx[i] = 0;
+        a.dy[i] = 0;
+        return;
+    }
     int cx, cy;
     choose_exact(a, i, (uint64_t)a.sc->step, &cx, &cy);
     a.dx[i] = cx;
@@ -745,6 +752,8 @@ static PlanCommon make_common(fp_ctx* ctx, double k_s, uint64_t seed) {
     a.k_s = k_s;
     a.seed = seed;
     a.sc = ctx->d_sc;
+    a.strip_lo = ctx->strip_lo;
+    a.strip_hi = ctx->strip_hi;
     return a;
 }
 

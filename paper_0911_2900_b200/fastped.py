@@ -78,6 +78,8 @@ SIGNATURES = {
     "fp_set_potential": (C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     "fp_set_desired": (C.c_int, [C.c_void_p, _i32p, _i32p]),
     "fp_plan": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64]),
+    "fp_plan_strip": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.c_int32]),
+    "fp_desired_device": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "fp_move": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(_StepStats)]),
     "fp_step": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.POINTER(_StepStats)]),
     "fp_run": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.POINTER(_RunStats)]),
@@ -441,6 +443,16 @@ class SimState:
         _check(library().fp_get_choice(self._ctx, agent, k_s, cx, cy, w, p, 128, C.byref(n)), self._ctx)
         k = n.value
         return cx[:k].copy(), cy[:k].copy(), w[:k].copy(), p[:k].copy()
+
+    def plan_strip(self, k_s: float, seed: int, x_lo: int, x_hi: int):
+        """plan_phase restricted to agents with x in [x_lo, x_hi); the others get desired (0, 0)."""
+        _check(library().fp_plan_strip(self._ctx, k_s, seed, x_lo, x_hi), self._ctx)
+
+    def desired_device(self):
+        """Device addresses of the desired x / y arrays (int32[n]) for an in-place collective."""
+        dx, dy = C.c_void_p(), C.c_void_p()
+        _check(library().fp_desired_device(self._ctx, C.byref(dx), C.byref(dy)), self._ctx)
+        return dx.value, dy.value
 
     def time_plan_kernel(self, k_s: float, seed: int, iters: int = 10) -> float:
         """Average plan-kernel launch duration in ms (CUDA events), for the roofline."""
