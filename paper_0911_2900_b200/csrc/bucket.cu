@@ -9,10 +9,13 @@
 
 #include "internal.cuh"
 
-// Agents outside the planned x strip [strip_lo, strip_hi) (multi-GPU decomposition, DESIGN.md
-// §6) are not bucketed and get desired = (0, 0), so a sum over the ranks' strips is the plan.
-__global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
-                                    int tile_w, int tile_h, int tiles_x, uint32_t* cnt, uint32_t* tile_of,
+// Agents are counted per (tile, v_max) sub-bucket, so each tile's agents come out ordered by
+// v_max and the plan kernel's warps run one ball size (mixed-v rosters otherwise diverge over
+// four unrolled variants and thrash the instruction cache).  Agents outside the planned x strip
+// [strip_lo, strip_hi) (multi-GPU decomposition) are not bucketed and get
+// desired = (0, 0), so a sum over the ranks' strips is the plan.
+__global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* v, const uint8_t* alive,
+                                    uint32_t n, int tile_w, int tile_h, int tiles_x, uint32_t* cnt, uint32_t* tile_of,
                                     uint32_t* slot, int strip_lo, int strip_hi, int32_t* dx, int32_t* dy) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         if (!alive[i]) continue;
@@ -23,7 +26,8 @@ __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, c
             dy[i] = 0;
             continue;
         }
-        const uint32_t t = (uint32_t)(py / tile_h) * (uint32_t)tiles_x + (uint32_t)(px / tile_w);
+        const uint32_t t = ((uint32_t)(py / tile_h) * (uint32_t)tiles_x + (uint32_t)(px / tile_w)) * 5u +
+                           (uint32_t)(v[i] - 1);  // v_max in 1..5
         tile_of[i] = t;
         slot[i] = atomicAdd(&cnt[t], 1u);
     }
@@ -34,6 +38,16 @@ __global__ void bucket_scatter_kernel(const uint8_t* alive, uint32_t n, const ui
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         if (!alive[i] || tile_of[i] == FP_NONE) continue;
         bucket[off[tile_of[i]] + slot[i]] = i;
+    }
+}
+
+// per-tile count and offset from the (tile, v_max) sub-buckets
+__global__ void tile_sums_kernel(const uint32_t* sub_cnt, const uint32_t* sub_off, uint32_t nt, uint32_t* cnt,
+                                 uint32_t* off) {
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        const uint32_t* c = sub_cnt + (size_t)t * 5;
+        cnt[t] = c[0] + c[1] + c[2] + c[3] + c[4];
+        off[t] = sub_off[(size_t)t * 5];
     }
 }
 
@@ -48,6 +62,10 @@ int fp_bucket_reserve(fp_ctx* ctx) {
         if (ctx->d_tile_cnt) cudaFree(ctx->d_tile_cnt);
         if (ctx->d_tile_off) cudaFree(ctx->d_tile_off);
         if (ctx->d_tile_list) cudaFree(ctx->d_tile_list);
+        if (ctx->d_sub_cnt) cudaFree(ctx->d_sub_cnt);
+        if (ctx->d_sub_off) cudaFree(ctx->d_sub_off);
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_sub_cnt, nt * 5 * 4));
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_sub_off, nt * 5 * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_cnt, nt * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_off, nt * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_list, nt * 4));
@@ -55,7 +73,7 @@ int fp_bucket_reserve(fp_ctx* ctx) {
         ctx->graph_valid = false;
     }
     size_t need1 = 0, need2 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_tile_cnt, ctx->d_tile_off, (int)nt, ctx->stream);
+    cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_sub_cnt, ctx->d_sub_off, (int)(nt * 5), ctx->stream);
     thrust::counting_iterator<uint32_t> it(0);
     cub::DeviceSelect::If(nullptr, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt,
                           NonEmpty{ctx->d_tile_cnt}, ctx->stream);
@@ -77,23 +95,26 @@ int fp_bucket_launch(fp_ctx* ctx) {
     cudaStream_t s = ctx->stream;
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
     const uint32_t n = ctx->n;
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_cnt, 0, nt * 4, s));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_sub_cnt, 0, nt * 5 * 4, s));
     const unsigned G = (unsigned)std::min<size_t>(fp_blocks(n, 256), (size_t)ctx->sm_count * 16);
-    bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_alive, n, ctx->tile_w, ctx->tile_h,
-                                          ctx->tiles_x, ctx->d_tile_cnt, ctx->d_flags, ctx->d_cursor_b, ctx->strip_lo,
-                                          ctx->strip_hi, ctx->d_dx, ctx->d_dy);
+    bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, ctx->d_alive, n, ctx->tile_w,
+                                          ctx->tile_h, ctx->tiles_x, ctx->d_sub_cnt, ctx->d_flags, ctx->d_cursor_b,
+                                          ctx->strip_lo, ctx->strip_hi, ctx->d_dx, ctx->d_dy);
     FP_LAUNCHED(ctx);
     size_t need1 = 0, need2 = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_tile_cnt, ctx->d_tile_off, (int)nt, s);
+    cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_sub_cnt, ctx->d_sub_off, (int)(nt * 5), s);
     thrust::counting_iterator<uint32_t> it(0);
     cub::DeviceSelect::If(nullptr, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt, NonEmpty{ctx->d_tile_cnt}, s);
     if (std::max(need1, need2) > ctx->temp_b_bytes) return fp_fail(ctx, FP_ERUNTIME, "bucket: scratch not reserved");
-    FP_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_temp_b, need1, ctx->d_tile_cnt, ctx->d_tile_off, (int)nt, s));
+    FP_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_temp_b, need1, ctx->d_sub_cnt, ctx->d_sub_off, (int)(nt * 5), s));
     ctx->ctr.kernel_launches += 2;
+    tile_sums_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s>>>(
+        ctx->d_sub_cnt, ctx->d_sub_off, (uint32_t)nt, ctx->d_tile_cnt, ctx->d_tile_off);
+    FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cub::DeviceSelect::If(ctx->d_temp_b, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt,
                                        NonEmpty{ctx->d_tile_cnt}, s));
     ctx->ctr.kernel_launches += 2;
-    bucket_scatter_kernel<<<G, 256, 0, s>>>(ctx->d_alive, n, ctx->d_flags, ctx->d_cursor_b, ctx->d_tile_off, ctx->d_bucket);
+    bucket_scatter_kernel<<<G, 256, 0, s>>>(ctx->d_alive, n, ctx->d_flags, ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
