@@ -366,8 +366,13 @@ extern "C" int fp_set_agents(fp_ctx* c, uint32_t n, const int32_t* x, const int3
                              const uint8_t* alive, int64_t step) {
     if (!c) return fail(nullptr, FP_EINVAL, "fp_set_agents: null context");
     if (n && (!x || !y || !v_max)) return fail(c, FP_EINVAL, "fp_set_agents: null roster arrays");
-    for (uint32_t i = 0; i < n; ++i)
+    bool mixed = false;
+    for (uint32_t i = 0; i < n; ++i) {
         if (v_max[i] < 1 || v_max[i] > 5) return fail(c, FP_EINVAL, "make_state: v_max must be in [1,5]");
+        mixed |= v_max[i] != v_max[0];
+    }
+    if (mixed != c->mixed_v) c->graph_valid = false;  // the plan kernel variant changes
+    c->mixed_v = mixed;
     cudaSetDevice(c->device);
     if (int rc = ensure_agents(c, n)) return rc;
     c->n = n;

@@ -254,6 +254,7 @@ struct TileArgs {
     uint32_t* p1;          // contention marks
     uint32_t* p2;
     int emit;
+    int mixed;  // roster has more than one v_max: the masked radius-5 variant for everyone
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -328,12 +329,17 @@ __device__ __forceinline__ double exit_weight(uint32_t w, int cp_biased /* C_p +
 //           visible) contribute their weight to an fp64 row sum;
 //   pass 2  u*total picks the row; the row is replayed in list order (wrapped-x sorted at a
 //           periodic seam) to find the first cumulative weight > threshold; guard band.
-template <int V, bool DRIVE>
+// MASKED: one radius-V code path for every v_max <= V (mixed rosters): rows and columns beyond
+// the agent's own radius vr are masked out, which leaves exactly its Chebyshev ball (the line
+// of sight to a cell of the ball only crosses cells of the ball), so decisions are unchanged
+// while the warps of a mixed roster share one instruction stream.
+template <int V, bool DRIVE, bool MASKED = false>
 __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* buf, const uint32_t* occs, int osh0,
                                            int x0, int y0, int px, int py, double u, const double* drive_tab,
-                                           int* ox, int* oy) {
+                                           int* ox, int* oy, int vr = V) {
     constexpr int D = 2 * V + 1;
     const PlanCommon& a = A.c;
+    const uint32_t colmask = MASKED ? (((1u << (2 * vr + 1)) - 1u) << (V - vr)) : ((1u << D) - 1u);
     const int X0 = x0 - 8;  // box origin (TMA inner coordinates stay 16-byte aligned)
     const int lx = px - X0, ly = py - (y0 - FP_HALO);
     int cpb = 0;
@@ -362,7 +368,8 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
         const uint32_t* orow = occs + (ly + dy) * A.occw;
         uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
         if (dy == 0) occ &= ~(1u << V);  // the own cell stays a candidate (planning.hpp:45-46)
-        uint32_t valid = rowok ? (~(spec | occ) & ((1u << D) - 1u)) : 0u;
+        const bool inball = !MASKED || (dy <= vr && -dy <= vr);
+        uint32_t valid = (rowok && inball) ? (~(spec | occ) & colmask) : 0u;
         if (wm.lo | wm.hi) {
 #pragma unroll
             for (int k = 0; k < D; ++k)
@@ -395,12 +402,13 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
     const uint32_t* orow = occs + (ly + dy) * A.occw;
     uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
     if (dy == 0) occ &= ~(1u << V);
-    int a0 = -V, a1 = V, b0 = 0, b1 = -1;
+    const int R = MASKED ? vr : V;  // the agent's radius
+    int a0 = -R, a1 = R, b0 = 0, b1 = -1;
     if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {  // wrapped-x order at the seam (planning.hpp:50-53)
-        if (px + V >= a.g.W) {
-            a0 = a.g.W - px; b0 = -V; b1 = a.g.W - px - 1;
-        } else if (px - V < 0) {
-            a0 = -px; b0 = -V; b1 = -px - 1;
+        if (px + R >= a.g.W) {
+            a0 = a.g.W - px; b0 = -R; b1 = a.g.W - px - 1;
+        } else if (px - R < 0) {
+            a0 = -px; b0 = -R; b1 = -px - 1;
         }
     }
     const bool anywall = (wm.lo | wm.hi) != 0ull;
@@ -442,6 +450,8 @@ template <bool DRIVE>
 __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint32_t* buf, const uint32_t* occs,
                                            int osh0, int x0, int y0, int px, int py, double u,
                                            const double* drive_tab, int* ox, int* oy) {
+    if (A.mixed)  // one instruction stream for a mixed-v roster (see plan_fast_t)
+        return plan_fast_t<5, DRIVE, true>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy, v);
     switch (v) {
         case 1: return plan_fast_t<1, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
         case 2: return plan_fast_t<2, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
@@ -797,6 +807,7 @@ static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& s
     A.p1 = ctx->d_p1;
     A.p2 = ctx->d_p2;
     A.emit = 1;
+    A.mixed = ctx->mixed_v ? 1 : 0;
     tile_geometry(ctx, A, smem);
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
     grid = (unsigned)std::min<size_t>((size_t)ctx->sm_count, nt);
