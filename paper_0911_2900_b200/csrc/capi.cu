@@ -141,7 +141,7 @@ static void free_agents(fp_ctx* c) {
                     c->d_order, c->d_j, c->d_cnt, c->d_off, c->d_cursor, c->d_bucket, c->d_succ,
                     c->d_nxt, c->d_V, c->d_pend_a, c->d_pend_b, c->d_exits, c->d_exits_sorted,
                     c->d_fy_bucket, c->d_flags, c->d_cursor_b, c->d_fallback, c->d_rec_a, c->d_rec_b,
-                    c->d_rec0, c->d_entry};
+                    c->d_rec0, c->d_entry, c->d_brec};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     c->d_entry = nullptr;
@@ -154,6 +154,7 @@ static void free_agents(fp_ctx* c) {
     c->d_fy_bucket = c->d_flags = c->d_cursor_b = nullptr;
     c->d_fallback = nullptr;
     c->d_rec_a = c->d_rec_b = c->d_rec0 = nullptr;
+    c->d_brec = nullptr;
     c->rec_fresh = false;
     c->cap = 0;
     c->graph_valid = false;
@@ -178,6 +179,7 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
     FP_CUDA(c, cudaMalloc(&c->d_rec_a, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_rec_b, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_rec0, m * sizeof(uint4)));
+    FP_CUDA(c, cudaMalloc(&c->d_brec, m * sizeof(uint4)));
     FP_CUDA(c, cudaMalloc(&c->d_fallback, m * sizeof(uint2)));
     c->cap = (uint32_t)m;
     c->graph_valid = false;

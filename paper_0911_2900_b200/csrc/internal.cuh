@@ -180,6 +180,7 @@ struct fp_ctx {
     // tile buckets
     uint32_t *d_tile_cnt = nullptr, *d_tile_off = nullptr, *d_tile_list = nullptr, *d_bucket = nullptr;
     uint32_t *d_sub_cnt = nullptr, *d_sub_off = nullptr;  // (tile, v_max) sub-buckets
+    uint4* d_brec = nullptr;  // per bucket slot: (id, x, y, v_max) for the plan kernel
     size_t n_tiles_alloc = 0;
 
     // order scratch (sized by cap)

@@ -243,6 +243,7 @@ struct TileArgs {
     int PW;
     const uint32_t* plane;
     const uint32_t* bucket;
+    const uint4* brec;
     const uint32_t* tile_off;
     const uint32_t* tile_cnt;
     const uint32_t* tile_list;
@@ -586,9 +587,10 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         }
         int mine = 0;
         for (; k < cnt; k += PLAN_THREADS) {
-            const uint32_t id = A.bucket[off + k];
-            const int px = a.g.wrap(a.x[id]), py = a.y[id];
-            const int v = a.v[id];
+            const uint4 br = __ldcg(&A.brec[off + k]);  // (id, wrapped x, y, v_max), bucket.cu
+            const uint32_t id = br.x;
+            const int px = (int)br.y, py = (int)br.z;
+            const int v = (int)br.w;
             const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
             int cx = 0, cy = 0;
             const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
@@ -796,6 +798,7 @@ static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& s
     A.plane = ctx->d_plane;
     A.use_tma = ctx->use_tma;
     A.bucket = ctx->d_bucket;
+    A.brec = ctx->d_brec;
     A.tile_off = ctx->d_tile_off;
     A.tile_cnt = ctx->d_tile_cnt;
     A.tile_list = ctx->d_tile_list;
