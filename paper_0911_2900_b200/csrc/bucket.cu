@@ -56,6 +56,34 @@ __global__ void tile_sums_kernel(const uint32_t* sub_cnt, const uint32_t* sub_of
     }
 }
 
+// Deals the non-empty tiles to the plan kernel's G CTAs in DEAL_PASSES passes: the list is cut
+// into G * DEAL_PASSES contiguous ranges of near-equal agent counts (the range of entry e is
+// floor(agent offset * G * DEAL_PASSES / total)), and range p*G + b goes to CTA b in its pass p.
+// Crowded tiles do not pile up on a few CTAs, and at any time the CTAs work on neighbouring
+// parts of the list (DRAM/L2 locality of the concurrent TMA fetches).  The range index is
+// monotonic in e, so each boundary first[r] is written by exactly one entry.
+__global__ void tile_deal_kernel(const uint32_t* list, const uint32_t* off, const uint32_t* cnt,
+                                 const unsigned long long* n_tiles_p, int G, int passes, uint32_t* first) {
+    G *= passes;  // ranges
+    const uint32_t n = (uint32_t)*n_tiles_p;
+    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    if (n == 0) {
+        for (uint32_t b = gt; b <= (uint32_t)G; b += gs) first[b] = 0;
+        return;
+    }
+    const uint32_t last = list[n - 1];
+    const unsigned long long total = (unsigned long long)off[last] + cnt[last];
+    auto owner = [&](uint32_t e) -> int {
+        return (int)min((unsigned long long)(G - 1), (unsigned long long)off[list[e]] * (unsigned)G / total);
+    };
+    for (uint32_t e = gt; e < n; e += gs) {
+        const int o = owner(e), prev = e ? owner(e - 1) : -1;
+        for (int b = prev + 1; b <= o; ++b) first[b] = e;
+        if (e == n - 1)
+            for (int b = o + 1; b <= G; ++b) first[b] = n;
+    }
+}
+
 struct NonEmpty {
     const uint32_t* cnt;
     __device__ __forceinline__ bool operator()(uint32_t t) const { return cnt[t] != 0; }
@@ -70,6 +98,8 @@ int fp_bucket_reserve(fp_ctx* ctx) {
         if (ctx->d_sub_cnt) cudaFree(ctx->d_sub_cnt);
         if (ctx->d_sub_off) cudaFree(ctx->d_sub_off);
         FP_CUDA(ctx, cudaMalloc(&ctx->d_sub_cnt, nt * 5 * 4));
+        if (!ctx->d_tile_deal)
+            FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_deal, ((size_t)ctx->sm_count * DEAL_PASSES + 1) * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_sub_off, nt * 5 * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_cnt, nt * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_off, nt * 4));
@@ -119,6 +149,10 @@ int fp_bucket_launch(fp_ctx* ctx) {
     FP_CUDA(ctx, cub::DeviceSelect::If(ctx->d_temp_b, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt,
                                        NonEmpty{ctx->d_tile_cnt}, s));
     ctx->ctr.kernel_launches += 2;
+    tile_deal_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s>>>(
+        ctx->d_tile_list, ctx->d_tile_off, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->sm_count, ctx->deal_passes,
+        ctx->d_tile_deal);
+    FP_LAUNCHED(ctx);
     bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, ctx->d_alive, n, ctx->d_flags,
                                             ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket, ctx->d_brec);
     FP_LAUNCHED(ctx);

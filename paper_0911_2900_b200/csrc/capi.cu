@@ -217,6 +217,7 @@ extern "C" int fp_create(const fp_grid_desc* g, const uint8_t* cells, const doub
         return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaStreamCreate"));
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (const char* e2 = getenv("FP_NO_TMA")) c->use_tma = (e2[0] == '1') ? 0 : 1;
+    if (const char* e3 = getenv("FP_DEAL_PASSES")) c->deal_passes = std::max(1, std::min(DEAL_PASSES, atoi(e3)));
     c->W = g->width;
     c->H = g->height;
     c->boundary = g->boundary;
@@ -264,7 +265,8 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
     void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_counters, c->d_temp, c->d_temp_b,
-                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_sc,
+                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal,
+                    c->d_sc,
                     c->d_p1, c->d_p2,
                     c->d_bkt, c->d_pool_owner};
     for (void* p : ptrs)

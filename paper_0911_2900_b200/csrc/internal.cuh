@@ -26,6 +26,7 @@
 #define FP_XPAD_BITS 32  // ghost columns left of x = 0 in the bitplanes
 #define FP_XPAD_W 8      // ghost columns left of x = 0 in the weight plane
 #define FP_HALO 5        // largest v_max (agents.hpp:10)
+#define DEAL_PASSES 16   // plan-tile deal: most passes over the tile list (bucket.cu)
 
 // weight-plane word encoding (plane.cu)
 #define FP_W_WALL 0xFFFFFFFFu
@@ -181,6 +182,8 @@ struct fp_ctx {
     uint32_t *d_tile_cnt = nullptr, *d_tile_off = nullptr, *d_tile_list = nullptr, *d_bucket = nullptr;
     uint32_t *d_sub_cnt = nullptr, *d_sub_off = nullptr;  // (tile, v_max) sub-buckets
     uint4* d_brec = nullptr;  // per bucket slot: (id, x, y, v_max) for the plan kernel
+    uint32_t* d_tile_deal = nullptr;  // [sm_count * DEAL_PASSES + 1] first tile-list entry per range
+    int deal_passes = 1;              // passes actually used (FP_DEAL_PASSES, 1..DEAL_PASSES)
     size_t n_tiles_alloc = 0;
 
     // order scratch (sized by cap)

@@ -247,6 +247,8 @@ struct TileArgs {
     const uint32_t* tile_off;
     const uint32_t* tile_cnt;
     const uint32_t* tile_list;
+    const uint32_t* deal;  // [gridDim.x * passes + 1] first list entry of each range
+    int passes;
     int tile_w, tile_h, tiles_x;
     int use_tma;  // 0: stage the box with coalesced loads (debug / comparison path)
     int boxw, boxh, occw;  // shared-memory strides (words)
@@ -489,17 +491,24 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath_p[0][0][0])[k];
     const PlanCommon& a = A.c;
     const uint64_t step = (uint64_t)a.sc->step;
-    const int n_tiles = (int)a.sc->n_tiles;
     // fetch number i into slot i & 1 (one thread)
     auto fetch = [&](int i) {
         const int slot = i & 1;
         s_gen[slot] = -1;  // seqlock: readers that raced with this refill see a changed generation
         __threadfence_block();
-        // static deal: fetch i of this CTA is list entry blockIdx.x + i * gridDim.x, so fetch
-        // numbers map monotonically onto the list and an exhausted fetch ends every later one
-        // (refills complete out of order; a shared dynamic cursor would break that)
-        const int t = (int)blockIdx.x + i * (int)gridDim.x;
-        if (t < n_tiles) {
+        // fetch i of this CTA is the i-th entry of its ranges (one per pass, bucket.cu
+        // tile_deal_kernel) taken in order, so fetch numbers map monotonically onto the list and
+        // an exhausted fetch ends every later one (refills complete out of order)
+        int t = -1;
+        for (int p = 0, k = i; p < A.passes; ++p) {
+            const int lo = (int)A.deal[p * gridDim.x + blockIdx.x], hi = (int)A.deal[p * gridDim.x + blockIdx.x + 1];
+            if (k < hi - lo) {
+                t = lo + k;
+                break;
+            }
+            k -= hi - lo;
+        }
+        if (t >= 0) {
             const uint32_t tile = A.tile_list[t];
             const int tx = (int)(tile % (uint32_t)A.tiles_x), ty = (int)(tile / (uint32_t)A.tiles_x);
             const int x0 = tx * A.tile_w, y0 = ty * A.tile_h;
@@ -802,6 +811,8 @@ static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& s
     A.tile_off = ctx->d_tile_off;
     A.tile_cnt = ctx->d_tile_cnt;
     A.tile_list = ctx->d_tile_list;
+    A.deal = ctx->d_tile_deal;
+    A.passes = ctx->deal_passes;
     A.tile_w = ctx->tile_w;
     A.tile_h = ctx->tile_h;
     A.tiles_x = ctx->tiles_x;
@@ -813,7 +824,8 @@ static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& s
     A.mixed = ctx->mixed_v ? 1 : 0;
     tile_geometry(ctx, A, smem);
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
-    grid = (unsigned)std::min<size_t>((size_t)ctx->sm_count, nt);
+    grid = (unsigned)ctx->sm_count;  // tile_deal_kernel deals to exactly sm_count CTAs
+    (void)nt;
     return A;
 }
 
