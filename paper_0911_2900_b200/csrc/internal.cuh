@@ -182,6 +182,7 @@ struct fp_ctx {
     uint32_t *d_tile_cnt = nullptr, *d_tile_off = nullptr, *d_tile_list = nullptr, *d_bucket = nullptr;
     uint32_t *d_sub_cnt = nullptr, *d_sub_off = nullptr;  // (tile, v_max) sub-buckets
     uint4* d_brec = nullptr;  // per bucket slot: (id, x, y, v_max) for the plan kernel
+    uint8_t* d_tile_exit = nullptr;   // per plan tile: an Exit within its halo window (plane.cu)
     uint32_t* d_tile_deal = nullptr;  // [sm_count * DEAL_PASSES + 1] first tile-list entry per range
     int deal_passes = 1;              // passes actually used (FP_DEAL_PASSES, 1..DEAL_PASSES)
     size_t n_tiles_alloc = 0;

@@ -247,6 +247,7 @@ struct TileArgs {
     const uint32_t* tile_off;
     const uint32_t* tile_cnt;
     const uint32_t* tile_list;
+    const uint8_t* tile_exit;  // an Exit within the tile's window
     const uint32_t* deal;  // [gridDim.x * passes + 1] first list entry of each range
     int passes;
     int tile_w, tile_h, tiles_x;
@@ -449,6 +450,37 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
     return 1;
 }
 
+// record_of (motion_rec.cuh) for a fast-path decision inside the staged tile: the target lies in
+// the ball, the Wall test reads the staged plane words, and the Exit test (global bitplane) runs
+// only in tiles whose window holds an Exit.
+__device__ __forceinline__ uint4 record_of_tile(const Geo& g, const uint32_t* occ, bool tile_exit, const uint32_t* buf,
+                                                int boxw, int lx, int ly, uint32_t id, int sx, int sy, int tx, int ty,
+                                                int v, const signed char (*bp)[5][2]) {
+    const int ddx = g.segment_dx(sx, tx), ddy = ty - sy;
+    const int o = (ddy + 5) * 11 + ddx + 5;
+    const int len = min(max(abs(ddx), abs(ddy)), v);
+    int m = 0, ex_x = 0, ex_y = 0;
+    bool ex = false;
+    for (int j = 0; j < len; ++j) {
+        const int ox = bp[o][j][0], oy = bp[o][j][1];
+        if (buf[(ly + oy) * boxw + lx + ox] == FP_W_WALL) break;
+        ++m;
+        if (tile_exit) {
+            const int x = g.wrap(sx + ox), y = sy + oy;
+            if (g.is_exit(x, y)) {
+                ex = true;
+                ex_x = x;
+                ex_y = y;
+                break;
+            }
+        }
+    }
+    const bool exit_free = ex && !((__ldcg(&occ[g.word(ex_x, ex_y)]) >> (ex_x & 31)) & 1u);
+    return make_uint4(id, 0u,
+                      (uint32_t)sx | (exit_free ? REC_EXIT_FREE : 0u) | ((uint32_t)m << 28) | (ex ? 0x80000000u : 0u),
+                      (uint32_t)sy | ((uint32_t)o << 24));
+}
+
 template <bool DRIVE>
 __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint32_t* buf, const uint32_t* occs,
                                            int osh0, int x0, int y0, int px, int py, double u,
@@ -569,7 +601,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // a refill racing with these reads may already have written tile = -1 for fetch i+2)
         if (s_gen[slot] != i) continue;  // fetch i already completed without this thread's help
         if (tile < 0) break;
-        int k = ((int)threadIdx.x - i * 160) & (PLAN_THREADS - 1);
+        int k = ((int)threadIdx.x - i * (PLAN_THREADS * 5 / 16)) & (PLAN_THREADS - 1);
         if (k >= cnt) continue;  // no agent of this fetch for this thread
         uint32_t* buf = smem + slot * box_stride;
         uint32_t* occs = smem + 2 * box_stride + slot * occ_stride;
@@ -608,7 +640,9 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
             if (st == 1) {
                 a.dx[id] = cx;
                 a.dy[id] = cy;
-                if (A.emit) A.rec0[off + k] = record_of(a.g, a.occ, id, px, py, cx, cy, v, s_bp);  // motion's walk record
+                if (A.emit)  // the motion's walk record, walls from the staged plane
+                    A.rec0[off + k] = record_of_tile(a.g, a.occ, A.tile_exit[tile], buf, A.boxw, px - (x0 - 8),
+                                                     py - (y0 - FP_HALO), id, px, py, cx, cy, v, s_bp);
             } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
                 A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, (uint32_t)(off + k));
             }
@@ -812,6 +846,7 @@ static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& s
     A.tile_cnt = ctx->d_tile_cnt;
     A.tile_list = ctx->d_tile_list;
     A.deal = ctx->d_tile_deal;
+    A.tile_exit = ctx->d_tile_exit;
     A.passes = ctx->deal_passes;
     A.tile_w = ctx->tile_w;
     A.tile_h = ctx->tile_h;

@@ -164,6 +164,28 @@ static PFN_encodeTiled get_encode() {
     return fn;
 }
 
+// Marks every tile whose window (tile + FP_HALO cells, wrapped at a periodic seam) holds an Exit.
+__global__ void tile_exit_kernel(Geo g, int tile_w, int tile_h, int tiles_x, int tiles_y, uint8_t* flag) {
+    const size_t nwords = (size_t)g.P * g.H;
+    for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < nwords; w += (size_t)gridDim.x * blockDim.x) {
+        uint32_t bits = g.exitb[w];
+        const int y = (int)(w / g.P), x0 = (int)(w % g.P) * 32 - FP_XPAD_BITS;
+        while (bits) {
+            const int b = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int x = x0 + b;
+            if (x < 0 || x >= g.W) continue;  // ghost column (mirrors a real one)
+            for (int ty = max(0, (y - FP_HALO) / tile_h); ty <= min(tiles_y - 1, (y + FP_HALO) / tile_h); ++ty)
+                for (int dx = -FP_HALO; dx <= FP_HALO; ++dx) {
+                    int xx = x + dx;
+                    if (g.boundary == FP_BOUNDARY_PERIODIC_X) xx = ((xx % g.W) + g.W) % g.W;
+                    else if (xx < 0 || xx >= g.W) continue;
+                    flag[(size_t)ty * tiles_x + xx / tile_w] = 1;
+                }
+        }
+    }
+}
+
 // Chooses the plan tile for this grid and encodes the TMA box (tile + FP_HALO halo rows,
 // tile + 6 columns each side so the inner box width stays a multiple of 16 bytes).
 static int make_tmap(fp_ctx* ctx) {
@@ -202,6 +224,16 @@ static int make_tmap(fp_ctx* ctx) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled(occ) failed (" + std::to_string((int)r) + ")");
+    // per tile: does its 5-cell halo window hold an Exit?  (the plan kernel's walk records skip
+    // exit lookups elsewhere)
+    const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_exit, nt));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_exit, 0, nt, ctx->stream));
+    const size_t nwords = (size_t)ctx->P * ctx->H;
+    tile_exit_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nwords, 256), (size_t)ctx->sm_count * 16), 256, 0,
+                       ctx->stream>>>(fp_geo(ctx), ctx->tile_w, ctx->tile_h, ctx->tiles_x, ctx->tiles_y,
+                                      ctx->d_tile_exit);
+    FP_LAUNCHED(ctx);
     return FP_OK;
 }
 
