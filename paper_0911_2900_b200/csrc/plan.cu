@@ -497,6 +497,7 @@ __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint3
 }
 
 #define PLAN_THREADS 512
+#define PLAN_SLOTS 3  // tiles resident per CTA (one fetching while two compute)
 
 // Persistent CTA per SM.  Tiles are fetched in pairs of buffer slots (TMA, mbarrier); the
 // agents of fetch i are dealt to threads round-robin starting at thread (i*160) mod 512, one
@@ -513,19 +514,20 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     const int occ_words = A.boxh * A.occw;
     const int occ_stride = (occ_words + 31) & ~31;
     const unsigned tx_bytes = (unsigned)(box_words + occ_words) * 4u;
-    uint64_t* bars = (uint64_t*)(smem + 2 * box_stride + 2 * occ_stride);
+    uint64_t* bars = (uint64_t*)(smem + PLAN_SLOTS * box_stride + PLAN_SLOTS * occ_stride);
     // slot metadata is written by one thread and read by others without a CTA barrier: volatile
-    __shared__ volatile int s_tile[2], s_cnt[2], s_off[2], s_x0[2], s_y0[2];
-    __shared__ volatile int s_gen[2];
-    __shared__ int s_done[2];
+    __shared__ volatile int s_tile[PLAN_SLOTS], s_cnt[PLAN_SLOTS], s_off[PLAN_SLOTS], s_x0[PLAN_SLOTS],
+        s_y0[PLAN_SLOTS];
+    __shared__ volatile int s_gen[PLAN_SLOTS];
+    __shared__ int s_done[PLAN_SLOTS];
     __shared__ double s_drive[11];
     __shared__ signed char s_bp[121][5][2];
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath_p[0][0][0])[k];
     const PlanCommon& a = A.c;
     const uint64_t step = (uint64_t)a.sc->step;
-    // fetch number i into slot i & 1 (one thread)
+    // fetch number i into slot i % PLAN_SLOTS (one thread)
     auto fetch = [&](int i) {
-        const int slot = i & 1;
+        const int slot = i % PLAN_SLOTS;
         s_gen[slot] = -1;  // seqlock: readers that raced with this refill see a changed generation
         __threadfence_block();
         // fetch i of this CTA is the i-th entry of its ranges (one per pass, bucket.cu
@@ -555,7 +557,8 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&bars[slot], tx_bytes);
                 tma_load_2d(smem + slot * box_stride, &tmap, &bars[slot], x0 - 8 + FP_XPAD_W, y0 - FP_HALO);
-                tma_load_2d(smem + 2 * box_stride + slot * occ_stride, &tmap_occ, &bars[slot], gws, y0 - FP_HALO);
+                tma_load_2d(smem + PLAN_SLOTS * box_stride + slot * occ_stride, &tmap_occ, &bars[slot], gws,
+                            y0 - FP_HALO);
             }
         } else {
             s_tile[slot] = -1;
@@ -564,11 +567,9 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         s_gen[slot] = i;
     };
     if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int s = 0; s < PLAN_SLOTS; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        s_gen[0] = -1;
-        s_gen[1] = -1;
+        for (int s = 0; s < PLAN_SLOTS; ++s) s_gen[s] = -1;
     }
     if (threadIdx.x < 11) {
         s_drive[threadIdx.x] = (a.potential == FP_POTENTIAL_DRIVE_X)
@@ -577,11 +578,10 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        fetch(0);
-        fetch(1);
+        for (int s = 0; s < PLAN_SLOTS; ++s) fetch(s);
     }
     for (int i = 0;; ++i) {
-        const int slot = i & 1;
+        const int slot = i % PLAN_SLOTS;
         // bounded wait: a scheduling bug must surface as an error flag, never as a hung GPU
         // (-1 while a refill is being published; a generation past i means fetch i already
         // completed without this thread -- it had no agent there -- and the slot moved on)
@@ -604,11 +604,11 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         int k = ((int)threadIdx.x - i * (PLAN_THREADS * 5 / 16)) & (PLAN_THREADS - 1);
         if (k >= cnt) continue;  // no agent of this fetch for this thread
         uint32_t* buf = smem + slot * box_stride;
-        uint32_t* occs = smem + 2 * box_stride + slot * occ_stride;
+        uint32_t* occs = smem + PLAN_SLOTS * box_stride + slot * occ_stride;
         const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
         const int osh0 = x0 - 8 + FP_XPAD_BITS - gws * 32;  // staged-occupancy bit of box column 0
         if (A.use_tma) {
-            if (!mbar_wait(&bars[slot], (unsigned)(i >> 1) & 1u)) {
+            if (!mbar_wait(&bars[slot], (unsigned)(i / PLAN_SLOTS) & 1u)) {
                 atomicOr(&a.sc->err, 2ull);
                 return;
             }
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         __threadfence_block();
         if (atomicAdd(&s_done[slot], mine) + mine == cnt) {  // last agent of fetch i
             __threadfence_block();
-            fetch(i + 2);
+            fetch(i + PLAN_SLOTS);
         }
     }
 }
@@ -831,7 +831,8 @@ static void tile_geometry(const fp_ctx* ctx, TileArgs& A, size_t& smem) {
     A.occw = 16;  // TMA box of the occupancy plane: 16 words (512 bits) from a 16-byte aligned word
     const size_t box_stride = ((size_t)A.boxw * A.boxh + 31) & ~(size_t)31;
     const size_t occ_stride = ((size_t)A.boxh * A.occw + 31) & ~(size_t)31;
-    smem = (2 * box_stride + 2 * occ_stride) * 4 + 16 /* barriers */ + 128 /* alignment slack */;
+    smem = (PLAN_SLOTS * box_stride + PLAN_SLOTS * occ_stride) * 4 + 8 * PLAN_SLOTS /* barriers */ +
+           128 /* alignment slack */;
 }
 
 static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& smem, unsigned& grid) {

@@ -192,7 +192,7 @@ static int make_tmap(fp_ctx* ctx) {
     const size_t cells = (size_t)ctx->W * ctx->H;
     if (cells >= (size_t)16 << 20) {
         ctx->tile_w = 240;
-        ctx->tile_h = 64;
+        ctx->tile_h = 48;  // three 63 KB slots fit in shared memory
     } else if (cells >= (size_t)1 << 20) {
         ctx->tile_w = 120;
         ctx->tile_h = 32;
