@@ -301,7 +301,7 @@ def main():
     stepper2 = StripStepper(st2) if world > 1 else None
     for _ in range(e2e_steps):
         st2.set_agents(hx, hy, ha)
-        upd2 += int(ha.sum())
+        upd2 += st2.alive  # counted on the device by the upload's validation pass
         fp.step(st2, params) if stepper2 is None else stepper2.step(params)
         st2.agents(out=(hx, hy, ha))  # D2H into the same pinned buffers: next step's input
     torch.cuda.synchronize()

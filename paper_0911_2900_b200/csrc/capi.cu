@@ -268,7 +268,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
                     c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal, c->d_tile_exit,
                     c->d_sc,
                     c->d_p1, c->d_p2,
-                    c->d_bkt, c->d_pool_owner};
+                    c->d_bkt, c->d_pool_owner, c->d_pool_n};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);
@@ -870,5 +870,6 @@ extern "C" int fp_debug_rounds(fp_ctx* c, int64_t* t_ns, int64_t* pending, int64
         p1_max[r] = (int64_t)h.p1_max[r];
     }
     if (cap >= 64) chk_max[63] = (int64_t)h.chk_max[63];  // largest bucket of the phase
+    for (int r = n; r < std::min(cap, 64); ++r) p1_max[r] = (int64_t)h.p1_max[r];  // spare debug slots
     return n;
 }

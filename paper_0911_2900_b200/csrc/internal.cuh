@@ -201,6 +201,7 @@ struct fp_ctx {
     // motion reservation rounds (move.cu): rank buckets (8-word chunk per cell + overflow pool,
     // all-empty between phases) and per-agent entries
     uint32_t *d_bkt = nullptr, *d_pool_owner = nullptr;
+    uint32_t* d_pool_n = nullptr;  // per-sub-pool taken counts (BK_SUBPOOLS, 128 B apart), zero between phases
     uint32_t* d_entry = nullptr;
     unsigned bk_pool_cap = 0, bk_agent_cap = 0;
     bool bucket_fresh = false;  // plan-tile buckets match the current positions

@@ -65,8 +65,9 @@ struct MoveArgs {
                                    // then pool_cap overflow chunks; all-empty between phases
     unsigned base_words;           // 8 * base chunks (W, H padded to 64, 32); pool chunks follow
     unsigned bk_bw;                // 64-cell block columns
-    unsigned pool_cap;
-    unsigned* pool_n;              // overflow chunks taken this phase
+    unsigned pool_cap;             // BK_SUBPOOLS * pool_sub
+    unsigned pool_sub;             // chunks per sub-pool
+    unsigned* pool_n;              // chunks taken from each sub-pool this phase (BK_SUB_STRIDE apart)
     unsigned* pool_owner;          // chunk that links to each taken pool chunk
     unsigned* entry;               // 6 per contended agent: word index of its bucket entries
     // contended-index pending lists (ping-pong), carved from rec[0] (free after step 2)
@@ -200,23 +201,30 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
 // ------------------------------------------------------------------ grid-wide reservation rounds
 // Every contended agent enters its rank into the bucket of each footprint cell.  A bucket is a
 // chain of chunks addressed by word index into one array: the cell's base chunk (8 words = one
-// 32-byte sector: entry count, 6 entries, link) then, when crowded, 64-word overflow chunks
-// from a pool (count, 62 entries, link).  An agent is the earliest pending agent on a cell iff
+// 32-byte sector: entry count, 6 entries, link) then, when crowded, BK_PW-word overflow chunks
+// from a pool (count, 14 entries, link).  An agent is the earliest pending agent on a cell iff
 // its rank is the bucket minimum; holding all of its cells it walks (everything before it in
 // the reference order on those cells has run) and clears its entries.  A blocked agent
 // watches the entry of one blocker (the latest-ranked) and re-checks only once that entry is
 // cleared, so a waiting agent costs one load per round.  Entries are never reused within a
 // phase, so "entry still holds the rank" == "still pending".
 #define BK_EMPTY 0xFFFFFFFFu
+// Release/acquire is all the walk -> cleared-entry handoff needs (MEMBAR.ALL.GPU, not the
+// sequentially consistent MEMBAR.SC.GPU that __threadfence() emits).
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 #define BK_NIL 0xFFFFFFFFu
 #define BK_NOWATCH 0xFFFFFFFFu
+#define BK_PW 16u  // words per overflow chunk: count, BK_PW - 2 entries, link (one 64-byte read)
+#define BK_SUBPOOL_BITS 6
+#define BK_SUBPOOLS (1 << BK_SUBPOOL_BITS)
+#define BK_SUB_STRIDE 32  // words between sub-pool counters (one 128-byte line each)
 
 __device__ __forceinline__ bool bk_pool(const MoveArgs& a, unsigned c) { return c >= a.base_words; }
-__device__ __forceinline__ unsigned bk_cap(const MoveArgs& a, unsigned c) { return bk_pool(a, c) ? 62u : 6u; }
-__device__ __forceinline__ unsigned bk_link(const MoveArgs& a, unsigned c) { return c + (bk_pool(a, c) ? 63u : 7u); }
+__device__ __forceinline__ unsigned bk_cap(const MoveArgs& a, unsigned c) { return bk_pool(a, c) ? BK_PW - 2u : 6u; }
+__device__ __forceinline__ unsigned bk_link(const MoveArgs& a, unsigned c) { return c + (bk_pool(a, c) ? BK_PW - 1u : 7u); }
 // first word of the chunk holding entry word e
 __device__ __forceinline__ unsigned bk_start(const MoveArgs& a, unsigned e) {
-    return bk_pool(a, e) ? a.base_words + ((e - a.base_words) & ~63u) : (e & ~7u);
+    return bk_pool(a, e) ? a.base_words + ((e - a.base_words) & ~(BK_PW - 1u)) : (e & ~7u);
 }
 
 // Base chunk (word index) of cell (x, y): 64x32-cell blocks stored contiguously (64 KB of
@@ -246,9 +254,18 @@ __device__ unsigned bk_next(const MoveArgs& a, unsigned c) {
     unsigned* link = &a.bkt[bk_link(a, c)];
     const unsigned nx = __ldcg(link);
     if (nx != BK_NIL) return nx;
-    const unsigned q = atomicAdd(a.pool_n, 1u);
-    if (q >= a.pool_cap) return BK_NIL;
-    const unsigned fresh = a.base_words + q * 64u;  // pool chunks are all-empty between phases
+    // overflow chunks come from BK_SUBPOOLS sub-pools picked by a hash of the chunk, each with
+    // its own counter: tens of thousands of allocations per phase would serialise on one address
+    unsigned s = (c * 2654435761u) >> (32 - BK_SUBPOOL_BITS), q = BK_NIL;
+    for (int t = 0; t < BK_SUBPOOLS; ++t, s = (s + 1) & (BK_SUBPOOLS - 1)) {
+        const unsigned k = atomicAdd(&a.pool_n[s * BK_SUB_STRIDE], 1u);
+        if (k < a.pool_sub) {
+            q = s * a.pool_sub + k;
+            break;
+        }
+    }
+    if (q == BK_NIL) return BK_NIL;
+    const unsigned fresh = a.base_words + q * BK_PW;  // pool chunks are all-empty between phases
     const unsigned old = atomicCAS(link, BK_NIL, fresh);
     a.pool_owner[q] = old == BK_NIL ? c : BK_NIL;  // a lost race leaves the chunk unused
     return old == BK_NIL ? fresh : old;
@@ -271,7 +288,7 @@ __device__ unsigned bk_insert(const MoveArgs& a, unsigned c, unsigned rank) {
 }
 
 // Minimum pending rank in the bucket chain at chunk `c` and the word holding it.  Base chunks
-// are one 32-byte sector; overflow chunks (62 entries, 256 bytes) are read with all their loads
+// are one 32-byte sector; overflow chunks (14 entries, 64 bytes) are read with all their loads
 // in flight, so even the most crowded cell is at most a couple of dependent hops.
 __device__ __forceinline__ unsigned bk_min(const MoveArgs& a, unsigned c, unsigned& at) {
     unsigned mn = BK_EMPTY;
@@ -290,22 +307,22 @@ __device__ __forceinline__ unsigned bk_min(const MoveArgs& a, unsigned c, unsign
                 }
             nx = e[7];
         } else {
-            uint4 q[16];
+            uint4 q[BK_PW / 4];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) q[i] = __ldcg(p + i);
+            for (int i = 0; i < BK_PW / 4; ++i) q[i] = __ldcg(p + i);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
+            for (int i = 0; i < BK_PW / 4; ++i) {
                 const unsigned e[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int w = 4 * i + k;
-                    if (w >= 1 && w <= 62 && e[k] < mn) {
+                    if (w >= 1 && w <= BK_PW - 2 && e[k] < mn) {
                         mn = e[k];
                         at = c + w;
                     }
                 }
             }
-            nx = q[15].w;
+            nx = q[BK_PW / 4 - 1].w;
         }
         c = nx;
     } while (c != BK_NIL);
@@ -344,15 +361,41 @@ __device__ __forceinline__ void bk_prep(const MoveArgs& a, unsigned ci, const si
 __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2],
                                          unsigned long long* hops, unsigned* watch) {
     const uint4 r = __ldcg(&a.crec[ci]);
-    unsigned cell[6];
+    unsigned cell[6], ent[6];
     const int m = footprint(a, r, bp, cell);
+#pragma unroll
+    for (int j = 0; j < 6; ++j)  // in flight with the bucket loads
+        ent[j] = j <= m ? __ldcg(&a.entry[(size_t)ci * 6 + j]) : BK_NIL;
     unsigned best = 0, best_at = BK_NIL;
     bool own = true;
+    // every footprint cell's base chunk in one trip; the rare overflow chains afterwards
+    uint4 lo[6], hi[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j)
+        if (j <= m) {
+            const uint4* p = reinterpret_cast<const uint4*>(a.bkt + cell[j]);
+            lo[j] = __ldcg(p);
+            hi[j] = __ldcg(p + 1);
+        }
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
         if (j > m) continue;
-        unsigned at;
-        const unsigned mn = bk_min(a, cell[j], at);
+        const unsigned e[8] = {lo[j].x, lo[j].y, lo[j].z, lo[j].w, hi[j].x, hi[j].y, hi[j].z, hi[j].w};
+        unsigned mn = BK_EMPTY, at = BK_NIL;
+#pragma unroll
+        for (int k = 1; k < 7; ++k)
+            if (e[k] < mn) {
+                mn = e[k];
+                at = cell[j] + k;
+            }
+        if (e[7] != BK_NIL) {
+            unsigned at2;
+            const unsigned m2 = bk_min(a, e[7], at2);
+            if (m2 < mn) {
+                mn = m2;
+                at = at2;
+            }
+        }
         if (mn != r.y) {
             own = false;
             if (best_at == BK_NIL || mn > best) {
@@ -365,15 +408,14 @@ __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const s
         *watch = best_at;
         return false;
     }
-    __threadfence();  // acquire: the walks of the earlier agents on these cells are visible
+    fence_acq_rel_gpu();  // acquire: the walks of the earlier agents on these cells are visible
     int cx[5], cy[5];
     const int mw = path_of(a, r, bp, cx, cy);  // the walk covers the whole path (m >= mf)
     walk_owned(a, r, cx, cy, mw, hops);
-    __threadfence();  // release: this walk before the cleared entries
+    fence_acq_rel_gpu();  // release: this walk before the cleared entries
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-        if (j > m) continue;
-        const unsigned e = __ldcg(&a.entry[(size_t)ci * 6 + j]);
+        const unsigned e = ent[j];
         if (e == BK_NIL) continue;
         a.bkt[e] = BK_EMPTY;
         a.bkt[bk_start(a, e)] = BK_EMPTY;  // the chunk's entry counter (no insertions during the rounds)
@@ -381,14 +423,43 @@ __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const s
     return true;
 }
 
-// End of phase: every used pool chunk back to empty and unlinked (all-ones, 16 threads per
-// chunk).
-__device__ void bk_reset_pool(const MoveArgs& a, unsigned used, unsigned part, unsigned parts) {
+// End of phase: every used pool chunk back to empty and unlinked (all-ones, BK_PW / 4 threads
+// per chunk).
+// pref[s] = chunks taken from sub-pools before s (pref[BK_SUBPOOLS] = all), read once per CTA.
+__device__ void bk_pool_prefix(const MoveArgs& a, unsigned* pref) {
+    if (threadIdx.x < 32) {
+        unsigned u[2], incl = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            u[h] = min(__ldcg(&a.pool_n[(2 * threadIdx.x + h) * BK_SUB_STRIDE]), a.pool_sub);
+        const unsigned pair = u[0] + u[1];
+        incl = pair;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((int)threadIdx.x >= o) incl += t;
+        }
+        pref[2 * threadIdx.x] = incl - pair;
+        pref[2 * threadIdx.x + 1] = incl - pair + u[0];
+        if (threadIdx.x == 31) pref[BK_SUBPOOLS] = incl;
+    }
+    __syncthreads();
+}
+
+// End of phase: every used pool chunk back to empty and unlinked (all-ones, BK_PW / 4 threads
+// per chunk).
+__device__ void bk_reset_pool(const MoveArgs& a, const unsigned* pref, unsigned part, unsigned parts) {
     const uint4 ones = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
-    for (unsigned i = part * blockDim.x + threadIdx.x; i < used * 16u; i += parts * blockDim.x) {
-        const unsigned q = i >> 4;
-        reinterpret_cast<uint4*>(a.bkt + a.base_words + q * 64u)[i & 15u] = ones;
-        if ((i & 15u) == 0) {
+    const unsigned used = pref[BK_SUBPOOLS];
+    constexpr unsigned V4 = BK_PW / 4;  // uint4 per chunk
+    for (unsigned i = part * blockDim.x + threadIdx.x; i < used * V4; i += parts * blockDim.x) {
+        const unsigned f = i / V4;  // f-th taken chunk overall -> (sub-pool, index)
+        unsigned lo = 0;
+#pragma unroll
+        for (unsigned step = BK_SUBPOOLS / 2; step; step >>= 1)
+            if (pref[lo + step] <= f) lo += step;
+        const unsigned q = lo * a.pool_sub + (f - pref[lo]);
+        reinterpret_cast<uint4*>(a.bkt + a.base_words + q * BK_PW)[i % V4] = ones;
+        if (i % V4 == 0) {
             const unsigned owner = a.pool_owner[q];
             if (owner != BK_NIL) a.bkt[bk_link(a, owner)] = BK_NIL;
         }
@@ -763,6 +834,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     __shared__ unsigned int s_app[2 + 2 * SEED_GROUPS];
     __shared__ unsigned long long s_hops[1 + SEED_GROUPS];
     __shared__ unsigned int s_q[3];  // round queue counts and the flush base
+    __shared__ unsigned int s_pool[BK_SUBPOOLS + 1];  // overflow chunks taken per sub-pool (prefix)
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
     if (threadIdx.x < 3) s_q[threadIdx.x] = 0;
     if (threadIdx.x < 2 + 2 * SEED_GROUPS) s_app[threadIdx.x] = 0;
@@ -833,7 +905,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     // the other blocks clean up (contention bitplanes, overflow chunks)
     const unsigned nc = cta_load(&a.pcount[1]);
     const bool rounds = nc > TAIL_MAX;
-    unsigned r = 0, pool_used = 0;
+    unsigned r = 0;
     const uint2* list = nullptr;  // null: the tail takes crec[0, np) directly
     unsigned np = nc;
     if (rounds) {
@@ -849,7 +921,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         }
         grid.sync();
         if (gtid == 0) a.sc->t_prep = globaltimer();
-        pool_used = min(cta_load(a.pool_n), a.pool_cap);
+        bk_pool_prefix(a, s_pool);
         // Per round and CTA, in the (now free) dynamic shared memory: a queue of agents whose
         // watched blocker has walked (full check) and a queue of still-pending (agent, watch)
         // pairs flushed to the next list with one global atomic.
@@ -926,7 +998,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     }
     if (gridDim.x > 1 && blockIdx.x != 0) {
         zero_marks(a, blockIdx.x - 1, gridDim.x - 1);
-        if (rounds) bk_reset_pool(a, pool_used, blockIdx.x - 1, gridDim.x - 1);
+        if (rounds) bk_reset_pool(a, s_pool, blockIdx.x - 1, gridDim.x - 1);
         return;
     }
     if (threadIdx.x == 0) {
@@ -940,13 +1012,14 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     }
     if (gridDim.x == 1) {
         zero_marks(a, 0, 1);
-        if (rounds) bk_reset_pool(a, pool_used, 0, 1);
+        if (rounds) bk_reset_pool(a, s_pool, 0, 1);
     }
+    // sub-pool counters: every CTA read them (bk_pool_prefix) before a later grid barrier
+    if (blockIdx.x == 0 && threadIdx.x < BK_SUBPOOLS) a.pool_n[threadIdx.x * BK_SUB_STRIDE] = 0;
     if (gtid == 0) {
         a.sc->t_motion[3] = globaltimer();
         a.sc->pad[1] += r;  // grid rounds executed (observability; the tail adds its own)
         for (int k = 0; k < 10; ++k) a.pcount[k] = 0;  // list counts, seed cursors
-        *a.pool_n = 0;
         const unsigned long long ne = a.sc->n_exits;
         a.sc->alive -= ne;
         a.sc->tot_exits += ne;
@@ -984,19 +1057,25 @@ int fp_ensure_res(fp_ctx* ctx) {
 
 static int g_move_blocks = 0;
 
-// Rank buckets (one 32-byte chunk per cell plus 256-byte overflow chunks, enough for every cell
+// Rank buckets (one 32-byte chunk per cell plus 64-byte overflow chunks, enough for every cell
 // to overflow: six entries per agent, seven to overflow a cell) and the per-agent round state;
 // all-empty between phases.
 static int ensure_buckets(fp_ctx* ctx) {
     const size_t cells = (size_t)((ctx->W + 63) / 64 * 64) * (size_t)((ctx->H + 31) / 32 * 32);  // cell_of
-    const size_t pool = (size_t)ctx->cap * 6 / 7 + 64;
+    // overflow chunks for the worst case (six entries per agent, seven to overflow a cell), split
+    // into BK_SUBPOOLS equal sub-pools with some slack
+    const size_t pool_sub = ((size_t)ctx->cap * 6 / 7 + 64) / BK_SUBPOOLS + 16;
+    const size_t pool = pool_sub * BK_SUBPOOLS;
     if (ctx->d_bkt && ctx->bk_pool_cap >= pool && ctx->bk_agent_cap >= ctx->cap) return FP_OK;
-    const size_t words = cells * 8 + pool * 64;
+    const size_t words = cells * 8 + pool * BK_PW;
     if (words >= 0xFFFFFFFFull)
         return fp_fail(ctx, FP_ERUNTIME, "motion: grid too large for 32-bit bucket word indices");
     cudaStreamSynchronize(ctx->stream);
-    for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_pool_owner, (void*)ctx->d_entry})
+    for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_pool_owner, (void*)ctx->d_entry, (void*)ctx->d_pool_n})
         if (p) cudaFree(p);
+    ctx->d_pool_n = nullptr;
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_n, BK_SUBPOOLS * BK_SUB_STRIDE * 4));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_pool_n, 0, BK_SUBPOOLS * BK_SUB_STRIDE * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_bkt, words * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0xFF, words * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_owner, pool * 4));
@@ -1061,7 +1140,8 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.bk_bw = (unsigned)((ctx->W + 63) / 64);
     a.base_words = (unsigned)((size_t)a.bk_bw * 64 * (size_t)((ctx->H + 31) / 32 * 32) * 8);
     a.pool_cap = ctx->bk_pool_cap;
-    a.pool_n = a.pcount + 10;
+    a.pool_sub = ctx->bk_pool_cap / BK_SUBPOOLS;
+    a.pool_n = ctx->d_pool_n;
     a.pool_owner = ctx->d_pool_owner;
     a.entry = ctx->d_entry;
     uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
