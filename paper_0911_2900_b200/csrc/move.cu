@@ -48,6 +48,7 @@ struct MoveArgs {
     const uint32_t* seed_list;     // mode B: alive ids to build records from
     const uint4* rec0;             // mode A: records emitted by the plan kernel (n_alive of them)
     int premade;                   // 1: mode A, 0: mode B
+    int seed_static;               // seed tiles dealt round-robin instead of from a cursor
     uint4* rec[2];                 // pending records, ping-pong
     unsigned int* pcount;          // [0..1] pending counts, [2..3] seed tile cursors (zero between phases)
     DevScalars* sc;
@@ -667,7 +668,10 @@ __device__ __forceinline__ long long seed_global(const MoveArgs& a, const SeedWi
 }
 
 // Next tile for this worker group (dynamic: tiles differ a lot in agent count).
-__device__ __forceinline__ uint32_t seed_next(unsigned int* cursor, unsigned int* slot) {
+__device__ __forceinline__ uint32_t seed_next(const MoveArgs& a, unsigned int* cursor, unsigned int* slot,
+                                              unsigned& k) {
+    if (a.seed_static)  // round-robin over the groups of the grid
+        return blockIdx.x * SEED_GROUPS + threadIdx.x / SEED_GROUP + (k++) * gridDim.x * SEED_GROUPS;
     if (threadIdx.x % SEED_GROUP == 0) *slot = atomicAdd(cursor, 1u);
     group_sync();
     const uint32_t e = *slot;
@@ -688,8 +692,9 @@ __device__ __forceinline__ void record_footprint(const MoveArgs& a, const uint4&
 __device__ void seed_mark(const MoveArgs& a, uint32_t* win, unsigned int* slot, const signed char (*bp)[5][2]) {
     const unsigned lt = threadIdx.x % SEED_GROUP;
     const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
+    unsigned k = 0;
     for (;;) {
-        const uint32_t e = seed_next(&a.pcount[2], slot);
+        const uint32_t e = seed_next(a, &a.pcount[2], slot, k);
         if (e >= nt) break;
         const uint32_t t = a.tile_list[e];
         const SeedWin s = seed_window(a, t);
@@ -746,8 +751,9 @@ __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, 
                               unsigned long long* hops) {
     const unsigned lt = threadIdx.x % SEED_GROUP;
     const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
+    unsigned k = 0;
     for (;;) {
-        const uint32_t e = seed_next(&a.pcount[3], slot);
+        const uint32_t e = seed_next(a, &a.pcount[3], slot, k);
         if (e >= nt) break;
         const uint32_t t = a.tile_list[e];
         const SeedWin s = seed_window(a, t);
@@ -1142,6 +1148,10 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.pool_cap = ctx->bk_pool_cap;
     a.pool_sub = ctx->bk_pool_cap / BK_SUBPOOLS;
     a.pool_n = ctx->d_pool_n;
+    {
+        static const int st = getenv("FP_SEED_STATIC") ? atoi(getenv("FP_SEED_STATIC")) : 0;
+        a.seed_static = st;
+    }
     a.pool_owner = ctx->d_pool_owner;
     a.entry = ctx->d_entry;
     uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
