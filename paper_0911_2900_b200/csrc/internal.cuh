@@ -158,6 +158,7 @@ struct fp_ctx {
     int plane_potential = -1;
     CUtensorMap tmap_plane;          // TMA descriptor of the plane (one tile box)
     CUtensorMap tmap_occ;            // TMA descriptor of the occupancy bitplane (16-word box)
+    CUtensorMap tmap_wall;           // the same box over the wall bitplane (line-of-sight masks)
     int tile_w = 0, tile_h = 0;      // plan tile (cells)
     int strip_lo = 0, strip_hi = 0x7FFFFFFF;  // x range planned (fp_plan_strip; full otherwise)
     int tiles_x = 0, tiles_y = 0;

@@ -11,14 +11,17 @@
 //   pass 1  rows centre-out, so the line-of-sight test of a cell only needs the wall bits of
 //           rows already seen (ball wall mask, 121 bits) AND a per-offset Bresenham path mask
 //           (constant memory); each valid candidate's weight m_c*2^(C_p-C_c) is built from the
-//           plane word with integer ops (exact fp64 value of an fp32-rounded weight) and summed
-//           per row in fp64;
+//           plane word with integer ops (the exact value of an fp32-rounded weight) and summed
+//           per row pairwise in fp32, the row sums in fp64;
 //   pass 2  threshold u*total picks the row, the row is replayed in the reference's list order
 //           (rotated at a periodic seam) to find the first cumulative weight > threshold.
-// Guard band: every weight is the reference weight times a common factor to within 2^-24, the
-// fp64 sums add < 1e-14.  If the threshold lies further than 1.5e-7*total from both cumulative
-// boundaries of the chosen candidate, the reference (serial fp64 sum, glibc exp) picks the same
-// candidate; otherwise the agent is re-sampled on the exact path.
+// Guard band: every weight is the reference weight times a common factor to within 2^-24
+// (1.5e-7 covered that with exact sums).  The pairwise fp32 row sums (depth <= 4 for <= 11
+// terms) are within gamma_4 = 4*2^-24/(1-4*2^-24) < 2.4e-7 of the exact row sums, so the total,
+// the threshold and every cumulative boundary move by at most 2.4e-7*total each: 1.5e-7 + 2 *
+// 2.4e-7 < 8e-7.  If the threshold lies further than 8e-7*total from both cumulative boundaries
+// of the chosen candidate, the reference (serial fp64 sum, glibc exp) picks the same candidate;
+// otherwise the agent is re-sampled on the exact path.
 //
 // Exact path (choose_exact): one thread, candidates in list order, weights through the
 // bit-exact restated glibc exp (fp_exp.h), serial fp64 total and scan -- bitwise the
@@ -30,7 +33,7 @@
 #include "internal.cuh"
 #include "motion_rec.cuh"
 
-#define FP_GUARD 1.5e-7
+#define FP_GUARD 8e-7  // see the guard-band note above
 
 // Walk records (motion_rec.cuh): the plan emits them for the motion phase.
 __constant__ signed char c_bpath_p[121][5][2];
@@ -259,6 +262,7 @@ struct TileArgs {
     uint32_t* p2;
     int emit;
     int mixed;  // roster has more than one v_max: the masked radius-5 variant for everyone
+    int rot;    // thread rotation between consecutive fetches (multiple of the lanes per agent)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -326,22 +330,61 @@ __device__ __forceinline__ double exit_weight(uint32_t w, int cp_biased /* C_p +
     return __hiloint2double(hi, lo);
 }
 
-// Plans one agent from the staged tile (V = its v_max, DRIVE = DriveX potential).  Returns
-// 1 when the fast path decided (result in *ox, *oy), 2 when the exact path must decide.
-//   pass 1  rows centre-out so the line-of-sight test of a cell only needs wall bits of rows
-//           already seen; valid candidates (not Wall/unreachable, not occupied by another agent,
-//           visible) contribute their weight to an fp64 row sum;
+__device__ __forceinline__ unsigned long long globaltimer_p() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Path mask test against the shared-memory copy of c_pathmask (lanes index it divergently).
+__device__ __forceinline__ bool path_blocked_s(const uint4* pm, const Mask121& m, int o) {
+    const uint4 q = pm[o];
+    const unsigned long long plo = ((unsigned long long)q.y << 32) | q.x;
+    const unsigned long long phi = ((unsigned long long)q.w << 32) | q.z;
+    return ((m.lo & plo) | (m.hi & phi)) != 0ull;
+}
+
+// The same weight as an fp32 number -- exact: the plane keeps a 23-bit mantissa and
+// |C_p - C_c| <= 60 stays inside the fp32 exponent range.
+__device__ __forceinline__ float exit_weight32(uint32_t w, int cp_biased) {
+    const uint32_t t = (uint32_t)(cp_biased - (int)(w >> 23)) & 127u;  // d + 64
+    return __uint_as_float(((t + 63u) << 23) | (w & 0x7FFFFFu));
+}
+
+// Pairwise fp32 sum of x[0..N) (depth ceil(log2 N): the error bound the guard band assumes).
+template <int N>
+__device__ __forceinline__ float pairwise_sum(const float* x) {
+    if constexpr (N == 1) {
+        return x[0];
+    } else {
+        constexpr int H = (N + 1) / 2;
+        return pairwise_sum<H>(x) + pairwise_sum<N - H>(x + H);
+    }
+}
+
+// Plans one agent from the staged tile (V = its v_max, DRIVE = DriveX potential) with P lanes
+// (P consecutive threads of a warp, all calling with the same agent).  Returns 1 when the fast
+// path decided (result in *ox, *oy, identical in every lane), 2 when the exact path must decide.
+//   walls   every lane ORs the ball's wall bits (staged wall bitplane, one word pair per row)
+//   pass 1  lane l takes rows t = l, l+P, ... of the centre-out order: valid candidates (not
+//           Wall/unreachable, not occupied by another agent, visible) contribute their exact
+//           fp32 weight to a pairwise fp32 row sum; the row sums are gathered into every lane
+//           and accumulated in fp64
 //   pass 2  u*total picks the row; the row is replayed in list order (wrapped-x sorted at a
 //           periodic seam) to find the first cumulative weight > threshold; guard band.
+// Every sum is taken in the same order for any P, so the decision does not depend on P.
 // MASKED: one radius-V code path for every v_max <= V (mixed rosters): rows and columns beyond
 // the agent's own radius vr are masked out, which leaves exactly its Chebyshev ball (the line
 // of sight to a cell of the ball only crosses cells of the ball), so decisions are unchanged
 // while the warps of a mixed roster share one instruction stream.
-template <int V, bool DRIVE, bool MASKED = false>
-__device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* buf, const uint32_t* occs, int osh0,
-                                           int x0, int y0, int px, int py, double u, const double* drive_tab,
-                                           int* ox, int* oy, int vr = V) {
+template <int V, bool DRIVE, bool MASKED = false, int P = 1>
+__device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* buf, const uint32_t* occs,
+                                           const uint32_t* walls, const uint4* pathm, int osh0, int x0, int y0,
+                                           int px, int py, double u, const double* drive_tab, int* ox, int* oy,
+                                           int vr = V) {
     constexpr int D = 2 * V + 1;
+    constexpr int RPL = (D + P - 1) / P;  // rows per lane
+    const int lane = P > 1 ? (int)(threadIdx.x & (P - 1)) : 0;
+    const unsigned gmask = P > 1 ? (((1u << P) - 1u) << ((threadIdx.x & 31u) & ~(unsigned)(P - 1))) : 0xffffffffu;
     const PlanCommon& a = A.c;
     const uint32_t colmask = MASKED ? (((1u << (2 * vr + 1)) - 1u) << (V - vr)) : ((1u << D) - 1u);
     const int X0 = x0 - 8;  // box origin (TMA inner coordinates stay 16-byte aligned)
@@ -352,40 +395,59 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
         if (own & (FP_W_SPECIAL | FP_W_UNSAFE)) return 2;  // "ones" pocket / unsafe centre
         cpb = (int)((own >> 23) & 0x7Fu) + 64 + 128;
     }
-    const int osh = osh0 + lx - V;  // staged occupancy bit of dx = -V
+    const int osh = osh0 + lx - V;  // staged bitplane bit of dx = -V
     Mask121 wm{0ull, 0ull};
-    double rs[D];  // row sums, indexed by dy + V
 #pragma unroll
-    for (int t = 0; t < D; ++t) {
-        const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);  // centre-out: 0, -1, 1, -2, 2, ...
-        const bool rowok = (unsigned)(py + dy) < (unsigned)a.g.H;
-        const uint32_t* row = buf + (ly + dy) * A.boxw + lx - V;
-        uint32_t wv[D];
-        uint32_t wall = 0u, spec = 0u;
+    for (int dy = -V; dy <= V; ++dy) {
+        if ((unsigned)(py + dy) >= (unsigned)a.g.H) continue;
+        const uint32_t* wrow = walls + (ly + dy) * A.occw;
+        const uint32_t wb = __funnelshift_r(wrow[osh >> 5], wrow[(osh >> 5) + 1], osh & 31) & ((1u << D) - 1u);
+        mask_or_row(wm, wb, (dy + 5) * 11 + 5 - V);
+    }
+    const bool anywall = (wm.lo | wm.hi) != 0ull;
+    float dw[D];  // DriveX weights by column (exact fp32 values)
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            wv[k] = row[k];
-            wall |= (uint32_t)(wv[k] == FP_W_WALL) << k;
-            spec |= (wv[k] >> 31) << k;
-        }
-        if (rowok) mask_or_row(wm, wall, (dy + 5) * 11 + 5 - V);
-        const uint32_t* orow = occs + (ly + dy) * A.occw;
-        uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
-        if (dy == 0) occ &= ~(1u << V);  // the own cell stays a candidate (planning.hpp:45-46)
-        const bool inball = !MASKED || (dy <= vr && -dy <= vr);
-        uint32_t valid = (rowok && inball) ? (~(spec | occ) & colmask) : 0u;
-        if (wm.lo | wm.hi) {
+    for (int k = 0; k < D; ++k) dw[k] = DRIVE ? (float)drive_tab[k - V + 5] : 0.0f;
+    float rso[RPL];
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+        const int t = j * P + lane;  // centre-out row index: 0, -1, 1, -2, 2, ...
+        float s = 0.0f;
+        if (t < D) {
+            const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);
+            const bool rowok = (unsigned)(py + dy) < (unsigned)a.g.H;
+            const uint32_t* row = buf + (ly + dy) * A.boxw + lx - V;
+            uint32_t wv[D];
+            uint32_t spec = 0u;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                wv[k] = row[k];
+                spec |= (wv[k] >> 31) << k;
+            }
+            const uint32_t* orow = occs + (ly + dy) * A.occw;
+            uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
+            if (dy == 0) occ &= ~(1u << V);  // the own cell stays a candidate (planning.hpp:45-46)
+            const bool inball = !MASKED || (dy <= vr && -dy <= vr);
+            uint32_t valid = (rowok && inball) ? (~(spec | occ) & colmask) : 0u;
+            if (anywall) {
+#pragma unroll
+                for (int k = 0; k < D; ++k)
+                    if (path_blocked_s(pathm, wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
+            }
+            float w[D];
 #pragma unroll
             for (int k = 0; k < D; ++k)
-                if (path_blocked(wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
+                w[k] = ((valid >> k) & 1u) ? (DRIVE ? dw[k] : exit_weight32(wv[k], cpb)) : 0.0f;
+            s = pairwise_sum<D>(w);
         }
-        double s = 0.0;
+        rso[j] = s;
+    }
+    double rs[D];  // row sums, indexed by dy + V
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const double w = DRIVE ? drive_tab[k - V + 5] : exit_weight(wv[k], cpb);
-            if ((valid >> k) & 1u) s += w;
-        }
-        rs[dy + V] = s;
+    for (int k = 0; k < D; ++k) {
+        const int dy = k - V;
+        const int t = dy >= 0 ? 2 * dy : -2 * dy - 1;
+        rs[k] = (double)(P > 1 ? __shfl_sync(gmask, rso[t / P], t % P, P) : rso[t]);
     }
     double T = 0.0;
 #pragma unroll
@@ -415,7 +477,6 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
             a0 = -px; b0 = -R; b1 = -px - 1;
         }
     }
-    const bool anywall = (wm.lo | wm.hi) != 0ull;
     double prefix = before, lower = 0.0, upper = 0.0;
     int kx = 0;
     bool found = false;
@@ -425,7 +486,7 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
             const uint32_t w = row[dx];
             if (w >> 31) continue;                 // wall / unreachable (weight 0)
             if ((occ >> (dx + V)) & 1u) continue;  // occupied by another agent
-            if (anywall && path_blocked(wm, (dy + 5) * 11 + dx + 5)) continue;
+            if (anywall && path_blocked_s(pathm, wm, (dy + 5) * 11 + dx + 5)) continue;
             const double wt = DRIVE ? drive_tab[dx + 5] : exit_weight(w, cpb);
             const double next = prefix + wt;
             if (next > theta) {
@@ -481,19 +542,21 @@ __device__ __forceinline__ uint4 record_of_tile(const Geo& g, const uint32_t* oc
                       (uint32_t)sy | ((uint32_t)o << 24));
 }
 
-template <bool DRIVE>
+template <bool DRIVE, int P>
 __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint32_t* buf, const uint32_t* occs,
-                                           int osh0, int x0, int y0, int px, int py, double u,
-                                           const double* drive_tab, int* ox, int* oy) {
+                                           const uint32_t* walls, const uint4* pathm, int osh0, int x0, int y0,
+                                           int px, int py, double u, const double* drive_tab, int* ox, int* oy) {
+#define FP_PLAN_ARGS A, buf, occs, walls, pathm, osh0, x0, y0, px, py, u, drive_tab, ox, oy
     if (A.mixed)  // one instruction stream for a mixed-v roster (see plan_fast_t)
-        return plan_fast_t<5, DRIVE, true>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy, v);
+        return plan_fast_t<5, DRIVE, true, P>(FP_PLAN_ARGS, v);
     switch (v) {
-        case 1: return plan_fast_t<1, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
-        case 2: return plan_fast_t<2, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
-        case 3: return plan_fast_t<3, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
-        case 4: return plan_fast_t<4, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
-        default: return plan_fast_t<5, DRIVE>(A, buf, occs, osh0, x0, y0, px, py, u, drive_tab, ox, oy);
+        case 1: return plan_fast_t<1, DRIVE, false, P>(FP_PLAN_ARGS);
+        case 2: return plan_fast_t<2, DRIVE, false, P>(FP_PLAN_ARGS);
+        case 3: return plan_fast_t<3, DRIVE, false, P>(FP_PLAN_ARGS);
+        case 4: return plan_fast_t<4, DRIVE, false, P>(FP_PLAN_ARGS);
+        default: return plan_fast_t<5, DRIVE, false, P>(FP_PLAN_ARGS);
     }
+#undef FP_PLAN_ARGS
 }
 
 #define PLAN_THREADS 512
@@ -504,8 +567,15 @@ __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint3
 // agent per thread.  There is no CTA-wide barrier per tile: a thread finishing its agents of
 // fetch i moves on to fetch i+1; the thread that completes the last agent of fetch i refills
 // that slot with fetch i+2.  Slot metadata is published with a generation number (seqlock).
+__device__ unsigned long long g_plan_dbg[4 * 256];  // DEBUG: per-fetch issue, ready, done, count of CTA 5
+extern "C" int fp_debug_plan(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_plan_dbg, sizeof(g_plan_dbg));
+}
+// P consecutive threads plan each agent together (plan_fast_t).
+template <int P>
 __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                     const __grid_constant__ CUtensorMap tmap_occ,
+                                                                    const __grid_constant__ CUtensorMap tmap_wall,
                                                                     TileArgs A) {
     extern __shared__ __align__(128) uint32_t smem_raw[];
     uint32_t* smem = smem_raw + (((128u - (smem_u32(smem_raw) & 127u)) & 127u) >> 2);
@@ -513,8 +583,8 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     const int box_stride = (box_words + 31) & ~31;  // words, 128-byte multiple
     const int occ_words = A.boxh * A.occw;
     const int occ_stride = (occ_words + 31) & ~31;
-    const unsigned tx_bytes = (unsigned)(box_words + occ_words) * 4u;
-    uint64_t* bars = (uint64_t*)(smem + PLAN_SLOTS * box_stride + PLAN_SLOTS * occ_stride);
+    const unsigned tx_bytes = (unsigned)(box_words + 2 * occ_words) * 4u;
+    uint64_t* bars = (uint64_t*)(smem + PLAN_SLOTS * box_stride + 2 * PLAN_SLOTS * occ_stride);
     // slot metadata is written by one thread and read by others without a CTA barrier: volatile
     __shared__ volatile int s_tile[PLAN_SLOTS], s_cnt[PLAN_SLOTS], s_off[PLAN_SLOTS], s_x0[PLAN_SLOTS],
         s_y0[PLAN_SLOTS];
@@ -522,7 +592,10 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     __shared__ int s_done[PLAN_SLOTS];
     __shared__ double s_drive[11];
     __shared__ signed char s_bp[121][5][2];
+    __shared__ uint4 s_pathm[121];
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath_p[0][0][0])[k];
+    for (int k = threadIdx.x; k < 121; k += blockDim.x)
+        s_pathm[k] = make_uint4(c_pathmask[k][0], c_pathmask[k][1], c_pathmask[k][2], c_pathmask[k][3]);
     const PlanCommon& a = A.c;
     const uint64_t step = (uint64_t)a.sc->step;
     // fetch number i into slot i % PLAN_SLOTS (one thread)
@@ -542,6 +615,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
             }
             k -= hi - lo;
         }
+        if (blockIdx.x == 5 && i < 256) g_plan_dbg[i] = globaltimer_p();
         if (t >= 0) {
             const uint32_t tile = A.tile_list[t];
             const int tx = (int)(tile % (uint32_t)A.tiles_x), ty = (int)(tile / (uint32_t)A.tiles_x);
@@ -559,6 +633,8 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
                 tma_load_2d(smem + slot * box_stride, &tmap, &bars[slot], x0 - 8 + FP_XPAD_W, y0 - FP_HALO);
                 tma_load_2d(smem + PLAN_SLOTS * box_stride + slot * occ_stride, &tmap_occ, &bars[slot], gws,
                             y0 - FP_HALO);
+                tma_load_2d(smem + PLAN_SLOTS * box_stride + (PLAN_SLOTS + slot) * occ_stride, &tmap_wall,
+                            &bars[slot], gws, y0 - FP_HALO);
             }
         } else {
             s_tile[slot] = -1;
@@ -601,10 +677,12 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // a refill racing with these reads may already have written tile = -1 for fetch i+2)
         if (s_gen[slot] != i) continue;  // fetch i already completed without this thread's help
         if (tile < 0) break;
-        int k = ((int)threadIdx.x - i * (PLAN_THREADS * 5 / 16)) & (PLAN_THREADS - 1);
+        // agent slot of this thread's lane group (the rotation keeps groups P-aligned)
+        int k = (((int)threadIdx.x - i * A.rot) & (PLAN_THREADS - 1)) / P;
         if (k >= cnt) continue;  // no agent of this fetch for this thread
         uint32_t* buf = smem + slot * box_stride;
         uint32_t* occs = smem + PLAN_SLOTS * box_stride + slot * occ_stride;
+        uint32_t* walls = smem + PLAN_SLOTS * box_stride + (PLAN_SLOTS + slot) * occ_stride;
         const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
         const int osh0 = x0 - 8 + FP_XPAD_BITS - gws * 32;  // staged-occupancy bit of box column 0
         if (A.use_tma) {
@@ -612,6 +690,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
                 atomicOr(&a.sc->err, 2ull);
                 return;
             }
+            if (blockIdx.x == 5 && i < 256 && g_plan_dbg[256 + i] < g_plan_dbg[i]) g_plan_dbg[256 + i] = globaltimer_p();
         } else if (true) {
             // comparison path: each thread fills what it reads (slow; debugging only)
             const int gx0 = x0 - 8 + FP_XPAD_W, gy0 = y0 - FP_HALO;
@@ -623,11 +702,14 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
             for (int e = 0; e < occ_words; ++e) {
                 const int r = e / A.occw, wcol = e % A.occw;
                 const int gy = gy0 + r, gw = gws + wcol;
-                occs[e] = (gy >= 0 && gy < a.g.H && gw < a.g.P) ? a.occ[(size_t)gy * a.g.P + gw] : 0u;
+                const bool in = gy >= 0 && gy < a.g.H && gw < a.g.P;
+                occs[e] = in ? a.occ[(size_t)gy * a.g.P + gw] : 0u;
+                walls[e] = in ? a.g.wall[(size_t)gy * a.g.P + gw] : 0u;
             }
         }
         int mine = 0;
-        for (; k < cnt; k += PLAN_THREADS) {
+        const bool lead = (threadIdx.x & (P - 1)) == 0;
+        for (; k < cnt; k += PLAN_THREADS / P) {
             const uint4 br = __ldcg(&A.brec[off + k]);  // (id, wrapped x, y, v_max), bucket.cu
             const uint32_t id = br.x;
             const int px = (int)br.y, py = (int)br.z;
@@ -635,9 +717,13 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
             const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
             int cx = 0, cy = 0;
             const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
-                               ? plan_fast_v<true>(v, A, buf, occs, osh0, x0, y0, px, py, u, s_drive, &cx, &cy)
-                               : plan_fast_v<false>(v, A, buf, occs, osh0, x0, y0, px, py, u, s_drive, &cx, &cy);
-            if (st == 1) {
+                               ? plan_fast_v<true, P>(v, A, buf, occs, walls, s_pathm, osh0, x0, y0, px, py, u,
+                                                      s_drive, &cx, &cy)
+                               : plan_fast_v<false, P>(v, A, buf, occs, walls, s_pathm, osh0, x0, y0, px, py, u,
+                                                       s_drive, &cx, &cy);
+            if (!lead) {
+                // the group's other lanes: nothing to write
+            } else if (st == 1) {
                 a.dx[id] = cx;
                 a.dy[id] = cy;
                 if (A.emit)  // the motion's walk record, walls from the staged plane
@@ -652,8 +738,12 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // fence the compiler may sink shared loads below the relaxed atomic and the refill
         // TMA would overwrite data still being read); the last finisher acquires, then refills
         __threadfence_block();
-        if (atomicAdd(&s_done[slot], mine) + mine == cnt) {  // last agent of fetch i
+        if (atomicAdd(&s_done[slot], mine) + mine == cnt * P) {  // last lane of fetch i
             __threadfence_block();
+            if (blockIdx.x == 5 && i < 256) {
+                g_plan_dbg[512 + i] = globaltimer_p();
+                g_plan_dbg[768 + i] = cnt;
+            }
             fetch(i + PLAN_SLOTS);
         }
     }
@@ -831,7 +921,7 @@ static void tile_geometry(const fp_ctx* ctx, TileArgs& A, size_t& smem) {
     A.occw = 16;  // TMA box of the occupancy plane: 16 words (512 bits) from a 16-byte aligned word
     const size_t box_stride = ((size_t)A.boxw * A.boxh + 31) & ~(size_t)31;
     const size_t occ_stride = ((size_t)A.boxh * A.occw + 31) & ~(size_t)31;
-    smem = (PLAN_SLOTS * box_stride + PLAN_SLOTS * occ_stride) * 4 + 8 * PLAN_SLOTS /* barriers */ +
+    smem = (PLAN_SLOTS * box_stride + 2 * PLAN_SLOTS * occ_stride) * 4 + 8 * PLAN_SLOTS /* barriers */ +
            128 /* alignment slack */;
 }
 
@@ -858,6 +948,10 @@ static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& s
     A.p2 = ctx->d_p2;
     A.emit = 1;
     A.mixed = ctx->mixed_v ? 1 : 0;
+    {
+        static const int rot = getenv("FP_PLAN_ROT") ? atoi(getenv("FP_PLAN_ROT")) : PLAN_THREADS * 5 / 16;
+        A.rot = rot;
+    }
     tile_geometry(ctx, A, smem);
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
     grid = (unsigned)ctx->sm_count;  // tile_deal_kernel deals to exactly sm_count CTAs
@@ -879,16 +973,40 @@ int fp_plan_prepare(fp_ctx* ctx, double k_s) {
     tile_geometry(ctx, A, smem);
     static size_t configured = 0;
     if (smem > configured) {
-        FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
     return FP_OK;
 }
 
+// Threads per agent in the plan kernel (FP_PLAN_LANES: 1, 2 or 4).
+static int plan_lanes() {
+    static const int p = getenv("FP_PLAN_LANES") ? atoi(getenv("FP_PLAN_LANES")) : 1;
+    return (p == 2 || p == 4) ? p : 1;
+}
+
+static void plan_kernel_launch(fp_ctx* ctx, const TileArgs& A, size_t smem, unsigned grid) {
+    switch (plan_lanes()) {
+        case 4:
+            plan_tile_kernel<4><<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
+                                                                           ctx->tmap_wall, A);
+            break;
+        case 2:
+            plan_tile_kernel<2><<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
+                                                                           ctx->tmap_wall, A);
+            break;
+        default:
+            plan_tile_kernel<1><<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
+                                                                           ctx->tmap_wall, A);
+    }
+}
+
 static int launch_tile(fp_ctx* ctx, const TileArgs& A, size_t smem, unsigned grid) {
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
-    plan_tile_kernel<<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ, A);
+    plan_kernel_launch(ctx, A, smem, grid);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -939,7 +1057,7 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
         cudaEventRecord(e0, ctx->stream);
-        plan_tile_kernel<<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ, A);
+        plan_kernel_launch(ctx, A, smem, grid);
         FP_LAUNCHED(ctx);
         cudaEventRecord(e1, ctx->stream);
         FP_CUDA(ctx, cudaEventSynchronize(e1));

@@ -224,6 +224,10 @@ static int make_tmap(fp_ctx* ctx) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled(occ) failed (" + std::to_string((int)r) + ")");
+    r = enc(&ctx->tmap_wall, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, ctx->d_wall, odims, ostr, obox, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled(wall) failed (" + std::to_string((int)r) + ")");
     // per tile: does its 5-cell halo window hold an Exit?  (the plan kernel's walk records skip
     // exit lookups elsewhere)
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
