@@ -203,8 +203,9 @@ struct fp_ctx {
     // all-empty between phases) and per-agent entries
     uint32_t *d_bkt = nullptr, *d_pool_owner = nullptr;
     uint32_t* d_pool_n = nullptr;  // per-sub-pool taken counts (BK_SUBPOOLS, 128 B apart), zero between phases
-    uint32_t* d_entry = nullptr;
-    unsigned bk_pool_cap = 0, bk_agent_cap = 0;
+    uint2* d_entry = nullptr;    // (entry word, base chunk) per footprint cell of a contended agent
+    uint2* d_pw = nullptr;       // per bitplane word: (contended cells before it, its P2 bits)
+    unsigned bk_pool_cap = 0, bk_agent_cap = 0, bk_nb_cap = 0;
     bool bucket_fresh = false;  // plan-tile buckets match the current positions
     bool rec_fresh = false;     // d_rec0 + contention marks match the current desired cells
     bool marks_dirty = false;   // contention bitplanes hold marks no motion phase consumed

@@ -64,13 +64,16 @@ struct MoveArgs {
     const uint4* crec;
     uint32_t* bkt;                 // rank buckets: 8-word chunks, base chunk of a cell = cell index,
                                    // then pool_cap overflow chunks; all-empty between phases
-    unsigned base_words;           // 8 * base chunks (W, H padded to 64, 32); pool chunks follow
-    unsigned bk_bw;                // 64-cell block columns
+    unsigned base_words;           // 8 * nb_cap; pool chunks follow
+    unsigned nb_cap;               // base chunks: one per contended cell (<= 3 per contended agent)
+    uint2* pw;                     // per bitplane word: (contended cells before it, its P2 bits)
+    unsigned* scan;                // per-CTA contended-cell counts (p2_count -> p2_number)
     unsigned pool_cap;             // BK_SUBPOOLS * pool_sub
     unsigned pool_sub;             // chunks per sub-pool
     unsigned* pool_n;              // chunks taken from each sub-pool this phase (BK_SUB_STRIDE apart)
     unsigned* pool_owner;          // chunk that links to each taken pool chunk
-    unsigned* entry;               // 6 per contended agent: word index of its bucket entries
+    uint2* entry;                  // 6 per contended agent: (its entry word, the cell's base chunk)
+                                   // per footprint cell; BK_NIL/BK_NIL for an uncontended cell
     // contended-index pending lists (ping-pong), carved from rec[0] (free after step 2)
     uint2* alist[2];               // (contended index, entry of the blocker it waits on)
 };
@@ -228,24 +231,27 @@ __device__ __forceinline__ unsigned bk_start(const MoveArgs& a, unsigned e) {
     return bk_pool(a, e) ? a.base_words + ((e - a.base_words) & ~(BK_PW - 1u)) : (e & ~7u);
 }
 
-// Base chunk (word index) of cell (x, y): 64x32-cell blocks stored contiguously (64 KB of
-// buckets each), so the buckets of neighbouring agents share DRAM pages and L2 lines.
-__device__ __forceinline__ unsigned cell_of(const MoveArgs& a, int x, int y) {
-    return (((((unsigned)y >> 5) * a.bk_bw + ((unsigned)x >> 6)) << 11) | (((unsigned)y & 31u) << 6) |
-            ((unsigned)x & 63u))
-           << 3;
+// Base chunk (word index) of cell (x, y) when two or more footprints cover it (P2), else BK_NIL.
+// The contended cells are numbered densely in bitplane order (p2_number), so their buckets are
+// 32 bytes each in one compact array (L2-sized) instead of one chunk per grid cell; a cell only
+// one footprint covers needs no bucket (its agent is trivially the earliest there).
+__device__ __forceinline__ unsigned bucket_of(const MoveArgs& a, int x, int y) {
+    const uint2 q = __ldcg(&a.pw[a.g.word(x, y)]);
+    const uint32_t bit = 1u << (x & 31);
+    return (q.y & bit) ? (q.x + (unsigned)__popc(q.y & (bit - 1u))) << 3 : BK_NIL;
 }
 
-// Footprint cells of a record: [0] start, [1..mf] path (motion_rec.cuh); returns mf.
+// Base chunks of a record's footprint cells: [0] start, [1..mf] path (motion_rec.cuh), BK_NIL
+// for cells no other footprint covers; returns mf.
 __device__ __forceinline__ int footprint(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
                                          unsigned* cell) {
     int cx[5], cy[5];
     path_of(a, r, bp, cx, cy);
     const int m = rec_mf(r);
-    cell[0] = cell_of(a, rec_x(r), rec_y(r));
+    cell[0] = bucket_of(a, rec_x(r), rec_y(r));
 #pragma unroll
     for (int j = 0; j < 5; ++j)
-        if (j < m) cell[j + 1] = cell_of(a, cx[j], cy[j]);
+        if (j < m) cell[j + 1] = bucket_of(a, cx[j], cy[j]);
     return m;
 }
 
@@ -338,21 +344,27 @@ __device__ __forceinline__ void bk_prep(const MoveArgs& a, unsigned ci, const si
     const int m = footprint(a, r, bp, cell);
 #pragma unroll
     for (int j = 0; j < 6; ++j)
-        if (j <= m) k[j] = atomicAdd(&a.bkt[cell[j]], 1u) + 1u;
+        if (j <= m && cell[j] != BK_NIL) k[j] = atomicAdd(&a.bkt[cell[j]], 1u) + 1u;
+    uint2 eb[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-        if (j > m) continue;
-        unsigned e;
-        if (k[j] < 6) {
-            e = cell[j] + 1 + k[j];
-            a.bkt[e] = r.y;
-        } else {
-            const unsigned nx = bk_next(a, cell[j]);
-            e = nx == BK_NIL ? BK_NIL : bk_insert(a, nx, r.y);
+        unsigned e = BK_NIL;
+        const unsigned c = j <= m ? cell[j] : BK_NIL;
+        if (c != BK_NIL) {
+            if (k[j] < 6) {
+                e = c + 1 + k[j];
+                a.bkt[e] = r.y;
+            } else {
+                const unsigned nx = bk_next(a, c);
+                e = nx == BK_NIL ? BK_NIL : bk_insert(a, nx, r.y);
+            }
+            if (e == BK_NIL) atomicOr(&a.sc->err, 8ull);  // pool exhausted (sized for the worst case)
         }
-        if (e == BK_NIL) atomicOr(&a.sc->err, 8ull);  // pool exhausted (sized for the worst case)
-        a.entry[(size_t)ci * 6 + j] = e;
+        eb[j] = make_uint2(e, c);
     }
+    uint4* out = reinterpret_cast<uint4*>(a.entry + (size_t)ci * 6);
+#pragma unroll
+    for (int h = 0; h < 3; ++h) out[h] = make_uint4(eb[2 * h].x, eb[2 * h].y, eb[2 * h + 1].x, eb[2 * h + 1].y);
 }
 
 // Full check of pending agent ci (its watched blocker, if any, has walked).  Holding every cell
@@ -361,26 +373,34 @@ __device__ __forceinline__ void bk_prep(const MoveArgs& a, unsigned ci, const si
 // occupancy reads after this walk.  Otherwise returns the entry of the latest-ranked blocker.
 __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2],
                                          unsigned long long* hops, unsigned* watch) {
+    // the record and the (entry, base chunk) pairs in one trip, every contended cell's base chunk
+    // in the next, the rare overflow chains afterwards
     const uint4 r = __ldcg(&a.crec[ci]);
     unsigned cell[6], ent[6];
-    const int m = footprint(a, r, bp, cell);
+    {
+        const uint4* p = reinterpret_cast<const uint4*>(a.entry + (size_t)ci * 6);
 #pragma unroll
-    for (int j = 0; j < 6; ++j)  // in flight with the bucket loads
-        ent[j] = j <= m ? __ldcg(&a.entry[(size_t)ci * 6 + j]) : BK_NIL;
+        for (int h = 0; h < 3; ++h) {
+            const uint4 q = __ldcg(p + h);
+            ent[2 * h] = q.x;
+            cell[2 * h] = q.y;
+            ent[2 * h + 1] = q.z;
+            cell[2 * h + 1] = q.w;
+        }
+    }
     unsigned best = 0, best_at = BK_NIL;
     bool own = true;
-    // every footprint cell's base chunk in one trip; the rare overflow chains afterwards
     uint4 lo[6], hi[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j)
-        if (j <= m) {
+        if (cell[j] != BK_NIL) {
             const uint4* p = reinterpret_cast<const uint4*>(a.bkt + cell[j]);
             lo[j] = __ldcg(p);
             hi[j] = __ldcg(p + 1);
         }
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-        if (j > m) continue;
+        if (cell[j] == BK_NIL) continue;
         const unsigned e[8] = {lo[j].x, lo[j].y, lo[j].z, lo[j].w, hi[j].x, hi[j].y, hi[j].z, hi[j].w};
         unsigned mn = BK_EMPTY, at = BK_NIL;
 #pragma unroll
@@ -502,7 +522,7 @@ struct TailSmem {
 #define QC_CAP 8192
 static_assert(QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) <= sizeof(TailSmem), "round queues");
 
-__device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y) {
+__device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y, bool buckets) {
     const unsigned cell = (unsigned)y * (unsigned)a.g.W + (unsigned)x;
     unsigned h = (cell * 2654435761u) >> (32 - 13);
     for (;;) {
@@ -512,9 +532,12 @@ __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, 
             // only tail agents (and walkers whose release is in flight) still have entries in
             // this cell's base chunk: empty it for the next phase (overflow chunks are reset
             // by the other blocks)
-            uint32_t* b = a.bkt + cell_of(a, x, y);
-            reinterpret_cast<uint4*>(b)[0] = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
-            b[4] = b[5] = b[6] = BK_EMPTY;
+            const unsigned c = buckets ? bucket_of(a, x, y) : BK_NIL;
+            if (c != BK_NIL) {
+                uint32_t* b = a.bkt + c;
+                reinterpret_cast<uint4*>(b)[0] = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
+                b[4] = b[5] = b[6] = BK_EMPTY;
+            }
             return h;
         }
         if (old == cell) return h;
@@ -524,7 +547,7 @@ __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, 
 
 // Pending records: crec[list[t]] (or crec[t] when list is null), t < np <= TAIL_MAX.
 __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, const uint2* list, unsigned np,
-                          const signed char (*bp)[5][2], unsigned long long* hops) {
+                          bool buckets, const signed char (*bp)[5][2], unsigned long long* hops) {
     for (unsigned k = threadIdx.x; k < TAIL_SLOTS; k += blockDim.x) {
         T.key[k] = TAIL_EMPTY;
         T.res[k] = 0xFFFFFFFFu;
@@ -537,10 +560,10 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
         int cx[5], cy[5];
         path_of(a, r, bp, cx, cy);
         const int m = rec_mf(r);  // footprint cells only (a free exit ending the walk has no slot)
-        T.slot[t][0] = (unsigned short)tail_insert(T, a, rec_x(r), rec_y(r));
+        T.slot[t][0] = (unsigned short)tail_insert(T, a, rec_x(r), rec_y(r), buckets);
 #pragma unroll
         for (int i = 0; i < 5; ++i)
-            if (i < m) T.slot[t][1 + i] = (unsigned short)tail_insert(T, a, cx[i], cy[i]);
+            if (i < m) T.slot[t][1 + i] = (unsigned short)tail_insert(T, a, cx[i], cy[i], buckets);
     }
     if (threadIdx.x == 0) {
         T.count[0] = np;
@@ -608,6 +631,80 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
         else atomicAnd(&a.occ[a.g.word(x, y)], ~bit);
     }
     if (threadIdx.x == 0) a.sc->pad[1] += rounds;
+}
+
+// ------------------------------------------------------------------ dense bucket numbering
+// Contended cells (P2 bits) numbered in bitplane order: each CTA counts the bits of its slice of
+// words (p2_count), then, after a grid barrier, numbers them from its prefix (p2_number), writing
+// (contended cells before the word, the word's P2 bits) per word for bucket_of.
+__device__ __forceinline__ void p2_slice(const MoveArgs& a, size_t& w0, size_t& w1) {
+    const size_t nw = (size_t)a.g.P * (size_t)a.g.H;  // P is a multiple of 4
+    const size_t per = ((nw / 4 + gridDim.x - 1) / gridDim.x) * 4;
+    w0 = min(nw, (size_t)blockIdx.x * per);
+    w1 = min(nw, w0 + per);
+}
+
+// Block-wide sum of v (every thread gets it); red = 32 words of shared scratch.
+__device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();  // red is free
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    unsigned t = 0;
+    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) t += red[w];
+    return t;
+}
+
+__device__ void p2_count(const MoveArgs& a, unsigned* red) {
+    size_t w0, w1;
+    p2_slice(a, w0, w1);
+    unsigned c = 0;
+    for (size_t w = w0 + 4 * (size_t)threadIdx.x; w < w1; w += 4 * (size_t)blockDim.x) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(a.p2 + w));
+        c += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    }
+    c = block_sum(c, red);
+    if (threadIdx.x == 0) a.scan[blockIdx.x] = c;
+}
+
+__device__ void p2_number(const MoveArgs& a, unsigned* red) {
+    size_t w0, w1;
+    p2_slice(a, w0, w1);
+    unsigned off = 0;
+    for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) off += __ldcg(&a.scan[b]);
+    off = block_sum(off, red);
+    // each thread numbers a contiguous run of words: count, one block scan, number
+    const size_t per = (((w1 - w0) / 4 + blockDim.x - 1) / blockDim.x) * 4;
+    const size_t t0 = min(w1, w0 + threadIdx.x * per), t1 = min(w1, t0 + per);
+    unsigned mine = 0;
+#pragma unroll 4
+    for (size_t w = t0; w < t1; w += 4) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(a.p2 + w));
+        mine += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    }
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    unsigned incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    __syncthreads();  // red is free
+    if (lane == 31) red[warp] = incl;
+    __syncthreads();
+    unsigned before = 0;
+    for (unsigned k = 0; k < warp; ++k) before += red[k];
+    unsigned e = off + before + incl - mine;
+#pragma unroll 4
+    for (size_t w = t0; w < t1; w += 4) {
+        const uint4 q = __ldcg(reinterpret_cast<const uint4*>(a.p2 + w));
+        const unsigned c0 = __popc(q.x), c1 = __popc(q.y), c2 = __popc(q.z);
+        uint4* out = reinterpret_cast<uint4*>(a.pw + w);
+        out[0] = make_uint4(e, q.x, e + c0, q.y);
+        out[1] = make_uint4(e + c0 + c1, q.z, e + c0 + c1 + c2, q.w);
+        e += c0 + c1 + c2 + __popc(q.w);
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1 && e > a.nb_cap)
+        atomicOr(&a.sc->err, 16ull);  // cannot happen: <= 3 contended cells per contended agent
 }
 
 // Zeroes the contention bitplanes (dead after step 2) so the next phase starts from all-clear.
@@ -840,6 +937,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     __shared__ unsigned int s_app[2 + 2 * SEED_GROUPS];
     __shared__ unsigned long long s_hops[1 + SEED_GROUPS];
     __shared__ unsigned int s_q[3];  // round queue counts and the flush base
+    __shared__ unsigned int s_red[32];  // block reductions (dense bucket numbering)
     __shared__ unsigned int s_pool[BK_SUBPOOLS + 1];  // overflow chunks taken per sub-pool (prefix)
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
     if (threadIdx.x < 3) s_q[threadIdx.x] = 0;
@@ -871,6 +969,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
             append(B, &a.pcount[0], a.rec[0], take, rec);
         }
         grid.sync();
+        p2_count(a, s_red);
         cand = a.rec[0];
         ncand = cta_load(&a.pcount[0]);
     } else {
@@ -881,6 +980,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
         seed_mark(a, win, slot, s_bp);
         grid.sync();
         if (gtid == 0) a.sc->t_marked = globaltimer();
+        p2_count(a, s_red);
         unsigned long long hops = 0;
         seed_classify(a, Gs, win, slot, s_bp, &hops);
         flush_hops(B, a.sc, hops);
@@ -915,6 +1015,8 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     const uint2* list = nullptr;  // null: the tail takes crec[0, np) directly
     unsigned np = nc;
     if (rounds) {
+        p2_number(a, s_red);
+        grid.sync();
         for (unsigned ci = gtid; ci < nc; ci += nthreads) {
             bk_prep(a, ci, s_bp);
             a.alist[0][ci] = make_uint2(ci, BK_NOWATCH);
@@ -1013,7 +1115,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     }
     if (np) {
         unsigned long long hops = 0;
-        tail_smem(a, *reinterpret_cast<TailSmem*>(s_dyn), a.crec, list, np, s_bp, &hops);
+        tail_smem(a, *reinterpret_cast<TailSmem*>(s_dyn), a.crec, list, np, rounds, s_bp, &hops);
         flush_hops(B, a.sc, hops);
     }
     if (gridDim.x == 1) {
@@ -1054,6 +1156,7 @@ int fp_ensure_res(fp_ctx* ctx) {
         const size_t nwords = (size_t)ctx->P * ctx->H;
         FP_CUDA(ctx, cudaMalloc(&ctx->d_p1, nwords * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_p2, nwords * 4));
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_pw, nwords * sizeof(uint2)));
         FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
         FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
         ctx->marks_dirty = false;
@@ -1063,30 +1166,30 @@ int fp_ensure_res(fp_ctx* ctx) {
 
 static int g_move_blocks = 0;
 
-// Rank buckets (one 32-byte chunk per cell plus 64-byte overflow chunks, enough for every cell
-// to overflow: six entries per agent, seven to overflow a cell) and the per-agent round state;
-// all-empty between phases.
+// Rank buckets: one 32-byte base chunk per contended cell (<= 3 per agent: every contended cell
+// is covered by >= 2 of the <= 6-cell footprints) plus 64-byte overflow chunks (six entries per
+// agent, seven to overflow a cell), the per-agent (entry, base chunk) pairs, the per-word dense
+// numbering and its per-CTA counts; buckets all-empty between phases.
 static int ensure_buckets(fp_ctx* ctx) {
-    const size_t cells = (size_t)((ctx->W + 63) / 64 * 64) * (size_t)((ctx->H + 31) / 32 * 32);  // cell_of
-    // overflow chunks for the worst case (six entries per agent, seven to overflow a cell), split
-    // into BK_SUBPOOLS equal sub-pools with some slack
+    const size_t nb = (size_t)ctx->cap * 3 + 64;
     const size_t pool_sub = ((size_t)ctx->cap * 6 / 7 + 64) / BK_SUBPOOLS + 16;
     const size_t pool = pool_sub * BK_SUBPOOLS;
     if (ctx->d_bkt && ctx->bk_pool_cap >= pool && ctx->bk_agent_cap >= ctx->cap) return FP_OK;
-    const size_t words = cells * 8 + pool * BK_PW;
+    const size_t words = nb * 8 + pool * BK_PW;
     if (words >= 0xFFFFFFFFull)
-        return fp_fail(ctx, FP_ERUNTIME, "motion: grid too large for 32-bit bucket word indices");
+        return fp_fail(ctx, FP_ERUNTIME, "motion: roster too large for 32-bit bucket word indices");
     cudaStreamSynchronize(ctx->stream);
     for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_pool_owner, (void*)ctx->d_entry, (void*)ctx->d_pool_n})
         if (p) cudaFree(p);
     ctx->d_pool_n = nullptr;
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_n, BK_SUBPOOLS * BK_SUB_STRIDE * 4));
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_pool_n, 0, BK_SUBPOOLS * BK_SUB_STRIDE * 4, ctx->stream));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_n, BK_SUBPOOLS * BK_SUB_STRIDE * 4 + 1024 * 4));  // + p2 scan counts
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_pool_n, 0, BK_SUBPOOLS * BK_SUB_STRIDE * 4 + 1024 * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_bkt, words * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0xFF, words * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_owner, pool * 4));
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * 6 * 4));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * 6 * sizeof(uint2)));
     ctx->bk_pool_cap = (unsigned)pool;
+    ctx->bk_nb_cap = (unsigned)nb;
     ctx->bk_agent_cap = ctx->cap;
     ctx->graph_valid = false;
     return FP_OK;
@@ -1143,8 +1246,10 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.tiles_x = ctx->tiles_x;
     a.crec = ctx->d_rec_b;
     a.bkt = ctx->d_bkt;
-    a.bk_bw = (unsigned)((ctx->W + 63) / 64);
-    a.base_words = (unsigned)((size_t)a.bk_bw * 64 * (size_t)((ctx->H + 31) / 32 * 32) * 8);
+    a.nb_cap = ctx->bk_nb_cap;
+    a.base_words = ctx->bk_nb_cap * 8u;
+    a.pw = ctx->d_pw;
+    a.scan = ctx->d_pool_n + BK_SUBPOOLS * BK_SUB_STRIDE;
     a.pool_cap = ctx->bk_pool_cap;
     a.pool_sub = ctx->bk_pool_cap / BK_SUBPOOLS;
     a.pool_n = ctx->d_pool_n;

@@ -560,6 +560,9 @@ __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint3
 }
 
 #define PLAN_THREADS 512
+#ifndef FP_PLAN_NAP_MAX
+#define FP_PLAN_NAP_MAX 1024  // ns
+#endif
 #define PLAN_SLOTS 3  // tiles resident per CTA (one fetching while two compute)
 
 // Persistent CTA per SM.  Tiles are fetched in pairs of buffer slots (TMA, mbarrier); the
@@ -661,10 +664,13 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // bounded wait: a scheduling bug must surface as an error flag, never as a hung GPU
         // (-1 while a refill is being published; a generation past i means fetch i already
         // completed without this thread -- it had no agent there -- and the slot moved on)
+        // (exponential backoff: idle threads must not steal issue slots from the computing warps)
         int gen;
+        unsigned nap = 32;
         for (long long spin = 0; (gen = s_gen[slot]) < i; ++spin) {
-            __nanosleep(64);
-            if (spin > (1ll << 24)) {
+            __nanosleep(nap);
+            nap = min(nap * 2u, (unsigned)FP_PLAN_NAP_MAX);
+            if (spin > (1ll << 22)) {
                 atomicOr(&a.sc->err, 1ull);
                 return;
             }
