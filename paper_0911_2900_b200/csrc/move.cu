@@ -218,6 +218,9 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 #define BK_NIL 0xFFFFFFFFu
 #define BK_NOWATCH 0xFFFFFFFFu
+#ifndef BK_PREP_BATCH
+#define BK_PREP_BATCH 2  // contended agents per thread per prep step
+#endif
 #define BK_PW 16u  // words per overflow chunk: count, BK_PW - 2 entries, link (one 64-byte read)
 #define BK_SUBPOOL_BITS 6
 #define BK_SUBPOOLS (1 << BK_SUBPOOL_BITS)
@@ -336,35 +339,50 @@ __device__ __forceinline__ unsigned bk_min(const MoveArgs& a, unsigned c, unsign
     return mn;
 }
 
-// Round-0 entry of contended agent ci: the six first-chunk counters taken in parallel, the rare
-// overflows chained afterwards.
-__device__ __forceinline__ void bk_prep(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2]) {
-    const uint4 r = __ldcg(&a.crec[ci]);
-    unsigned cell[6], k[6];
-    const int m = footprint(a, r, bp, cell);
+// Round-0 entries of contended agents ci[0..B): the first-chunk counters of every contended
+// footprint cell taken in parallel, the rare overflows chained afterwards.
+template <int B>
+__device__ __forceinline__ void bk_prep(const MoveArgs& a, const unsigned* ci, const bool* ok,
+                                        const signed char (*bp)[5][2]) {
+    // B agents at once: their records, then all their bucket lookups, then all their counter
+    // atomics in flight together (each stage is one dependent trip)
+    uint4 r[B];
 #pragma unroll
-    for (int j = 0; j < 6; ++j)
-        if (j <= m && cell[j] != BK_NIL) k[j] = atomicAdd(&a.bkt[cell[j]], 1u) + 1u;
-    uint2 eb[6];
+    for (int b = 0; b < B; ++b) r[b] = ok[b] ? __ldcg(&a.crec[ci[b]]) : make_uint4(0, 0, 0, 0);
+    unsigned cell[B][6], k[B][6];
+    int m[B];
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        unsigned e = BK_NIL;
-        const unsigned c = j <= m ? cell[j] : BK_NIL;
-        if (c != BK_NIL) {
-            if (k[j] < 6) {
-                e = c + 1 + k[j];
-                a.bkt[e] = r.y;
-            } else {
-                const unsigned nx = bk_next(a, c);
-                e = nx == BK_NIL ? BK_NIL : bk_insert(a, nx, r.y);
+    for (int b = 0; b < B; ++b) m[b] = ok[b] ? footprint(a, r[b], bp, cell[b]) : -1;
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+            if (j <= m[b] && cell[b][j] != BK_NIL) k[b][j] = atomicAdd(&a.bkt[cell[b][j]], 1u) + 1u;
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        if (!ok[b]) continue;
+        uint2 eb[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) {
+            unsigned e = BK_NIL;
+            const unsigned c = j <= m[b] ? cell[b][j] : BK_NIL;
+            if (c != BK_NIL) {
+                if (k[b][j] < 6) {
+                    e = c + 1 + k[b][j];
+                    a.bkt[e] = r[b].y;
+                } else {
+                    const unsigned nx = bk_next(a, c);
+                    e = nx == BK_NIL ? BK_NIL : bk_insert(a, nx, r[b].y);
+                }
+                if (e == BK_NIL) atomicOr(&a.sc->err, 8ull);  // pool exhausted (sized for the worst case)
             }
-            if (e == BK_NIL) atomicOr(&a.sc->err, 8ull);  // pool exhausted (sized for the worst case)
+            eb[j] = make_uint2(e, c);
         }
-        eb[j] = make_uint2(e, c);
-    }
-    uint4* out = reinterpret_cast<uint4*>(a.entry + (size_t)ci * 6);
+        uint4* out = reinterpret_cast<uint4*>(a.entry + (size_t)ci[b] * 6);
 #pragma unroll
-    for (int h = 0; h < 3; ++h) out[h] = make_uint4(eb[2 * h].x, eb[2 * h].y, eb[2 * h + 1].x, eb[2 * h + 1].y);
+        for (int h = 0; h < 3; ++h) out[h] = make_uint4(eb[2 * h].x, eb[2 * h].y, eb[2 * h + 1].x, eb[2 * h + 1].y);
+        a.alist[0][ci[b]] = make_uint2(ci[b], BK_NOWATCH);
+    }
 }
 
 // Full check of pending agent ci (its watched blocker, if any, has walked).  Holding every cell
@@ -1017,9 +1035,15 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
     if (rounds) {
         p2_number(a, s_red);
         grid.sync();
-        for (unsigned ci = gtid; ci < nc; ci += nthreads) {
-            bk_prep(a, ci, s_bp);
-            a.alist[0][ci] = make_uint2(ci, BK_NOWATCH);
+        for (unsigned base = gtid; base < nc; base += BK_PREP_BATCH * nthreads) {
+            unsigned ci[BK_PREP_BATCH];
+            bool ok[BK_PREP_BATCH];
+#pragma unroll
+            for (int b = 0; b < BK_PREP_BATCH; ++b) {
+                ci[b] = base + b * nthreads;
+                ok[b] = ci[b] < nc;
+            }
+            bk_prep<BK_PREP_BATCH>(a, ci, ok, s_bp);
         }
         if (gtid == 0) {
             // pending counts rotate over pcount[4..6]: round r reads its own, fills the next and
