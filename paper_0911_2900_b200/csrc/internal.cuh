@@ -202,7 +202,8 @@ struct fp_ctx {
     // motion reservation rounds (move.cu): rank buckets (8-word chunk per cell + overflow pool,
     // all-empty between phases) and per-agent entries
     uint32_t *d_bkt = nullptr, *d_pool_owner = nullptr;
-    uint32_t* d_pool_n = nullptr;  // per-sub-pool taken counts (BK_SUBPOOLS, 128 B apart), zero between phases
+    uint32_t* d_pool_n = nullptr;
+    uint32_t* d_bnext = nullptr;   // successor entry word of each bucket entry (rank order)  // per-sub-pool taken counts (BK_SUBPOOLS, 128 B apart), zero between phases
     uint2* d_entry = nullptr;    // (entry word, base chunk) per footprint cell of a contended agent
     uint2* d_pw = nullptr;       // per bitplane word: (contended cells before it, its P2 bits)
     unsigned bk_pool_cap = 0, bk_agent_cap = 0, bk_nb_cap = 0;

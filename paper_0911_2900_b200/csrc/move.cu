@@ -72,6 +72,8 @@ struct MoveArgs {
     unsigned pool_sub;             // chunks per sub-pool
     unsigned* pool_n;              // chunks taken from each sub-pool this phase (BK_SUB_STRIDE apart)
     unsigned* pool_owner;          // chunk that links to each taken pool chunk
+    unsigned* bnext;               // per bucket entry word: the entry of the next agent in rank order
+    unsigned* long_list;           // buckets longer than a base chunk (bk_sort -> bk_sort_long)
     uint2* entry;                  // 6 per contended agent: (its entry word, the cell's base chunk)
                                    // per footprint cell; BK_NIL/BK_NIL for an uncontended cell
     // contended-index pending lists (ping-pong), carved from rec[0] (free after step 2)
@@ -204,8 +206,8 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
 
 // ------------------------------------------------------------------ grid-wide reservation rounds
 // Every contended agent enters its rank into the bucket of each footprint cell.  A bucket is a
-// chain of chunks addressed by word index into one array: the cell's base chunk (8 words = one
-// 32-byte sector: entry count, 6 entries, link) then, when crowded, BK_PW-word overflow chunks
+// chain of chunks addressed by word index into one array: the cell's base chunk (BK_BW words:
+// entry count, 14 entries, link) then, when crowded, BK_PW-word overflow chunks
 // from a pool (count, 14 entries, link).  An agent is the earliest pending agent on a cell iff
 // its rank is the bucket minimum; holding all of its cells it walks (everything before it in
 // the reference order on those cells has run) and clears its entries.  A blocked agent
@@ -221,18 +223,15 @@ __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_re
 #ifndef BK_PREP_BATCH
 #define BK_PREP_BATCH 2  // contended agents per thread per prep step
 #endif
+#define BK_BW 16u  // words per base chunk: count / current entry, BK_BW - 2 entries, link (64 bytes)
 #define BK_PW 16u  // words per overflow chunk: count, BK_PW - 2 entries, link (one 64-byte read)
 #define BK_SUBPOOL_BITS 6
 #define BK_SUBPOOLS (1 << BK_SUBPOOL_BITS)
 #define BK_SUB_STRIDE 32  // words between sub-pool counters (one 128-byte line each)
 
 __device__ __forceinline__ bool bk_pool(const MoveArgs& a, unsigned c) { return c >= a.base_words; }
-__device__ __forceinline__ unsigned bk_cap(const MoveArgs& a, unsigned c) { return bk_pool(a, c) ? BK_PW - 2u : 6u; }
-__device__ __forceinline__ unsigned bk_link(const MoveArgs& a, unsigned c) { return c + (bk_pool(a, c) ? BK_PW - 1u : 7u); }
-// first word of the chunk holding entry word e
-__device__ __forceinline__ unsigned bk_start(const MoveArgs& a, unsigned e) {
-    return bk_pool(a, e) ? a.base_words + ((e - a.base_words) & ~(BK_PW - 1u)) : (e & ~7u);
-}
+__device__ __forceinline__ unsigned bk_cap(const MoveArgs& a, unsigned c) { return bk_pool(a, c) ? BK_PW - 2u : BK_BW - 2u; }
+__device__ __forceinline__ unsigned bk_link(const MoveArgs& a, unsigned c) { return c + (bk_pool(a, c) ? BK_PW - 1u : BK_BW - 1u); }
 
 // Base chunk (word index) of cell (x, y) when two or more footprints cover it (P2), else BK_NIL.
 // The contended cells are numbered densely in bitplane order (p2_number), so their buckets are
@@ -241,7 +240,7 @@ __device__ __forceinline__ unsigned bk_start(const MoveArgs& a, unsigned e) {
 __device__ __forceinline__ unsigned bucket_of(const MoveArgs& a, int x, int y) {
     const uint2 q = __ldcg(&a.pw[a.g.word(x, y)]);
     const uint32_t bit = 1u << (x & 31);
-    return (q.y & bit) ? (q.x + (unsigned)__popc(q.y & (bit - 1u))) << 3 : BK_NIL;
+    return (q.y & bit) ? (q.x + (unsigned)__popc(q.y & (bit - 1u))) * BK_BW : BK_NIL;
 }
 
 // Base chunks of a record's footprint cells: [0] start, [1..mf] path (motion_rec.cuh), BK_NIL
@@ -297,47 +296,6 @@ __device__ unsigned bk_insert(const MoveArgs& a, unsigned c, unsigned rank) {
     }
 }
 
-// Minimum pending rank in the bucket chain at chunk `c` and the word holding it.  Base chunks
-// are one 32-byte sector; overflow chunks (14 entries, 64 bytes) are read with all their loads
-// in flight, so even the most crowded cell is at most a couple of dependent hops.
-__device__ __forceinline__ unsigned bk_min(const MoveArgs& a, unsigned c, unsigned& at) {
-    unsigned mn = BK_EMPTY;
-    at = BK_NIL;
-    do {
-        const uint4* p = reinterpret_cast<const uint4*>(a.bkt + c);
-        unsigned nx;
-        if (c < a.base_words) {
-            const uint4 lo = __ldcg(p), hi = __ldcg(p + 1);
-            const unsigned e[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-            for (int k = 1; k < 7; ++k)
-                if (e[k] < mn) {
-                    mn = e[k];
-                    at = c + k;
-                }
-            nx = e[7];
-        } else {
-            uint4 q[BK_PW / 4];
-#pragma unroll
-            for (int i = 0; i < BK_PW / 4; ++i) q[i] = __ldcg(p + i);
-#pragma unroll
-            for (int i = 0; i < BK_PW / 4; ++i) {
-                const unsigned e[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int w = 4 * i + k;
-                    if (w >= 1 && w <= BK_PW - 2 && e[k] < mn) {
-                        mn = e[k];
-                        at = c + w;
-                    }
-                }
-            }
-            nx = q[BK_PW / 4 - 1].w;
-        }
-        c = nx;
-    } while (c != BK_NIL);
-    return mn;
-}
 
 // Round-0 entries of contended agents ci[0..B): the first-chunk counters of every contended
 // footprint cell taken in parallel, the rare overflows chained afterwards.
@@ -367,7 +325,7 @@ __device__ __forceinline__ void bk_prep(const MoveArgs& a, const unsigned* ci, c
             unsigned e = BK_NIL;
             const unsigned c = j <= m[b] ? cell[b][j] : BK_NIL;
             if (c != BK_NIL) {
-                if (k[b][j] < 6) {
+                if (k[b][j] < BK_BW - 2) {
                     e = c + 1 + k[b][j];
                     a.bkt[e] = r[b].y;
                 } else {
@@ -385,14 +343,97 @@ __device__ __forceinline__ void bk_prep(const MoveArgs& a, const unsigned* ci, c
     }
 }
 
-// Full check of pending agent ci (its watched blocker, if any, has walked).  Holding every cell
-// it walks and clears its entries right after the walk (release fence between), so a later
-// agent that sees them cleared may walk in the same round: its acquire fence orders its
-// occupancy reads after this walk.  Otherwise returns the entry of the latest-ranked blocker.
+// After prep: every contended cell's entries in rank order.  Agents leave a bucket in rank
+// order (an agent walks only as the earliest pending agent of each contended cell it has), so a
+// bucket's order is fixed once it is built: word 0 of the base chunk (the insertion counter so
+// far) becomes the entry word of the cell's current earliest agent, bnext[e] the entry after e
+// (BK_NIL after the last), and a walker advances each of its cells to its successor.  One
+// thread per bucket: up to six entries (the base chunk) sorted in registers, longer chains
+// gathered into local memory (a cell is covered by at most 121 footprints).
+#define BK_SORT_MAX 128
+// A bucket longer than its base chunk, one warp: the chain gathered into shared memory (one
+// 64-byte chunk per trip), each entry placed by counting the smaller ranks, successors written.
+// sw = 3 * BK_SORT_MAX words of this warp's shared scratch.
+__device__ void bk_sort_chain(const MoveArgs& a, unsigned c, unsigned* sw) {
+    const unsigned lane = threadIdx.x & 31;
+    unsigned* srk = sw;
+    unsigned* swd = sw + BK_SORT_MAX;
+    unsigned* ord = sw + 2 * BK_SORT_MAX;
+    unsigned n = 0;
+    for (unsigned p = c; p != BK_NIL && n < BK_SORT_MAX;) {
+        const unsigned v = lane < 16 ? __ldcg(&a.bkt[p + lane]) : 0u;  // count, 14 entries, link
+        const unsigned cnt = __shfl_sync(0xffffffffu, v, 0), link = __shfl_sync(0xffffffffu, v, 15);
+        const unsigned k = min(cnt + 1u, 14u);  // entries in this chunk (all-ones count = none)
+        if (lane >= 1 && lane <= k && n + lane - 1 < BK_SORT_MAX) {
+            srk[n + lane - 1] = v;
+            swd[n + lane - 1] = p + lane;
+        }
+        n = min(n + k, (unsigned)BK_SORT_MAX);
+        p = link;
+    }
+    __syncwarp();
+    for (unsigned i = lane; i < n; i += 32) {
+        const unsigned r = srk[i];
+        unsigned pos = 0;
+        for (unsigned j = 0; j < n; ++j) pos += srk[j] < r;
+        ord[pos] = swd[i];
+    }
+    __syncwarp();
+    if (lane == 0) a.bkt[c] = ord[0];
+    for (unsigned i = lane; i < n; i += 32) a.bnext[ord[i]] = i + 1 < n ? ord[i + 1] : BK_NIL;
+    __syncwarp();
+}
+
+__device__ void bk_sort_long(const MoveArgs& a, unsigned* scratch) {
+    const unsigned nl = cta_load(&a.pcount[7]);
+    const unsigned warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned* sw = scratch + warp * 3 * BK_SORT_MAX;
+    for (unsigned l = blockIdx.x * nw + warp; l < nl; l += gridDim.x * nw) bk_sort_chain(a, __ldcg(&a.long_list[l]), sw);
+}
+
+__device__ void bk_sort(const MoveArgs& a, unsigned nbu, unsigned gtid, unsigned nthreads) {
+    constexpr int E = BK_BW - 2;  // entries of a base chunk
+    for (unsigned b = gtid; b < nbu; b += nthreads) {
+        const unsigned c = b * BK_BW;
+        const uint4* p = reinterpret_cast<const uint4*>(a.bkt + c);
+        const uint4 q0 = __ldcg(p), q1 = __ldcg(p + 1), q2 = __ldcg(p + 2), q3 = __ldcg(p + 3);
+        const unsigned n = q0.x + 1u;  // entries inserted (all-ones = none)
+        if (n == 0) continue;
+        if (n > (unsigned)E) {  // handed to a warp (bk_sort_long)
+            a.long_list[atomicAdd(&a.pcount[7], 1u)] = c;
+            continue;
+        }
+        // keys (rank << 4 | slot) sorted in registers; empty slots (all-ones) sort last
+        const unsigned e[E] = {q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z};
+        unsigned key[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) key[i] = e[i] == BK_EMPTY ? 0xFFFFFFFFu : (e[i] << 4) | (unsigned)i;
+#pragma unroll
+        for (int rd = 0; rd < E; ++rd)  // odd-even transposition sort
+#pragma unroll
+            for (int i = rd & 1; i + 1 < E; i += 2) {
+                const unsigned x = min(key[i], key[i + 1]), y = max(key[i], key[i + 1]);
+                key[i] = x;
+                key[i + 1] = y;
+            }
+        a.bkt[c] = c + 1 + (key[0] & 15u);
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+            if ((unsigned)i < n)
+                a.bnext[c + 1 + (key[i] & 15u)] = (unsigned)(i + 1) < n ? c + 1 + (key[i + 1 < E ? i + 1 : E - 1] & 15u) : BK_NIL;
+    }
+}
+
+// Full check of pending agent ci (its watched blocker, if any, has walked): it is the earliest
+// pending agent on every contended cell it has when each of those cells' current-entry word
+// (word 0 of the base chunk, bk_sort) is its own entry.  Holding them all it walks, then
+// advances each cell to the entry after its own and clears its entries (release fence between),
+// so a later agent that sees them may walk in the same round: its acquire fence orders its
+// occupancy reads after this walk.  Otherwise returns the entry of a blocker to watch.
 __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2],
                                          unsigned long long* hops, unsigned* watch) {
-    // the record and the (entry, base chunk) pairs in one trip, every contended cell's base chunk
-    // in the next, the rare overflow chains afterwards
+    // the record and the (entry, base chunk) pairs in one trip; the current entries of the
+    // contended cells and this agent's successors in the next
     const uint4 r = __ldcg(&a.crec[ci]);
     unsigned cell[6], ent[6];
     {
@@ -406,58 +447,41 @@ __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const s
             cell[2 * h + 1] = q.w;
         }
     }
-    unsigned best = 0, best_at = BK_NIL;
-    bool own = true;
-    uint4 lo[6], hi[6];
+    unsigned cur[6], nx[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j)
-        if (cell[j] != BK_NIL) {
-            const uint4* p = reinterpret_cast<const uint4*>(a.bkt + cell[j]);
-            lo[j] = __ldcg(p);
-            hi[j] = __ldcg(p + 1);
+        if (cell[j] != BK_NIL && ent[j] != BK_NIL) {
+            cur[j] = __ldcg(&a.bkt[cell[j]]);
+            nx[j] = __ldcg(&a.bnext[ent[j]]);
         }
+    bool own = true;
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        if (cell[j] == BK_NIL) continue;
-        const unsigned e[8] = {lo[j].x, lo[j].y, lo[j].z, lo[j].w, hi[j].x, hi[j].y, hi[j].z, hi[j].w};
-        unsigned mn = BK_EMPTY, at = BK_NIL;
+    for (int j = 0; j < 6; ++j) own &= cell[j] == BK_NIL || ent[j] == BK_NIL || cur[j] == ent[j];
+    if (!own) {  // watch the latest-ranked blocker (the others walk before it)
+        unsigned rk[6];
 #pragma unroll
-        for (int k = 1; k < 7; ++k)
-            if (e[k] < mn) {
-                mn = e[k];
-                at = cell[j] + k;
+        for (int j = 0; j < 6; ++j)
+            rk[j] = (cell[j] != BK_NIL && ent[j] != BK_NIL && cur[j] != ent[j]) ? __ldcg(&a.bkt[cur[j]]) : 0u;
+        unsigned best = 0, blocker = BK_NIL;
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+            if (cell[j] != BK_NIL && ent[j] != BK_NIL && cur[j] != ent[j] && (blocker == BK_NIL || rk[j] > best)) {
+                best = rk[j];
+                blocker = cur[j];
             }
-        if (e[7] != BK_NIL) {
-            unsigned at2;
-            const unsigned m2 = bk_min(a, e[7], at2);
-            if (m2 < mn) {
-                mn = m2;
-                at = at2;
-            }
-        }
-        if (mn != r.y) {
-            own = false;
-            if (best_at == BK_NIL || mn > best) {
-                best = mn;
-                best_at = at;
-            }
-        }
-    }
-    if (!own) {
-        *watch = best_at;
+        *watch = blocker;
         return false;
     }
     fence_acq_rel_gpu();  // acquire: the walks of the earlier agents on these cells are visible
     int cx[5], cy[5];
     const int mw = path_of(a, r, bp, cx, cy);  // the walk covers the whole path (m >= mf)
     walk_owned(a, r, cx, cy, mw, hops);
-    fence_acq_rel_gpu();  // release: this walk before the cleared entries
+    fence_acq_rel_gpu();  // release: this walk before the advanced cells and cleared entries
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-        const unsigned e = ent[j];
-        if (e == BK_NIL) continue;
-        a.bkt[e] = BK_EMPTY;
-        a.bkt[bk_start(a, e)] = BK_EMPTY;  // the chunk's entry counter (no insertions during the rounds)
+        if (cell[j] == BK_NIL || ent[j] == BK_NIL) continue;
+        a.bkt[cell[j]] = nx[j];
+        a.bkt[ent[j]] = BK_EMPTY;
     }
     return true;
 }
@@ -539,6 +563,7 @@ struct TailSmem {
 #define QP_CAP 8192
 #define QC_CAP 8192
 static_assert(QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) <= sizeof(TailSmem), "round queues");
+static_assert((MOVE_THREADS / 32) * 3 * BK_SORT_MAX * sizeof(unsigned) <= sizeof(TailSmem), "long-bucket sort");
 
 __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y, bool buckets) {
     const unsigned cell = (unsigned)y * (unsigned)a.g.W + (unsigned)x;
@@ -552,9 +577,10 @@ __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, 
             // by the other blocks)
             const unsigned c = buckets ? bucket_of(a, x, y) : BK_NIL;
             if (c != BK_NIL) {
-                uint32_t* b = a.bkt + c;
-                reinterpret_cast<uint4*>(b)[0] = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
-                b[4] = b[5] = b[6] = BK_EMPTY;
+                uint32_t* b = a.bkt + c;  // everything but the link (reset with the pool)
+                const uint4 ones = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
+                for (int q = 0; q < 3; ++q) reinterpret_cast<uint4*>(b)[q] = ones;
+                b[12] = b[13] = b[14] = BK_EMPTY;
             }
             return h;
         }
@@ -721,8 +747,10 @@ __device__ void p2_number(const MoveArgs& a, unsigned* red) {
         out[1] = make_uint4(e + c0 + c1, q.z, e + c0 + c1 + c2, q.w);
         e += c0 + c1 + c2 + __popc(q.w);
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1 && e > a.nb_cap)
-        atomicOr(&a.sc->err, 16ull);  // cannot happen: <= 3 contended cells per contended agent
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) {
+        a.scan[gridDim.x] = e;  // contended cells (buckets) this phase
+        if (e > a.nb_cap) atomicOr(&a.sc->err, 16ull);  // cannot happen: <= 3 per contended agent
+    }
 }
 
 // Zeroes the contention bitplanes (dead after step 2) so the next phase starts from all-clear.
@@ -947,7 +975,7 @@ __device__ __forceinline__ bool classify(const MoveArgs& a, uint4& rec, const si
     return true;
 }
 
-__global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
+__global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ signed char s_bp[121][5][2];
     extern __shared__ __align__(16) unsigned char s_dyn[];  // TailSmem (block 0's tail) / seed windows
@@ -1051,6 +1079,10 @@ __global__ void __launch_bounds__(MOVE_THREADS) move_rounds_kernel(MoveArgs a) {
             a.pcount[4] = nc;
             a.pcount[5] = a.pcount[6] = 0;
         }
+        grid.sync();
+        bk_sort(a, cta_load(&a.scan[gridDim.x]), gtid, nthreads);
+        grid.sync();
+        bk_sort_long(a, reinterpret_cast<unsigned*>(s_dyn));
         grid.sync();
         if (gtid == 0) a.sc->t_prep = globaltimer();
         bk_pool_prefix(a, s_pool);
@@ -1190,7 +1222,7 @@ int fp_ensure_res(fp_ctx* ctx) {
 
 static int g_move_blocks = 0;
 
-// Rank buckets: one 32-byte base chunk per contended cell (<= 3 per agent: every contended cell
+// Rank buckets: one 64-byte base chunk per contended cell (<= 3 per agent: every contended cell
 // is covered by >= 2 of the <= 6-cell footprints) plus 64-byte overflow chunks (six entries per
 // agent, seven to overflow a cell), the per-agent (entry, base chunk) pairs, the per-word dense
 // numbering and its per-CTA counts; buckets all-empty between phases.
@@ -1199,16 +1231,18 @@ static int ensure_buckets(fp_ctx* ctx) {
     const size_t pool_sub = ((size_t)ctx->cap * 6 / 7 + 64) / BK_SUBPOOLS + 16;
     const size_t pool = pool_sub * BK_SUBPOOLS;
     if (ctx->d_bkt && ctx->bk_pool_cap >= pool && ctx->bk_agent_cap >= ctx->cap) return FP_OK;
-    const size_t words = nb * 8 + pool * BK_PW;
+    const size_t words = nb * BK_BW + pool * BK_PW;
     if (words >= 0xFFFFFFFFull)
         return fp_fail(ctx, FP_ERUNTIME, "motion: roster too large for 32-bit bucket word indices");
     cudaStreamSynchronize(ctx->stream);
-    for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_pool_owner, (void*)ctx->d_entry, (void*)ctx->d_pool_n})
+    for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_pool_owner, (void*)ctx->d_entry, (void*)ctx->d_pool_n,
+                    (void*)ctx->d_bnext})
         if (p) cudaFree(p);
     ctx->d_pool_n = nullptr;
     FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_n, BK_SUBPOOLS * BK_SUB_STRIDE * 4 + 1024 * 4));  // + p2 scan counts
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_pool_n, 0, BK_SUBPOOLS * BK_SUB_STRIDE * 4 + 1024 * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_bkt, words * 4));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_bnext, words * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0xFF, words * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_owner, pool * 4));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * 6 * sizeof(uint2)));
@@ -1271,7 +1305,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.crec = ctx->d_rec_b;
     a.bkt = ctx->d_bkt;
     a.nb_cap = ctx->bk_nb_cap;
-    a.base_words = ctx->bk_nb_cap * 8u;
+    a.base_words = ctx->bk_nb_cap * BK_BW;
     a.pw = ctx->d_pw;
     a.scan = ctx->d_pool_n + BK_SUBPOOLS * BK_SUB_STRIDE;
     a.pool_cap = ctx->bk_pool_cap;
@@ -1282,10 +1316,12 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
         a.seed_static = st;
     }
     a.pool_owner = ctx->d_pool_owner;
+    a.bnext = ctx->d_bnext;
     a.entry = ctx->d_entry;
     uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
     a.alist[0] = lists;
     a.alist[1] = lists + ctx->cap;
+    a.long_list = reinterpret_cast<unsigned*>(lists + ctx->cap);  // alist[1] is free until round 0
     if (premade && (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4 > sizeof(TailSmem))
         return fp_fail(ctx, FP_ERUNTIME, "motion: seed window exceeds shared memory");
     const unsigned blocks = (unsigned)std::min<size_t>((size_t)g_move_blocks,
