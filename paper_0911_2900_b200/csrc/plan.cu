@@ -601,6 +601,15 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         s_pathm[k] = make_uint4(c_pathmask[k][0], c_pathmask[k][1], c_pathmask[k][2], c_pathmask[k][3]);
     const PlanCommon& a = A.c;
     const uint64_t step = (uint64_t)a.sc->step;
+    // list entry of fetch number i, or -1 past the end
+    auto fetch_entry = [&](int i) {
+        for (int p = 0, k = i; p < A.passes; ++p) {
+            const int lo = (int)A.deal[p * gridDim.x + blockIdx.x], hi = (int)A.deal[p * gridDim.x + blockIdx.x + 1];
+            if (k < hi - lo) return lo + k;
+            k -= hi - lo;
+        }
+        return -1;
+    };
     // fetch number i into slot i % PLAN_SLOTS (one thread)
     auto fetch = [&](int i) {
         const int slot = i % PLAN_SLOTS;
@@ -609,15 +618,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // fetch i of this CTA is the i-th entry of its ranges (one per pass, bucket.cu
         // tile_deal_kernel) taken in order, so fetch numbers map monotonically onto the list and
         // an exhausted fetch ends every later one (refills complete out of order)
-        int t = -1;
-        for (int p = 0, k = i; p < A.passes; ++p) {
-            const int lo = (int)A.deal[p * gridDim.x + blockIdx.x], hi = (int)A.deal[p * gridDim.x + blockIdx.x + 1];
-            if (k < hi - lo) {
-                t = lo + k;
-                break;
-            }
-            k -= hi - lo;
-        }
+        const int t = fetch_entry(i);
         if (blockIdx.x == 5 && i < 256) g_plan_dbg[i] = globaltimer_p();
         if (t >= 0) {
             const uint32_t tile = A.tile_list[t];
