@@ -561,9 +561,9 @@ __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint3
 
 #define PLAN_THREADS 512
 #ifndef FP_PLAN_NAP_MAX
-#define FP_PLAN_NAP_MAX 1024  // ns
+#define FP_PLAN_NAP_MAX 256  // ns
 #endif
-#define PLAN_SLOTS 3  // tiles resident per CTA (one fetching while two compute)
+#define PLAN_SLOTS 3  // tiles resident per CTA
 
 // Persistent CTA per SM.  Tiles are fetched in pairs of buffer slots (TMA, mbarrier); the
 // agents of fetch i are dealt to threads round-robin starting at thread (i*160) mod 512, one
