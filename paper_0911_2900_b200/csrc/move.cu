@@ -561,6 +561,10 @@ struct TailSmem {
 
 // Round queues in the same dynamic buffer (see the rounds in move_rounds_kernel).
 #define QP_CAP 8192
+#ifndef MOVE_LOCAL_ITERS
+#define MOVE_LOCAL_ITERS 3     // extra in-CTA check passes per grid round
+#endif
+#define MOVE_LOCAL_MAX 2048    // ... while the CTA holds at most this many pending agents
 #define QC_CAP 8192
 static_assert(QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) <= sizeof(TailSmem), "round queues");
 static_assert((MOVE_THREADS / 32) * 3 * BK_SORT_MAX * sizeof(unsigned) <= sizeof(TailSmem), "long-bucket sort");
@@ -1144,6 +1148,42 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                     const unsigned s = atomicAdd(qpn, 1u);
                     if (s < QP_CAP) qp[s] = make_uint2(ci, w);
                     else next[atomicAdd(ncount, 1u)] = make_uint2(ci, w);
+                }
+            }
+            // local iterations: this CTA's still-pending agents whose watched blocker walked
+            // during this round (in any CTA) are checked again at once, so a chain of agents can
+            // advance several links per grid round.  Each pending agent lives in one CTA's
+            // queue, so no agent is checked twice at the same time.
+            for (int it = 0; it < MOVE_LOCAL_ITERS; ++it) {
+                __syncthreads();
+                const unsigned nq0 = min(*qpn, (unsigned)QP_CAP);
+                if (nq0 == 0 || nq0 > MOVE_LOCAL_MAX) break;  // uniform: read after the barrier
+                constexpr int PER = MOVE_LOCAL_MAX / MOVE_THREADS;
+                uint2 e[PER];
+                unsigned v[PER];
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const unsigned idx = threadIdx.x + k * MOVE_THREADS;
+                    e[k] = idx < nq0 ? qp[idx] : make_uint2(BK_NIL, BK_NOWATCH);
+                }
+#pragma unroll
+                for (int k = 0; k < PER; ++k) v[k] = e[k].y != BK_NOWATCH ? __ldcg(&a.bkt[e[k].y]) : BK_EMPTY;
+                __syncthreads();
+                if (threadIdx.x == 0) *qpn = *qcn = 0;
+                __syncthreads();
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    if (e[k].x == BK_NIL) continue;
+                    if (v[k] != BK_EMPTY) qp[atomicAdd(qpn, 1u)] = e[k];
+                    else qc[atomicAdd(qcn, 1u)] = e[k].x;
+                }
+                __syncthreads();
+                const unsigned nl = *qcn;
+                if (nl == 0) break;  // uniform
+                for (unsigned i = threadIdx.x; i < nl; i += blockDim.x) {
+                    const unsigned ci = qc[i];
+                    unsigned w;
+                    if (!bk_check(a, ci, s_bp, &hops, &w)) qp[atomicAdd(qpn, 1u)] = make_uint2(ci, w);
                 }
             }
             flush_hops(B, a.sc, hops);  // (its barriers also complete the queue)
