@@ -893,20 +893,26 @@ __device__ void seed_mark(const MoveArgs& a, uint32_t* win, unsigned int* slot, 
 }
 
 // S2: uncontended movers walk now; the rest go to the rounds (list rec[1]) with their rank.
-__device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, unsigned int* slot,
-                              const signed char (*bp)[5][2],
+// Tiles are dealt round-robin to the worker groups; the next tile's header is fetched while
+// the current one is classified, and a tile's first records and their ranks travel with the
+// window staging (the latency of a tile is what bounds this pass).
+__device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, const signed char (*bp)[5][2],
                               unsigned long long* hops) {
     const unsigned lt = threadIdx.x % SEED_GROUP;
     const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
-    unsigned k = 0;
-    for (;;) {
-        const uint32_t e = seed_next(a, &a.pcount[3], slot, k);
-        if (e >= nt) break;
-        const uint32_t t = a.tile_list[e];
+    const uint32_t ng = gridDim.x * SEED_GROUPS;
+    uint32_t e = blockIdx.x * SEED_GROUPS + threadIdx.x / SEED_GROUP;
+    uint32_t t = e < nt ? __ldcg(&a.tile_list[e]) : 0u;
+    uint32_t off = e < nt ? __ldcg(&a.tile_off[t]) : 0u, cnt = e < nt ? __ldcg(&a.tile_cnt[t]) : 0u;
+    for (; e < nt; e += ng) {
+        // next tile's header in flight
+        const uint32_t en = e + ng;
+        const uint32_t tn = en < nt ? __ldcg(&a.tile_list[en]) : 0u;
         const SeedWin s = seed_window(a, t);
         const int nw = s.ww * s.wh;
         uint32_t* C2 = win;       // P2 window
         uint32_t* CO = win + nw;  // occupancy window
+        const uint4 r0 = lt < cnt ? __ldcg(&a.rec0[off + lt]) : make_uint4(0, 0, 0, 0);
 #pragma unroll 4
         for (int w = lt; w < nw; w += SEED_GROUP) {
             uint32_t v2 = 0, vo = 0;
@@ -918,14 +924,15 @@ __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, 
             C2[w] = v2;
             CO[w] = vo;
         }
+        const uint32_t rk0 = (lt < cnt && rec_m(r0)) ? __ldcg(&a.rank[r0.x]) : 0u;
+        const uint32_t offn = en < nt ? __ldcg(&a.tile_off[tn]) : 0u, cntn = en < nt ? __ldcg(&a.tile_cnt[tn]) : 0u;
         group_sync();
-        const uint32_t off = a.tile_off[t], cnt = a.tile_cnt[t];
         for (uint32_t base = 0; base < cnt; base += SEED_GROUP) {
             const uint32_t k = base + lt;
             bool contended = false;
             uint4 r = make_uint4(0, 0, 0, 0);
             if (k < cnt) {
-                r = __ldcg(&a.rec0[off + k]);
+                r = base == 0 ? r0 : __ldcg(&a.rec0[off + k]);
                 if (rec_m(r)) {
                     int cx[6], cy[6], m, mf;
                     record_footprint(a, r, bp, cx, cy, m, mf);
@@ -948,12 +955,15 @@ __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, 
                         if (i > 0) blocked[i - 1] = (vo >> sh) & 1u;
                     }
                     if (!contended) walk_apply(a, r, cx + 1, cy + 1, m, blocked, hops);
-                    else r.y = a.rank[r.x];
+                    else r.y = base == 0 ? rk0 : __ldcg(&a.rank[r.x]);
                 }
             }
             append(G, &a.pcount[1], a.rec[1], contended, r);
         }
         group_sync();
+        t = tn;
+        off = offn;
+        cnt = cntn;
     }
 }
 
@@ -1032,7 +1042,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
         if (gtid == 0) a.sc->t_marked = globaltimer();
         p2_count(a, s_red);
         unsigned long long hops = 0;
-        seed_classify(a, Gs, win, slot, s_bp, &hops);
+        seed_classify(a, Gs, win, s_bp, &hops);
         flush_hops(B, a.sc, hops);
         ncand = 0;  // step 2 done
     }
@@ -1352,7 +1362,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.pool_sub = ctx->bk_pool_cap / BK_SUBPOOLS;
     a.pool_n = ctx->d_pool_n;
     {
-        static const int st = getenv("FP_SEED_STATIC") ? atoi(getenv("FP_SEED_STATIC")) : 0;
+        static const int st = getenv("FP_SEED_STATIC") ? atoi(getenv("FP_SEED_STATIC")) : 1;
         a.seed_static = st;
     }
     a.pool_owner = ctx->d_pool_owner;
