@@ -268,7 +268,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
                     c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal, c->d_tile_exit,
                     c->d_sc,
                     c->d_p1, c->d_p2,
-                    c->d_bkt, c->d_pool_owner, c->d_pool_n, c->d_pw, c->d_bnext};
+                    c->d_bkt, c->d_bdone, c->d_pw};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);

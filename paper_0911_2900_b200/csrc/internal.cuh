@@ -201,12 +201,11 @@ struct fp_ctx {
     uint4* d_rec0 = nullptr;    // walk records in plan-tile order, emitted by the plan phase
     // motion reservation rounds (move.cu): rank buckets (8-word chunk per cell + overflow pool,
     // all-empty between phases) and per-agent entries
-    uint32_t *d_bkt = nullptr, *d_pool_owner = nullptr;
-    uint32_t* d_pool_n = nullptr;
-    uint32_t* d_bnext = nullptr;   // successor entry word of each bucket entry (rank order)  // per-sub-pool taken counts (BK_SUBPOOLS, 128 B apart), zero between phases
-    uint2* d_entry = nullptr;    // (entry word, base chunk) per footprint cell of a contended agent
-    uint2* d_pw = nullptr;       // per bitplane word: (contended cells before it, its P2 bits)
-    unsigned bk_pool_cap = 0, bk_agent_cap = 0, bk_nb_cap = 0;
+    uint32_t* d_bkt = nullptr;     // motion buckets: counters, bases, current positions, ranks, scan counts
+    uint8_t* d_bdone = nullptr;    // motion buckets: per-position done flags
+    uint2* d_entry = nullptr;      // (position, bucket) per footprint cell of a contended agent
+    uint2* d_pw = nullptr;         // per bitplane word: (contended cells before it, its P2 bits)
+    unsigned bk_agent_cap = 0, bk_nb_cap = 0, bk_npos_cap = 0;
     bool bucket_fresh = false;  // plan-tile buckets match the current positions
     bool rec_fresh = false;     // d_rec0 + contention marks match the current desired cells
     bool marks_dirty = false;   // contention bitplanes hold marks no motion phase consumed

@@ -60,24 +60,23 @@ struct MoveArgs {
     const uint32_t* tile_off;
     const uint32_t* tile_cnt;
     int tile_w, tile_h, tiles_x;
-    // reservation rounds: contended records crec (= rec[1]), their hash slots, ping-pong lists
-    const uint4* crec;
-    uint32_t* bkt;                 // rank buckets: 8-word chunks, base chunk of a cell = cell index,
-                                   // then pool_cap overflow chunks; all-empty between phases
-    unsigned base_words;           // 8 * nb_cap; pool chunks follow
-    unsigned nb_cap;               // base chunks: one per contended cell (<= 3 per contended agent)
+    // reservation rounds (see the bucket notes below)
+    const uint4* crec;             // contended records (= rec[1]), rank in .y
     uint2* pw;                     // per bitplane word: (contended cells before it, its P2 bits)
-    unsigned* scan;                // per-CTA contended-cell counts (p2_count -> p2_number)
-    unsigned pool_cap;             // BK_SUBPOOLS * pool_sub
-    unsigned pool_sub;             // chunks per sub-pool
-    unsigned* pool_n;              // chunks taken from each sub-pool this phase (BK_SUB_STRIDE apart)
-    unsigned* pool_owner;          // chunk that links to each taken pool chunk
-    unsigned* bnext;               // per bucket entry word: the entry of the next agent in rank order
-    unsigned* long_list;           // buckets longer than a base chunk (bk_sort -> bk_sort_long)
-    uint2* entry;                  // 6 per contended agent: (its entry word, the cell's base chunk)
-                                   // per footprint cell; BK_NIL/BK_NIL for an uncontended cell
+    unsigned* scan;                // [0, G) per-CTA contended cells, [G] their total;
+                                   // [BK_SCAN2, BK_SCAN2 + G) per-CTA bucket entries, + G total
+    unsigned nb_cap;               // buckets (contended cells): <= 3 per contended agent
+    unsigned npos_cap;             // bucket positions: <= 6 per contended agent
+    unsigned* bcnt;                // per bucket: entries counted (zero between phases)
+    unsigned* bbase;               // per bucket: its first position
+    unsigned* bcur;                // per bucket: position of its current earliest agent
+    uint2* brank;                  // per position (placement order): (rank, agent * 8 + cell)
+    unsigned* long_list;           // buckets longer than BK_SORT_REG (ranked by warps)
+    uint8_t* bdone;                // per position (rank order): that agent has walked
+    uint2* entry;                  // 6 per contended agent: (slot, then position; bucket) per
+                                   // footprint cell; BK_NIL/BK_NIL for an uncontended cell
     // contended-index pending lists (ping-pong), carved from rec[0] (free after step 2)
-    uint2* alist[2];               // (contended index, entry of the blocker it waits on)
+    uint2* alist[2];               // (contended index, position of the predecessor it waits on)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -205,46 +204,42 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
 }
 
 // ------------------------------------------------------------------ grid-wide reservation rounds
-// Every contended agent enters its rank into the bucket of each footprint cell.  A bucket is a
-// chain of chunks addressed by word index into one array: the cell's base chunk (BK_BW words:
-// entry count, 14 entries, link) then, when crowded, BK_PW-word overflow chunks
-// from a pool (count, 14 entries, link).  An agent is the earliest pending agent on a cell iff
-// its rank is the bucket minimum; holding all of its cells it walks (everything before it in
-// the reference order on those cells has run) and clears its entries.  A blocked agent
-// watches the entry of one blocker (the latest-ranked) and re-checks only once that entry is
-// cleared, so a waiting agent costs one load per round.  Entries are never reused within a
-// phase, so "entry still holds the rank" == "still pending".
+// Every contended cell (covered by two or more footprints, P2) is numbered densely (p2_number)
+// and holds a bucket: the contended agents whose footprint has the cell, in rank (processing)
+// order, at positions [bbase[b], bbase[b] + n_b) of one array.  Agents leave a bucket in rank
+// order -- an agent walks only as the earliest pending agent of every contended cell it has --
+// so bcur[b], the position of the cell's current earliest agent, only ever steps by one: the
+// agent at position p owns the cell iff bcur[b] == p, and after its walk it sets bcur[b] = p + 1
+// and bdone[p].  A blocked agent at p waits for bdone[p - 1]: its predecessor in the bucket
+// walks only after everyone before it, so one byte says when the cell is its own.  cur and done
+// are a few MB and stay in L2 through the rounds.  Built per phase by
+//   bk_count  per contended agent: its slot k in each of its buckets (one atomic counter each)
+//   bk_scan   bbase = exclusive prefix of the bucket sizes (two passes like p2_number)
+//   bk_place  brank[bbase + k] = (rank, agent * 8 + cell)
+//   bk_sort   per bucket: each entry's position = bbase + #{ranks below its own}, handed to its
+//             agent; bcur = bbase; the bucket's done flags cleared
 #define BK_EMPTY 0xFFFFFFFFu
-// Release/acquire is all the walk -> cleared-entry handoff needs (MEMBAR.ALL.GPU, not the
+// Release/acquire is all the walk -> advanced-cell handoff needs (MEMBAR.ALL.GPU, not the
 // sequentially consistent MEMBAR.SC.GPU that __threadfence() emits).
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 #define BK_NIL 0xFFFFFFFFu
 #define BK_NOWATCH 0xFFFFFFFFu
+#define BK_SCAN2 1024  // offset of the bucket-size scan counts in MoveArgs::scan
 #ifndef BK_PREP_BATCH
 #define BK_PREP_BATCH 2  // contended agents per thread per prep step
 #endif
-#define BK_BW 16u  // words per base chunk: count / current entry, BK_BW - 2 entries, link (64 bytes)
-#define BK_PW 16u  // words per overflow chunk: count, BK_PW - 2 entries, link (one 64-byte read)
-#define BK_SUBPOOL_BITS 6
-#define BK_SUBPOOLS (1 << BK_SUBPOOL_BITS)
-#define BK_SUB_STRIDE 32  // words between sub-pool counters (one 128-byte line each)
 
-__device__ __forceinline__ bool bk_pool(const MoveArgs& a, unsigned c) { return c >= a.base_words; }
-__device__ __forceinline__ unsigned bk_cap(const MoveArgs& a, unsigned c) { return bk_pool(a, c) ? BK_PW - 2u : BK_BW - 2u; }
-__device__ __forceinline__ unsigned bk_link(const MoveArgs& a, unsigned c) { return c + (bk_pool(a, c) ? BK_PW - 1u : BK_BW - 1u); }
-
-// Base chunk (word index) of cell (x, y) when two or more footprints cover it (P2), else BK_NIL.
-// The contended cells are numbered densely in bitplane order (p2_number), so their buckets are
-// 32 bytes each in one compact array (L2-sized) instead of one chunk per grid cell; a cell only
-// one footprint covers needs no bucket (its agent is trivially the earliest there).
+// Bucket of cell (x, y) when two or more footprints cover it (P2), else BK_NIL.  The contended
+// cells are numbered densely in bitplane order (p2_number); a cell only one footprint covers
+// needs no bucket (its agent is trivially the earliest there).
 __device__ __forceinline__ unsigned bucket_of(const MoveArgs& a, int x, int y) {
     const uint2 q = __ldcg(&a.pw[a.g.word(x, y)]);
     const uint32_t bit = 1u << (x & 31);
-    return (q.y & bit) ? (q.x + (unsigned)__popc(q.y & (bit - 1u))) * BK_BW : BK_NIL;
+    return (q.y & bit) ? q.x + (unsigned)__popc(q.y & (bit - 1u)) : BK_NIL;
 }
 
-// Base chunks of a record's footprint cells: [0] start, [1..mf] path (motion_rec.cuh), BK_NIL
-// for cells no other footprint covers; returns mf.
+// Buckets of a record's footprint cells: [0] start, [1..mf] path (motion_rec.cuh), BK_NIL for
+// cells no other footprint covers; returns mf.
 __device__ __forceinline__ int footprint(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
                                          unsigned* cell) {
     int cx[5], cy[5];
@@ -257,276 +252,209 @@ __device__ __forceinline__ int footprint(const MoveArgs& a, const uint4& r, cons
     return m;
 }
 
-// The overflow chunk linked from chunk c, linking a fresh one from the pool if there is none
-// (BK_NIL when the pool is exhausted).
-__device__ unsigned bk_next(const MoveArgs& a, unsigned c) {
-    unsigned* link = &a.bkt[bk_link(a, c)];
-    const unsigned nx = __ldcg(link);
-    if (nx != BK_NIL) return nx;
-    // overflow chunks come from BK_SUBPOOLS sub-pools picked by a hash of the chunk, each with
-    // its own counter: tens of thousands of allocations per phase would serialise on one address
-    unsigned s = (c * 2654435761u) >> (32 - BK_SUBPOOL_BITS), q = BK_NIL;
-    for (int t = 0; t < BK_SUBPOOLS; ++t, s = (s + 1) & (BK_SUBPOOLS - 1)) {
-        const unsigned k = atomicAdd(&a.pool_n[s * BK_SUB_STRIDE], 1u);
-        if (k < a.pool_sub) {
-            q = s * a.pool_sub + k;
-            break;
-        }
-    }
-    if (q == BK_NIL) return BK_NIL;
-    const unsigned fresh = a.base_words + q * BK_PW;  // pool chunks are all-empty between phases
-    const unsigned old = atomicCAS(link, BK_NIL, fresh);
-    a.pool_owner[q] = old == BK_NIL ? c : BK_NIL;  // a lost race leaves the chunk unused
-    return old == BK_NIL ? fresh : old;
-}
-
-// Enters `rank` into the bucket chain starting at chunk `c`; returns the entry's word index, or
-// BK_NIL when the overflow pool is exhausted.  Word 0 of a chunk counts its taken entries
-// (all-ones = none, so the all-ones reset state needs no separate zeroing): the atomicAdd hands
-// out entries without retries; the last word links the next chunk.
-__device__ unsigned bk_insert(const MoveArgs& a, unsigned c, unsigned rank) {
-    for (;;) {
-        const unsigned k = atomicAdd(&a.bkt[c], 1u) + 1u;  // 0-based slot
-        if (k < bk_cap(a, c)) {
-            a.bkt[c + 1 + k] = rank;
-            return c + 1 + k;
-        }
-        c = bk_next(a, c);
-        if (c == BK_NIL) return BK_NIL;
+__device__ __forceinline__ void load_pairs(const MoveArgs& a, unsigned ci, unsigned* slot, unsigned* cell) {
+    const uint4* p = reinterpret_cast<const uint4*>(a.entry + (size_t)ci * 6);
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+        const uint4 q = __ldcg(p + h);
+        slot[2 * h] = q.x;
+        cell[2 * h] = q.y;
+        slot[2 * h + 1] = q.z;
+        cell[2 * h + 1] = q.w;
     }
 }
 
+__device__ __forceinline__ void store_pairs(const MoveArgs& a, unsigned ci, const unsigned* slot,
+                                            const unsigned* cell) {
+    uint4* p = reinterpret_cast<uint4*>(a.entry + (size_t)ci * 6);
+#pragma unroll
+    for (int h = 0; h < 3; ++h) p[h] = make_uint4(slot[2 * h], cell[2 * h], slot[2 * h + 1], cell[2 * h + 1]);
+}
 
-// Round-0 entries of contended agents ci[0..B): the first-chunk counters of every contended
-// footprint cell taken in parallel, the rare overflows chained afterwards.
+// B contended agents at once: records, then their bucket lookups, then the counter atomics.
 template <int B>
-__device__ __forceinline__ void bk_prep(const MoveArgs& a, const unsigned* ci, const bool* ok,
-                                        const signed char (*bp)[5][2]) {
-    // B agents at once: their records, then all their bucket lookups, then all their counter
-    // atomics in flight together (each stage is one dependent trip)
+__device__ __forceinline__ void bk_count(const MoveArgs& a, const unsigned* ci, const bool* ok,
+                                         const signed char (*bp)[5][2]) {
     uint4 r[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) r[b] = ok[b] ? __ldcg(&a.crec[ci[b]]) : make_uint4(0, 0, 0, 0);
-    unsigned cell[B][6], k[B][6];
+    unsigned cell[B][6];
     int m[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) m[b] = ok[b] ? footprint(a, r[b], bp, cell[b]) : -1;
 #pragma unroll
-    for (int b = 0; b < B; ++b)
-#pragma unroll
-        for (int j = 0; j < 6; ++j)
-            if (j <= m[b] && cell[b][j] != BK_NIL) k[b][j] = atomicAdd(&a.bkt[cell[b][j]], 1u) + 1u;
-#pragma unroll
     for (int b = 0; b < B; ++b) {
         if (!ok[b]) continue;
-        uint2 eb[6];
+        unsigned slot[6], c6[6];
 #pragma unroll
         for (int j = 0; j < 6; ++j) {
-            unsigned e = BK_NIL;
-            const unsigned c = j <= m[b] ? cell[b][j] : BK_NIL;
-            if (c != BK_NIL) {
-                if (k[b][j] < BK_BW - 2) {
-                    e = c + 1 + k[b][j];
-                    a.bkt[e] = r[b].y;
-                } else {
-                    const unsigned nx = bk_next(a, c);
-                    e = nx == BK_NIL ? BK_NIL : bk_insert(a, nx, r[b].y);
-                }
-                if (e == BK_NIL) atomicOr(&a.sc->err, 8ull);  // pool exhausted (sized for the worst case)
-            }
-            eb[j] = make_uint2(e, c);
+            c6[j] = j <= m[b] ? cell[b][j] : BK_NIL;
+            slot[j] = c6[j] != BK_NIL ? atomicAdd(&a.bcnt[c6[j]], 1u) : BK_NIL;
         }
-        uint4* out = reinterpret_cast<uint4*>(a.entry + (size_t)ci[b] * 6);
-#pragma unroll
-        for (int h = 0; h < 3; ++h) out[h] = make_uint4(eb[2 * h].x, eb[2 * h].y, eb[2 * h + 1].x, eb[2 * h + 1].y);
+        store_pairs(a, ci[b], slot, c6);
         a.alist[0][ci[b]] = make_uint2(ci[b], BK_NOWATCH);
     }
 }
 
-// After prep: every contended cell's entries in rank order.  Agents leave a bucket in rank
-// order (an agent walks only as the earliest pending agent of each contended cell it has), so a
-// bucket's order is fixed once it is built: word 0 of the base chunk (the insertion counter so
-// far) becomes the entry word of the cell's current earliest agent, bnext[e] the entry after e
-// (BK_NIL after the last), and a walker advances each of its cells to its successor.  One
-// thread per bucket: up to six entries (the base chunk) sorted in registers, longer chains
-// gathered into local memory (a cell is covered by at most 121 footprints).
-#define BK_SORT_MAX 128
-// A bucket longer than its base chunk, one warp: the chain gathered into shared memory (one
-// 64-byte chunk per trip), each entry placed by counting the smaller ranks, successors written.
-// sw = 3 * BK_SORT_MAX words of this warp's shared scratch.
-__device__ void bk_sort_chain(const MoveArgs& a, unsigned c, unsigned* sw) {
-    const unsigned lane = threadIdx.x & 31;
-    unsigned* srk = sw;
-    unsigned* swd = sw + BK_SORT_MAX;
-    unsigned* ord = sw + 2 * BK_SORT_MAX;
-    unsigned n = 0;
-    for (unsigned p = c; p != BK_NIL && n < BK_SORT_MAX;) {
-        const unsigned v = lane < 16 ? __ldcg(&a.bkt[p + lane]) : 0u;  // count, 14 entries, link
-        const unsigned cnt = __shfl_sync(0xffffffffu, v, 0), link = __shfl_sync(0xffffffffu, v, 15);
-        const unsigned k = min(cnt + 1u, 14u);  // entries in this chunk (all-ones count = none)
-        if (lane >= 1 && lane <= k && n + lane - 1 < BK_SORT_MAX) {
-            srk[n + lane - 1] = v;
-            swd[n + lane - 1] = p + lane;
-        }
-        n = min(n + k, (unsigned)BK_SORT_MAX);
-        p = link;
-    }
-    __syncwarp();
-    for (unsigned i = lane; i < n; i += 32) {
-        const unsigned r = srk[i];
-        unsigned pos = 0;
-        for (unsigned j = 0; j < n; ++j) pos += srk[j] < r;
-        ord[pos] = swd[i];
-    }
-    __syncwarp();
-    if (lane == 0) a.bkt[c] = ord[0];
-    for (unsigned i = lane; i < n; i += 32) a.bnext[ord[i]] = i + 1 < n ? ord[i + 1] : BK_NIL;
-    __syncwarp();
+__device__ __forceinline__ void bk_slice(unsigned nbu, unsigned& b0, unsigned& b1) {
+    const unsigned per = (nbu + gridDim.x - 1) / gridDim.x;
+    b0 = min(nbu, blockIdx.x * per);
+    b1 = min(nbu, b0 + per);
 }
 
-__device__ void bk_sort_long(const MoveArgs& a, unsigned* scratch) {
-    const unsigned nl = cta_load(&a.pcount[7]);
-    const unsigned warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    unsigned* sw = scratch + warp * 3 * BK_SORT_MAX;
-    for (unsigned l = blockIdx.x * nw + warp; l < nl; l += gridDim.x * nw) bk_sort_chain(a, __ldcg(&a.long_list[l]), sw);
+__device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* red);
+
+__device__ void bk_scan_count(const MoveArgs& a, unsigned nbu, unsigned* red) {
+    unsigned b0, b1;
+    bk_slice(nbu, b0, b1);
+    unsigned c = 0;
+    for (unsigned b = b0 + threadIdx.x; b < b1; b += blockDim.x) c += __ldcg(&a.bcnt[b]);
+    c = block_sum(c, red);
+    if (threadIdx.x == 0) a.scan[BK_SCAN2 + blockIdx.x] = c;
+}
+
+__device__ void bk_scan_base(const MoveArgs& a, unsigned nbu, unsigned* red) {
+    unsigned b0, b1;
+    bk_slice(nbu, b0, b1);
+    unsigned off = 0;
+    for (unsigned b = threadIdx.x; b < blockIdx.x; b += blockDim.x) off += __ldcg(&a.scan[BK_SCAN2 + b]);
+    off = block_sum(off, red);
+    const unsigned per = (b1 - b0 + blockDim.x - 1) / blockDim.x;
+    const unsigned t0 = min(b1, b0 + threadIdx.x * per), t1 = min(b1, t0 + per);
+    unsigned mine = 0;
+    for (unsigned b = t0; b < t1; ++b) mine += __ldcg(&a.bcnt[b]);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= (unsigned)o) incl += t;
+    }
+    __syncthreads();  // red is free
+    if (lane == 31) red[warp] = incl;
+    __syncthreads();
+    unsigned before = 0;
+    for (unsigned k = 0; k < warp; ++k) before += red[k];
+    unsigned e = off + before + incl - mine;
+    for (unsigned b = t0; b < t1; ++b) {
+        a.bbase[b] = e;
+        e += __ldcg(&a.bcnt[b]);
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1 && e > a.npos_cap)
+        atomicOr(&a.sc->err, 16ull);  // cannot happen: <= 6 positions per contended agent
+}
+
+template <int B>
+__device__ __forceinline__ void bk_place(const MoveArgs& a, const unsigned* ci, const bool* ok) {
+    unsigned rank[B], slot[B][6], cell[B][6], base[B][6];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+        if (ok[b]) {
+            rank[b] = __ldcg(&a.crec[ci[b]]).y;
+            load_pairs(a, ci[b], slot[b], cell[b]);
+        }
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+            if (ok[b] && cell[b][j] != BK_NIL) base[b][j] = __ldcg(&a.bbase[cell[b][j]]);
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+            if (ok[b] && cell[b][j] != BK_NIL)
+                a.brank[base[b][j] + slot[b][j]] = make_uint2(rank[b], ci[b] * 8u + (unsigned)j);
+}
+
+// Bucket b in rank order: entry i (placement order) goes to position base + #{ranks below its
+// own}; every agent learns its position, the cell's current position is its first, and the
+// done flags of the bucket's positions are cleared.  Up to BK_SORT_REG entries in registers,
+// longer buckets are handed to warps (bk_sort_long).
+#define BK_SORT_REG 16
+#define BK_SORT_MAX 128  // a cell is covered by at most 121 footprints
+__device__ __forceinline__ void bk_hand_out(const MoveArgs& a, uint2 e, unsigned pos) {
+    a.entry[(size_t)(e.y >> 3) * 6 + (e.y & 7u)].x = pos;
+    a.bdone[pos] = 0;
 }
 
 __device__ void bk_sort(const MoveArgs& a, unsigned nbu, unsigned gtid, unsigned nthreads) {
-    constexpr int E = BK_BW - 2;  // entries of a base chunk
     for (unsigned b = gtid; b < nbu; b += nthreads) {
-        const unsigned c = b * BK_BW;
-        const uint4* p = reinterpret_cast<const uint4*>(a.bkt + c);
-        const uint4 q0 = __ldcg(p), q1 = __ldcg(p + 1), q2 = __ldcg(p + 2), q3 = __ldcg(p + 3);
-        const unsigned n = q0.x + 1u;  // entries inserted (all-ones = none)
-        if (n == 0) continue;
-        if (n > (unsigned)E) {  // handed to a warp (bk_sort_long)
-            a.long_list[atomicAdd(&a.pcount[7], 1u)] = c;
+        const unsigned base = __ldcg(&a.bbase[b]), n = __ldcg(&a.bcnt[b]);
+        a.bcur[b] = base;
+        if (n > BK_SORT_REG) {
+            a.long_list[atomicAdd(&a.pcount[7], 1u)] = b;
             continue;
         }
-        // keys (rank << 4 | slot) sorted in registers; empty slots (all-ones) sort last
-        const unsigned e[E] = {q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z};
-        unsigned key[E];
+        uint2 e[BK_SORT_REG];
 #pragma unroll
-        for (int i = 0; i < E; ++i) key[i] = e[i] == BK_EMPTY ? 0xFFFFFFFFu : (e[i] << 4) | (unsigned)i;
+        for (int i = 0; i < BK_SORT_REG; ++i) e[i] = (unsigned)i < n ? __ldcg(&a.brank[base + i]) : make_uint2(BK_EMPTY, 0);
 #pragma unroll
-        for (int rd = 0; rd < E; ++rd)  // odd-even transposition sort
+        for (int i = 0; i < BK_SORT_REG; ++i) {
+            if ((unsigned)i >= n) continue;
+            unsigned below = 0;
 #pragma unroll
-            for (int i = rd & 1; i + 1 < E; i += 2) {
-                const unsigned x = min(key[i], key[i + 1]), y = max(key[i], key[i + 1]);
-                key[i] = x;
-                key[i + 1] = y;
-            }
-        a.bkt[c] = c + 1 + (key[0] & 15u);
-#pragma unroll
-        for (int i = 0; i < E; ++i)
-            if ((unsigned)i < n)
-                a.bnext[c + 1 + (key[i] & 15u)] = (unsigned)(i + 1) < n ? c + 1 + (key[i + 1 < E ? i + 1 : E - 1] & 15u) : BK_NIL;
+            for (int k = 0; k < BK_SORT_REG; ++k) below += e[k].x < e[i].x;
+            bk_hand_out(a, e[i], base + below);
+        }
     }
 }
 
-// Full check of pending agent ci (its watched blocker, if any, has walked): it is the earliest
-// pending agent on every contended cell it has when each of those cells' current-entry word
-// (word 0 of the base chunk, bk_sort) is its own entry.  Holding them all it walks, then
-// advances each cell to the entry after its own and clears its entries (release fence between),
-// so a later agent that sees them may walk in the same round: its acquire fence orders its
-// occupancy reads after this walk.  Otherwise returns the entry of a blocker to watch.
+// One warp per long bucket: its entries staged in shared memory, each placed by counting.
+__device__ void bk_sort_long(const MoveArgs& a, unsigned* scratch) {
+    const unsigned nl = cta_load(&a.pcount[7]);
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned* srk = scratch + warp * BK_SORT_MAX;
+    for (unsigned l = blockIdx.x * nw + warp; l < nl; l += gridDim.x * nw) {
+        const unsigned b = __ldcg(&a.long_list[l]);
+        const unsigned base = __ldcg(&a.bbase[b]), n = min(__ldcg(&a.bcnt[b]), (unsigned)BK_SORT_MAX);
+        for (unsigned i = lane; i < n; i += 32) srk[i] = __ldcg(&a.brank[base + i]).x;
+        __syncwarp();
+        for (unsigned i = lane; i < n; i += 32) {
+            const uint2 e = __ldcg(&a.brank[base + i]);
+            unsigned below = 0;
+            for (unsigned k = 0; k < n; ++k) below += srk[k] < e.x;
+            bk_hand_out(a, e, base + below);
+        }
+        __syncwarp();
+    }
+}
+
+// Full check of pending agent ci (its watched predecessor, if any, has walked): it owns every
+// contended cell it has when each cell's current position is its own.  Holding them all it
+// walks, then advances each cell and marks its positions done (release fence between), so a
+// later agent that sees them may walk in the same round: its acquire fence orders its
+// occupancy reads after this walk.  Otherwise returns the predecessor position to watch.
 __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2],
                                          unsigned long long* hops, unsigned* watch) {
-    // the record and the (entry, base chunk) pairs in one trip; the current entries of the
-    // contended cells and this agent's successors in the next
+    // the record and the (position, bucket) pairs in one trip, the cells' current positions in
+    // the next
     const uint4 r = __ldcg(&a.crec[ci]);
-    unsigned cell[6], ent[6];
-    {
-        const uint4* p = reinterpret_cast<const uint4*>(a.entry + (size_t)ci * 6);
+    unsigned pos[6], cell[6], cur[6];
+    load_pairs(a, ci, pos, cell);
 #pragma unroll
-        for (int h = 0; h < 3; ++h) {
-            const uint4 q = __ldcg(p + h);
-            ent[2 * h] = q.x;
-            cell[2 * h] = q.y;
-            ent[2 * h + 1] = q.z;
-            cell[2 * h + 1] = q.w;
-        }
-    }
-    unsigned cur[6], nx[6];
+    for (int j = 0; j < 6; ++j) cur[j] = cell[j] != BK_NIL ? __ldcg(&a.bcur[cell[j]]) : 0u;
+    unsigned behind = 0, w = BK_NOWATCH;
 #pragma unroll
     for (int j = 0; j < 6; ++j)
-        if (cell[j] != BK_NIL && ent[j] != BK_NIL) {
-            cur[j] = __ldcg(&a.bkt[cell[j]]);
-            nx[j] = __ldcg(&a.bnext[ent[j]]);
+        if (cell[j] != BK_NIL && cur[j] != pos[j] && (w == BK_NOWATCH || pos[j] - cur[j] > behind)) {
+            behind = pos[j] - cur[j];  // wait where the most agents are still ahead
+            w = pos[j] - 1;
         }
-    bool own = true;
-#pragma unroll
-    for (int j = 0; j < 6; ++j) own &= cell[j] == BK_NIL || ent[j] == BK_NIL || cur[j] == ent[j];
-    if (!own) {  // watch the latest-ranked blocker (the others walk before it)
-        unsigned rk[6];
-#pragma unroll
-        for (int j = 0; j < 6; ++j)
-            rk[j] = (cell[j] != BK_NIL && ent[j] != BK_NIL && cur[j] != ent[j]) ? __ldcg(&a.bkt[cur[j]]) : 0u;
-        unsigned best = 0, blocker = BK_NIL;
-#pragma unroll
-        for (int j = 0; j < 6; ++j)
-            if (cell[j] != BK_NIL && ent[j] != BK_NIL && cur[j] != ent[j] && (blocker == BK_NIL || rk[j] > best)) {
-                best = rk[j];
-                blocker = cur[j];
-            }
-        *watch = blocker;
+    if (w != BK_NOWATCH) {
+        *watch = w;
         return false;
     }
     fence_acq_rel_gpu();  // acquire: the walks of the earlier agents on these cells are visible
     int cx[5], cy[5];
     const int mw = path_of(a, r, bp, cx, cy);  // the walk covers the whole path (m >= mf)
     walk_owned(a, r, cx, cy, mw, hops);
-    fence_acq_rel_gpu();  // release: this walk before the advanced cells and cleared entries
+    fence_acq_rel_gpu();  // release: this walk before the advanced cells
 #pragma unroll
     for (int j = 0; j < 6; ++j) {
-        if (cell[j] == BK_NIL || ent[j] == BK_NIL) continue;
-        a.bkt[cell[j]] = nx[j];
-        a.bkt[ent[j]] = BK_EMPTY;
+        if (cell[j] == BK_NIL) continue;
+        a.bcur[cell[j]] = pos[j] + 1;
+        a.bdone[pos[j]] = 1;
     }
     return true;
-}
-
-// End of phase: every used pool chunk back to empty and unlinked (all-ones, BK_PW / 4 threads
-// per chunk).
-// pref[s] = chunks taken from sub-pools before s (pref[BK_SUBPOOLS] = all), read once per CTA.
-__device__ void bk_pool_prefix(const MoveArgs& a, unsigned* pref) {
-    if (threadIdx.x < 32) {
-        unsigned u[2], incl = 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-            u[h] = min(__ldcg(&a.pool_n[(2 * threadIdx.x + h) * BK_SUB_STRIDE]), a.pool_sub);
-        const unsigned pair = u[0] + u[1];
-        incl = pair;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((int)threadIdx.x >= o) incl += t;
-        }
-        pref[2 * threadIdx.x] = incl - pair;
-        pref[2 * threadIdx.x + 1] = incl - pair + u[0];
-        if (threadIdx.x == 31) pref[BK_SUBPOOLS] = incl;
-    }
-    __syncthreads();
-}
-
-// End of phase: every used pool chunk back to empty and unlinked (all-ones, BK_PW / 4 threads
-// per chunk).
-__device__ void bk_reset_pool(const MoveArgs& a, const unsigned* pref, unsigned part, unsigned parts) {
-    const uint4 ones = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
-    const unsigned used = pref[BK_SUBPOOLS];
-    constexpr unsigned V4 = BK_PW / 4;  // uint4 per chunk
-    for (unsigned i = part * blockDim.x + threadIdx.x; i < used * V4; i += parts * blockDim.x) {
-        const unsigned f = i / V4;  // f-th taken chunk overall -> (sub-pool, index)
-        unsigned lo = 0;
-#pragma unroll
-        for (unsigned step = BK_SUBPOOLS / 2; step; step >>= 1)
-            if (pref[lo + step] <= f) lo += step;
-        const unsigned q = lo * a.pool_sub + (f - pref[lo]);
-        reinterpret_cast<uint4*>(a.bkt + a.base_words + q * BK_PW)[i % V4] = ones;
-        if (i % V4 == 0) {
-            const unsigned owner = a.pool_owner[q];
-            if (owner != BK_NIL) a.bkt[bk_link(a, owner)] = BK_NIL;
-        }
-    }
 }
 
 // Adds the group's hop counts to the phase displacement.  Every thread of the group calls it.
@@ -567,25 +495,15 @@ struct TailSmem {
 #define MOVE_LOCAL_MAX 2048    // ... while the CTA holds at most this many pending agents
 #define QC_CAP 8192
 static_assert(QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) <= sizeof(TailSmem), "round queues");
-static_assert((MOVE_THREADS / 32) * 3 * BK_SORT_MAX * sizeof(unsigned) <= sizeof(TailSmem), "long-bucket sort");
+static_assert((MOVE_THREADS / 32) * BK_SORT_MAX * sizeof(unsigned) <= sizeof(TailSmem), "long-bucket ranking");
 
-__device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y, bool buckets) {
+__device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y) {
     const unsigned cell = (unsigned)y * (unsigned)a.g.W + (unsigned)x;
     unsigned h = (cell * 2654435761u) >> (32 - 13);
     for (;;) {
         const unsigned old = atomicCAS(&T.key[h], TAIL_EMPTY, cell);
         if (old == TAIL_EMPTY) {  // new entry: its occupancy as of the tail's start
             T.occ[h] = (unsigned char)((__ldcg(&a.occ[a.g.word(x, y)]) >> (x & 31)) & 1u);
-            // only tail agents (and walkers whose release is in flight) still have entries in
-            // this cell's base chunk: empty it for the next phase (overflow chunks are reset
-            // by the other blocks)
-            const unsigned c = buckets ? bucket_of(a, x, y) : BK_NIL;
-            if (c != BK_NIL) {
-                uint32_t* b = a.bkt + c;  // everything but the link (reset with the pool)
-                const uint4 ones = make_uint4(BK_EMPTY, BK_EMPTY, BK_EMPTY, BK_EMPTY);
-                for (int q = 0; q < 3; ++q) reinterpret_cast<uint4*>(b)[q] = ones;
-                b[12] = b[13] = b[14] = BK_EMPTY;
-            }
             return h;
         }
         if (old == cell) return h;
@@ -595,7 +513,7 @@ __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, 
 
 // Pending records: crec[list[t]] (or crec[t] when list is null), t < np <= TAIL_MAX.
 __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, const uint2* list, unsigned np,
-                          bool buckets, const signed char (*bp)[5][2], unsigned long long* hops) {
+                          const signed char (*bp)[5][2], unsigned long long* hops) {
     for (unsigned k = threadIdx.x; k < TAIL_SLOTS; k += blockDim.x) {
         T.key[k] = TAIL_EMPTY;
         T.res[k] = 0xFFFFFFFFu;
@@ -608,10 +526,10 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
         int cx[5], cy[5];
         path_of(a, r, bp, cx, cy);
         const int m = rec_mf(r);  // footprint cells only (a free exit ending the walk has no slot)
-        T.slot[t][0] = (unsigned short)tail_insert(T, a, rec_x(r), rec_y(r), buckets);
+        T.slot[t][0] = (unsigned short)tail_insert(T, a, rec_x(r), rec_y(r));
 #pragma unroll
         for (int i = 0; i < 5; ++i)
-            if (i < m) T.slot[t][1 + i] = (unsigned short)tail_insert(T, a, cx[i], cy[i], buckets);
+            if (i < m) T.slot[t][1 + i] = (unsigned short)tail_insert(T, a, cx[i], cy[i]);
     }
     if (threadIdx.x == 0) {
         T.count[0] = np;
@@ -757,8 +675,10 @@ __device__ void p2_number(const MoveArgs& a, unsigned* red) {
     }
 }
 
-// Zeroes the contention bitplanes (dead after step 2) so the next phase starts from all-clear.
-__device__ void zero_marks(const MoveArgs& a, unsigned part, unsigned parts) {
+// Zeroes the contention bitplanes (dead after step 2) and the bucket counters of the phase's
+// nbu buckets so the next phase starts from all-clear.
+__device__ void zero_marks(const MoveArgs& a, unsigned nbu, unsigned part, unsigned parts) {
+    for (unsigned b = part * blockDim.x + threadIdx.x; b < nbu; b += parts * blockDim.x) a.bcnt[b] = 0;
     const size_t nwords = (size_t)a.g.P * (size_t)a.g.H;  // P is a multiple of 4
     uint4* p1 = reinterpret_cast<uint4*>(a.p1);
     uint4* p2 = reinterpret_cast<uint4*>(a.p2);
@@ -998,7 +918,6 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     __shared__ unsigned long long s_hops[1 + SEED_GROUPS];
     __shared__ unsigned int s_q[3];  // round queue counts and the flush base
     __shared__ unsigned int s_red[32];  // block reductions (dense bucket numbering)
-    __shared__ unsigned int s_pool[BK_SUBPOOLS + 1];  // overflow chunks taken per sub-pool (prefix)
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
     if (threadIdx.x < 3) s_q[threadIdx.x] = 0;
     if (threadIdx.x < 2 + 2 * SEED_GROUPS) s_app[threadIdx.x] = 0;
@@ -1071,7 +990,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     // the other blocks clean up (contention bitplanes, overflow chunks)
     const unsigned nc = cta_load(&a.pcount[1]);
     const bool rounds = nc > TAIL_MAX;
-    unsigned r = 0;
+    unsigned r = 0, nbu = 0;
     const uint2* list = nullptr;  // null: the tail takes crec[0, np) directly
     unsigned np = nc;
     if (rounds) {
@@ -1085,7 +1004,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                 ci[b] = base + b * nthreads;
                 ok[b] = ci[b] < nc;
             }
-            bk_prep<BK_PREP_BATCH>(a, ci, ok, s_bp);
+            bk_count<BK_PREP_BATCH>(a, ci, ok, s_bp);
         }
         if (gtid == 0) {
             // pending counts rotate over pcount[4..6]: round r reads its own, fills the next and
@@ -1094,12 +1013,27 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
             a.pcount[5] = a.pcount[6] = 0;
         }
         grid.sync();
-        bk_sort(a, cta_load(&a.scan[gridDim.x]), gtid, nthreads);
+        nbu = cta_load(&a.scan[gridDim.x]);  // buckets (p2_number)
+        bk_scan_count(a, nbu, s_red);
+        grid.sync();
+        bk_scan_base(a, nbu, s_red);
+        grid.sync();
+        for (unsigned base = gtid; base < nc; base += BK_PREP_BATCH * nthreads) {
+            unsigned ci[BK_PREP_BATCH];
+            bool ok[BK_PREP_BATCH];
+#pragma unroll
+            for (int b = 0; b < BK_PREP_BATCH; ++b) {
+                ci[b] = base + b * nthreads;
+                ok[b] = ci[b] < nc;
+            }
+            bk_place<BK_PREP_BATCH>(a, ci, ok);
+        }
+        grid.sync();
+        bk_sort(a, nbu, gtid, nthreads);
         grid.sync();
         bk_sort_long(a, reinterpret_cast<unsigned*>(s_dyn));
         grid.sync();
         if (gtid == 0) a.sc->t_prep = globaltimer();
-        bk_pool_prefix(a, s_pool);
         // Per round and CTA, in the (now free) dynamic shared memory: a queue of agents whose
         // watched blocker has walked (full check) and a queue of still-pending (agent, watch)
         // pairs flushed to the next list with one global atomic.
@@ -1129,11 +1063,11 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                     e[i] = k < np ? __ldcg(&list[k]) : make_uint2(BK_NIL, BK_NOWATCH);
                 }
 #pragma unroll
-                for (int i = 0; i < 4; ++i) v[i] = e[i].y != BK_NOWATCH ? __ldcg(&a.bkt[e[i].y]) : BK_EMPTY;
+                for (int i = 0; i < 4; ++i) v[i] = e[i].y != BK_NOWATCH ? __ldcg(&a.bdone[e[i].y]) : 1u;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     if (e[i].x == BK_NIL) continue;
-                    if (v[i] != BK_EMPTY) {  // blocker still pending: carry over as is
+                    if (!v[i]) {  // predecessor still pending: carry over as is
                         const unsigned s = atomicAdd(qpn, 1u);
                         if (s < QP_CAP) qp[s] = e[i];
                         else next[atomicAdd(ncount, 1u)] = e[i];
@@ -1177,14 +1111,14 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                     e[k] = idx < nq0 ? qp[idx] : make_uint2(BK_NIL, BK_NOWATCH);
                 }
 #pragma unroll
-                for (int k = 0; k < PER; ++k) v[k] = e[k].y != BK_NOWATCH ? __ldcg(&a.bkt[e[k].y]) : BK_EMPTY;
+                for (int k = 0; k < PER; ++k) v[k] = e[k].y != BK_NOWATCH ? __ldcg(&a.bdone[e[k].y]) : 1u;
                 __syncthreads();
                 if (threadIdx.x == 0) *qpn = *qcn = 0;
                 __syncthreads();
 #pragma unroll
                 for (int k = 0; k < PER; ++k) {
                     if (e[k].x == BK_NIL) continue;
-                    if (v[k] != BK_EMPTY) qp[atomicAdd(qpn, 1u)] = e[k];
+                    if (!v[k]) qp[atomicAdd(qpn, 1u)] = e[k];
                     else qc[atomicAdd(qcn, 1u)] = e[k].x;
                 }
                 __syncthreads();
@@ -1211,8 +1145,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
         }
     }
     if (gridDim.x > 1 && blockIdx.x != 0) {
-        zero_marks(a, blockIdx.x - 1, gridDim.x - 1);
-        if (rounds) bk_reset_pool(a, s_pool, blockIdx.x - 1, gridDim.x - 1);
+        zero_marks(a, nbu, blockIdx.x - 1, gridDim.x - 1);
         return;
     }
     if (threadIdx.x == 0) {
@@ -1221,15 +1154,10 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     }
     if (np) {
         unsigned long long hops = 0;
-        tail_smem(a, *reinterpret_cast<TailSmem*>(s_dyn), a.crec, list, np, rounds, s_bp, &hops);
+        tail_smem(a, *reinterpret_cast<TailSmem*>(s_dyn), a.crec, list, np, s_bp, &hops);
         flush_hops(B, a.sc, hops);
     }
-    if (gridDim.x == 1) {
-        zero_marks(a, 0, 1);
-        if (rounds) bk_reset_pool(a, s_pool, 0, 1);
-    }
-    // sub-pool counters: every CTA read them (bk_pool_prefix) before a later grid barrier
-    if (blockIdx.x == 0 && threadIdx.x < BK_SUBPOOLS) a.pool_n[threadIdx.x * BK_SUB_STRIDE] = 0;
+    if (gridDim.x == 1) zero_marks(a, nbu, 0, 1);
     if (gtid == 0) {
         a.sc->t_motion[3] = globaltimer();
         a.sc->pad[1] += r;  // grid rounds executed (observability; the tail adds its own)
@@ -1272,32 +1200,25 @@ int fp_ensure_res(fp_ctx* ctx) {
 
 static int g_move_blocks = 0;
 
-// Rank buckets: one 64-byte base chunk per contended cell (<= 3 per agent: every contended cell
-// is covered by >= 2 of the <= 6-cell footprints) plus 64-byte overflow chunks (six entries per
-// agent, seven to overflow a cell), the per-agent (entry, base chunk) pairs, the per-word dense
-// numbering and its per-CTA counts; buckets all-empty between phases.
+// Buckets: per contended cell (<= 3 per contended agent: every contended cell is covered by >= 2
+// of the <= 6-cell footprints) a counter, a base and a current position; per position (<= 6 per
+// contended agent) a rank and a done flag; the per-agent (position, bucket) pairs; the scan
+// counts.  Counters zero between phases.
 static int ensure_buckets(fp_ctx* ctx) {
-    const size_t nb = (size_t)ctx->cap * 3 + 64;
-    const size_t pool_sub = ((size_t)ctx->cap * 6 / 7 + 64) / BK_SUBPOOLS + 16;
-    const size_t pool = pool_sub * BK_SUBPOOLS;
-    if (ctx->d_bkt && ctx->bk_pool_cap >= pool && ctx->bk_agent_cap >= ctx->cap) return FP_OK;
-    const size_t words = nb * BK_BW + pool * BK_PW;
-    if (words >= 0xFFFFFFFFull)
-        return fp_fail(ctx, FP_ERUNTIME, "motion: roster too large for 32-bit bucket word indices");
+    const size_t nb = ((size_t)ctx->cap * 3 + 64 + 1) & ~(size_t)1;  // even: brank stays 8-byte aligned
+    const size_t npos = (size_t)ctx->cap * 6 + 64;
+    if (ctx->d_bkt && ctx->bk_agent_cap >= ctx->cap) return FP_OK;
+    const size_t words = 3 * nb + 2 * npos + 2048;
+    if (words >= 0xFFFFFFFFull) return fp_fail(ctx, FP_ERUNTIME, "motion: roster too large for 32-bit positions");
     cudaStreamSynchronize(ctx->stream);
-    for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_pool_owner, (void*)ctx->d_entry, (void*)ctx->d_pool_n,
-                    (void*)ctx->d_bnext})
+    for (void* p : {(void*)ctx->d_bkt, (void*)ctx->d_bdone, (void*)ctx->d_entry})
         if (p) cudaFree(p);
-    ctx->d_pool_n = nullptr;
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_n, BK_SUBPOOLS * BK_SUB_STRIDE * 4 + 1024 * 4));  // + p2 scan counts
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_pool_n, 0, BK_SUBPOOLS * BK_SUB_STRIDE * 4 + 1024 * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_bkt, words * 4));
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_bnext, words * 4));
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0xFF, words * 4, ctx->stream));
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_pool_owner, pool * 4));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0, words * 4, ctx->stream));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_bdone, npos));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * 6 * sizeof(uint2)));
-    ctx->bk_pool_cap = (unsigned)pool;
     ctx->bk_nb_cap = (unsigned)nb;
+    ctx->bk_npos_cap = (unsigned)npos;
     ctx->bk_agent_cap = ctx->cap;
     ctx->graph_valid = false;
     return FP_OK;
@@ -1353,20 +1274,19 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.tile_h = ctx->tile_h;
     a.tiles_x = ctx->tiles_x;
     a.crec = ctx->d_rec_b;
-    a.bkt = ctx->d_bkt;
     a.nb_cap = ctx->bk_nb_cap;
-    a.base_words = ctx->bk_nb_cap * BK_BW;
+    a.npos_cap = ctx->bk_npos_cap;
     a.pw = ctx->d_pw;
-    a.scan = ctx->d_pool_n + BK_SUBPOOLS * BK_SUB_STRIDE;
-    a.pool_cap = ctx->bk_pool_cap;
-    a.pool_sub = ctx->bk_pool_cap / BK_SUBPOOLS;
-    a.pool_n = ctx->d_pool_n;
+    a.bcnt = ctx->d_bkt;
+    a.bbase = ctx->d_bkt + ctx->bk_nb_cap;
+    a.bcur = ctx->d_bkt + 2 * (size_t)ctx->bk_nb_cap;
+    a.brank = reinterpret_cast<uint2*>(ctx->d_bkt + 3 * (size_t)ctx->bk_nb_cap);
+    a.scan = reinterpret_cast<unsigned*>(a.brank + ctx->bk_npos_cap);
+    a.bdone = ctx->d_bdone;
     {
         static const int st = getenv("FP_SEED_STATIC") ? atoi(getenv("FP_SEED_STATIC")) : 1;
         a.seed_static = st;
     }
-    a.pool_owner = ctx->d_pool_owner;
-    a.bnext = ctx->d_bnext;
     a.entry = ctx->d_entry;
     uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
     a.alist[0] = lists;
