@@ -1052,14 +1052,16 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
             if (gtid == 0) a.pcount[4 + (r + 2) % 3] = 0;
             uint2* next = a.alist[(r + 1) & 1];
             unsigned int* ncount = &a.pcount[4 + (r + 1) % 3];
-            // pass 1: watch tests, four list entries per thread in flight
+            // pass 1: watch tests, four list entries per thread in flight; entry k goes to CTA
+            // k mod G, so a short list (late rounds) still spreads over every CTA
             const long long c_p1 = clock64();
-            for (unsigned base = gtid; base < np; base += 4 * nthreads) {
+            for (unsigned base = threadIdx.x; blockIdx.x + (size_t)gridDim.x * base < np; base += 4 * blockDim.x) {
                 uint2 e[4];
                 unsigned v[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const unsigned k = base + i * nthreads;
+                    const size_t kk = blockIdx.x + (size_t)gridDim.x * (base + i * blockDim.x);
+                    const unsigned k = kk < np ? (unsigned)kk : np;
                     e[i] = k < np ? __ldcg(&list[k]) : make_uint2(BK_NIL, BK_NOWATCH);
                 }
 #pragma unroll
