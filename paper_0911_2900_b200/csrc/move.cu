@@ -492,7 +492,7 @@ struct TailSmem {
 #ifndef MOVE_LOCAL_ITERS
 #define MOVE_LOCAL_ITERS 3     // extra in-CTA check passes per grid round
 #endif
-#define MOVE_LOCAL_MAX 2048    // ... while the CTA holds at most this many pending agents
+#define MOVE_LOCAL_MAX 4096    // ... while the CTA holds at most this many pending agents
 #define QC_CAP 8192
 static_assert(QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) <= sizeof(TailSmem), "round queues");
 static_assert((MOVE_THREADS / 32) * BK_SORT_MAX * sizeof(unsigned) <= sizeof(TailSmem), "long-bucket ranking");
