@@ -48,9 +48,8 @@ struct MoveArgs {
     const uint32_t* seed_list;     // mode B: alive ids to build records from
     const uint4* rec0;             // mode A: records emitted by the plan kernel (n_alive of them)
     int premade;                   // 1: mode A, 0: mode B
-    int seed_static;               // seed tiles dealt round-robin instead of from a cursor
     uint4* rec[2];                 // pending records, ping-pong
-    unsigned int* pcount;          // [0..1] pending counts, [2..3] seed tile cursors (zero between phases)
+    unsigned int* pcount;          // [0..1] list counts, [4..6] round pending counts, [7] long buckets (zero between phases)
     DevScalars* sc;
     unsigned long long* exits;     // (rank << 32 | id)
     uint32_t* p1;                  // contention bitplanes, zero between phases
@@ -734,17 +733,6 @@ __device__ __forceinline__ long long seed_global(const MoveArgs& a, const SeedWi
     return (long long)y * a.g.P + (s.wx0 + w - yi * s.ww);
 }
 
-// Next tile for this worker group (dynamic: tiles differ a lot in agent count).
-__device__ __forceinline__ uint32_t seed_next(const MoveArgs& a, unsigned int* cursor, unsigned int* slot,
-                                              unsigned& k) {
-    if (a.seed_static)  // round-robin over the groups of the grid
-        return blockIdx.x * SEED_GROUPS + threadIdx.x / SEED_GROUP + (k++) * gridDim.x * SEED_GROUPS;
-    if (threadIdx.x % SEED_GROUP == 0) *slot = atomicAdd(cursor, 1u);
-    group_sync();
-    const uint32_t e = *slot;
-    group_sync();  // everyone has read it before the next fetch overwrites it
-    return e;
-}
 
 // Start cell [0] and path cells [1..m]; the footprint is [0..mf] (motion_rec.cuh).
 __device__ __forceinline__ void record_footprint(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
@@ -755,24 +743,29 @@ __device__ __forceinline__ void record_footprint(const MoveArgs& a, const uint4&
     cy[0] = rec_y(r);
 }
 
-// S1: every footprint of the group's tiles marked in P1/P2.
-__device__ void seed_mark(const MoveArgs& a, uint32_t* win, unsigned int* slot, const signed char (*bp)[5][2]) {
+// S1: every footprint of the group's tiles marked in P1/P2.  Tiles are dealt round-robin to
+// the worker groups; the next tile's header and first records are fetched while the current
+// tile's marks merge into the global bitplanes.
+__device__ void seed_mark(const MoveArgs& a, uint32_t* win, const signed char (*bp)[5][2]) {
     const unsigned lt = threadIdx.x % SEED_GROUP;
     const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
-    unsigned k = 0;
-    for (;;) {
-        const uint32_t e = seed_next(a, &a.pcount[2], slot, k);
-        if (e >= nt) break;
-        const uint32_t t = a.tile_list[e];
+    const uint32_t ng = gridDim.x * SEED_GROUPS;
+    uint32_t e = blockIdx.x * SEED_GROUPS + threadIdx.x / SEED_GROUP;
+    uint32_t t = e < nt ? __ldcg(&a.tile_list[e]) : 0u;
+    uint32_t off = e < nt ? __ldcg(&a.tile_off[t]) : 0u, cnt = e < nt ? __ldcg(&a.tile_cnt[t]) : 0u;
+    uint4 r0 = lt < cnt ? __ldcg(&a.rec0[off + lt]) : make_uint4(0, 0, 0, 0);
+    for (; e < nt; e += ng) {
+        const uint32_t en = e + ng;
+        const uint32_t tn = en < nt ? __ldcg(&a.tile_list[en]) : 0u;
         const SeedWin s = seed_window(a, t);
         const int nw = s.ww * s.wh;
         uint32_t* L1 = win;
         uint32_t* L2 = win + nw;
         for (int w = lt; w < 2 * nw; w += SEED_GROUP) win[w] = 0;
+        const uint32_t offn = en < nt ? __ldcg(&a.tile_off[tn]) : 0u, cntn = en < nt ? __ldcg(&a.tile_cnt[tn]) : 0u;
         group_sync();
-        const uint32_t off = a.tile_off[t], cnt = a.tile_cnt[t];
         for (uint32_t k = lt; k < cnt; k += SEED_GROUP) {
-            const uint4 r = __ldcg(&a.rec0[off + k]);
+            const uint4 r = k == lt ? r0 : __ldcg(&a.rec0[off + k]);
             if (!rec_m(r)) continue;
             int cx[6], cy[6], m, mf;
             record_footprint(a, r, bp, cx, cy, m, mf);
@@ -790,6 +783,7 @@ __device__ void seed_mark(const MoveArgs& a, uint32_t* win, unsigned int* slot, 
             }
         }
         group_sync();
+        r0 = lt < cntn ? __ldcg(&a.rec0[offn + lt]) : make_uint4(0, 0, 0, 0);  // next tile, in flight
         // merge: four words per thread in flight at once, then the P2 updates fire-and-forget
         for (int w0 = lt; w0 < nw; w0 += 4 * SEED_GROUP) {
             uint32_t l1[4], old[4];
@@ -809,6 +803,9 @@ __device__ void seed_mark(const MoveArgs& a, uint32_t* win, unsigned int* slot, 
             }
         }
         group_sync();
+        t = tn;
+        off = offn;
+        cnt = cntn;
     }
 }
 
@@ -913,7 +910,6 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     cg::grid_group grid = cg::this_grid();
     __shared__ signed char s_bp[121][5][2];
     extern __shared__ __align__(16) unsigned char s_dyn[];  // TailSmem (block 0's tail) / seed windows
-    __shared__ unsigned int s_slot[SEED_GROUPS];
     __shared__ unsigned int s_app[2 + 2 * SEED_GROUPS];
     __shared__ unsigned long long s_hops[1 + SEED_GROUPS];
     __shared__ unsigned int s_q[3];  // round queue counts and the flush base
@@ -955,8 +951,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
         // steps 1 and 2 tile by tile over the plan's records
         const int nwmax = seed_ww(a.tile_w) * (a.tile_h + 10);
         uint32_t* win = reinterpret_cast<uint32_t*>(s_dyn) + (threadIdx.x / SEED_GROUP) * 2 * nwmax;
-        unsigned int* slot = &s_slot[threadIdx.x / SEED_GROUP];
-        seed_mark(a, win, slot, s_bp);
+        seed_mark(a, win, s_bp);
         grid.sync();
         if (gtid == 0) a.sc->t_marked = globaltimer();
         p2_count(a, s_red);
@@ -1285,10 +1280,6 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.brank = reinterpret_cast<uint2*>(ctx->d_bkt + 3 * (size_t)ctx->bk_nb_cap);
     a.scan = reinterpret_cast<unsigned*>(a.brank + ctx->bk_npos_cap);
     a.bdone = ctx->d_bdone;
-    {
-        static const int st = getenv("FP_SEED_STATIC") ? atoi(getenv("FP_SEED_STATIC")) : 1;
-        a.seed_static = st;
-    }
     a.entry = ctx->d_entry;
     uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
     a.alist[0] = lists;
