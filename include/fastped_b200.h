@@ -117,6 +117,10 @@ int fp_update_agents(fp_ctx* ctx, const int32_t* x, const int32_t* y, const uint
 int fp_set_step(fp_ctx* ctx, int64_t step);
 int fp_get_step(const fp_ctx* ctx, int64_t* step);
 int fp_get_alive_count(const fp_ctx* ctx, int64_t* alive);
+/* Sum over all agents of segment_dx(x before, x after) for the last move phase (step / move /
+ * each step of run): the per-step x displacement fundamental_diagram accumulates on the host
+ * from positions (bench.hpp:291-302), reduced on the device during the walks instead. */
+int fp_get_last_dx(const fp_ctx* ctx, int64_t* dx);
 /* SimState::potential / drive_gradient -- state.hpp:32-33 */
 int fp_set_potential(fp_ctx* ctx, int kind, double drive_gradient);
 /* SimState::desired (scratch between phases); injected by motion-only tests. */

@@ -262,6 +262,12 @@ def ref():
             fn.restype = C.c_int
             fn.argtypes = [C.c_double, C.c_double if name.endswith("corridor") else C.c_int,
                            C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_void_p]
+        L.ref_fundamental_diagram.restype = C.c_int
+        L.ref_fundamental_diagram.argtypes = [C.c_int, C.c_int, C.c_double, _u8p, C.c_int, _f64p, C.c_int,
+                                              C.c_uint64, C.c_int, C.c_int, C.c_double, _f64p, _f64p, _f64p]
+        L.ref_capacity_from_table.restype = C.c_int
+        L.ref_capacity_from_table.argtypes = [C.POINTER(C.c_int64), _f64p, C.c_int, C.c_double, C.c_int64,
+                                              C.c_int64, C.POINTER(C.c_int64), _f64p]
         _ref = L
     return _ref
 
@@ -362,6 +368,35 @@ class RefState:
 
     def hash(self):
         return ref().ref_state_hash(self.p)
+
+
+def ref_fundamental_diagram(cells, cell_size, v_max, densities, seed, warmup=100, measure=296,
+                            drive_gradient=8.0):
+    """The reference's fundamental_diagram (bench.hpp:244-305) on a periodic-x corridor:
+    (density, mean_speed, flow) arrays."""
+    cells = np.ascontiguousarray(cells, np.uint8)
+    h, w = cells.shape
+    d = np.ascontiguousarray(densities, np.float64)
+    out = [np.empty(len(d), np.float64) for _ in range(3)]
+    if ref().ref_fundamental_diagram(w, h, cell_size, cells.ravel(), v_max, d, len(d), seed, warmup, measure,
+                                     drive_gradient, *out) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return out
+
+
+def ref_capacity_from_table(ns, ts, budget, start_n=1000, max_n=(2 ** 63 - 1) // 2):
+    """The reference's realtime_capacity (bench.hpp:162-208) over a (n -> wall time) table:
+    dict of its CapacityResult fields plus the number of probes it made."""
+    ns = np.ascontiguousarray(ns, np.int64)
+    ts = np.ascontiguousarray(ts, np.float64)
+    o6 = np.zeros(6, np.int64)
+    o3 = np.zeros(3, np.float64)
+    if ref().ref_capacity_from_table(ns.ctypes.data_as(C.POINTER(C.c_int64)), ts, len(ns), budget, start_n, max_n,
+                                     o6.ctypes.data_as(C.POINTER(C.c_int64)), o3) != 0:
+        raise ValueError(ref().ref_last_error().decode())
+    return dict(capacity=int(o6[0]), n_low=int(o6[1]), n_high=int(o6[2]), below_start=bool(o6[3]),
+                capped=bool(o6[4]), probes=int(o6[5]), t_low_s=float(o3[0]), t_high_s=float(o3[1]),
+                budget_s=float(o3[2]))
 
 
 def ref_static_field(cells, boundary=0):

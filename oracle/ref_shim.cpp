@@ -257,4 +257,55 @@ int ref_make_corridor(double len_m, double width_m, double cell, int* w, int* h,
     }
 }
 
+// fundamental_diagram (bench.hpp:244-305) on a periodic-x corridor given as cells: one
+// (density, mean_speed, flow) triple per requested density.
+int ref_fundamental_diagram(int w, int h, double cell, const uint8_t* cells, int v_max, const double* densities,
+                            int nd, uint64_t seed, int warmup, int measure, double drive_gradient,
+                            double* density, double* mean_speed, double* flow) {
+    try {
+        Grid g(w, h, cell, Boundary::PeriodicX, to_cells(w, h, cells));
+        const std::vector<double> rho(densities, densities + nd);
+        const auto fd = fundamental_diagram(g, v_max, rho, seed, warmup, measure, drive_gradient);
+        for (size_t i = 0; i < fd.size(); ++i) {
+            density[i] = fd[i].density;
+            mean_speed[i] = fd[i].mean_speed;
+            flow[i] = fd[i].flow;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// realtime_capacity (bench.hpp:165-208) driven by a timing table: wall_time_of(n) is looked up
+// in (ns[i], ts[i]) (exact n required), so the bracket logic can be pinned without timing.
+int ref_capacity_from_table(const int64_t* ns, const double* ts, int nt, double budget, int64_t start_n, int64_t max_n,
+                            int64_t* out6 /* capacity, n_low, n_high, below_start, capped, probes */,
+                            double* out3 /* t_low, t_high, budget */) {
+    try {
+        int64_t probes = 0;
+        auto fn = [&](int64_t n) {
+            ++probes;
+            for (int i = 0; i < nt; ++i)
+                if (ns[i] == n) return ts[i];
+            throw std::runtime_error("ref_capacity_from_table: no timing for n=" + std::to_string(n));
+        };
+        const CapacityResult r = realtime_capacity(fn, budget, start_n, max_n);
+        out6[0] = r.capacity;
+        out6[1] = r.n_low;
+        out6[2] = r.n_high;
+        out6[3] = r.below_start;
+        out6[4] = r.capped;
+        out6[5] = probes;
+        out3[0] = r.t_low_s;
+        out3[1] = r.t_high_s;
+        out3[2] = r.budget_s;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 }  // extern "C"

@@ -412,6 +412,11 @@ extern "C" int fp_get_step(const fp_ctx* c, int64_t* step) {
     *step = c->step;
     return FP_OK;
 }
+extern "C" int fp_get_last_dx(const fp_ctx* c, int64_t* dx) {
+    if (!c || !dx) return fail(nullptr, FP_EINVAL, "null argument");
+    *dx = c->last_dx;
+    return FP_OK;
+}
 extern "C" int fp_get_alive_count(const fp_ctx* c, int64_t* a) {
     if (!c || !a) return fail(nullptr, FP_EINVAL, "null argument");
     *a = c->alive;
@@ -492,6 +497,7 @@ static int move_impl(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
     c->n_order = (uint32_t)c->h_sc->n_alive;
     c->n_exits = (uint32_t)c->h_sc->n_exits;
     c->last_displacement = (int64_t)c->h_sc->disp;
+    c->last_dx = (int64_t)c->h_sc->step_dx;
     if (int rc = fp_exits_finish(c)) return rc;
     FP_CUDA(c, cudaStreamSynchronize(c->stream));
     if (out) {
@@ -519,6 +525,7 @@ extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out)
         c->n_order = 0;
         c->n_exits = 0;
         c->last_displacement = 0;
+        c->last_dx = 0;
         c->step++;
         if (out) *out = fp_step_stats{c->alive, 0, 0};
         return sync_scalars(c);
@@ -536,6 +543,7 @@ extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out)
     c->n_order = (uint32_t)c->h_sc->n_alive;
     c->n_exits = (uint32_t)c->h_sc->n_exits;
     c->last_displacement = (int64_t)c->h_sc->disp;
+    c->last_dx = (int64_t)c->h_sc->step_dx;
     if (int rc = fp_exits_finish(c)) return rc;
     if (out) {
         out->alive = c->alive;

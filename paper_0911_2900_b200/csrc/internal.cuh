@@ -111,7 +111,9 @@ struct DevScalars {
     unsigned long long round_seq; // motion round stamp counter
     unsigned long long pend;      // pending count (motion)
     unsigned long long n_exits;   // exits of the current move phase
-    unsigned long long disp;      // displacement of the current move phase
+    unsigned long long disp;      // displacement of the current move phase (low 32 bits: hops;
+                                  //   high 32 bits: sum of segment_dx, split off at the end)
+    long long step_dx;            // sum of segment_dx(start, end) over the last move phase
     unsigned long long tot_exits; // accumulated over a run
     unsigned long long tot_disp;  // accumulated over a run
     unsigned long long tot_updates;  // sum of alive counts entering each step
@@ -212,6 +214,7 @@ struct fp_ctx {
     unsigned long long* d_exits = nullptr;  // (rank << 32 | id) records of the last move
     unsigned long long* d_exits_sorted = nullptr;
     int64_t last_displacement = 0;
+    int64_t last_dx = 0;          // sum of segment_dx of the last move phase (fundamental diagram)
     uint32_t n_exits = 0;
 
     DevScalars* d_sc = nullptr;   // device scalars

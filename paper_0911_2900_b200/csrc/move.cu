@@ -167,6 +167,15 @@ __device__ __forceinline__ void load_blocked(const MoveArgs& a, const int* cx, c
     for (int i = 0; i < 5; ++i) blocked[i] = i < m && occ_test(a, cx[i], cy[i]);
 }
 
+// Per-thread displacement accumulator word: hops in the low 32 bits, the signed sum of
+// segment_dx (engine end x minus start x, periodic shorter wrap; the fundamental diagram's
+// flow, bench.hpp:291-302) in the high 32 bits.  Phase totals stay below 2^31, so the halves
+// never carry into each other; the motion kernel splits them at the end of the phase.
+__device__ __forceinline__ unsigned long long hop_word(int h, int dx) {
+    return (unsigned long long)(unsigned)h + ((unsigned long long)(unsigned)dx << 32);
+}
+
+
 // The walk (engine.hpp:116-129) of an agent that owns its footprint, net effect on occupancy.
 __device__ __forceinline__ void walk_apply(const MoveArgs& a, const uint4& r, const int* cx, const int* cy, int m,
                                            const bool* blocked, unsigned long long* hops_acc) {
@@ -176,11 +185,13 @@ __device__ __forceinline__ void walk_apply(const MoveArgs& a, const uint4& r, co
     for (int i = 0; i < 5; ++i)
         if (i < m && h == i && !blocked[i]) h = i + 1;
     const bool exited = (h == m) && (r.z & 0x80000000u);
+    int dxs = 0;
     if (h > 0) {
         const uint32_t id = r.x;
         atomicAnd(&a.occ[a.g.word(sx, sy)], ~(1u << (sx & 31)));
         int fx, fy;
         pick(cx, cy, h - 1, fx, fy);
+        dxs = a.g.segment_dx(sx, fx);
         a.x[id] = fx;
         a.y[id] = fy;
         if (exited) {
@@ -192,7 +203,7 @@ __device__ __forceinline__ void walk_apply(const MoveArgs& a, const uint4& r, co
             atomicOr(&a.occ[a.g.word(fx, fy)], 1u << (fx & 31));
         }
     }
-    *hops_acc += (unsigned long long)h;
+    *hops_acc += hop_word(h, dxs);
 }
 
 __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, const int* cx, const int* cy, int m,
@@ -563,6 +574,7 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
             int h = 0;  // the walk (engine.hpp:116-129) against the shared occupancy
             while (h < mf && !T.occ[T.slot[t][1 + h]]) ++h;
             if (h == mf) h = m;  // a free exit ending the walk never blocks
+            int dxs = 0;
             if (h > 0) {
                 const bool exited = (h == m) && (r.z & 0x80000000u);
                 T.occ[T.slot[t][0]] = 0;
@@ -571,6 +583,7 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
                 const uint32_t id = r.x;
                 int fx, fy;
                 pick(cx, cy, h - 1, fx, fy);
+                dxs = a.g.segment_dx(rec_x(r), fx);
                 a.x[id] = fx;
                 a.y[id] = fy;
                 if (exited) {
@@ -581,7 +594,7 @@ __device__ void tail_smem(const MoveArgs& a, TailSmem& T, const uint4* crec, con
                     T.occ[T.slot[t][h]] = 1;
                 }
             }
-            *hops += (unsigned long long)h;
+            *hops += hop_word(h, dxs);
         }
         __syncthreads();
         cur = nxt;
@@ -1162,7 +1175,10 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
         const unsigned long long ne = a.sc->n_exits;
         a.sc->alive -= ne;
         a.sc->tot_exits += ne;
-        a.sc->tot_disp += a.sc->disp;
+        const unsigned long long d = a.sc->disp;
+        a.sc->disp = d & 0xFFFFFFFFull;
+        a.sc->step_dx = (long long)(int)(unsigned)(d >> 32);
+        a.sc->tot_disp += d & 0xFFFFFFFFull;
     }
 }
 

@@ -75,6 +75,7 @@ SIGNATURES = {
     "fp_set_step": (C.c_int, [C.c_void_p, C.c_int64]),
     "fp_get_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "fp_get_alive_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "fp_get_last_dx": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "fp_set_potential": (C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     "fp_set_desired": (C.c_int, [C.c_void_p, _i32p, _i32p]),
     "fp_plan": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64]),
@@ -382,6 +383,13 @@ class SimState:
     def alive(self) -> int:
         v = C.c_int64()
         _check(library().fp_get_alive_count(self._ctx, C.byref(v)), self._ctx)
+        return v.value
+
+    @property
+    def last_dx(self) -> int:
+        """Sum of segment_dx(x before, x after) over all agents in the last move phase."""
+        v = C.c_int64()
+        _check(library().fp_get_last_dx(self._ctx, C.byref(v)), self._ctx)
         return v.value
 
     # -- dumps
