@@ -381,9 +381,14 @@ __device__ __forceinline__ void bk_place(const MoveArgs& a, const unsigned* ci, 
 // longer buckets are handed to warps (bk_sort_long).
 #define BK_SORT_REG 16
 #define BK_SORT_MAX 128  // a cell is covered by at most 121 footprints
-__device__ __forceinline__ void bk_hand_out(const MoveArgs& a, uint2 e, unsigned pos) {
-    a.entry[(size_t)(e.y >> 3) * 6 + (e.y & 7u)].x = pos;
+// An agent behind others in a bucket starts the rounds watching its predecessor there instead
+// of being checked in round 0 (any blocked bucket's predecessor is a valid watch: it only
+// schedules the next check; concurrent writers from different buckets may pick any of them).
+__device__ __forceinline__ void bk_hand_out(const MoveArgs& a, uint2 e, unsigned pos, unsigned base) {
+    const unsigned ci = e.y >> 3;
+    a.entry[(size_t)ci * 6 + (e.y & 7u)].x = pos;
     a.bdone[pos] = 0;
+    if (pos > base) a.alist[0][ci].y = pos - 1;
 }
 
 __device__ void bk_sort(const MoveArgs& a, unsigned nbu, unsigned gtid, unsigned nthreads) {
@@ -403,7 +408,7 @@ __device__ void bk_sort(const MoveArgs& a, unsigned nbu, unsigned gtid, unsigned
             unsigned below = 0;
 #pragma unroll
             for (int k = 0; k < BK_SORT_REG; ++k) below += e[k].x < e[i].x;
-            bk_hand_out(a, e[i], base + below);
+            bk_hand_out(a, e[i], base + below, base);
         }
     }
 }
@@ -422,7 +427,7 @@ __device__ void bk_sort_long(const MoveArgs& a, unsigned* scratch) {
             const uint2 e = __ldcg(&a.brank[base + i]);
             unsigned below = 0;
             for (unsigned k = 0; k < n; ++k) below += srk[k] < e.x;
-            bk_hand_out(a, e, base + below);
+            bk_hand_out(a, e, base + below, base);
         }
         __syncwarp();
     }
