@@ -57,30 +57,53 @@ __global__ void tile_sums_kernel(const uint32_t* sub_cnt, const uint32_t* sub_of
 }
 
 // Deals the non-empty tiles to the plan kernel's G CTAs in DEAL_PASSES passes: the list is cut
-// into G * DEAL_PASSES contiguous ranges of near-equal agent counts (the range of entry e is
-// floor(agent offset * G * DEAL_PASSES / total)), and range p*G + b goes to CTA b in its pass p.
+// into G * DEAL_PASSES contiguous ranges of near-equal cost (the range of entry e is
+// floor(cost before e * G * DEAL_PASSES / total), a tile's cost its agent count with a floor),
+// and range p*G + b goes to CTA b in its pass p.
 // Crowded tiles do not pile up on a few CTAs, and at any time the CTAs work on neighbouring
 // parts of the list (DRAM/L2 locality of the concurrent TMA fetches).  The range index is
 // monotonic in e, so each boundary first[r] is written by exactly one entry.
-__global__ void tile_deal_kernel(const uint32_t* list, const uint32_t* off, const uint32_t* cnt,
-                                 const unsigned long long* n_tiles_p, int G, int passes, uint32_t* first) {
+__global__ void __launch_bounds__(1024) tile_deal_kernel(const uint32_t* list, const uint32_t* cnt,
+                                                          const unsigned long long* n_tiles_p, int G, int passes,
+                                                          unsigned floor_cost, uint32_t* first) {
+    // cost of a tile = max(its agents, floor_cost): a tile costs at least a fetch, so the
+    // grid's partial last row/column of tiles does not pile onto one CTA.  One block: each
+    // thread sums a contiguous run of the list, one block scan, then every entry's range.
+    __shared__ unsigned long long s_part[32];
     G *= passes;  // ranges
     const uint32_t n = (uint32_t)*n_tiles_p;
-    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
     if (n == 0) {
-        for (uint32_t b = gt; b <= (uint32_t)G; b += gs) first[b] = 0;
+        for (uint32_t b = threadIdx.x; b <= (uint32_t)G; b += blockDim.x) first[b] = 0;
         return;
     }
-    const uint32_t last = list[n - 1];
-    const unsigned long long total = (unsigned long long)off[last] + cnt[last];
-    auto owner = [&](uint32_t e) -> int {
-        return (int)min((unsigned long long)(G - 1), (unsigned long long)off[list[e]] * (unsigned)G / total);
-    };
-    for (uint32_t e = gt; e < n; e += gs) {
-        const int o = owner(e), prev = e ? owner(e - 1) : -1;
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t e0 = min(n, threadIdx.x * per), e1 = min(n, e0 + per);
+    unsigned long long mine = 0;
+    for (uint32_t e = e0; e < e1; ++e) mine += max(cnt[list[e]], floor_cost);
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((threadIdx.x & 31) >= (unsigned)o) incl += t;
+    }
+    if ((threadIdx.x & 31) == 31) s_part[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    unsigned long long before = incl - mine, total = 0;
+    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
+        if (w < (threadIdx.x >> 5)) before += s_part[w];
+        total += s_part[w];
+    }
+    int prev = -1;
+    if (e0 > 0) {  // range of the entry before this run
+        const unsigned long long c = max(cnt[list[e0 - 1]], floor_cost);
+        prev = (int)min((unsigned long long)(G - 1), (before - c) * (unsigned)G / total);
+    }
+    for (uint32_t e = e0; e < e1; ++e) {
+        const int o = (int)min((unsigned long long)(G - 1), before * (unsigned)G / total);
         for (int b = prev + 1; b <= o; ++b) first[b] = e;
         if (e == n - 1)
             for (int b = o + 1; b <= G; ++b) first[b] = n;
+        prev = o;
+        before += max(cnt[list[e]], floor_cost);
     }
 }
 
@@ -88,6 +111,12 @@ struct NonEmpty {
     const uint32_t* cnt;
     __device__ __forceinline__ bool operator()(uint32_t t) const { return cnt[t] != 0; }
 };
+
+// Least cost of a tile in the deal, in agent units (FP_DEAL_TILE_COST).
+static unsigned deal_tile_cost() {
+    static const unsigned c = getenv("FP_DEAL_TILE_COST") ? (unsigned)atoi(getenv("FP_DEAL_TILE_COST")) : 96u;
+    return c;
+}
 
 int fp_bucket_reserve(fp_ctx* ctx) {
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
@@ -149,9 +178,8 @@ int fp_bucket_launch(fp_ctx* ctx) {
     FP_CUDA(ctx, cub::DeviceSelect::If(ctx->d_temp_b, need2, it, ctx->d_tile_list, &ctx->d_sc->n_tiles, (int)nt,
                                        NonEmpty{ctx->d_tile_cnt}, s));
     ctx->ctr.kernel_launches += 2;
-    tile_deal_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s>>>(
-        ctx->d_tile_list, ctx->d_tile_off, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->sm_count, ctx->deal_passes,
-        ctx->d_tile_deal);
+    tile_deal_kernel<<<1, 1024, 0, s>>>(ctx->d_tile_list, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->sm_count,
+                                        ctx->deal_passes, deal_tile_cost(), ctx->d_tile_deal);
     FP_LAUNCHED(ctx);
     bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, ctx->d_alive, n, ctx->d_flags,
                                             ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket, ctx->d_brec);

@@ -570,9 +570,15 @@ __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint3
 // agent per thread.  There is no CTA-wide barrier per tile: a thread finishing its agents of
 // fetch i moves on to fetch i+1; the thread that completes the last agent of fetch i refills
 // that slot with fetch i+2.  Slot metadata is published with a generation number (seqlock).
-__device__ unsigned long long g_plan_dbg[4 * 256];  // DEBUG: per-fetch issue, ready, done, count of CTA 5
+// Diagnostics read by tools/debug_plan.py and tools/debug_plan_cta.py: the fetch timeline of CTA
+// 5 (issue, TMA ready, last agent done, agents) and every CTA's start, end and fetch count.
+__device__ unsigned long long g_plan_dbg[4 * 256];
 extern "C" int fp_debug_plan(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, g_plan_dbg, sizeof(g_plan_dbg));
+}
+__device__ unsigned long long g_plan_cta[3 * 256];
+extern "C" int fp_debug_plan_cta(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, g_plan_cta, sizeof(g_plan_cta));
 }
 // P consecutive threads plan each agent together (plan_fast_t).
 template <int P>
@@ -658,6 +664,10 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        if (blockIdx.x < 256) {
+            g_plan_cta[blockIdx.x] = globaltimer_p();
+            g_plan_cta[256 + blockIdx.x] = 0;
+        }
         for (int s = 0; s < PLAN_SLOTS; ++s) fetch(s);
     }
     for (int i = 0;; ++i) {
@@ -683,7 +693,13 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // validate the snapshot before acting on any of it (including the end-of-list marker:
         // a refill racing with these reads may already have written tile = -1 for fetch i+2)
         if (s_gen[slot] != i) continue;  // fetch i already completed without this thread's help
-        if (tile < 0) break;
+        if (tile < 0) {
+            if (blockIdx.x < 256 && (threadIdx.x & 31) == 0) {
+                atomicMax(&g_plan_cta[256 + blockIdx.x], globaltimer_p());
+                g_plan_cta[512 + blockIdx.x] = i;
+            }
+            break;
+        }
         // agent slot of this thread's lane group (the rotation keeps groups P-aligned)
         int k = (((int)threadIdx.x - i * A.rot) & (PLAN_THREADS - 1)) / P;
         if (k >= cnt) continue;  // no agent of this fetch for this thread
