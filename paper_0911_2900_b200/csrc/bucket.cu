@@ -63,9 +63,33 @@ __global__ void tile_sums_kernel(const uint32_t* sub_cnt, const uint32_t* sub_of
 // Crowded tiles do not pile up on a few CTAs, and at any time the CTAs work on neighbouring
 // parts of the list (DRAM/L2 locality of the concurrent TMA fetches).  The range index is
 // monotonic in e, so each boundary first[r] is written by exactly one entry.
+// Block-wide exclusive scan of v (one value per thread); s_part = 32 slots of scratch.
+__device__ __forceinline__ unsigned long long block_exclusive(unsigned long long v, unsigned long long* s_part,
+                                                              unsigned long long* total) {
+    unsigned long long incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((threadIdx.x & 31) >= (unsigned)o) incl += t;
+    }
+    __syncthreads();  // s_part free
+    if ((threadIdx.x & 31) == 31) s_part[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    unsigned long long before = incl - v, t = 0;
+    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
+        if (w < (threadIdx.x >> 5)) before += s_part[w];
+        t += s_part[w];
+    }
+    *total = t;
+    return before;
+}
+
+// Also cuts every tile into seed work items of at most SEED_ITEM agents for the motion's seed
+// passes (a crowded exit tile would otherwise occupy one worker group for its whole length):
+// items[i] = (tile-list entry, chunk), *n_items their count.
 __global__ void __launch_bounds__(1024) tile_deal_kernel(const uint32_t* list, const uint32_t* cnt,
                                                           const unsigned long long* n_tiles_p, int G, int passes,
-                                                          unsigned floor_cost, uint32_t* first) {
+                                                          unsigned floor_cost, uint32_t* first, uint2* items,
+                                                          unsigned long long* n_items) {
     // cost of a tile = max(its agents, floor_cost): a tile costs at least a fetch, so the
     // grid's partial last row/column of tiles does not pile onto one CTA.  One block: each
     // thread sums a contiguous run of the list, one block scan, then every entry's range.
@@ -74,24 +98,25 @@ __global__ void __launch_bounds__(1024) tile_deal_kernel(const uint32_t* list, c
     const uint32_t n = (uint32_t)*n_tiles_p;
     if (n == 0) {
         for (uint32_t b = threadIdx.x; b <= (uint32_t)G; b += blockDim.x) first[b] = 0;
+        if (threadIdx.x == 0) *n_items = 0;
         return;
     }
     const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
     const uint32_t e0 = min(n, threadIdx.x * per), e1 = min(n, e0 + per);
-    unsigned long long mine = 0;
-    for (uint32_t e = e0; e < e1; ++e) mine += max(cnt[list[e]], floor_cost);
-    unsigned long long incl = mine;
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
-        if ((threadIdx.x & 31) >= (unsigned)o) incl += t;
+    unsigned long long mine = 0, my_items = 0;
+    for (uint32_t e = e0; e < e1; ++e) {
+        const unsigned c = cnt[list[e]];
+        mine += max(c, floor_cost);
+        my_items += (c + SEED_ITEM - 1) / SEED_ITEM;
     }
-    if ((threadIdx.x & 31) == 31) s_part[threadIdx.x >> 5] = incl;
-    __syncthreads();
-    unsigned long long before = incl - mine, total = 0;
-    for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
-        if (w < (threadIdx.x >> 5)) before += s_part[w];
-        total += s_part[w];
+    unsigned long long total, n_it;
+    unsigned long long before = block_exclusive(mine, s_part, &total);
+    unsigned long long ib = block_exclusive(my_items, s_part, &n_it);
+    for (uint32_t e = e0; e < e1; ++e) {
+        const unsigned k = (cnt[list[e]] + SEED_ITEM - 1) / SEED_ITEM;
+        for (unsigned c = 0; c < k; ++c) items[ib++] = make_uint2(e, c);
     }
+    if (threadIdx.x == 0) *n_items = n_it;
     int prev = -1;
     if (e0 > 0) {  // range of the entry before this run
         const unsigned long long c = max(cnt[list[e0 - 1]], floor_cost);
@@ -134,6 +159,13 @@ int fp_bucket_reserve(fp_ctx* ctx) {
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_off, nt * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_list, nt * 4));
         ctx->n_tiles_alloc = nt;
+        ctx->graph_valid = false;
+    }
+    const size_t items = ctx->n_tiles_alloc + (size_t)ctx->cap / SEED_ITEM + 16;
+    if (items > ctx->seed_items_alloc) {
+        if (ctx->d_seed_items) cudaFree(ctx->d_seed_items);
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_seed_items, items * sizeof(uint2)));
+        ctx->seed_items_alloc = items;
         ctx->graph_valid = false;
     }
     size_t need1 = 0, need2 = 0;
@@ -179,7 +211,8 @@ int fp_bucket_launch(fp_ctx* ctx) {
                                        NonEmpty{ctx->d_tile_cnt}, s));
     ctx->ctr.kernel_launches += 2;
     tile_deal_kernel<<<1, 1024, 0, s>>>(ctx->d_tile_list, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->sm_count,
-                                        ctx->deal_passes, deal_tile_cost(), ctx->d_tile_deal);
+                                        ctx->deal_passes, deal_tile_cost(), ctx->d_tile_deal, ctx->d_seed_items,
+                                        &ctx->d_sc->n_items);
     FP_LAUNCHED(ctx);
     bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, ctx->d_alive, n, ctx->d_flags,
                                             ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket, ctx->d_brec);

@@ -27,6 +27,7 @@
 #define FP_XPAD_W 8      // ghost columns left of x = 0 in the weight plane
 #define FP_HALO 5        // largest v_max (agents.hpp:10)
 #define DEAL_PASSES 16   // plan-tile deal: most passes over the tile list (bucket.cu)
+#define SEED_ITEM 128    // agents per motion seed work item (= the seed worker group size)
 
 // weight-plane word encoding (plane.cu)
 #define FP_W_WALL 0xFFFFFFFFu
@@ -119,6 +120,7 @@ struct DevScalars {
     unsigned long long tot_updates;  // sum of alive counts entering each step
     unsigned long long fallbacks; // exact-path re-samples
     unsigned long long n_tiles;   // non-empty plan tiles this step
+    unsigned long long n_items;   // motion seed work items (<= SEED_ITEM agents of one tile)
     unsigned long long tile_next; // dynamic tile scheduler cursor
     unsigned long long err;       // device-detected errors (bit flags)
     unsigned long long pad[2];    // [0] unsafe plane cells, [1] motion rounds executed
@@ -189,6 +191,8 @@ struct fp_ctx {
     uint32_t* d_tile_deal = nullptr;  // [sm_count * DEAL_PASSES + 1] first tile-list entry per range
     int deal_passes = 1;              // passes actually used (FP_DEAL_PASSES, 1..DEAL_PASSES)
     size_t n_tiles_alloc = 0;
+    uint2* d_seed_items = nullptr;    // (tile-list entry, chunk) per motion seed work item
+    size_t seed_items_alloc = 0;
 
     // order scratch (sized by cap)
     uint32_t *d_alive_ids = nullptr, *d_order = nullptr, *d_j = nullptr, *d_cnt = nullptr,

@@ -58,6 +58,7 @@ struct MoveArgs {
     const uint32_t* tile_list;
     const uint32_t* tile_off;
     const uint32_t* tile_cnt;
+    const uint2* items;            // seed work items: (tile-list entry, chunk of SEED_ITEM agents)
     int tile_w, tile_h, tiles_x;
     // reservation rounds (see the bucket notes below)
     const uint4* crec;             // contended records (= rec[1]), rank in .y
@@ -737,6 +738,20 @@ __device__ __forceinline__ SeedWin seed_window(const MoveArgs& a, uint32_t t) {
     return s;
 }
 
+// Seed work item e: its tile and its agents [off, off + cnt) -- at most SEED_ITEM of the tile's.
+__device__ __forceinline__ void seed_item(const MoveArgs& a, uint32_t e, uint32_t ni, uint32_t& t, uint32_t& off,
+                                          uint32_t& cnt) {
+    if (e >= ni) {
+        t = off = cnt = 0;
+        return;
+    }
+    const uint2 it = __ldcg(&a.items[e]);
+    t = __ldcg(&a.tile_list[it.x]);
+    const uint32_t c0 = it.y * SEED_ITEM, tc = __ldcg(&a.tile_cnt[t]);
+    off = __ldcg(&a.tile_off[t]) + c0;
+    cnt = min((uint32_t)SEED_ITEM, tc - c0);
+}
+
 // Local word index of cell (x, y) in the window, or -1 when it lies outside (periodic seam).
 __device__ __forceinline__ int seed_local(const SeedWin& s, int x, int y) {
     const int wi = ((x + FP_XPAD_BITS) >> 5) - s.wx0, yi = y - s.ys;
@@ -766,21 +781,21 @@ __device__ __forceinline__ void record_footprint(const MoveArgs& a, const uint4&
 // tile's marks merge into the global bitplanes.
 __device__ void seed_mark(const MoveArgs& a, uint32_t* win, const signed char (*bp)[5][2]) {
     const unsigned lt = threadIdx.x % SEED_GROUP;
-    const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
+    const uint32_t ni = (uint32_t)cta_load(&a.sc->n_items);
     const uint32_t ng = gridDim.x * SEED_GROUPS;
     uint32_t e = blockIdx.x * SEED_GROUPS + threadIdx.x / SEED_GROUP;
-    uint32_t t = e < nt ? __ldcg(&a.tile_list[e]) : 0u;
-    uint32_t off = e < nt ? __ldcg(&a.tile_off[t]) : 0u, cnt = e < nt ? __ldcg(&a.tile_cnt[t]) : 0u;
+    uint32_t t, off, cnt;
+    seed_item(a, e, ni, t, off, cnt);
     uint4 r0 = lt < cnt ? __ldcg(&a.rec0[off + lt]) : make_uint4(0, 0, 0, 0);
-    for (; e < nt; e += ng) {
+    for (; e < ni; e += ng) {
         const uint32_t en = e + ng;
-        const uint32_t tn = en < nt ? __ldcg(&a.tile_list[en]) : 0u;
+        uint32_t tn, offn, cntn;
+        seed_item(a, en, ni, tn, offn, cntn);
         const SeedWin s = seed_window(a, t);
         const int nw = s.ww * s.wh;
         uint32_t* L1 = win;
         uint32_t* L2 = win + nw;
         for (int w = lt; w < 2 * nw; w += SEED_GROUP) win[w] = 0;
-        const uint32_t offn = en < nt ? __ldcg(&a.tile_off[tn]) : 0u, cntn = en < nt ? __ldcg(&a.tile_cnt[tn]) : 0u;
         group_sync();
         for (uint32_t k = lt; k < cnt; k += SEED_GROUP) {
             const uint4 r = k == lt ? r0 : __ldcg(&a.rec0[off + k]);
@@ -834,15 +849,16 @@ __device__ void seed_mark(const MoveArgs& a, uint32_t* win, const signed char (*
 __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, const signed char (*bp)[5][2],
                               unsigned long long* hops) {
     const unsigned lt = threadIdx.x % SEED_GROUP;
-    const uint32_t nt = (uint32_t)cta_load(&a.sc->n_tiles);
+    const uint32_t ni = (uint32_t)cta_load(&a.sc->n_items);
     const uint32_t ng = gridDim.x * SEED_GROUPS;
     uint32_t e = blockIdx.x * SEED_GROUPS + threadIdx.x / SEED_GROUP;
-    uint32_t t = e < nt ? __ldcg(&a.tile_list[e]) : 0u;
-    uint32_t off = e < nt ? __ldcg(&a.tile_off[t]) : 0u, cnt = e < nt ? __ldcg(&a.tile_cnt[t]) : 0u;
-    for (; e < nt; e += ng) {
-        // next tile's header in flight
+    uint32_t t, off, cnt;
+    seed_item(a, e, ni, t, off, cnt);
+    for (; e < ni; e += ng) {
+        // next item's header in flight
         const uint32_t en = e + ng;
-        const uint32_t tn = en < nt ? __ldcg(&a.tile_list[en]) : 0u;
+        uint32_t tn, offn, cntn;
+        seed_item(a, en, ni, tn, offn, cntn);
         const SeedWin s = seed_window(a, t);
         const int nw = s.ww * s.wh;
         uint32_t* C2 = win;       // P2 window
@@ -860,7 +876,6 @@ __device__ void seed_classify(const MoveArgs& a, const Group& G, uint32_t* win, 
             CO[w] = vo;
         }
         const uint32_t rk0 = (lt < cnt && rec_m(r0)) ? __ldcg(&a.rank[r0.x]) : 0u;
-        const uint32_t offn = en < nt ? __ldcg(&a.tile_off[tn]) : 0u, cntn = en < nt ? __ldcg(&a.tile_cnt[tn]) : 0u;
         group_sync();
         for (uint32_t base = 0; base < cnt; base += SEED_GROUP) {
             const uint32_t k = base + lt;
@@ -1288,6 +1303,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.tile_list = ctx->d_tile_list;
     a.tile_off = ctx->d_tile_off;
     a.tile_cnt = ctx->d_tile_cnt;
+    a.items = ctx->d_seed_items;
     a.tile_w = ctx->tile_w;
     a.tile_h = ctx->tile_h;
     a.tiles_x = ctx->tiles_x;
