@@ -145,6 +145,7 @@ static unsigned deal_tile_cost() {
 
 int fp_bucket_reserve(fp_ctx* ctx) {
     const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
+    if (ctx->bucket_reserved_nt == nt && ctx->bucket_reserved_cap == ctx->cap && ctx->d_temp_b) return FP_OK;
     if (nt > ctx->n_tiles_alloc) {
         if (ctx->d_tile_cnt) cudaFree(ctx->d_tile_cnt);
         if (ctx->d_tile_off) cudaFree(ctx->d_tile_off);
@@ -183,6 +184,8 @@ int fp_bucket_reserve(fp_ctx* ctx) {
         ctx->temp_b_bytes = need;
         ctx->graph_valid = false;
     }
+    ctx->bucket_reserved_nt = nt;
+    ctx->bucket_reserved_cap = ctx->cap;
     return FP_OK;
 }
 

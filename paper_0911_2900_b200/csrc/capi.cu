@@ -297,10 +297,14 @@ extern "C" int fp_get_field(const fp_ctx* cc, double* out) {
     return FP_OK;
 }
 
-// host mirror (step, alive) -> device scalars
+// host mirror (step, alive) -> device scalars; skipped when the device already holds them (the
+// last read_scalars or sync_scalars left them there and the host has not changed them since)
 static int sync_scalars(fp_ctx* c) {
+    if (c->dev_step == c->step && c->dev_alive == c->alive) return FP_OK;
     sc_set_kernel<<<1, 1, 0, c->stream>>>(c->d_sc, (long long)c->step, (unsigned long long)c->alive);
     FP_LAUNCHED(c);
+    c->dev_step = c->step;
+    c->dev_alive = c->alive;
     return FP_OK;
 }
 
@@ -316,6 +320,8 @@ static int read_scalars(fp_ctx* c) {
     }
     c->alive = (int64_t)c->h_sc->alive;
     c->step = (int64_t)c->h_sc->step;
+    c->dev_step = c->step;
+    c->dev_alive = c->alive;
     c->ctr.plan_fallbacks = (int64_t)c->h_sc->fallbacks;
     c->ctr.motion_rounds = (int64_t)c->h_sc->pad[1];
     const unsigned long long* tm = c->h_sc->t_motion;

@@ -121,6 +121,7 @@ struct DevScalars {
     unsigned long long fallbacks; // exact-path re-samples
     unsigned long long n_tiles;   // non-empty plan tiles this step
     unsigned long long n_items;   // motion seed work items (<= SEED_ITEM agents of one tile)
+    unsigned long long exits_sorted;  // the motion graph sorted this phase's exit records
     unsigned long long tile_next; // dynamic tile scheduler cursor
     unsigned long long err;       // device-detected errors (bit flags)
     unsigned long long pad[2];    // [0] unsafe plane cells, [1] motion rounds executed
@@ -219,6 +220,10 @@ struct fp_ctx {
     unsigned long long* d_exits_sorted = nullptr;
     int64_t last_displacement = 0;
     int64_t last_dx = 0;          // sum of segment_dx of the last move phase (fundamental diagram)
+    int64_t dev_step = -1, dev_alive = -1;  // what the device scalars hold (sync_scalars skips repeats)
+    uint32_t order_reserved_n = 0;          // fp_order_reserve done for this roster size
+    size_t bucket_reserved_nt = 0;          // fp_bucket_reserve done for this tile count / roster
+    uint32_t bucket_reserved_cap = 0;
     uint32_t n_exits = 0;
 
     DevScalars* d_sc = nullptr;   // device scalars

@@ -1202,10 +1202,32 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     }
 }
 
+// The phase's exit records (rank << 32 | id) into processing order on the device when they are
+// few (the usual case: a handful per step); more than EXITS_SMEM are left to the host's radix sort.
+#define EXITS_SMEM 4096
+__global__ void __launch_bounds__(1024) exits_sort_kernel(unsigned long long* exits, DevScalars* sc) {
+    __shared__ unsigned long long key[EXITS_SMEM];
+    const unsigned n = (unsigned)sc->n_exits;
+    if (n > EXITS_SMEM) {
+        if (threadIdx.x == 0) sc->exits_sorted = 0;
+        return;
+    }
+    for (unsigned i = threadIdx.x; i < n; i += blockDim.x) key[i] = exits[i];
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < n; i += blockDim.x) {  // keys are distinct (one per rank)
+        const unsigned long long k = key[i];
+        unsigned below = 0;
+        for (unsigned j = 0; j < n; ++j) below += key[j] < k;
+        exits[below] = k;
+    }
+    if (threadIdx.x == 0) sc->exits_sorted = 1;
+}
+
 __global__ void move_begin_kernel(DevScalars* sc) {
     for (int r = threadIdx.x; r < 64; r += blockDim.x) sc->chk_max[r] = sc->chk_cnt[r] = sc->p1_max[r] = 0;
     if (threadIdx.x) return;
     sc->n_exits = 0;
+    sc->exits_sorted = 0;
     sc->disp = 0;
     sc->tot_updates += sc->alive;
 }
@@ -1338,6 +1360,8 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     cfg.numAttrs = 1;
     FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel, a));
     ctx->ctr.kernel_launches++;
+    exits_sort_kernel<<<1, 1024, 0, s>>>(ctx->d_exits, ctx->d_sc);
+    FP_LAUNCHED(ctx);
     ctx->rec_fresh = false;
     ctx->marks_dirty = false;
     return fp_ghost_occ(ctx);
@@ -1346,7 +1370,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
 // Sorts the exit records of the last phase by rank (processing order) for fp_get_exited.
 int fp_exits_finish(fp_ctx* ctx) {
     const uint32_t ne = ctx->n_exits;
-    if (ne <= 1) return FP_OK;
+    if (ne <= 1 || ctx->h_sc->exits_sorted) return FP_OK;  // sorted in the motion graph
     size_t need = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, need, ctx->d_exits, ctx->d_exits_sorted, (int)ne, 0, 64, ctx->stream);
     if (int rc = fp_ensure_temp(ctx, need)) return rc;

@@ -155,12 +155,15 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
 // Reserves the CUB scratch of the order + bucketing stages (outside any graph capture).
 int fp_order_reserve(fp_ctx* ctx) {
     const uint32_t n = std::max<uint32_t>(ctx->n, 1);
+    if (ctx->order_reserved_n == n && ctx->d_temp) return FP_OK;
     size_t a = 0, b = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, a, ctx->d_cnt, ctx->d_off, (int)n, ctx->stream);
     thrust::counting_iterator<uint32_t> it(0);
     cub::DeviceSelect::If(nullptr, b, it, ctx->d_alive_ids, &ctx->d_sc->n_alive, (int)n, IsAlive{ctx->d_alive},
                           ctx->stream);
-    return fp_ensure_temp(ctx, std::max(a, b) * 2 + 4096);
+    if (int rc = fp_ensure_temp(ctx, std::max(a, b) * 2 + 4096)) return rc;
+    ctx->order_reserved_n = n;
+    return FP_OK;
 }
 
 int fp_order_positions(fp_ctx* ctx, uint32_t n, uint64_t seed, int64_t step, uint32_t* d_out) {
