@@ -27,7 +27,7 @@
 #define FP_XPAD_W 8      // ghost columns left of x = 0 in the weight plane
 #define FP_HALO 5        // largest v_max (agents.hpp:10)
 #define DEAL_PASSES 16   // plan-tile deal: most passes over the tile list (bucket.cu)
-#define SEED_ITEM 128    // agents per motion seed work item (= the seed worker group size)
+#define SEED_ITEM 512    // agents per motion seed work item (a worker group takes it in passes of 128)
 
 // weight-plane word encoding (plane.cu)
 #define FP_W_WALL 0xFFFFFFFFu
