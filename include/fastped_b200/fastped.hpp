@@ -85,10 +85,13 @@ public:
     Boundary boundary() const { return boundary_; }
     std::int64_t free_count() const { return free_count_; }
     std::int64_t exit_count() const { return exit_count_; }
+    std::int64_t free_cell_count() const { return free_count_; }  // the reference's names (world.hpp)
+    std::int64_t exit_cell_count() const { return exit_count_; }
     std::size_t index(Cell c) const {
         return static_cast<std::size_t>(c.y) * static_cast<std::size_t>(width_) + static_cast<std::size_t>(c.x);
     }
     CellKind at(Cell c) const { return cells_[index(c)]; }
+    CellKind at(int x, int y) const { return at(Cell{x, y}); }
     const std::vector<CellKind>& cells() const { return cells_; }
     fp_grid_desc desc() const {
         return fp_grid_desc{width_, height_, cell_size_, static_cast<int32_t>(boundary_)};
