@@ -510,8 +510,11 @@ struct TailSmem {
 #endif
 #define MOVE_LOCAL_MAX 4096    // ... while the CTA holds at most this many pending agents
 #define QC_CAP 8192
-static_assert(QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) <= sizeof(TailSmem), "round queues");
-static_assert((MOVE_THREADS / 32) * BK_SORT_MAX * sizeof(unsigned) <= sizeof(TailSmem), "long-bucket ranking");
+// The kernel's dynamic shared memory serves, one after another, the seed windows, the long-bucket
+// ranking, the round queues and the tail.
+#define MOVE_DYN_SMEM (sizeof(TailSmem) > QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) \
+                           ? sizeof(TailSmem) : QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned))
+static_assert((MOVE_THREADS / 32) * BK_SORT_MAX * sizeof(unsigned) <= MOVE_DYN_SMEM, "long-bucket ranking");
 
 __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y) {
     const unsigned cell = (unsigned)y * (unsigned)a.g.W + (unsigned)x;
@@ -1296,10 +1299,10 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     }
     if (!g_move_blocks) {
         FP_CUDA(ctx, cudaFuncSetAttribute(move_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)sizeof(TailSmem)));
+                                          (int)MOVE_DYN_SMEM));
         int per_sm = 0;
         FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS,
-                                                                   sizeof(TailSmem)));
+                                                                   MOVE_DYN_SMEM));
         g_move_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
     }
     MoveArgs a;
@@ -1344,14 +1347,14 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.alist[0] = lists;
     a.alist[1] = lists + ctx->cap;
     a.long_list = reinterpret_cast<unsigned*>(lists + ctx->cap);  // alist[1] is free until round 0
-    if (premade && (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4 > sizeof(TailSmem))
+    if (premade && (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4 > MOVE_DYN_SMEM)
         return fp_fail(ctx, FP_ERUNTIME, "motion: seed window exceeds shared memory");
     const unsigned blocks = (unsigned)std::min<size_t>((size_t)g_move_blocks,
                                                         std::max<size_t>(1, fp_blocks(ctx->n, MOVE_THREADS)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(MOVE_THREADS);
-    cfg.dynamicSmemBytes = sizeof(TailSmem);
+    cfg.dynamicSmemBytes = MOVE_DYN_SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
