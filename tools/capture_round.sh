@@ -11,3 +11,6 @@ ncu --set full --import-source on --clock-control none -k regex:plan_tile -s 200
     python tools/profile_step.py --warm 198 --steps 4 --mode run > gpurun_out/ncu_plan.log 2>&1; echo "plan rc=$?"
 ncu --set full --import-source on --clock-control none -k regex:move_rounds -s 200 -c 1 -o gpurun_out/move_full \
     python tools/profile_step.py --warm 198 --steps 4 --mode run > gpurun_out/ncu_move.log 2>&1; echo "move rc=$?"
+python tools/profile_step.py --warm 4 --steps 2 --mode run > gpurun_out/prof_start.log 2>&1 && \
+ncu --set full --import-source on --clock-control none -k regex:plan_tile -s 5 -c 1 -o gpurun_out/plan_start \
+    python tools/profile_step.py --warm 4 --steps 2 --mode run > gpurun_out/ncu_plan_start.log 2>&1; echo "plan start rc=$?"
