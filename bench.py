@@ -124,13 +124,20 @@ def build_workload(cfg, seed):
     return scenarios.build(cfg, seed=seed)
 
 
-def reference_cpu(wl, field, max_steps, cores, budget_s):
+def reference_cpu(wl, field, max_steps, cores, budget_s, warmup=0):
     """The reference's own run() (oracle/_ref, unmodified headers) on this workload, from step 0:
     one calibration step, then as many more (<= max_steps - 1) as fit in ~budget_s seconds.
+    `warmup` untimed steps run first on a throwaway state built from the same inputs (threads,
+    page faults), so the timed run still starts at step 0.
     Returns (agent-updates/s over all timed steps, kind, cores, steps, seconds)."""
     import oracle as O
     ro = wl.roster
     if O.have_reference():
+        if warmup > 0:
+            w = O.RefState(wl.grid.cells, field, ro.x, ro.y, ro.v_max, ro.alive, wl.grid.boundary,
+                           potential=wl.potential, drive_gradient=wl.drive_gradient)
+            w.run(wl.k_s, wl.seed, warmup, cores)
+            del w
         st = O.RefState(wl.grid.cells, field, ro.x, ro.y, ro.v_max, ro.alive, wl.grid.boundary,
                         potential=wl.potential, drive_gradient=wl.drive_gradient)
         upd, secs, steps = 0.0, 0.0, 0
@@ -228,13 +235,13 @@ def main():
         field = O.static_field(wl.grid.cells, wl.grid.boundary)
         cores = os.cpu_count() or 1
         # each "step" of this arm is the reference's own step; the run is bounded to ~60 s of work
-        v, kind, c, steps_done, secs = reference_cpu(wl, field, max(1, args.steps), cores, 60.0)
+        v, kind, c, steps_done, secs = reference_cpu(wl, field, max(1, args.steps), cores, 60.0, args.warmup)
         config_desc.update(n_agents=int(len(wl.roster)), grid=[wl.grid.width, wl.grid.height])
         sample = (f"{steps_done} of the {args.steps} steps of {args.config} from step 0 "
                   f"({secs:.1f} s, reference run() with ScheduleParams{{cores={c}}}, {cpu_model()})")
         out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps_done,
-               "warmup": 0, "ms_per_step": secs / steps_done * 1e3, "higher_is_better": True,
-               "impl": "reference", "dtype": "f64", "data": "synthetic", "scaling": "strong",
+               "warmup": args.warmup if kind == "reference" else 0, "ms_per_step": secs / steps_done * 1e3,
+               "higher_is_better": True, "impl": "reference", "dtype": "f64", "data": "synthetic", "scaling": "strong",
                "vs_baseline": None, "config": config_desc,
                "cpu_baseline": {"value": v, "unit": UNIT, "cores": c, "kind": kind, "sample": sample},
                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -44,3 +44,26 @@ def test_two_rank_aggregation_gloo():
 def test_single_process_is_identity():
     from paper_0911_2900_b200.dist import aggregate
     assert aggregate(0.25, 123.0) == (0.25, 123.0)
+
+
+@pytest.mark.timeout(300)
+def test_reference_arm_under_torchrun_prints_one_line():
+    """bench.py --impl reference launched the driver's way for N=2: rank 0 alone runs the
+    reference CPU path and prints one JSON line; rank 1 exits 0 without work."""
+    import json
+    import subprocess
+    import sys
+    import oracle
+    if not oracle.have_reference():
+        pytest.skip("oracle/_ref not built")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--impl", "reference",
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--config", "corridor"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=240)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["warmup"] == 3 and d["steps"] == 3
+    assert d["e2e"]["value"] == d["value"] and d["cpu_baseline"]["kind"] == "reference"
