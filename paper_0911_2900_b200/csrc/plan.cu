@@ -563,7 +563,9 @@ __device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint3
 #ifndef FP_PLAN_NAP_MAX
 #define FP_PLAN_NAP_MAX 256  // ns
 #endif
+#ifndef PLAN_SLOTS
 #define PLAN_SLOTS 3  // tiles resident per CTA
+#endif
 
 // Persistent CTA per SM.  Tiles are fetched in pairs of buffer slots (TMA, mbarrier); the
 // agents of fetch i are dealt to threads round-robin starting at thread (i*160) mod 512, one

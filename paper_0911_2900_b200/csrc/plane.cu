@@ -188,11 +188,14 @@ __global__ void tile_exit_kernel(Geo g, int tile_w, int tile_h, int tiles_x, int
 
 // Chooses the plan tile for this grid and encodes the TMA box (tile + FP_HALO halo rows,
 // tile + 6 columns each side so the inner box width stays a multiple of 16 bytes).
+#ifndef FP_BIG_TILE_H
+#define FP_BIG_TILE_H 48
+#endif
 static int make_tmap(fp_ctx* ctx) {
     const size_t cells = (size_t)ctx->W * ctx->H;
     if (cells >= (size_t)16 << 20) {
         ctx->tile_w = 240;
-        ctx->tile_h = 48;  // three 63 KB slots fit in shared memory
+        ctx->tile_h = FP_BIG_TILE_H;  // three 63 KB slots fit in shared memory
     } else if (cells >= (size_t)1 << 20) {
         ctx->tile_w = 120;
         ctx->tile_h = 32;
