@@ -34,7 +34,7 @@ extern "C" {
 #define FP_EINVAL 1   /* std::invalid_argument in the reference */
 #define FP_ERUNTIME 2 /* std::runtime_error in the reference */
 #define FP_ECUDA 3    /* CUDA runtime / device failure (no GPU, OOM, kernel fault) */
-#define FP_ENCCL 4    /* reserved for the multi-GPU strip path */
+#define FP_ENCCL 4    /* NCCL failure on the multi-GPU strip path */
 
 #define FP_CELL_FREE 0
 #define FP_CELL_WALL 1
@@ -161,6 +161,16 @@ int fp_state_hash(const fp_ctx* ctx, uint64_t* out);
  * probabilities of the production sampling path (fp32). */
 int fp_get_choice(fp_ctx* ctx, uint32_t agent, double k_s, int32_t* cx, int32_t* cy,
                   double* weights, float* probs, uint32_t cap, uint32_t* n);
+
+/* Host API of planning.hpp for ONE agent given by value against the context's current occupancy
+ * (the reference's `const SimState&` snapshot), computed on the device with the exact path:
+ *   choose_desired_cell(st, agent, params) -- planning.hpp:88-108, uniform
+ *       rng_u64(seed, id, step, 0); `step` is SimState::step as the caller holds it;
+ *   enumerate_candidates(st, agent) -- planning.hpp:23-57, list order (<= 121 cells). */
+int fp_choose_desired(fp_ctx* ctx, uint32_t id, int32_t x, int32_t y, int32_t v_max, int64_t step,
+                      double k_s, uint64_t seed, int32_t* out_x, int32_t* out_y);
+int fp_enumerate_candidates(fp_ctx* ctx, int32_t x, int32_t y, int32_t v_max, int32_t* cx, int32_t* cy,
+                            uint32_t cap, uint32_t* n);
 
 /* The movement permutation of positions 0..n-1 for (seed, step) computed by the device
  * (engine.hpp:99-111 Fisher-Yates), context-free. */

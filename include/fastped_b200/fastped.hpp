@@ -229,6 +229,11 @@ struct SimState {
 inline SimState make_state(std::shared_ptr<const Grid> grid, std::shared_ptr<const StaticField> field,
                            std::vector<Agent> roster, int device = 0) {
     if (!grid) throw std::invalid_argument("make_state: null grid");
+    if (field && (field->width != grid->width() || field->height != grid->height() ||
+                  field->s.size() != static_cast<std::size_t>(grid->width()) * static_cast<std::size_t>(grid->height())))
+        throw std::invalid_argument("make_state: field dimensions do not match grid");
+    for (const Agent& a : roster)  // state.hpp:56-57; per-agent v_max may be edited afterwards, as in the reference
+        if (a.v_max != roster.front().v_max) throw std::invalid_argument("make_state: all agents must share one v_max");
     SimState st;
     st.grid = grid;
     const fp_grid_desc d = grid->desc();

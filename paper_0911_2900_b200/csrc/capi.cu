@@ -272,6 +272,8 @@ extern "C" void fp_destroy(fp_ctx* c) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (c->h_counters) cudaFreeHost(c->h_counters);
+    if (c->d_scratch_small) cudaFree(c->d_scratch_small);
+    if (c->h_scratch_small) cudaFreeHost(c->h_scratch_small);
     if (c->h_sc) cudaFreeHost(c->h_sc);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -362,6 +364,9 @@ static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const ui
     FP_CUDA(c, cudaMemcpyAsync(c->h_counters + 8, c->d_counters + 8, 4 * 8, cudaMemcpyDeviceToHost, s));
     FP_CUDA(c, cudaStreamSynchronize(s));
     const unsigned long long* e = c->h_counters + 8;
+    // the device roster and occupancy are already replaced: a rejected roster poisons the context
+    // until the next successful upload (compute calls fail instead of running on a half state)
+    c->poisoned = e[0] != ~0ull || e[1] != ~0ull || e[2] != ~0ull;
     if (e[0] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[0]) + " is out of bounds");
     if (e[1] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[1]) + " placed on a Wall cell");
     if (e[2] != ~0ull) return fail(c, FP_EINVAL, "make_state: agent " + std::to_string(e[2]) + " shares a cell");
@@ -433,6 +438,8 @@ extern "C" int fp_set_potential(fp_ctx* c, int kind, double g) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     if (kind != FP_POTENTIAL_EXIT_DISTANCE && kind != FP_POTENTIAL_DRIVE_X)
         return fail(c, FP_EINVAL, "fp_set_potential: unknown potential");
+    // the plan graphs bake the potential and gradient into their kernel arguments
+    if (kind != c->potential || g != c->drive_gradient) c->graph_valid = false;
     c->potential = kind;
     c->drive_gradient = g;
     return FP_OK;
@@ -448,6 +455,12 @@ extern "C" int fp_set_desired(fp_ctx* c, const int32_t* x, const int32_t* y) {
     return FP_OK;
 }
 
+static int check_usable(fp_ctx* c) {
+    if (c->poisoned)
+        return fail(c, FP_EINVAL, "state invalid: the last agent upload was rejected; upload a valid roster first");
+    return FP_OK;
+}
+
 // Allocations / setup of every stage for (k_s): never inside a graph capture.
 static int prepare(fp_ctx* c, double k_s) {
     if (int rc = fp_plan_prepare(c, k_s)) return rc;
@@ -458,6 +471,7 @@ static int prepare(fp_ctx* c, double k_s) {
 
 extern "C" int fp_plan(fp_ctx* c, double k_s, uint64_t seed) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (int rc = check_usable(c)) return rc;
     cudaSetDevice(c->device);
     if (c->alive == 0) return FP_OK;  // engine.hpp:73
     if (int rc = prepare(c, k_s)) return rc;
@@ -516,6 +530,7 @@ static int move_impl(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
 
 extern "C" int fp_move(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (int rc = check_usable(c)) return rc;
     cudaSetDevice(c->device);
     return move_impl(c, seed, out);
 }
@@ -526,6 +541,7 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed);
 // the step advance), one host sync, then the exit list in processing order.
 extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (int rc = check_usable(c)) return rc;
     cudaSetDevice(c->device);
     if (c->alive == 0 || c->n == 0) {  // engine.hpp:73: nothing to plan or move
         c->n_order = 0;
@@ -619,6 +635,7 @@ __global__ void run_begin_kernel(DevScalars* sc) {
 // run(): `steps` steps as graph replays, CUDA events between phases; one host sync at the end.
 extern "C" int fp_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (int rc = check_usable(c)) return rc;
     if (steps < 1) return fail(c, FP_EINVAL, "SimParams: steps must be >= 1");
     cudaSetDevice(c->device);
     if (int rc = prepare(c, k_s)) return rc;
@@ -795,6 +812,51 @@ extern "C" int fp_get_choice(fp_ctx* c, uint32_t agent, double k_s, int32_t* cx,
     }
     cudaFree(d);
     return rc;
+}
+
+static int check_agent_arg(fp_ctx* c, int32_t x, int32_t y, int32_t v) {
+    if (v < 1 || v > 5) return fail(c, FP_EINVAL, "SimParams: v_max must be in [1,5]");
+    const int32_t xw = c->boundary == FP_BOUNDARY_PERIODIC_X ? ((x % c->W) + c->W) % c->W : x;
+    if (xw < 0 || xw >= c->W || y < 0 || y >= c->H) return fail(c, FP_EINVAL, "agent is out of bounds");
+    return FP_OK;
+}
+
+extern "C" int fp_choose_desired(fp_ctx* c, uint32_t id, int32_t x, int32_t y, int32_t v_max, int64_t step,
+                                 double k_s, uint64_t seed, int32_t* out_x, int32_t* out_y) {
+    if (!c || !out_x || !out_y) return fail(c, FP_EINVAL, "null argument");
+    if (int rc = check_usable(c)) return rc;
+    if (int rc = check_agent_arg(c, x, y, v_max)) return rc;
+    cudaSetDevice(c->device);
+    if (!c->d_scratch_small) FP_CUDA(c, cudaMalloc(&c->d_scratch_small, 4096));
+    if (!c->h_scratch_small) FP_CUDA(c, cudaMallocHost(&c->h_scratch_small, 4096));
+    int32_t* d = (int32_t*)c->d_scratch_small;
+    if (int rc = fp_choose_one_launch(c, id, x, y, v_max, step, k_s, seed, d)) return rc;
+    FP_CUDA(c, cudaMemcpyAsync(c->h_scratch_small, d, 8, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    *out_x = ((int32_t*)c->h_scratch_small)[0];
+    *out_y = ((int32_t*)c->h_scratch_small)[1];
+    return FP_OK;
+}
+
+extern "C" int fp_enumerate_candidates(fp_ctx* c, int32_t x, int32_t y, int32_t v_max, int32_t* cx, int32_t* cy,
+                                       uint32_t cap, uint32_t* n) {
+    if (!c || !n) return fail(c, FP_EINVAL, "null argument");
+    if (int rc = check_usable(c)) return rc;
+    if (int rc = check_agent_arg(c, x, y, v_max)) return rc;
+    cudaSetDevice(c->device);
+    if (!c->d_scratch_small) FP_CUDA(c, cudaMalloc(&c->d_scratch_small, 4096));
+    if (!c->h_scratch_small) FP_CUDA(c, cudaMallocHost(&c->h_scratch_small, 4096));
+    int32_t* d = (int32_t*)c->d_scratch_small;  // 121 x, 121 y, count
+    if (int rc = fp_candidates_one_launch(c, x, y, v_max, d, d + 128, (uint32_t*)(d + 256))) return rc;
+    FP_CUDA(c, cudaMemcpyAsync(c->h_scratch_small, d, 257 * 4, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    const int32_t* h = (const int32_t*)c->h_scratch_small;
+    *n = (uint32_t)h[256];
+    for (uint32_t i = 0; i < *n && i < cap; ++i) {
+        if (cx) cx[i] = h[i];
+        if (cy) cy[i] = h[128 + i];
+    }
+    return FP_OK;
 }
 
 extern "C" int fp_movement_order(int64_t n, uint64_t seed, int64_t step, int device, uint32_t* out) {

@@ -182,6 +182,7 @@ struct fp_ctx {
     int64_t step = 0;
     int64_t alive = 0;
     bool mixed_v = false;
+    bool poisoned = false;  // a failed upload left the device roster inconsistent (capi.cu)
     int vmax_all = 1;
 
     // tile buckets
@@ -230,6 +231,8 @@ struct fp_ctx {
     DevScalars* h_sc = nullptr;   // pinned mirror
     unsigned long long* d_counters = nullptr;  // legacy scratch (errors of uploads)
     unsigned long long* h_counters = nullptr;
+    void* d_scratch_small = nullptr;  // 4 KB: single-agent host-API calls (fp_choose_desired, ...)
+    void* h_scratch_small = nullptr;
 
     // cub temp: order stage (two halves: scan | select) and bucketing stage
     void* d_temp = nullptr;
@@ -287,6 +290,9 @@ int fp_exits_finish(fp_ctx* ctx);                                     // move.cu
 int fp_field_compute(fp_ctx* ctx, const uint8_t* d_cells);            // field.cu
 int fp_choice_launch(fp_ctx* ctx, uint32_t agent, double k_s, int32_t* d_cx, int32_t* d_cy,
                      double* d_w, float* d_p, uint32_t* d_n);         // plan.cu
+int fp_choose_one_launch(fp_ctx* ctx, uint32_t id, int px, int py, int v, int64_t step, double k_s, uint64_t seed,
+                         int32_t* d_out);                                  // plan.cu
+int fp_candidates_one_launch(fp_ctx* ctx, int px, int py, int v, int32_t* d_cx, int32_t* d_cy, uint32_t* d_n);
 int fp_order_positions(fp_ctx* ctx, uint32_t n, uint64_t seed, int64_t step, uint32_t* d_out);
 int fp_ensure_temp(fp_ctx* ctx, size_t bytes);
 int fp_ensure_res(fp_ctx* ctx);

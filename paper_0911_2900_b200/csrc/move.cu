@@ -1256,7 +1256,9 @@ int fp_ensure_res(fp_ctx* ctx) {
     return ensure_buckets(ctx);  // before any graph capture: allocation is not capturable
 }
 
-static int g_move_blocks = 0;
+// per device: the raised shared-memory limit and the occupancy are attributes of the device's
+// function instance, so a process driving several devices configures each one
+static int g_move_blocks[64] = {0};
 
 // Buckets: per contended cell (<= 3 per contended agent: every contended cell is covered by >= 2
 // of the <= 6-cell footprints) a counter, a base and a current position; per position (<= 6 per
@@ -1297,13 +1299,14 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
         FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, s));
         FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, s));
     }
-    if (!g_move_blocks) {
+    int& move_blocks = g_move_blocks[ctx->device & 63];
+    if (!move_blocks) {
         FP_CUDA(ctx, cudaFuncSetAttribute(move_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)MOVE_DYN_SMEM));
         int per_sm = 0;
         FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS,
                                                                    MOVE_DYN_SMEM));
-        g_move_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
+        move_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
     }
     MoveArgs a;
     a.g = fp_geo(ctx);
@@ -1349,7 +1352,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.long_list = reinterpret_cast<unsigned*>(lists + ctx->cap);  // alist[1] is free until round 0
     if (premade && (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4 > MOVE_DYN_SMEM)
         return fp_fail(ctx, FP_ERUNTIME, "motion: seed window exceeds shared memory");
-    const unsigned blocks = (unsigned)std::min<size_t>((size_t)g_move_blocks,
+    const unsigned blocks = (unsigned)std::min<size_t>((size_t)move_blocks,
                                                         std::max<size_t>(1, fp_blocks(ctx->n, MOVE_THREADS)));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(blocks);

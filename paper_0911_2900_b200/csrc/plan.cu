@@ -175,11 +175,10 @@ __device__ __forceinline__ ExactWeight make_weight(const PlanCommon& a, int px, 
     return w;
 }
 
-// choose_desired_cell, exact (planning.hpp:88-108 + sample_index :63-73)
-__device__ __noinline__ void choose_exact(const PlanCommon& a, uint32_t i, uint64_t step, int* ox, int* oy) {
-    const int px = a.g.wrap(a.x[i]);
-    const int py = a.y[i];
-    const int v = a.v[i];
+// choose_desired_cell, exact (planning.hpp:88-108 + sample_index :63-73), for agent id i standing
+// at (px, py) with radius v
+__device__ __noinline__ void choose_exact_at(const PlanCommon& a, uint32_t i, int px, int py, int v, uint64_t step,
+                                             int* ox, int* oy) {
     const ExactWeight wf = make_weight(a, px, py);
     double total = 0.0;
     int lastx = px, lasty = py;
@@ -204,6 +203,30 @@ __device__ __noinline__ void choose_exact(const PlanCommon& a, uint32_t i, uint6
     });
     *ox = cx;
     *oy = cy;
+}
+
+__device__ __forceinline__ void choose_exact(const PlanCommon& a, uint32_t i, uint64_t step, int* ox, int* oy) {
+    choose_exact_at(a, i, a.g.wrap(a.x[i]), a.y[i], a.v[i], step, ox, oy);
+}
+
+// Host-API single-agent entry points (fp_choose_desired / fp_enumerate_candidates): an agent
+// given by value against the context's occupancy snapshot (the reference's const SimState&).
+__global__ void choose_one_kernel(PlanCommon a, uint32_t id, int px, int py, int v, long long step, int32_t* out) {
+    int cx, cy;
+    choose_exact_at(a, id, a.g.wrap(px), py, v, (uint64_t)step, &cx, &cy);
+    out[0] = cx;
+    out[1] = cy;
+}
+
+__global__ void candidates_one_kernel(PlanCommon a, int px, int py, int v, int32_t* cx, int32_t* cy, uint32_t* n_out) {
+    uint32_t n = 0;
+    for_each_candidate(a, a.g.wrap(px), py, v, [&](int x, int y) {
+        cx[n] = x;
+        cy[n] = y;
+        ++n;
+        return true;
+    });
+    *n_out = n;
 }
 
 __global__ void plan_exact_kernel(PlanCommon a) {
@@ -627,7 +650,9 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // tile_deal_kernel) taken in order, so fetch numbers map monotonically onto the list and
         // an exhausted fetch ends every later one (refills complete out of order)
         const int t = fetch_entry(i);
+#ifdef FP_PLAN_DEBUG
         if (blockIdx.x == 5 && i < 256) g_plan_dbg[i] = globaltimer_p();
+#endif
         if (t >= 0) {
             const uint32_t tile = A.tile_list[t];
             const int tx = (int)(tile % (uint32_t)A.tiles_x), ty = (int)(tile / (uint32_t)A.tiles_x);
@@ -666,10 +691,12 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+#ifdef FP_PLAN_DEBUG
         if (blockIdx.x < 256) {
             g_plan_cta[blockIdx.x] = globaltimer_p();
             g_plan_cta[256 + blockIdx.x] = 0;
         }
+#endif
         for (int s = 0; s < PLAN_SLOTS; ++s) fetch(s);
     }
     for (int i = 0;; ++i) {
@@ -696,10 +723,12 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         // a refill racing with these reads may already have written tile = -1 for fetch i+2)
         if (s_gen[slot] != i) continue;  // fetch i already completed without this thread's help
         if (tile < 0) {
+#ifdef FP_PLAN_DEBUG
             if (blockIdx.x < 256 && (threadIdx.x & 31) == 0) {
                 atomicMax(&g_plan_cta[256 + blockIdx.x], globaltimer_p());
                 g_plan_cta[512 + blockIdx.x] = i;
             }
+#endif
             break;
         }
         // agent slot of this thread's lane group (the rotation keeps groups P-aligned)
@@ -715,7 +744,9 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
                 atomicOr(&a.sc->err, 2ull);
                 return;
             }
+#ifdef FP_PLAN_DEBUG
             if (blockIdx.x == 5 && i < 256 && g_plan_dbg[256 + i] < g_plan_dbg[i]) g_plan_dbg[256 + i] = globaltimer_p();
+#endif
         } else if (true) {
             // comparison path: each thread fills what it reads (slow; debugging only)
             const int gx0 = x0 - 8 + FP_XPAD_W, gy0 = y0 - FP_HALO;
@@ -765,10 +796,12 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
         __threadfence_block();
         if (atomicAdd(&s_done[slot], mine) + mine == cnt * P) {  // last lane of fetch i
             __threadfence_block();
+#ifdef FP_PLAN_DEBUG
             if (blockIdx.x == 5 && i < 256) {
                 g_plan_dbg[512 + i] = globaltimer_p();
                 g_plan_dbg[768 + i] = cnt;
             }
+#endif
             fetch(i + PLAN_SLOTS);
         }
     }
@@ -996,7 +1029,8 @@ int fp_plan_prepare(fp_ctx* ctx, double k_s) {
     TileArgs A;
     size_t smem;
     tile_geometry(ctx, A, smem);
-    static size_t configured = 0;
+    static size_t configured_by_device[64] = {0};  // the attribute is per device
+    size_t& configured = configured_by_device[ctx->device & 63];
     if (smem > configured) {
         FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1111,6 +1145,24 @@ int fp_choice_launch(fp_ctx* ctx, uint32_t agent, double k_s, int32_t* d_cx, int
         plane = ctx->d_plane;
     }
     choice_kernel<<<1, 1, 0, ctx->stream>>>(a, plane, ctx->PW, agent, d_cx, d_cy, d_w, d_p, d_n);
+    FP_LAUNCHED(ctx);
+    return FP_OK;
+}
+
+// choose_desired_cell(st, agent, params) for one agent given by value (planning.hpp:88-108).
+int fp_choose_one_launch(fp_ctx* ctx, uint32_t id, int px, int py, int v, int64_t step, double k_s, uint64_t seed,
+                         int32_t* d_out) {
+    if (int rc = ensure_pathmasks(ctx)) return rc;
+    PlanCommon a = make_common(ctx, k_s, seed);
+    choose_one_kernel<<<1, 1, 0, ctx->stream>>>(a, id, px, py, v, (long long)step, d_out);
+    FP_LAUNCHED(ctx);
+    return FP_OK;
+}
+
+// enumerate_candidates(st, agent) for one agent given by value (planning.hpp:23-57).
+int fp_candidates_one_launch(fp_ctx* ctx, int px, int py, int v, int32_t* d_cx, int32_t* d_cy, uint32_t* d_n) {
+    PlanCommon a = make_common(ctx, 0.0, 0);
+    candidates_one_kernel<<<1, 1, 0, ctx->stream>>>(a, px, py, v, d_cx, d_cy, d_n);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }

@@ -92,6 +92,10 @@ SIGNATURES = {
     "fp_state_hash": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "fp_get_choice": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, _i32p, _i32p, _f64p, _f32p,
                                 C.c_uint32, C.POINTER(C.c_uint32)]),
+    "fp_choose_desired": (C.c_int, [C.c_void_p, C.c_uint32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_double,
+                                    C.c_uint64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fp_enumerate_candidates": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _i32p, _i32p, C.c_uint32,
+                                          C.POINTER(C.c_uint32)]),
     "fp_movement_order": (C.c_int, [C.c_int64, C.c_uint64, C.c_int64, C.c_int, _u32p]),
     "fp_spawn_agents": (C.c_int, [C.c_int32, C.c_int32, _u8p, C.c_int64, C.c_uint64, _i32p, _i32p]),
     "fp_get_counters": (C.c_int, [C.c_void_p, C.POINTER(_Counters)]),

@@ -12,7 +12,8 @@ import pytest
 import oracle as O
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-CASES = sorted(os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(HERE, "*.npz")))
+CASES = sorted(os.path.splitext(os.path.basename(p))[0] for p in glob.glob(os.path.join(HERE, "*.npz"))
+               if not os.path.basename(p).startswith("full_"))  # full_*: tests/test_fullsize_golden.py
 
 
 def load(name):
