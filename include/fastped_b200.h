@@ -129,14 +129,6 @@ int fp_set_desired(fp_ctx* ctx, const int32_t* x, const int32_t* y);
 /* plan_phase(st, params, sched) -- engine.hpp:71-84: desired cell of every alive agent,
  * bit-identical to choose_desired_cell (planning.hpp:88-108). */
 int fp_plan(fp_ctx* ctx, double k_s, uint64_t seed);
-/* Multi-GPU x-strip decomposition of plan_phase: plans only
- * the alive agents whose x lies in [x_lo, x_hi) and sets the desired cell of every other alive
- * agent to (0, 0), so that a SUM all-reduce of the desired arrays over ranks whose strips tile
- * the grid yields plan_phase's result bit for bit.  fp_desired_device exposes the two device
- * arrays (int32[n] each, on the context's device) for that in-place collective; the motion
- * (fp_move) then runs on every rank on identical inputs. */
-int fp_plan_strip(fp_ctx* ctx, double k_s, uint64_t seed, int32_t x_lo, int32_t x_hi);
-int fp_desired_device(fp_ctx* ctx, void** dx, void** dy);
 /* move_phase(st, params) -- engine.hpp:95-135 (does not advance the step counter).
  * Exited ids (processing order) are kept for fp_get_exited. */
 int fp_move(fp_ctx* ctx, uint64_t seed, fp_step_stats* out);
@@ -155,6 +147,9 @@ int fp_get_exited(const fp_ctx* ctx, uint32_t* ids, uint32_t cap, uint32_t* n);
 int fp_get_order(const fp_ctx* ctx, uint32_t* ids, uint32_t cap, uint32_t* n);
 /* state_hash(st) -- state.hpp:80-95. */
 int fp_state_hash(const fp_ctx* ctx, uint64_t* out);
+/* state_hash of a roster given by host arrays (e.g. merged from strip ranks). */
+int fp_hash_roster(int64_t step, int64_t alive, uint32_t n, const int32_t* x, const int32_t* y, const uint8_t* alive_flags,
+                   uint64_t* out);
 
 /* Test mode: candidate list of one agent in the reference order (enumerate_candidates,
  * planning.hpp:23-57), its exact fp64 weights (planning.hpp:93-103), and the choice
@@ -181,6 +176,33 @@ int fp_spawn_agents(int32_t width, int32_t height, const uint8_t* cells, int64_t
                     uint64_t seed, int32_t* x, int32_t* y);
 
 int fp_get_counters(const fp_ctx* ctx, fp_counters* out);
+
+/* ---- Multi-GPU: x-strip decomposition of one simulation (strip.cu) ----
+ * Rank r of N owns the agents standing in columns [x_lo, x_hi) (strips tile the grid; periodic
+ * grids form a ring).  Every rank gets the same grid, field and GLOBAL roster; ids stay global.
+ * Walks that can touch another strip (and everything sharing a cell with them) are exchanged
+ * and resolved on every rank each step, so the result equals the 1-GPU run bit for bit.
+ * fp_step / fp_run on a strip context run the decomposed step; fp_plan / fp_move do not.
+ * Transports: NCCL (fp_strip_set_nccl: one process per GPU, ncclAllGather on the context's
+ * stream; libnccl.so.2 is loaded at run time), a host allgather callback
+ * (fp_strip_set_exchange: recv receives the N payloads in rank order), or all ranks in this
+ * process (fp_strips_step / fp_strips_run: device-to-device copies, e.g. virtual strips on one
+ * GPU).  Positions of agents another rank owns are stale: fp_strip_get_owned says which of a
+ * rank's fp_get_agents entries are its own.  Exits, alive counts and stats are global. */
+typedef struct {
+    char internal[128];
+} fp_nccl_id; /* ncclUniqueId */
+typedef int (*fp_allgather_fn)(void* user, const void* send, size_t bytes, void* recv);
+int fp_strip_bounds(int32_t width, int rank, int nranks, int32_t* x_lo, int32_t* x_hi);
+/* cap_deferred / cap_exits: exchange capacity per rank and step (0 = defaults sized by the roster). */
+int fp_strip_config(fp_ctx* ctx, int rank, int nranks, int32_t x_lo, int32_t x_hi, uint32_t cap_deferred,
+                    uint32_t cap_exits);
+int fp_nccl_unique_id(fp_nccl_id* out);
+int fp_strip_set_nccl(fp_ctx* ctx, const fp_nccl_id* id);
+int fp_strip_set_exchange(fp_ctx* ctx, fp_allgather_fn fn, void* user);
+int fp_strips_step(fp_ctx* const* ctxs, int n, double k_s, uint64_t seed, fp_step_stats* out);
+int fp_strips_run(fp_ctx* const* ctxs, int n, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out);
+int fp_strip_get_owned(const fp_ctx* ctx, uint8_t* owned);
 
 /* Benchmark helper: average duration (ms, CUDA events) of `iters` launches of the planning
  * kernel alone on the current state (bucketing done once, untimed). */

@@ -11,21 +11,24 @@
 
 // Agents are counted per (tile, v_max) sub-bucket, so each tile's agents come out ordered by
 // v_max and the plan kernel's warps run one ball size (mixed-v rosters otherwise diverge over
-// four unrolled variants and thrash the instruction cache).  Agents outside the planned x strip
-// [strip_lo, strip_hi) (multi-GPU decomposition) are not bucketed and get
-// desired = (0, 0), so a sum over the ranks' strips is the plan.
+// four unrolled variants and thrash the instruction cache).  On a strip rank (strip.cu) only the
+// agents it owns are planned.  Counts the planned agents (= the plan's walk records) into
+// *n_planned.
 __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* v, const uint8_t* alive,
-                                    uint32_t n, int tile_w, int tile_h, int tiles_x, uint32_t* cnt, uint32_t* tile_of,
-                                    uint32_t* slot, int strip_lo, int strip_hi, int32_t* dx, int32_t* dy) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (!alive[i]) continue;
-        const int px = g.wrap(x[i]), py = y[i];
-        if (px < strip_lo || px >= strip_hi) {
+                                    const uint8_t* owned, uint32_t n, int tile_w, int tile_h, int tiles_x,
+                                    uint32_t* cnt, uint32_t* tile_of, uint32_t* slot,
+                                    unsigned long long* n_planned) {
+    for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
+        const uint32_t i = i0 + threadIdx.x;
+        const bool take = i < n && alive[i] && (!owned || owned[i]);
+        const unsigned b = __ballot_sync(0xffffffffu, take);
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_planned, (unsigned long long)__popc(b));
+        if (i >= n) continue;
+        if (!take) {
             tile_of[i] = FP_NONE;
-            dx[i] = 0;
-            dy[i] = 0;
             continue;
         }
+        const int px = g.wrap(x[i]), py = y[i];
         const uint32_t t = ((uint32_t)(py / tile_h) * (uint32_t)tiles_x + (uint32_t)(px / tile_w)) * 5u +
                            (uint32_t)(v[i] - 1);  // v_max in 1..5
         tile_of[i] = t;
@@ -39,7 +42,7 @@ __global__ void bucket_scatter_kernel(Geo g, const int32_t* x, const int32_t* y,
                                       const uint8_t* alive, uint32_t n, const uint32_t* tile_of, const uint32_t* slot,
                                       const uint32_t* off, uint32_t* bucket, uint4* brec) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (!alive[i] || tile_of[i] == FP_NONE) continue;
+        if (tile_of[i] == FP_NONE) continue;
         const uint32_t p = off[tile_of[i]] + slot[i];
         bucket[p] = i;
         brec[p] = make_uint4(i, (uint32_t)g.wrap(x[i]), (uint32_t)y[i], v[i]);
@@ -196,9 +199,11 @@ int fp_bucket_launch(fp_ctx* ctx) {
     const uint32_t n = ctx->n;
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_sub_cnt, 0, nt * 5 * 4, s));
     const unsigned G = (unsigned)std::min<size_t>(fp_blocks(n, 256), (size_t)ctx->sm_count * 16);
-    bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, ctx->d_alive, n, ctx->tile_w,
-                                          ctx->tile_h, ctx->tiles_x, ctx->d_sub_cnt, ctx->d_flags, ctx->d_cursor_b,
-                                          ctx->strip_lo, ctx->strip_hi, ctx->d_dx, ctx->d_dy);
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_planned, 0, 8, s));
+    bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, ctx->d_alive,
+                                          ctx->st.on ? ctx->st.d_owned : nullptr, n, ctx->tile_w, ctx->tile_h,
+                                          ctx->tiles_x, ctx->d_sub_cnt, ctx->d_flags, ctx->d_cursor_b,
+                                          &ctx->d_sc->n_planned);
     FP_LAUNCHED(ctx);
     size_t need1 = 0, need2 = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, need1, ctx->d_sub_cnt, ctx->d_sub_off, (int)(nt * 5), s);

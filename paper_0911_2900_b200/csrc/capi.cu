@@ -264,6 +264,19 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->stream2) cudaStreamSynchronize(c->stream2);
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
+    if (c->st.graph_fin) cudaGraphExecDestroy(c->st.graph_fin);
+    fp_strip_nccl_destroy(c);
+    {
+        StripCtx& S = c->st;
+        void* sp[] = {S.d_owned, S.d_dplane, S.d_dflag, S.d_clist, S.d_send, S.d_recv, S.d_hkey, S.d_hres,
+                      S.d_hocc, S.d_rslot, S.d_plist, S.d_rexits, S.d_rhdr};
+        for (void* p : sp)
+            if (p) cudaFree(p);
+        if (S.h_rhdr) cudaFreeHost(S.h_rhdr);
+        if (S.h_send) cudaFreeHost(S.h_send);
+        if (S.h_recv) cudaFreeHost(S.h_recv);
+        if (S.ev) cudaEventDestroy(S.ev);
+    }
     void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_counters, c->d_temp, c->d_temp_b,
                     c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal, c->d_tile_exit, c->d_seed_items,
                     c->d_sc,
@@ -374,6 +387,10 @@ static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const ui
     c->bucket_fresh = false;
     c->rec_fresh = false;
     if (int rc = fp_ghost_occ(c)) return rc;
+    if (c->st.on) {  // a strip rank owns the alive agents standing in its columns
+        if (int rc = fp_strip_reserve(c)) return rc;
+        if (int rc = fp_strip_owned_init(c)) return rc;
+    }
     return sync_scalars(c);
 }
 
@@ -466,12 +483,17 @@ static int prepare(fp_ctx* c, double k_s) {
     if (int rc = fp_plan_prepare(c, k_s)) return rc;
     if (int rc = fp_order_reserve(c)) return rc;
     if (int rc = fp_ensure_res(c)) return rc;
+    if (int rc = fp_strip_reserve(c)) return rc;
     return FP_OK;
 }
+
+static int strip_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out);
+static int strip_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out);
 
 extern "C" int fp_plan(fp_ctx* c, double k_s, uint64_t seed) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     if (int rc = check_usable(c)) return rc;
+    if (c->st.on) return fail(c, FP_EINVAL, "plan_phase on a strip rank: the decomposed step is fp_step / fp_run");
     cudaSetDevice(c->device);
     if (c->alive == 0) return FP_OK;  // engine.hpp:73
     if (int rc = prepare(c, k_s)) return rc;
@@ -479,29 +501,6 @@ extern "C" int fp_plan(fp_ctx* c, double k_s, uint64_t seed) {
     if (int rc = fp_plan_launch(c, k_s, seed)) return rc;
     c->ctr.planned_agents += c->alive;
     return read_scalars(c);
-}
-
-extern "C" int fp_plan_strip(fp_ctx* c, double k_s, uint64_t seed, int32_t x_lo, int32_t x_hi) {
-    if (!c) return fail(nullptr, FP_EINVAL, "null context");
-    if (x_lo < 0 || x_hi > c->W || x_lo >= x_hi)
-        return fail(c, FP_EINVAL, "fp_plan_strip: need 0 <= x_lo < x_hi <= width");
-    c->strip_lo = x_lo;
-    c->strip_hi = x_hi;
-    const int rc = fp_plan(c, k_s, seed);
-    c->strip_lo = 0;
-    c->strip_hi = 0x7FFFFFFF;
-    // the desired cells will be completed by the other ranks: the plan's walk records and tile
-    // buckets cover this strip only, so the motion builds its own from the order list
-    c->rec_fresh = false;
-    c->bucket_fresh = false;
-    return rc;
-}
-
-extern "C" int fp_desired_device(fp_ctx* c, void** dx, void** dy) {
-    if (!c || !dx || !dy) return fail(c, FP_EINVAL, "null argument");
-    *dx = c->d_dx;
-    *dy = c->d_dy;
-    return FP_OK;
 }
 
 // order + motion on the main stream (API path), then the exit list in processing order.
@@ -531,6 +530,7 @@ static int move_impl(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
 extern "C" int fp_move(fp_ctx* c, uint64_t seed, fp_step_stats* out) {
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     if (int rc = check_usable(c)) return rc;
+    if (c->st.on) return fail(c, FP_EINVAL, "move_phase on a strip rank: the decomposed step is fp_step / fp_run");
     cudaSetDevice(c->device);
     return move_impl(c, seed, out);
 }
@@ -543,6 +543,7 @@ extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out)
     if (!c) return fail(nullptr, FP_EINVAL, "null context");
     if (int rc = check_usable(c)) return rc;
     cudaSetDevice(c->device);
+    if (c->st.on) return strip_step(c, k_s, seed, out);
     if (c->alive == 0 || c->n == 0) {  // engine.hpp:73: nothing to plan or move
         c->n_order = 0;
         c->n_exits = 0;
@@ -581,14 +582,17 @@ extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out)
 static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
-    c->graph_plan = c->graph_move = nullptr;
+    if (c->st.graph_fin) cudaGraphExecDestroy(c->st.graph_fin);
+    c->graph_plan = c->graph_move = c->st.graph_fin = nullptr;
+    const bool strip = c->st.on;
     cudaGraph_t g = nullptr;
     const int64_t k0 = c->ctr.kernel_launches;
     FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     int rc = FP_OK;
+    if (strip) rc = fp_strip_begin_launch(c);
     cudaEventRecord(c->ev_fork, c->stream);
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
-    rc = fp_order_launch(c, seed, c->stream2);
+    if (rc == FP_OK) rc = fp_order_launch(c, seed, c->stream2);
     cudaEventRecord(c->ev_join, c->stream2);
     if (rc == FP_OK) rc = fp_plan_launch(c, k_s, seed);
     cudaStreamWaitEvent(c->stream, c->ev_join, 0);
@@ -603,9 +607,11 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(plan)");
     g = nullptr;
     FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    rc = fp_motion_launch(c, c->bucket_fresh);  // the plan graph re-buckets every step
+    if (strip) rc = fp_strip_defer_launch(c);  // band-connected walks leave the local motion
+    if (rc == FP_OK) rc = fp_motion_launch(c, c->bucket_fresh);  // the plan graph re-buckets every step
     c->bucket_fresh = false;
-    if (rc == FP_OK) {
+    if (rc == FP_OK && strip) rc = fp_strip_pack_launch(c);
+    if (rc == FP_OK && !strip) {
         sc_step_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
         c->ctr.kernel_launches++;
     }
@@ -618,6 +624,26 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     e = cudaGraphInstantiate(&c->graph_move, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(move)");
+    if (strip) {  // after the exchange: resolve the deferred walks, global exits, ++step
+        g = nullptr;
+        FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        rc = fp_strip_resolve_launch(c);
+        if (rc == FP_OK) rc = fp_exits_sort_launch(c);
+        if (rc == FP_OK) rc = fp_ghost_occ(c);
+        if (rc == FP_OK) {
+            sc_step_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+            c->ctr.kernel_launches++;
+        }
+        e = cudaStreamEndCapture(c->stream, &g);
+        if (rc != FP_OK) {
+            if (g) cudaGraphDestroy(g);
+            return rc;
+        }
+        if (e != cudaSuccess) return fp_cuda_fail(c, e, "capture(strip)");
+        e = cudaGraphInstantiate(&c->st.graph_fin, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(strip)");
+    }
     c->launches_per_step = c->ctr.kernel_launches - k0;  // captured, not yet executed
     c->ctr.kernel_launches = k0;
     c->graph_valid = true;
@@ -638,6 +664,7 @@ extern "C" int fp_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_ru
     if (int rc = check_usable(c)) return rc;
     if (steps < 1) return fail(c, FP_EINVAL, "SimParams: steps must be >= 1");
     cudaSetDevice(c->device);
+    if (c->st.on) return strip_run(c, k_s, seed, steps, out);
     if (int rc = prepare(c, k_s)) return rc;
     if (!c->graph_valid || c->graph_ks != k_s || c->graph_seed != seed)
         if (int rc = capture(c, k_s, seed)) return rc;
@@ -682,6 +709,302 @@ extern "C" int fp_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_ru
     c->n_order = (uint32_t)c->h_sc->n_alive;
     c->n_exits = 0;  // the per-phase exit list is only kept by fp_move / fp_step
     c->ctr.planned_agents += rs.agent_updates;
+    if (out) *out = rs;
+    return FP_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU x strips
+extern "C" int fp_strip_bounds(int32_t width, int rank, int nranks, int32_t* lo, int32_t* hi) {
+    if (width < 1 || nranks < 1 || rank < 0 || rank >= nranks || !lo || !hi)
+        return fail(nullptr, FP_EINVAL, "fp_strip_bounds: need width >= 1 and 0 <= rank < nranks");
+    *lo = (int32_t)((int64_t)rank * width / nranks);
+    *hi = (int32_t)((int64_t)(rank + 1) * width / nranks);
+    return FP_OK;
+}
+
+extern "C" int fp_strip_config(fp_ctx* c, int rank, int nranks, int32_t x_lo, int32_t x_hi, uint32_t cap_def,
+                               uint32_t cap_exit) {
+    if (!c) return fail(nullptr, FP_EINVAL, "null context");
+    if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks)
+        return fail(c, FP_EINVAL, "fp_strip_config: need 1 <= nranks <= 64 and 0 <= rank < nranks");
+    if (x_lo < 0 || x_hi > c->W || x_lo >= x_hi) return fail(c, FP_EINVAL, "fp_strip_config: need 0 <= x_lo < x_hi <= width");
+    if (c->boundary == FP_BOUNDARY_PERIODIC_X && c->W < 16)
+        return fail(c, FP_EINVAL, "fp_strip_config: periodic grids narrower than 16 columns are not decomposed");
+    StripCtx& S = c->st;
+    S.on = true;
+    S.rank = rank;
+    S.nranks = nranks;
+    S.x_lo = x_lo;
+    S.x_hi = x_hi;
+    S.cap_def_req = cap_def;
+    S.cap_exit_req = cap_exit;
+    S.cap_agents = 0;  // re-reserve with the new sizes
+    if (!S.ev) FP_CUDA(c, cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming));
+    c->graph_valid = false;
+    cudaSetDevice(c->device);
+    if (int rc = fp_strip_reserve(c)) return rc;
+    if (int rc = fp_strip_owned_init(c)) return rc;
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+extern "C" int fp_strip_set_nccl(fp_ctx* c, const fp_nccl_id* id) {
+    if (!c || !id) return fail(c, FP_EINVAL, "null argument");
+    if (!c->st.on) return fail(c, FP_EINVAL, "fp_strip_set_nccl: configure the strip first (fp_strip_config)");
+    fp_strip_nccl_destroy(c);
+    if (int rc = fp_strip_nccl_init(c, id)) return rc;
+    c->st.transport = FP_STRIP_NCCL;
+    c->st.cap_agents = 0;
+    return fp_strip_reserve(c);
+}
+
+extern "C" int fp_strip_set_exchange(fp_ctx* c, fp_allgather_fn fn, void* user) {
+    if (!c || !fn) return fail(c, FP_EINVAL, "null argument");
+    if (!c->st.on) return fail(c, FP_EINVAL, "fp_strip_set_exchange: configure the strip first (fp_strip_config)");
+    c->st.transport = FP_STRIP_HOST;
+    c->st.host_fn = fn;
+    c->st.host_user = user;
+    c->st.cap_agents = 0;  // pinned staging buffers
+    cudaSetDevice(c->device);
+    return fp_strip_reserve(c);
+}
+
+extern "C" int fp_strip_get_owned(const fp_ctx* cc, uint8_t* owned) {
+    fp_ctx* c = const_cast<fp_ctx*>(cc);
+    if (!c || !owned) return fail(c, FP_EINVAL, "null argument");
+    if (!c->st.on) return fail(c, FP_EINVAL, "not a strip context");
+    cudaSetDevice(c->device);
+    if (c->n) FP_CUDA(c, cudaMemcpyAsync(owned, c->st.d_owned, c->n, cudaMemcpyDeviceToHost, c->stream));
+    FP_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FP_OK;
+}
+
+// Everything a strip step needs, outside any capture; (re)captures the three step graphs.
+static int strip_ready(fp_ctx* c, double k_s, uint64_t seed) {
+    if (!c->st.on) return fail(c, FP_EINVAL, "not a strip context");
+    if (!fp_plan_tiled(c)) return fail(c, FP_EINVAL, "strip decomposition needs the tiled planning path");
+    if (int rc = prepare(c, k_s)) return rc;
+    if (!c->graph_valid || c->graph_ks != k_s || c->graph_seed != seed)
+        if (int rc = capture(c, k_s, seed)) return rc;
+    return sync_scalars(c);
+}
+
+static int strip_finish_stats(fp_ctx* c, int64_t alive0, fp_step_stats* out) {
+    if (int rc = read_scalars(c)) return rc;
+    c->ctr.planned_agents += alive0;
+    c->n_order = (uint32_t)c->h_sc->n_alive;
+    c->n_exits = (uint32_t)c->h_sc->n_exits;
+    c->last_displacement = (int64_t)c->h_sc->disp;
+    c->last_dx = (int64_t)c->h_sc->step_dx;
+    if (int rc = fp_exits_finish(c)) return rc;
+    if (out) {
+        out->alive = c->alive;
+        out->exited = alive0 - c->alive;
+        out->displacement_cells = c->last_displacement;
+    }
+    return FP_OK;
+}
+
+static int strip_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out) {
+    if (c->st.transport != FP_STRIP_NCCL && c->st.transport != FP_STRIP_HOST)
+        return fail(c, FP_EINVAL, "strip step: no exchange transport (fp_strip_set_nccl / fp_strip_set_exchange), "
+                                  "or drive all ranks with fp_strips_step");
+    if (int rc = strip_ready(c, k_s, seed)) return rc;
+    const int64_t alive0 = c->alive;
+    FP_CUDA(c, cudaGraphLaunch(c->graph_plan, c->stream));
+    FP_CUDA(c, cudaGraphLaunch(c->graph_move, c->stream));
+    if (int rc = fp_strip_exchange(c)) return rc;
+    FP_CUDA(c, cudaGraphLaunch(c->st.graph_fin, c->stream));
+    c->ctr.kernel_launches += c->launches_per_step;
+    return strip_finish_stats(c, alive0, out);
+}
+
+// fp_run on one strip rank (NCCL or host transport): the three graphs per step with the
+// exchange between, CUDA events between the plan and the rest of the step.
+static int strip_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out) {
+    if (c->st.transport != FP_STRIP_NCCL && c->st.transport != FP_STRIP_HOST)
+        return fail(c, FP_EINVAL, "strip run: no exchange transport");
+    if (int rc = strip_ready(c, k_s, seed)) return rc;
+    run_begin_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+    FP_LAUNCHED(c);
+    std::vector<cudaEvent_t> ev((size_t)2 * steps + 1);
+    for (auto& e : ev) FP_CUDA(c, cudaEventCreate(&e));
+    for (int s = 0; s < steps; ++s) {
+        cudaEventRecord(ev[2 * s], c->stream);
+        FP_CUDA(c, cudaGraphLaunch(c->graph_plan, c->stream));
+        cudaEventRecord(ev[2 * s + 1], c->stream);
+        FP_CUDA(c, cudaGraphLaunch(c->graph_move, c->stream));
+        if (int rc = fp_strip_exchange(c)) return rc;
+        FP_CUDA(c, cudaGraphLaunch(c->st.graph_fin, c->stream));
+    }
+    cudaEventRecord(ev[2 * steps], c->stream);
+    FP_CUDA(c, cudaEventSynchronize(ev[2 * steps]));
+    c->ctr.kernel_launches += (int64_t)steps * c->launches_per_step;
+    fp_run_stats rs{};
+    float plan_ms = 0, move_ms = 0, tot = 0;
+    for (int s = 0; s < steps; ++s) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ev[2 * s], ev[2 * s + 1]);
+        cudaEventElapsedTime(&b, ev[2 * s + 1], ev[2 * s + 2]);
+        plan_ms += a;
+        move_ms += b;
+    }
+    cudaEventElapsedTime(&tot, ev[0], ev[2 * steps]);
+    for (auto& e : ev) cudaEventDestroy(e);
+    if (int rc = read_scalars(c)) return rc;
+    rs.wall_time_s = tot * 1e-3;
+    rs.plan_time_s = plan_ms * 1e-3;
+    rs.move_time_s = move_ms * 1e-3;
+    rs.steps = steps;
+    rs.exited = (int64_t)c->h_sc->tot_exits;
+    rs.displacement_cells = (int64_t)c->h_sc->tot_disp;
+    rs.agent_updates = (int64_t)c->h_sc->tot_updates;
+    rs.alive = c->alive;
+    c->n_order = (uint32_t)c->h_sc->n_alive;
+    c->n_exits = 0;
+    c->ctr.planned_agents += rs.agent_updates;
+    if (out) *out = rs;
+    return FP_OK;
+}
+
+// All ranks in this process (the local transport): every rank's payload is copied into every
+// rank's receive buffer (peer copies across devices, plain device copies on one device).
+static int strips_check(fp_ctx* const* cs, int n) {
+    if (!cs || n < 1) return fail(nullptr, FP_EINVAL, "fp_strips_step: need at least one context");
+    for (int r = 0; r < n; ++r) {
+        if (!cs[r] || !cs[r]->st.on || cs[r]->st.nranks != n || cs[r]->st.rank != r)
+            return fail(cs[r], FP_EINVAL, "fp_strips_step: context r must be strip rank r of n");
+        if (int rc = check_usable(cs[r])) return rc;
+        cs[r]->st.transport = FP_STRIP_LOCAL;
+    }
+    return FP_OK;
+}
+
+static int strips_exchange_local(fp_ctx* const* cs, int n) {
+    // phase 1: every rank's header (counts) to every rank, then read them on the host
+    for (int q = 0; q < n; ++q) {
+        cudaSetDevice(cs[q]->device);
+        FP_CUDA(cs[q], cudaEventRecord(cs[q]->st.ev, cs[q]->stream));
+    }
+    const size_t hb = fp_strip_hdr_bytes();
+    for (int q = 0; q < n; ++q) {
+        fp_ctx* c = cs[q];
+        cudaSetDevice(c->device);
+        for (int p = 0; p < n; ++p) {
+            FP_CUDA(c, cudaStreamWaitEvent(c->stream, cs[p]->st.ev, 0));
+            FP_CUDA(c, cudaMemcpyPeerAsync((char*)c->st.d_rhdr + p * hb, c->device, cs[p]->st.d_send, cs[p]->device, hb,
+                                           c->stream));
+        }
+    }
+    fp_ctx* c0 = cs[0];
+    cudaSetDevice(c0->device);
+    FP_CUDA(c0, cudaMemcpyAsync(c0->st.h_rhdr, c0->st.d_rhdr, hb * n, cudaMemcpyDeviceToHost, c0->stream));
+    FP_CUDA(c0, cudaStreamSynchronize(c0->stream));
+    // phase 2: exactly the used records of every rank into every rank's slot for it
+    for (int q = 0; q < n; ++q) {
+        fp_ctx* c = cs[q];
+        cudaSetDevice(c->device);
+        for (int p = 0; p < n; ++p) {
+            const unsigned long long* h = c0->st.h_rhdr + (size_t)p * (hb / 8);
+            const size_t nd = std::min<unsigned long long>(h[0], c->st.cap_def);
+            const size_t ne = std::min<unsigned long long>(h[1], c->st.cap_exit);
+            char* dst = (char*)c->st.d_recv + (size_t)p * c->st.xbytes;
+            const char* src = (const char*)cs[p]->st.d_send;
+            if (nd)
+                FP_CUDA(c, cudaMemcpyPeerAsync(dst + fp_strip_def_off(), c->device, src + fp_strip_def_off(),
+                                               cs[p]->device, nd * 32, c->stream));
+            if (ne)
+                FP_CUDA(c, cudaMemcpyPeerAsync(dst + fp_strip_exit_off(c), c->device, src + fp_strip_exit_off(cs[p]),
+                                               cs[p]->device, ne * 8, c->stream));
+        }
+    }
+    // a rank's send buffer is rewritten next step only after every rank copied it
+    for (int q = 0; q < n; ++q) {
+        cudaSetDevice(cs[q]->device);
+        FP_CUDA(cs[q], cudaEventRecord(cs[q]->st.ev, cs[q]->stream));
+    }
+    for (int q = 0; q < n; ++q) {
+        cudaSetDevice(cs[q]->device);
+        for (int p = 0; p < n; ++p) FP_CUDA(cs[q], cudaStreamWaitEvent(cs[q]->stream, cs[p]->st.ev, 0));
+    }
+    return FP_OK;
+}
+
+extern "C" int fp_strips_step(fp_ctx* const* cs, int n, double k_s, uint64_t seed, fp_step_stats* out) {
+    if (int rc = strips_check(cs, n)) return rc;
+    std::vector<int64_t> alive0(n);
+    for (int r = 0; r < n; ++r) {
+        fp_ctx* c = cs[r];
+        cudaSetDevice(c->device);
+        if (c->st.xbytes != cs[0]->st.xbytes) return fail(c, FP_EINVAL, "fp_strips_step: ranks disagree on exchange sizes");
+        if (int rc = strip_ready(c, k_s, seed)) return rc;
+        alive0[r] = c->alive;
+        FP_CUDA(c, cudaGraphLaunch(c->graph_plan, c->stream));
+        FP_CUDA(c, cudaGraphLaunch(c->graph_move, c->stream));
+    }
+    if (int rc = strips_exchange_local(cs, n)) return rc;
+    for (int r = 0; r < n; ++r) {
+        cudaSetDevice(cs[r]->device);
+        FP_CUDA(cs[r], cudaGraphLaunch(cs[r]->st.graph_fin, cs[r]->stream));
+        cs[r]->ctr.kernel_launches += cs[r]->launches_per_step;
+    }
+    for (int r = 0; r < n; ++r) {
+        cudaSetDevice(cs[r]->device);
+        if (int rc = strip_finish_stats(cs[r], alive0[r], r == 0 ? out : nullptr)) return rc;
+    }
+    return FP_OK;
+}
+
+extern "C" int fp_strips_run(fp_ctx* const* cs, int n, double k_s, uint64_t seed, int32_t steps, fp_run_stats* out) {
+    if (int rc = strips_check(cs, n)) return rc;
+    if (steps < 1) return fail(cs[0], FP_EINVAL, "SimParams: steps must be >= 1");
+    std::vector<cudaEvent_t> e0(n), e1(n);
+    for (int r = 0; r < n; ++r) {
+        fp_ctx* c = cs[r];
+        cudaSetDevice(c->device);
+        if (int rc = strip_ready(c, k_s, seed)) return rc;
+        run_begin_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+        FP_LAUNCHED(c);
+        FP_CUDA(c, cudaEventCreate(&e0[r]));
+        FP_CUDA(c, cudaEventCreate(&e1[r]));
+        cudaEventRecord(e0[r], c->stream);
+    }
+    for (int s = 0; s < steps; ++s) {
+        for (int r = 0; r < n; ++r) {
+            cudaSetDevice(cs[r]->device);
+            FP_CUDA(cs[r], cudaGraphLaunch(cs[r]->graph_plan, cs[r]->stream));
+            FP_CUDA(cs[r], cudaGraphLaunch(cs[r]->graph_move, cs[r]->stream));
+        }
+        if (int rc = strips_exchange_local(cs, n)) return rc;
+        for (int r = 0; r < n; ++r) {
+            cudaSetDevice(cs[r]->device);
+            FP_CUDA(cs[r], cudaGraphLaunch(cs[r]->st.graph_fin, cs[r]->stream));
+        }
+    }
+    float tmax = 0;
+    for (int r = 0; r < n; ++r) {
+        fp_ctx* c = cs[r];
+        cudaSetDevice(c->device);
+        cudaEventRecord(e1[r], c->stream);
+        FP_CUDA(c, cudaEventSynchronize(e1[r]));
+        float t = 0;
+        cudaEventElapsedTime(&t, e0[r], e1[r]);
+        tmax = std::max(tmax, t);
+        cudaEventDestroy(e0[r]);
+        cudaEventDestroy(e1[r]);
+        c->ctr.kernel_launches += (int64_t)steps * c->launches_per_step;
+        if (int rc = read_scalars(c)) return rc;
+        c->n_order = (uint32_t)c->h_sc->n_alive;
+        c->n_exits = 0;
+    }
+    fp_ctx* c = cs[0];
+    fp_run_stats rs{};
+    rs.wall_time_s = tmax * 1e-3;  // max over ranks (every rank's stream, CUDA events)
+    rs.steps = steps;
+    rs.exited = (int64_t)c->h_sc->tot_exits;
+    rs.displacement_cells = (int64_t)c->h_sc->tot_disp;
+    rs.agent_updates = (int64_t)c->h_sc->tot_updates;
+    rs.alive = c->alive;
     if (out) *out = rs;
     return FP_OK;
 }
@@ -766,6 +1089,26 @@ extern "C" int fp_state_hash(const fp_ctx* cc, uint64_t* out) {
     mix((uint64_t)c->step);
     mix((uint64_t)c->alive);
     for (uint32_t i = 0; i < c->n; ++i) {
+        mix(i);
+        mix((uint32_t)x[i]);
+        mix((uint32_t)y[i]);
+        mix(a[i] ? 1 : 0);
+    }
+    *out = h;
+    return FP_OK;
+}
+
+extern "C" int fp_hash_roster(int64_t step, int64_t alive, uint32_t n, const int32_t* x, const int32_t* y,
+                              const uint8_t* a, uint64_t* out) {
+    if (!out || (n && (!x || !y || !a))) return fail(nullptr, FP_EINVAL, "null argument");
+    uint64_t h = 14695981039346656037ULL;  // state.hpp:80-95
+    auto mix = [&h](uint64_t v) {
+        h ^= v;
+        h *= 1099511628211ULL;
+    };
+    mix((uint64_t)step);
+    mix((uint64_t)alive);
+    for (uint32_t i = 0; i < n; ++i) {
         mix(i);
         mix((uint32_t)x[i]);
         mix((uint32_t)y[i]);

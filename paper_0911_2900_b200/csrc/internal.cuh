@@ -136,6 +136,43 @@ struct DevScalars {
     unsigned long long chk_max[64];  // diagnostics: longest full check of round r (SM clocks)
     unsigned long long chk_cnt[64];  //   full checks in round r
     unsigned long long p1_max[64];   //   longest pass-1 loop of a thread in round r (SM clocks)
+    unsigned long long n_planned;    // agents the plan bucketed this step (= records in rec0)
+    unsigned long long strip_nc;     // strip mode: contended walks listed for the deferral closure
+    unsigned long long strip_rexits; // strip mode: exits of the resolved (deferred) walks
+    unsigned long long strip_rhops;  // strip mode: hops | dx << 32 of the resolved walks
+};
+
+// x-strip decomposition of one simulation over several GPUs (strip.cu).
+#define FP_STRIP_NONE 0
+#define FP_STRIP_HOST 1   // host callback allgather (fp_strip_set_exchange)
+#define FP_STRIP_NCCL 2   // ncclAllGather on the context's stream (fp_strip_set_nccl)
+#define FP_STRIP_LOCAL 3  // every rank's context in this process (fp_strips_step / fp_strips_run)
+struct StripCtx {
+    bool on = false;
+    int rank = 0, nranks = 1, x_lo = 0, x_hi = 0;
+    int transport = FP_STRIP_NONE;
+    uint8_t* d_owned = nullptr;     // agent stands in this strip (alive and owned)
+    uint32_t* d_dplane = nullptr;   // deferred footprint cells (bitplane)
+    uint8_t* d_dflag = nullptr;     // per plan record: deferred
+    uint32_t* d_clist = nullptr;    // contended plan records (closure candidates)
+    void* d_send = nullptr;         // this rank's payload (header, deferred records, local exits)
+    void* d_recv = nullptr;         // every rank's payload
+    void* h_send = nullptr;         // pinned staging (host transport)
+    void* h_recv = nullptr;
+    size_t xbytes = 0;
+    uint32_t cap_def = 0, cap_exit = 0, cap_def_req = 0, cap_exit_req = 0, cap_agents = 0, owned_cap = 0;
+    uint64_t cap_total = 0;         // deferred records of all ranks the resolver takes
+    uint32_t nslots = 0;            // resolver cell hash slots (power of two)
+    uint32_t *d_hkey = nullptr, *d_hres = nullptr, *d_rslot = nullptr, *d_plist = nullptr;
+    uint8_t* d_hocc = nullptr;
+    unsigned long long* d_rexits = nullptr;
+    unsigned long long* d_rhdr = nullptr;  // every rank's payload header (counts)
+    unsigned long long* h_rhdr = nullptr;
+    fp_allgather_fn host_fn = nullptr;
+    void* host_user = nullptr;
+    void* nccl_comm = nullptr;
+    cudaEvent_t ev = nullptr;       // end of the send payload (local transport)
+    cudaGraphExec_t graph_fin = nullptr;
 };
 
 struct fp_ctx {
@@ -165,7 +202,6 @@ struct fp_ctx {
     CUtensorMap tmap_occ;            // TMA descriptor of the occupancy bitplane (16-word box)
     CUtensorMap tmap_wall;           // the same box over the wall bitplane (line-of-sight masks)
     int tile_w = 0, tile_h = 0;      // plan tile (cells)
-    int strip_lo = 0, strip_hi = 0x7FFFFFFF;  // x range planned (fp_plan_strip; full otherwise)
     int tiles_x = 0, tiles_y = 0;
     bool tiles_ok = false;           // tiled fast path usable for this grid
     int use_tma = 1;                 // FP_NO_TMA=1 stages plan tiles with plain loads
@@ -250,6 +286,7 @@ struct fp_ctx {
     int64_t launches_per_step = 0;  // kernels in one replay of the two step graphs
 
     fp_counters ctr{};
+    StripCtx st;
 };
 
 // -------------------------------------------------------------------------- error helpers
@@ -298,4 +335,18 @@ int fp_ensure_temp(fp_ctx* ctx, size_t bytes);
 int fp_ensure_res(fp_ctx* ctx);
 int fp_order_reserve(fp_ctx* ctx);                                    // order.cu
 int fp_plan_prepare(fp_ctx* ctx, double k_s);                         // plan.cu
+bool fp_plan_tiled(const fp_ctx* ctx);
 int fp_bucket_reserve(fp_ctx* ctx);                                   // bucket.cu
+int fp_exits_sort_launch(fp_ctx* ctx);                                // move.cu
+int fp_strip_reserve(fp_ctx* ctx);                                    // strip.cu
+int fp_strip_begin_launch(fp_ctx* ctx);
+int fp_strip_defer_launch(fp_ctx* ctx);
+int fp_strip_pack_launch(fp_ctx* ctx);
+int fp_strip_resolve_launch(fp_ctx* ctx);
+int fp_strip_owned_init(fp_ctx* ctx);
+int fp_strip_exchange(fp_ctx* ctx);
+size_t fp_strip_def_off();
+size_t fp_strip_exit_off(const fp_ctx* ctx);
+size_t fp_strip_hdr_bytes();
+int fp_strip_nccl_init(fp_ctx* ctx, const fp_nccl_id* id);
+void fp_strip_nccl_destroy(fp_ctx* ctx);

@@ -1373,6 +1373,12 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     return fp_ghost_occ(ctx);
 }
 
+int fp_exits_sort_launch(fp_ctx* ctx) {
+    exits_sort_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_exits, ctx->d_sc);
+    FP_LAUNCHED(ctx);
+    return FP_OK;
+}
+
 // Sorts the exit records of the last phase by rank (processing order) for fp_get_exited.
 int fp_exits_finish(fp_ctx* ctx) {
     const uint32_t ne = ctx->n_exits;

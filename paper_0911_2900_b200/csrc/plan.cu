@@ -91,7 +91,6 @@ struct PlanCommon {
     double k_s;
     uint64_t seed;
     DevScalars* sc;
-    int strip_lo, strip_hi;  // planned x range (full grid unless fp_plan_strip)
 };
 
 __device__ __forceinline__ bool occ_bit(const uint32_t* occ, const Geo& g, int x, int y) {
@@ -232,12 +231,6 @@ __global__ void candidates_one_kernel(PlanCommon a, int px, int py, int v, int32
 __global__ void plan_exact_kernel(PlanCommon a) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n || !a.alive[i]) return;
-    const int px = a.g.wrap(a.x[i]);
-    if (px < a.strip_lo || px >= a.strip_hi) {  // another rank's strip (bucket.cu)
-        a.dx[i] = 0;
-        a.dy[i] = 0;
-        return;
-    }
     int cx, cy;
     choose_exact(a, i, (uint64_t)a.sc->step, &cx, &cy);
     a.dx[i] = cx;
@@ -955,8 +948,6 @@ static PlanCommon make_common(fp_ctx* ctx, double k_s, uint64_t seed) {
     a.k_s = k_s;
     a.seed = seed;
     a.sc = ctx->d_sc;
-    a.strip_lo = ctx->strip_lo;
-    a.strip_hi = ctx->strip_hi;
     return a;
 }
 
@@ -964,6 +955,8 @@ static bool tiled_ok(const fp_ctx* ctx) {
     // the tile frame resolves the periodic seam through ghost columns: needs 2*5+1 distinct columns
     return !(ctx->boundary == FP_BOUNDARY_PERIODIC_X && ctx->W < 16);
 }
+
+bool fp_plan_tiled(const fp_ctx* ctx) { return tiled_ok(ctx); }
 
 int fp_plan_exact_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     if (ctx->n == 0) return FP_OK;

@@ -1,8 +1,17 @@
-"""Multi-GPU plumbing of the benchmark: one process per GPU (torchrun), each rank runs its own
-replica of the workload; the job's throughput is the sum of the ranks' agent
-updates over the slowest rank's device time."""
+"""Multi-GPU plumbing: one process per GPU (torchrun), torch.distributed for the rendezvous.
+
+The simulation itself is decomposed in the C library (strip.cu): each rank owns an
+x-strip of the grid and exchanges, once per step, the walks that can touch another strip.  This
+module only wires a rank's context to its transport:
+  * NCCL (one process per GPU): rank 0 makes the ncclUniqueId, torch.distributed broadcasts it,
+    and the library runs ncclAllGather on its own stream -- no Python in the step;
+  * host (e.g. gloo on CPU tensors): a Python allgather callback, used by the tests to run two
+    ranks on one GPU without their kernels waiting on each other.
+`aggregate` is the benchmark's max-over-ranks time / sum-over-ranks work reduction.
+"""
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -21,55 +30,38 @@ def aggregate(wall_s: float, updates: float, device: torch.device | None = None)
     return float(mx[0]), float(sm[1])
 
 
-# ----------------------------------------------------------------- x-strip decomposition
-# SURVEY 8e / DESIGN.md 6: rank r plans the agents standing in columns [x_lo, x_hi) of the grid
-# (fp_plan_strip; the others' desired cells are zeroed), one SUM all-reduce over NVLink
-# completes every rank's desired-cell arrays (each agent is planned by exactly one rank), and
-# the motion -- a sequential walk in one global order -- runs on every rank on identical
-# inputs, so every rank holds the whole, bit-identical state and nothing migrates.
-
 def strip_bounds(width: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous columns of rank `rank` out of `world` near-equal strips."""
+    """Columns [lo, hi) of rank `rank` out of `world` near-equal strips (fp_strip_bounds)."""
     return rank * width // world, (rank + 1) * width // world
 
 
-class _DeviceArray:
-    """Zero-copy view of an engine-owned device array (for torch.distributed collectives)."""
+def gloo_allgather(group=None):
+    """A host-transport allgather over torch.distributed CPU tensors (gloo)."""
+    def ag(send: memoryview, recv: memoryview):
+        world = dist.get_world_size(group)
+        src = torch.frombuffer(bytearray(send), dtype=torch.uint8)
+        out = torch.empty(world * len(send), dtype=torch.uint8)
+        dist.all_gather_into_tensor(out, src, group=group)
+        recv[:] = memoryview(out.numpy()).cast("B")
+    return ag
 
-    def __init__(self, ptr: int, n: int, typestr: str = "<i4"):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+def strip_rank(grid, field, roster, device: int, transport: str = "nccl", **kw):
+    """This process's StripRank of the default process group (rank r owns strip r)."""
+    from . import fastped as fp
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if transport == "nccl":
+        obj = [fp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return fp.StripRank(grid, field, roster, rank, world, device, nccl_id=obj[0], **kw)
+    return fp.StripRank(grid, field, roster, rank, world, device, exchange=gloo_allgather(), **kw)
 
 
-def device_int32(ptr: int, n: int) -> torch.Tensor:
-    return torch.as_tensor(_DeviceArray(ptr, n), device="cuda")
-
-
-class StripStepper:
-    """step()/run() of one simulation decomposed over the ranks of the default process group."""
-
-    def __init__(self, st, rank: int | None = None, world: int | None = None):
-        self.st = st
-        self.rank = dist.get_rank() if rank is None else rank
-        self.world = dist.get_world_size() if world is None else world
-        self.x_lo, self.x_hi = strip_bounds(st.grid.width, self.rank, self.world)
-
-    def combine(self):
-        """SUM all-reduce of the desired-cell arrays (in place, on the engine's device memory)."""
-        if self.world == 1:
-            return
-        dxp, dyp = self.st.desired_device()
-        n = self.st.n
-        if n == 0:
-            return
-        dx, dy = device_int32(dxp, n), device_int32(dyp, n)
-        dist.all_reduce(dx, op=dist.ReduceOp.SUM)
-        dist.all_reduce(dy, op=dist.ReduceOp.SUM)
-        torch.cuda.current_stream().synchronize()  # the engine's stream reads them next
-
-    def step(self, params):
-        from . import fastped as fp
-        self.st.plan_strip(params.k_s, params.seed, self.x_lo, self.x_hi)
-        self.combine()
-        out = fp.move_phase(self.st, params)
-        self.st.step = self.st.step + 1
-        return fp.StepStats(self.st.alive, len(out.exited), out.displacement_cells)
+def gather_state(st) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """The whole roster (x, y, alive) on every rank, each agent from the rank that owns it."""
+    from . import fastped as fp
+    x, y, a = st.agents()
+    o = st.owned()
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, (x.copy(), y.copy(), a.copy(), o.copy()))
+    return fp.merge_strip_agents(parts)

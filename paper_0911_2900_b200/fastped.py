@@ -79,8 +79,6 @@ SIGNATURES = {
     "fp_set_potential": (C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     "fp_set_desired": (C.c_int, [C.c_void_p, _i32p, _i32p]),
     "fp_plan": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64]),
-    "fp_plan_strip": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.c_int32]),
-    "fp_desired_device": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "fp_move": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(_StepStats)]),
     "fp_step": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.POINTER(_StepStats)]),
     "fp_run": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.POINTER(_RunStats)]),
@@ -90,6 +88,7 @@ SIGNATURES = {
     "fp_get_exited": (C.c_int, [C.c_void_p, _u32p, C.c_uint32, C.POINTER(C.c_uint32)]),
     "fp_get_order": (C.c_int, [C.c_void_p, _u32p, C.c_uint32, C.POINTER(C.c_uint32)]),
     "fp_state_hash": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "fp_hash_roster": (C.c_int, [C.c_int64, C.c_int64, C.c_uint32, _i32p, _i32p, _u8p, C.POINTER(C.c_uint64)]),
     "fp_get_choice": (C.c_int, [C.c_void_p, C.c_uint32, C.c_double, _i32p, _i32p, _f64p, _f32p,
                                 C.c_uint32, C.POINTER(C.c_uint32)]),
     "fp_choose_desired": (C.c_int, [C.c_void_p, C.c_uint32, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_double,
@@ -100,6 +99,15 @@ SIGNATURES = {
     "fp_spawn_agents": (C.c_int, [C.c_int32, C.c_int32, _u8p, C.c_int64, C.c_uint64, _i32p, _i32p]),
     "fp_get_counters": (C.c_int, [C.c_void_p, C.POINTER(_Counters)]),
     "fp_time_plan_kernel": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64, C.c_int32, C.POINTER(C.c_double)]),
+    # multi-GPU x strips (strip.cu)
+    "fp_strip_bounds": (C.c_int, [C.c_int32, C.c_int, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "fp_strip_config": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int32, C.c_int32, C.c_uint32, C.c_uint32]),
+    "fp_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "fp_strip_set_nccl": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "fp_strip_set_exchange": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "fp_strips_step": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.POINTER(_StepStats)]),
+    "fp_strips_run": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.c_int32, C.POINTER(_RunStats)]),
+    "fp_strip_get_owned": (C.c_int, [C.c_void_p, _u8p]),
 }
 
 _lib = None
@@ -456,16 +464,6 @@ class SimState:
         k = n.value
         return cx[:k].copy(), cy[:k].copy(), w[:k].copy(), p[:k].copy()
 
-    def plan_strip(self, k_s: float, seed: int, x_lo: int, x_hi: int):
-        """plan_phase restricted to agents with x in [x_lo, x_hi); the others get desired (0, 0)."""
-        _check(library().fp_plan_strip(self._ctx, k_s, seed, x_lo, x_hi), self._ctx)
-
-    def desired_device(self):
-        """Device addresses of the desired x / y arrays (int32[n]) for an in-place collective."""
-        dx, dy = C.c_void_p(), C.c_void_p()
-        _check(library().fp_desired_device(self._ctx, C.byref(dx), C.byref(dy)), self._ctx)
-        return dx.value, dy.value
-
     def time_plan_kernel(self, k_s: float, seed: int, iters: int = 10) -> float:
         """Average plan-kernel launch duration in ms (CUDA events), for the roofline."""
         ms = C.c_double()
@@ -542,3 +540,151 @@ def cuda_available() -> bool:
         return bool(torch.cuda.is_available())
     except Exception:
         return False
+
+
+# ---------------------------------------------------------------------------------- x strips
+# One simulation decomposed over N x-strips (strip.cu): rank r owns
+# the agents standing in columns strip_bounds(W, r, N); the step equals the 1-GPU step bit for
+# bit.  StripSet drives all ranks from this process (device-to-device exchange: virtual strips
+# on one GPU, or one context per GPU); StripRank is one rank of a multi-process job whose
+# exchange is NCCL (one process per GPU) or a host allgather callback (e.g. torch gloo).
+
+def strip_bounds(width: int, rank: int, nranks: int):
+    lo, hi = C.c_int32(), C.c_int32()
+    _check(library().fp_strip_bounds(width, rank, nranks, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+class StripRank(SimState):
+    """One strip rank: the global grid, field and roster, plus its strip.  `exchange` is
+    "nccl" (nccl_id: 128 bytes from nccl_unique_id(), shared by the ranks) or a Python callable
+    allgather(send: bytes-like memoryview, recv: memoryview of N * len(send)) for the host
+    transport."""
+
+    def __init__(self, grid: Grid, field, rost: Roster, rank: int, nranks: int, device: int = 0,
+                 exchange=None, nccl_id: Optional[bytes] = None, cap_deferred: int = 0, cap_exits: int = 0,
+                 x_bounds=None):
+        super().__init__(grid, field, rost, device)
+        self.rank, self.nranks = rank, nranks
+        lo, hi = x_bounds if x_bounds is not None else strip_bounds(grid.width, rank, nranks)
+        self.x_lo, self.x_hi = lo, hi
+        L = library()
+        _check(L.fp_strip_config(self._ctx, rank, nranks, lo, hi, cap_deferred, cap_exits), self._ctx)
+        self._cb = None
+        if nccl_id is not None:
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+            _check(L.fp_strip_set_nccl(self._ctx, buf), self._ctx)
+        elif exchange is not None:
+            AG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+            def _cb(user, send, nbytes, recv):
+                try:
+                    exchange(memoryview((C.c_char * nbytes).from_address(send)).cast("B"),
+                             memoryview((C.c_char * (nbytes * nranks)).from_address(recv)).cast("B"))
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported through the status code
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+
+            self._cb = AG(_cb)
+            _check(L.fp_strip_set_exchange(self._ctx, C.cast(self._cb, C.c_void_p), None), self._ctx)
+
+    def owned(self) -> np.ndarray:
+        o = np.empty(max(self.n, 1), np.uint8)
+        _check(library().fp_strip_get_owned(self._ctx, o), self._ctx)
+        return o[: self.n]
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(library().fp_nccl_unique_id(buf))
+    return buf.raw
+
+
+def merge_strip_agents(parts):
+    """(x, y, alive) of the whole roster from every rank's (x, y, alive, owned): each agent from
+    the rank that owns it (alive or exited there); agents no rank owns (exited in a resolved
+    walk, or dead from the start) hold identical positions on every rank."""
+    x, y, a, _ = (np.array(v) for v in parts[0])
+    for px, py, pa, po in parts:
+        sel = po.astype(bool)
+        x[sel], y[sel], a[sel] = px[sel], py[sel], pa[sel]
+    return x, y, a
+
+
+def hash_roster(step: int, alive_count: int, x, y, a) -> int:
+    """state_hash (state.hpp:80-95) of a roster given as host arrays."""
+    h = C.c_uint64()
+    n = len(x)
+    x = np.ascontiguousarray(x, np.int32) if n else np.zeros(1, np.int32)
+    y = np.ascontiguousarray(y, np.int32) if n else np.zeros(1, np.int32)
+    a = np.ascontiguousarray(a, np.uint8) if n else np.zeros(1, np.uint8)
+    _check(library().fp_hash_roster(step, alive_count, n, x, y, a, C.byref(h)))
+    return h.value
+
+
+class StripSet:
+    """All N strip ranks of one simulation in this process (fp_strips_step / fp_strips_run).
+    devices: one CUDA ordinal per rank (default: all on device 0 -- virtual strips)."""
+
+    def __init__(self, grid: Grid, field, rost: Roster, nranks: int, devices=None, cap_deferred: int = 0,
+                 cap_exits: int = 0, x_bounds=None):
+        devices = devices or [0] * nranks
+        self.grid, self.n, self.nranks = grid, len(rost), nranks
+        self.ranks = []
+        for r in range(nranks):
+            st = SimState(grid, field, rost, devices[r])
+            lo, hi = x_bounds[r] if x_bounds is not None else strip_bounds(grid.width, r, nranks)
+            _check(library().fp_strip_config(st._ctx, r, nranks, lo, hi, cap_deferred, cap_exits), st._ctx)
+            self.ranks.append(st)
+        self._arr = (C.c_void_p * nranks)(*[st._ctx.value for st in self.ranks])
+
+    def set_potential(self, kind: int, drive_gradient: float = 0.0):
+        for st in self.ranks:
+            st.set_potential(kind, drive_gradient)
+
+    def step(self, params: SimParams) -> StepStats:
+        s = _StepStats()
+        _check(library().fp_strips_step(self._arr, self.nranks, params.k_s, params.seed, C.byref(s)),
+               self.ranks[0]._ctx)
+        return StepStats(s.alive, s.exited, s.displacement_cells)
+
+    def run(self, params: SimParams) -> RunStats:
+        params.validate()
+        r = _RunStats()
+        _check(library().fp_strips_run(self._arr, self.nranks, params.k_s, params.seed, params.steps, C.byref(r)),
+               self.ranks[0]._ctx)
+        return RunStats(r.wall_time_s, r.plan_time_s, r.move_time_s, r.steps, r.exited,
+                        r.displacement_cells, r.alive, r.agent_updates)
+
+    def exited(self):
+        n = C.c_uint32()
+        buf = np.empty(max(self.n, 1), np.uint32)
+        _check(library().fp_get_exited(self.ranks[0]._ctx, buf, len(buf), C.byref(n)), self.ranks[0]._ctx)
+        return buf[: n.value].tolist()
+
+    def agents(self):
+        parts = []
+        for st in self.ranks:
+            x, y, a = st.agents()
+            o = np.empty(max(self.n, 1), np.uint8)
+            _check(library().fp_strip_get_owned(st._ctx, o), st._ctx)
+            parts.append((x.copy(), y.copy(), a.copy(), o[: self.n]))
+        return merge_strip_agents(parts)
+
+    @property
+    def step_index(self) -> int:
+        return self.ranks[0].step
+
+    @property
+    def alive(self) -> int:
+        return self.ranks[0].alive
+
+    def state_hash(self) -> int:
+        x, y, a = self.agents()
+        return hash_roster(self.step_index, self.alive, x, y, a)
+
+    def close(self):
+        for st in self.ranks:
+            st.close()

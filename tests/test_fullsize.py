@@ -8,7 +8,6 @@ import pytest
 
 from paper_0911_2900_b200 import fastped as fp
 from paper_0911_2900_b200 import scenarios
-from paper_0911_2900_b200.dist import strip_bounds
 
 pytestmark = pytest.mark.gpu
 
@@ -57,28 +56,6 @@ def test_run_is_deterministic_and_equals_stepping(config, steps):
         check_invariants(c, wl, x0, y0, a0)
     assert fp.state_hash(c) == fp.state_hash(a)
     assert ex == ra.exited and disp == ra.displacement_cells
-
-
-@pytest.mark.timeout(900)
-def test_plaza_strip_plan_equals_full_plan():
-    wl = scenarios.build("plaza")
-    p = fp.SimParams(k_s=wl.k_s, seed=wl.seed, steps=30)
-    full = fp.SimState(wl.grid, None, wl.roster)
-    fp.run(full, p)  # a crowded state
-    x, y, a = full.agents()
-    ro = fp.Roster(x.copy(), y.copy(), wl.roster.v_max.copy(), a.copy())
-    ranks = [fp.SimState(wl.grid, full.field(), ro, step=full.step) for _ in range(2)]
-    fp.plan_phase(full, p)
-    fdx, fdy = full.desired()
-    sdx, sdy = np.zeros_like(fdx), np.zeros_like(fdy)
-    for r, st in enumerate(ranks):
-        lo, hi = strip_bounds(wl.grid.width, r, 2)
-        st.plan_strip(p.k_s, p.seed, lo, hi)
-        dx, dy = st.desired()
-        sdx += dx
-        sdy += dy
-    al = a.astype(bool)
-    assert np.array_equal(sdx[al], fdx[al]) and np.array_equal(sdy[al], fdy[al])
 
 
 @pytest.mark.timeout(1200)
