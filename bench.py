@@ -325,12 +325,24 @@ def ours_arm(args):
         return plan_state_mode(args, fp, wl, local)
     ro = wl.roster
     n = len(ro)
-    st = new_state(fp, wl, local)
+    if world > 1:
+        # one simulation over `world` x-strips, one GPU each (strip.cu): the ranks
+        # exchange the band-connected walks once per step (NCCL allgatherv over NVLink)
+        from paper_0911_2900_b200.dist import strip_rank
+        transport = os.environ.get("FASTPED_STRIP_TRANSPORT", "nccl")
+
+        def make_state(field=None):
+            s_ = strip_rank(wl.grid, field, ro, local, transport=transport)
+            if wl.potential:
+                s_.set_potential(wl.potential, wl.drive_gradient)
+            return s_
+    else:
+        def make_state(field=None):
+            return new_state(fp, wl, local, field)
+    st = make_state()
     field = st.field()
     params = fp.SimParams(k_s=wl.k_s, seed=wl.seed, steps=max(1, args.warmup))
 
-    # replicas: every rank runs its own copy of the workload; the job's value is the
-    # sum of the ranks' agent-updates over the slowest rank's device time (weak scaling)
     if args.warmup > 0:
         fp.run(st, params)
     st.set_agents(ro.x, ro.y, ro.alive)
@@ -345,7 +357,10 @@ def ours_arm(args):
         rs = fp.run(st, params)
     torch.cuda.synchronize()
     c1 = st.counters()
-    wall, updates = aggregate(rs.wall_time_s, rs.agent_updates)
+    # max over ranks of the device time; the agent-updates are the simulation's (global on every
+    # strip rank, so rank 0's count is the job's)
+    wall, _ = aggregate(rs.wall_time_s, 0.0)
+    updates = float(rs.agent_updates)
     value = updates / wall
 
     # the whole 396-step run from step 0 (the reference's run length), when K is shorter
@@ -355,7 +370,8 @@ def ours_arm(args):
         st.step = 0
         with Clocks(local) as clk_full:
             rf = fp.run(st, fp.SimParams(k_s=wl.k_s, seed=wl.seed, steps=RUN_STEPS))
-        wf, uf = aggregate(rf.wall_time_s, rf.agent_updates)
+        wf, _ = aggregate(rf.wall_time_s, 0.0)
+        uf = float(rf.agent_updates)
         full = {"steps": RUN_STEPS, "value": uf / wf, "ms_per_step": wf / RUN_STEPS * 1e3,
                 "phases_ms": {"plan": rf.plan_time_s * 1e3, "move": rf.move_time_s * 1e3},
                 "clocks": clk_full.summary()}
@@ -364,12 +380,14 @@ def ours_arm(args):
         end_steps = args.steps
     # end state of the 396-step run (if the timed run was not it, `st` now holds it)
     x1, y1, a1 = st.agents()
+    x1, y1, a1 = x1.copy(), y1.copy(), a1.copy()
+    own1 = st.owned().astype(np.uint8) if world > 1 else None
     kernel_ms1 = st.time_plan_kernel(wl.k_s, wl.seed, 20)
 
     # e2e: the C ABI with host buffers, every step H2D roster + step + D2H positions/alive
     e2e_steps = args.e2e_steps or args.steps
     saved_affinity = gpu_local_affinity(local)
-    st2 = new_state(fp, wl, local, field)
+    st2 = make_state(field)
     hx = torch.from_numpy(ro.x.copy()).pin_memory().numpy()
     hy = torch.from_numpy(ro.y.copy()).pin_memory().numpy()
     ha = torch.from_numpy(ro.alive.copy()).pin_memory().numpy()
@@ -392,7 +410,7 @@ def ours_arm(args):
         st2.agents(out=(hx, hy, ha))
     torch.cuda.synchronize()
     e2e_wall = time.perf_counter() - t0
-    e2e_wall, upd2 = aggregate(e2e_wall, upd2)
+    e2e_wall, _ = aggregate(e2e_wall, 0.0)
     if saved_affinity is not None:
         os.sched_setaffinity(0, saved_affinity)
     st2.close()
@@ -400,7 +418,7 @@ def ours_arm(args):
            "steps": e2e_steps, "path": "fp_update_agents + fp_step + fp_get_agents (C ABI, pinned host arrays)"}
 
     capacity = None
-    if args.capacity:
+    if args.capacity and world == 1:
         capacity = capacity_probe(args, fp, wl, local, field)
 
     if rank != 0:
@@ -408,9 +426,14 @@ def ours_arm(args):
     peak, peak_kind = peaks()
     mixed = bool((ro.v_max != ro.v_max[0]).any()) if n else False
     drive = wl.potential == fp.DRIVE_X
-    U0 = coverage_u(wl.grid.cells, wl.grid.boundary, ro.x, ro.y, ro.v_max, ro.alive)
+    if world > 1:  # rank 0's strip: the agents it plans
+        a0m = ro.alive & (ro.x >= st.x_lo) & (ro.x < st.x_hi)
+        a1 = a1 & own1
+    else:
+        a0m = ro.alive
+    U0 = coverage_u(wl.grid.cells, wl.grid.boundary, ro.x, ro.y, ro.v_max, a0m)
     U1 = coverage_u(wl.grid.cells, wl.grid.boundary, x1, y1, ro.v_max, a1)
-    b0 = plan_bytes(int(ro.alive.sum()), U0, mixed, drive)
+    b0 = plan_bytes(int(a0m.sum()), U0, mixed, drive)
     b1 = plan_bytes(int(a1.sum()), U1, mixed, drive)
     a_start, a_end = b0 / (kernel_ms0 * 1e-3) / 1e9, b1 / (kernel_ms1 * 1e-3) / 1e9
     achieved = 0.5 * (a_start + a_end)
@@ -444,9 +467,11 @@ def ours_arm(args):
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": wall / max(rs.steps, 1) * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config_desc(args),
-           "parallelism": f"{world} replicas (one simulation per GPU)" if world > 1 else "single",
+           "parallelism": (f"x-strips{world}: one simulation, strip per GPU, band-connected walks exchanged "
+                           f"once per step ({os.environ.get('FASTPED_STRIP_TRANSPORT', 'nccl')})") if world > 1
+                          else "single",
            "phases_ms": {"plan": rs.plan_time_s * 1e3, "move": rs.move_time_s * 1e3, "total": rs.wall_time_s * 1e3},
            "full_run": full, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
            "realtime_capacity": capacity,
