@@ -278,7 +278,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
         if (S.ev) cudaEventDestroy(S.ev);
     }
     void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_counters, c->d_temp, c->d_temp_b,
-                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal, c->d_tile_exit, c->d_seed_items,
+                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal, c->d_tile_exit, c->d_seed_items, c->d_plan_items, c->d_scan_sums,
                     c->d_sc,
                     c->d_p1, c->d_p2,
                     c->d_bkt, c->d_bdone, c->d_pw};
@@ -1271,6 +1271,14 @@ extern "C" int fp_get_counters(const fp_ctx* c, fp_counters* out) {
     if (!c || !out) return fail(nullptr, FP_EINVAL, "null argument");
     *out = c->ctr;
     return FP_OK;
+}
+
+// Diagnostics (not in the header): the plan kernel's profile counters (FP_PLAN_PROF builds).
+extern "C" int fp_debug_plan_prof(fp_ctx* c, int64_t* out, int cap) {
+    DevScalars h;
+    if (cudaMemcpy(&h, c->d_sc, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    for (int k = 0; k < cap && k < 8; ++k) out[k] = (int64_t)h.plan_prof[k];
+    return 0;
 }
 
 // Diagnostics (not in the header): per grid round of the last motion phase, the globaltimer at

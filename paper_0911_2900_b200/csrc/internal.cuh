@@ -140,6 +140,8 @@ struct DevScalars {
     unsigned long long strip_nc;     // strip mode: contended walks listed for the deferral closure
     unsigned long long strip_rexits; // strip mode: exits of the resolved (deferred) walks
     unsigned long long strip_rhops;  // strip mode: hops | dx << 32 of the resolved walks
+    unsigned long long plan_prof[8]; // FP_PLAN_PROF builds: plan-kernel wait / work cycle counters
+    unsigned long long n_plan_items; // plan items this step (bucket.cu)
 };
 
 // x-strip decomposition of one simulation over several GPUs (strip.cu).
@@ -198,11 +200,12 @@ struct fp_ctx {
     bool plane_valid = false;
     double plane_ks = 0.0;
     int plane_potential = -1;
-    CUtensorMap tmap_plane;          // TMA descriptor of the plane (one tile box)
-    CUtensorMap tmap_occ;            // TMA descriptor of the occupancy bitplane (16-word box)
+    CUtensorMap tmap_plane;          // TMA descriptor of the plane: (tile_w + 16) words x 8 rows
+    CUtensorMap tmap_occ;            // occupancy bitplane: 16 words x 8 rows
     CUtensorMap tmap_wall;           // the same box over the wall bitplane (line-of-sight masks)
     int tile_w = 0, tile_h = 0;      // plan tile (cells)
     int tiles_x = 0, tiles_y = 0;
+    int cps = 0;                     // plan chunks (8 rows) per stripe: tiles_y * tile_h / 8
     bool tiles_ok = false;           // tiled fast path usable for this grid
     int use_tma = 1;                 // FP_NO_TMA=1 stages plan tiles with plain loads
 
@@ -229,6 +232,10 @@ struct fp_ctx {
     uint32_t* d_tile_deal = nullptr;  // [sm_count * DEAL_PASSES + 1] first tile-list entry per range
     int deal_passes = 1;              // passes actually used (FP_DEAL_PASSES, 1..DEAL_PASSES)
     size_t n_tiles_alloc = 0;
+    size_t n_chunks_alloc = 0;
+    uint32_t* d_scan_sums = nullptr;  // block sums of the chunk scan (bucket.cu)
+    uint4* d_plan_items = nullptr;     // plan kernel work items (bucket.cu)
+    size_t plan_items_alloc = 0;
     uint2* d_seed_items = nullptr;    // (tile-list entry, chunk) per motion seed work item
     size_t seed_items_alloc = 0;
 
@@ -337,6 +344,7 @@ int fp_order_reserve(fp_ctx* ctx);                                    // order.c
 int fp_plan_prepare(fp_ctx* ctx, double k_s);                         // plan.cu
 bool fp_plan_tiled(const fp_ctx* ctx);
 int fp_bucket_reserve(fp_ctx* ctx);                                   // bucket.cu
+uint32_t fp_plan_chunks(const fp_ctx* ctx);
 int fp_exits_sort_launch(fp_ctx* ctx);                                // move.cu
 int fp_strip_reserve(fp_ctx* ctx);                                    // strip.cu
 int fp_strip_begin_launch(fp_ctx* ctx);

@@ -256,29 +256,29 @@ __device__ __forceinline__ float drive_weight_f(double k_s, double g, int dx) {
     return (float)fpx_exp(FPX_MUL(k_s, FPX_MUL(g, (double)dx)));
 }
 
-// ------------------------------------------------------------------------------ tile kernel
-struct TileArgs {
+// ------------------------------------------------------------------------------ stream kernel
+// Ring of RING_SLOTS 8-row chunks of one stripe (tile_w columns + 8 each side): weight-plane
+// words, occupancy bits and wall bits, staged by TMA.  Chunk k of the stripe lives in ring slot
+// k % RING_SLOTS.
+#define PLAN_THREADS 512
+#ifndef RING_SLOTS
+#define RING_SLOTS 24
+#endif
+#define CHUNK_ROWS 8
+#define OCCW 16  // bit words per staged row: 512 bits from a 16-byte aligned word
+
+struct StreamArgs {
     PlanCommon c;
-    int PW;
-    const uint32_t* plane;
-    const uint32_t* bucket;
-    const uint4* brec;
-    const uint32_t* tile_off;
-    const uint32_t* tile_cnt;
-    const uint32_t* tile_list;
-    const uint8_t* tile_exit;  // an Exit within the tile's window
-    const uint32_t* deal;  // [gridDim.x * passes + 1] first list entry of each range
-    int passes;
-    int tile_w, tile_h, tiles_x;
-    int use_tma;  // 0: stage the box with coalesced loads (debug / comparison path)
-    int boxw, boxh, occw;  // shared-memory strides (words)
-    uint2* fallback;       // (id, bucket position) handed to plan_exact_list_kernel
-    uint4* rec0;           // walk records in bucket order (motion_rec.cuh), when emit
-    uint32_t* p1;          // contention marks
-    uint32_t* p2;
-    int emit;
-    int mixed;  // roster has more than one v_max: the masked radius-5 variant for everyone
-    int rot;    // thread rotation between consecutive fetches (multiple of the lanes per agent)
+    const uint4* brec;          // (id, wrapped x, y, v_max) per bucket position (bucket.cu)
+    const uint32_t* ccnt;       // agents per chunk
+    const uint32_t* coff;       // first bucket position per chunk
+    const uint4* items;         // plan items (bucket.cu): (first chunk, chunks - 1, first agent, end agent)
+    uint32_t nchunks;
+    const uint8_t* tile_exit;   // an Exit within the tile's window
+    int tile_w, tile_h, tiles_x, cps, boxw;
+    uint2* fallback;            // (id, bucket position) handed to plan_exact_list_kernel
+    uint4* rec0;                // walk records in bucket order (motion_rec.cuh)
+    int mixed;                  // roster has more than one v_max: the masked radius-5 variant
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -320,6 +320,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// The rows of one plan item staged in its half of the ring: item row 0 is grid row r0 =
+// 8 * (first chunk - 1); row r of the grid is item row r - r0 (weight words, occupancy bits,
+// wall bits), so a ball's rows are plain offsets from the agent's item row.
+struct Ring {
+    const uint32_t* w;
+    const uint32_t* o;
+    const uint32_t* l;
+    int boxw;
+    int r0;
+    __device__ __forceinline__ const uint32_t* wrow(int r) const { return w + (r - r0) * boxw; }
+    __device__ __forceinline__ const uint32_t* orow(int r) const { return o + (r - r0) * OCCW; }
+    __device__ __forceinline__ const uint32_t* lrow(int r) const { return l + (r - r0) * OCCW; }
+};
+
 // Pair of u64 words holding the 121-bit ball wall mask (bit (dy+5)*11 + dx+5).
 struct Mask121 {
     unsigned long long lo, hi;
@@ -331,12 +345,6 @@ __device__ __forceinline__ void mask_or_row(Mask121& m, uint32_t rowbits, int B)
     if (B + 11 > 64) m.hi |= (B >= 64) ? ((unsigned long long)rowbits << (B - 64)) : ((unsigned long long)rowbits >> (64 - B));
 }
 
-__device__ __forceinline__ bool path_blocked(const Mask121& m, int o) {
-    const unsigned long long plo = ((unsigned long long)c_pathmask[o][1] << 32) | c_pathmask[o][0];
-    const unsigned long long phi = ((unsigned long long)c_pathmask[o][3] << 32) | c_pathmask[o][2];
-    return ((m.lo & plo) | (m.hi & phi)) != 0ull;
-}
-
 // Weight of a reachable plane word in ExitDistance mode as an exact fp64 number:
 // m_c * 2^(C_p - C_c), with (C_p - C_c) recovered mod 128 (|d| <= 60 on safe cells).
 __device__ __forceinline__ double exit_weight(uint32_t w, int cp_biased /* C_p + 64 (+128) */) {
@@ -346,11 +354,6 @@ __device__ __forceinline__ double exit_weight(uint32_t w, int cp_biased /* C_p +
     return __hiloint2double(hi, lo);
 }
 
-__device__ __forceinline__ unsigned long long globaltimer_p() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 // Path mask test against the shared-memory copy of c_pathmask (lanes index it divergently).
 __device__ __forceinline__ bool path_blocked_s(const uint4* pm, const Mask121& m, int o) {
     const uint4 q = pm[o];
@@ -377,37 +380,29 @@ __device__ __forceinline__ float pairwise_sum(const float* x) {
     }
 }
 
-// Plans one agent from the staged tile (V = its v_max, DRIVE = DriveX potential) with P lanes
-// (P consecutive threads of a warp, all calling with the same agent).  Returns 1 when the fast
-// path decided (result in *ox, *oy, identical in every lane), 2 when the exact path must decide.
-//   walls   every lane ORs the ball's wall bits (staged wall bitplane, one word pair per row)
-//   pass 1  lane l takes rows t = l, l+P, ... of the centre-out order: valid candidates (not
-//           Wall/unreachable, not occupied by another agent, visible) contribute their exact
-//           fp32 weight to a pairwise fp32 row sum; the row sums are gathered into every lane
-//           and accumulated in fp64
+// Plans one agent from the staged stripe (V = its v_max, DRIVE = DriveX potential).  Returns 1
+// when the fast path decided (result in *ox, *oy), 2 when the exact path must decide.
+//   walls   the ball's wall bits (staged wall bitplane, one word pair per row)
+//   pass 1  rows centre-out: valid candidates (not Wall/unreachable, not occupied by another
+//           agent, visible) contribute their exact fp32 weight to a pairwise fp32 row sum; the
+//           row sums are accumulated in fp64
 //   pass 2  u*total picks the row; the row is replayed in list order (wrapped-x sorted at a
 //           periodic seam) to find the first cumulative weight > threshold; guard band.
-// Every sum is taken in the same order for any P, so the decision does not depend on P.
 // MASKED: one radius-V code path for every v_max <= V (mixed rosters): rows and columns beyond
 // the agent's own radius vr are masked out, which leaves exactly its Chebyshev ball (the line
 // of sight to a cell of the ball only crosses cells of the ball), so decisions are unchanged
 // while the warps of a mixed roster share one instruction stream.
-template <int V, bool DRIVE, bool MASKED = false, int P = 1>
-__device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* buf, const uint32_t* occs,
-                                           const uint32_t* walls, const uint4* pathm, int osh0, int x0, int y0,
+template <int V, bool DRIVE, bool MASKED = false>
+__device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, const uint4* pathm, int osh0, int X0,
                                            int px, int py, double u, const double* drive_tab, int* ox, int* oy,
                                            int vr = V) {
     constexpr int D = 2 * V + 1;
-    constexpr int RPL = (D + P - 1) / P;  // rows per lane
-    const int lane = P > 1 ? (int)(threadIdx.x & (P - 1)) : 0;
-    const unsigned gmask = P > 1 ? (((1u << P) - 1u) << ((threadIdx.x & 31u) & ~(unsigned)(P - 1))) : 0xffffffffu;
     const PlanCommon& a = A.c;
     const uint32_t colmask = MASKED ? (((1u << (2 * vr + 1)) - 1u) << (V - vr)) : ((1u << D) - 1u);
-    const int X0 = x0 - 8;  // box origin (TMA inner coordinates stay 16-byte aligned)
-    const int lx = px - X0, ly = py - (y0 - FP_HALO);
+    const int lx = px - X0;
     int cpb = 0;
     if (!DRIVE) {
-        const uint32_t own = buf[ly * A.boxw + lx];
+        const uint32_t own = R.wrow(py)[lx];
         if (own & (FP_W_SPECIAL | FP_W_UNSAFE)) return 2;  // "ones" pocket / unsafe centre
         cpb = (int)((own >> 23) & 0x7Fu) + 64 + 128;
     }
@@ -416,7 +411,7 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
 #pragma unroll
     for (int dy = -V; dy <= V; ++dy) {
         if ((unsigned)(py + dy) >= (unsigned)a.g.H) continue;
-        const uint32_t* wrow = walls + (ly + dy) * A.occw;
+        const uint32_t* wrow = R.lrow(py + dy);
         const uint32_t wb = __funnelshift_r(wrow[osh >> 5], wrow[(osh >> 5) + 1], osh & 31) & ((1u << D) - 1u);
         mask_or_row(wm, wb, (dy + 5) * 11 + 5 - V);
     }
@@ -424,46 +419,40 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
     float dw[D];  // DriveX weights by column (exact fp32 values)
 #pragma unroll
     for (int k = 0; k < D; ++k) dw[k] = DRIVE ? (float)drive_tab[k - V + 5] : 0.0f;
-    float rso[RPL];
+    float rso[D];
 #pragma unroll
-    for (int j = 0; j < RPL; ++j) {
-        const int t = j * P + lane;  // centre-out row index: 0, -1, 1, -2, 2, ...
-        float s = 0.0f;
-        if (t < D) {
-            const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);
-            const bool rowok = (unsigned)(py + dy) < (unsigned)a.g.H;
-            const uint32_t* row = buf + (ly + dy) * A.boxw + lx - V;
-            uint32_t wv[D];
-            uint32_t spec = 0u;
+    for (int t = 0; t < D; ++t) {
+        const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);  // centre-out: 0, -1, 1, -2, 2, ...
+        const bool rowok = (unsigned)(py + dy) < (unsigned)a.g.H;
+        const uint32_t* row = R.wrow(py + dy) + lx - V;
+        uint32_t wv[D];
+        uint32_t spec = 0u;
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
-                wv[k] = row[k];
-                spec |= (wv[k] >> 31) << k;
-            }
-            const uint32_t* orow = occs + (ly + dy) * A.occw;
-            uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
-            if (dy == 0) occ &= ~(1u << V);  // the own cell stays a candidate (planning.hpp:45-46)
-            const bool inball = !MASKED || (dy <= vr && -dy <= vr);
-            uint32_t valid = (rowok && inball) ? (~(spec | occ) & colmask) : 0u;
-            if (anywall) {
-#pragma unroll
-                for (int k = 0; k < D; ++k)
-                    if (path_blocked_s(pathm, wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
-            }
-            float w[D];
+        for (int k = 0; k < D; ++k) {
+            wv[k] = row[k];
+            spec |= (wv[k] >> 31) << k;
+        }
+        const uint32_t* orow = R.orow(py + dy);
+        uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
+        if (dy == 0) occ &= ~(1u << V);  // the own cell stays a candidate (planning.hpp:45-46)
+        const bool inball = !MASKED || (dy <= vr && -dy <= vr);
+        uint32_t valid = (rowok && inball) ? (~(spec | occ) & colmask) : 0u;
+        if (anywall) {
 #pragma unroll
             for (int k = 0; k < D; ++k)
-                w[k] = ((valid >> k) & 1u) ? (DRIVE ? dw[k] : exit_weight32(wv[k], cpb)) : 0.0f;
-            s = pairwise_sum<D>(w);
+                if (path_blocked_s(pathm, wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
         }
-        rso[j] = s;
+        float w[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+            w[k] = ((valid >> k) & 1u) ? (DRIVE ? dw[k] : exit_weight32(wv[k], cpb)) : 0.0f;
+        rso[t] = pairwise_sum<D>(w);
     }
     double rs[D];  // row sums, indexed by dy + V
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         const int dy = k - V;
-        const int t = dy >= 0 ? 2 * dy : -2 * dy - 1;
-        rs[k] = (double)(P > 1 ? __shfl_sync(gmask, rso[t / P], t % P, P) : rso[t]);
+        rs[k] = (double)rso[dy >= 0 ? 2 * dy : -2 * dy - 1];
     }
     double T = 0.0;
 #pragma unroll
@@ -480,17 +469,17 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
     }
     if (rstar < 0) return 2;  // u*total rounded up to total
     const int dy = rstar - V;
-    const uint32_t* row = buf + (ly + dy) * A.boxw + lx;
-    const uint32_t* orow = occs + (ly + dy) * A.occw;
+    const uint32_t* row = R.wrow(py + dy) + lx;
+    const uint32_t* orow = R.orow(py + dy);
     uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
     if (dy == 0) occ &= ~(1u << V);
-    const int R = MASKED ? vr : V;  // the agent's radius
-    int a0 = -R, a1 = R, b0 = 0, b1 = -1;
+    const int Rr = MASKED ? vr : V;  // the agent's radius
+    int a0 = -Rr, a1 = Rr, b0 = 0, b1 = -1;
     if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {  // wrapped-x order at the seam (planning.hpp:50-53)
-        if (px + R >= a.g.W) {
-            a0 = a.g.W - px; b0 = -R; b1 = a.g.W - px - 1;
-        } else if (px - R < 0) {
-            a0 = -px; b0 = -R; b1 = -px - 1;
+        if (px + Rr >= a.g.W) {
+            a0 = a.g.W - px; b0 = -Rr; b1 = a.g.W - px - 1;
+        } else if (px - Rr < 0) {
+            a0 = -px; b0 = -Rr; b1 = -px - 1;
         }
     }
     double prefix = before, lower = 0.0, upper = 0.0;
@@ -527,12 +516,12 @@ __device__ __forceinline__ int plan_fast_t(const TileArgs& A, const uint32_t* bu
     return 1;
 }
 
-// record_of (motion_rec.cuh) for a fast-path decision inside the staged tile: the target lies in
+// record_of (motion_rec.cuh) for a fast-path decision inside the staged stripe: the target lies in
 // the ball, the Wall test reads the staged plane words, and the Exit test (global bitplane) runs
 // only in tiles whose window holds an Exit.
-__device__ __forceinline__ uint4 record_of_tile(const Geo& g, const uint32_t* occ, bool tile_exit, const uint32_t* buf,
-                                                int boxw, int lx, int ly, uint32_t id, int sx, int sy, int tx, int ty,
-                                                int v, const signed char (*bp)[5][2]) {
+__device__ __forceinline__ uint4 record_of_ring(const Geo& g, const uint32_t* occ, bool tile_exit, const Ring& R,
+                                                int lx, uint32_t id, int sx, int sy, int tx, int ty, int v,
+                                                const signed char (*bp)[5][2]) {
     const int ddx = g.segment_dx(sx, tx), ddy = ty - sy;
     const int o = (ddy + 5) * 11 + ddx + 5;
     const int len = min(max(abs(ddx), abs(ddy)), v);
@@ -540,7 +529,7 @@ __device__ __forceinline__ uint4 record_of_tile(const Geo& g, const uint32_t* oc
     bool ex = false;
     for (int j = 0; j < len; ++j) {
         const int ox = bp[o][j][0], oy = bp[o][j][1];
-        if (buf[(ly + oy) * boxw + lx + ox] == FP_W_WALL) break;
+        if (R.wrow(sy + oy)[lx + ox] == FP_W_WALL) break;
         ++m;
         if (tile_exit) {
             const int x = g.wrap(sx + ox), y = sy + oy;
@@ -558,65 +547,63 @@ __device__ __forceinline__ uint4 record_of_tile(const Geo& g, const uint32_t* oc
                       (uint32_t)sy | ((uint32_t)o << 24));
 }
 
-template <bool DRIVE, int P>
-__device__ __forceinline__ int plan_fast_v(int v, const TileArgs& A, const uint32_t* buf, const uint32_t* occs,
-                                           const uint32_t* walls, const uint4* pathm, int osh0, int x0, int y0,
-                                           int px, int py, double u, const double* drive_tab, int* ox, int* oy) {
-#define FP_PLAN_ARGS A, buf, occs, walls, pathm, osh0, x0, y0, px, py, u, drive_tab, ox, oy
-    if (A.mixed)  // one instruction stream for a mixed-v roster (see plan_fast_t)
-        return plan_fast_t<5, DRIVE, true, P>(FP_PLAN_ARGS, v);
+template <bool DRIVE>
+__device__ __forceinline__ int plan_ring_v(int v, const StreamArgs& A, const Ring& R, const uint4* pathm, int osh0,
+                                           int X0, int px, int py, double u, const double* drive_tab, int* ox,
+                                           int* oy) {
+#define FP_PLAN_ARGS A, R, pathm, osh0, X0, px, py, u, drive_tab, ox, oy
+    if (A.mixed)  // one instruction stream for a mixed-v roster (see plan_ring_t)
+        return plan_ring_t<5, DRIVE, true>(FP_PLAN_ARGS, v);
     switch (v) {
-        case 1: return plan_fast_t<1, DRIVE, false, P>(FP_PLAN_ARGS);
-        case 2: return plan_fast_t<2, DRIVE, false, P>(FP_PLAN_ARGS);
-        case 3: return plan_fast_t<3, DRIVE, false, P>(FP_PLAN_ARGS);
-        case 4: return plan_fast_t<4, DRIVE, false, P>(FP_PLAN_ARGS);
-        default: return plan_fast_t<5, DRIVE, false, P>(FP_PLAN_ARGS);
+        case 1: return plan_ring_t<1, DRIVE>(FP_PLAN_ARGS);
+        case 2: return plan_ring_t<2, DRIVE>(FP_PLAN_ARGS);
+        case 3: return plan_ring_t<3, DRIVE>(FP_PLAN_ARGS);
+        case 4: return plan_ring_t<4, DRIVE>(FP_PLAN_ARGS);
+        default: return plan_ring_t<5, DRIVE>(FP_PLAN_ARGS);
     }
 #undef FP_PLAN_ARGS
 }
 
-#define PLAN_THREADS 512
-#ifndef FP_PLAN_NAP_MAX
-#define FP_PLAN_NAP_MAX 256  // ns
-#endif
-#ifndef PLAN_SLOTS
-#define PLAN_SLOTS 3  // tiles resident per CTA
-#endif
+__device__ __forceinline__ unsigned long long globaltimer_p() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
-// Persistent CTA per SM.  Tiles are fetched in pairs of buffer slots (TMA, mbarrier); the
-// agents of fetch i are dealt to threads round-robin starting at thread (i*160) mod 512, one
-// agent per thread.  There is no CTA-wide barrier per tile: a thread finishing its agents of
-// fetch i moves on to fetch i+1; the thread that completes the last agent of fetch i refills
-// that slot with fetch i+2.  Slot metadata is published with a generation number (seqlock).
-// Diagnostics read by tools/debug_plan.py and tools/debug_plan_cta.py: the fetch timeline of CTA
-// 5 (issue, TMA ready, last agent done, agents) and every CTA's start, end and fetch count.
-__device__ unsigned long long g_plan_dbg[4 * 256];
-extern "C" int fp_debug_plan(unsigned long long* out) {
-    return (int)cudaMemcpyFromSymbol(out, g_plan_dbg, sizeof(g_plan_dbg));
-}
-__device__ unsigned long long g_plan_cta[3 * 256];
-extern "C" int fp_debug_plan_cta(unsigned long long* out) {
-    return (int)cudaMemcpyFromSymbol(out, g_plan_cta, sizeof(g_plan_cta));
-}
-// P consecutive threads plan each agent together (plan_fast_t).
-template <int P>
-__global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                                    const __grid_constant__ CUtensorMap tmap_occ,
-                                                                    const __grid_constant__ CUtensorMap tmap_wall,
-                                                                    TileArgs A) {
+// Persistent CTA per SM, warp-specialised, dynamically scheduled.  Work units are plan items
+// (bucket.cu plan_items_kernel): up to PLAN_ITEM_CHUNKS consecutive chunks of one stripe and at
+// most PLAN_ITEM_AGENTS of their agents, taken from a global cursor (d_sc->tile_next) so crowded
+// and empty parts of the grid balance across the SMs.
+//   producer (warp 0): takes an item; it occupies the next nk + 2 ring slots (chunks kf-1 ..
+//     kl+1 of its stripe, kept in the ring in order); lane i looks after the item's slot i: it
+//     waits for the slot's previous rows to be released (reference count 0), reloads it by TMA
+//     (weight words, occupancy and wall bits; one full mbarrier per slot) and adds the item's
+//     references.  Lane 0 appends the item's agent run to the CTA's queue and publishes it.
+//   consumers (the other warps): claim 32 virtual agents at a time, plan each once it is
+//     published and the (at most three) slots its ball spans have landed, one agent per lane,
+//     then release those slots.
+// The ring holds two items, so the TMA of the next item overlaps the planning of the current one.
+#define PLAN_QUEUE 64  // published items a CTA remembers (the ring bounds the ones in flight)
+#define RING_HALF (RING_SLOTS / 2)  // slots per item (>= PLAN_ITEM_CHUNKS + 2, bucket.cu)
+
+__global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __grid_constant__ CUtensorMap tmap_w,
+                                                                      const __grid_constant__ CUtensorMap tmap_o,
+                                                                      const __grid_constant__ CUtensorMap tmap_l,
+                                                                      StreamArgs A) {
     extern __shared__ __align__(128) uint32_t smem_raw[];
-    uint32_t* smem = smem_raw + (((128u - (smem_u32(smem_raw) & 127u)) & 127u) >> 2);
-    const int box_words = A.boxw * A.boxh;
-    const int box_stride = (box_words + 31) & ~31;  // words, 128-byte multiple
-    const int occ_words = A.boxh * A.occw;
-    const int occ_stride = (occ_words + 31) & ~31;
-    const unsigned tx_bytes = (unsigned)(box_words + 2 * occ_words) * 4u;
-    uint64_t* bars = (uint64_t*)(smem + PLAN_SLOTS * box_stride + 2 * PLAN_SLOTS * occ_stride);
-    // slot metadata is written by one thread and read by others without a CTA barrier: volatile
-    __shared__ volatile int s_tile[PLAN_SLOTS], s_cnt[PLAN_SLOTS], s_off[PLAN_SLOTS], s_x0[PLAN_SLOTS],
-        s_y0[PLAN_SLOTS];
-    __shared__ volatile int s_gen[PLAN_SLOTS];
-    __shared__ int s_done[PLAN_SLOTS];
+    uint32_t* ringw = smem_raw + (((128u - (smem_u32(smem_raw) & 127u)) & 127u) >> 2);
+    uint32_t* ringo = ringw + RING_SLOTS * CHUNK_ROWS * A.boxw;
+    uint32_t* ringl = ringo + RING_SLOTS * CHUNK_ROWS * OCCW;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ringl + RING_SLOTS * CHUNK_ROWS * OCCW);
+    __shared__ volatile int s_gen[RING_SLOTS];
+    __shared__ int s_ref[RING_SLOTS];
+    __shared__ unsigned s_qv[PLAN_QUEUE];      // published item q: first virtual agent index
+    __shared__ unsigned s_qa[PLAN_QUEUE];      //   its first bucket position
+    __shared__ int s_qs[PLAN_QUEUE];           //   its ring half | first chunk << 1
+    __shared__ unsigned s_next;                // consumers' claim cursor (virtual agents)
+    __shared__ volatile unsigned s_pub;        // virtual agents published
+    __shared__ volatile unsigned s_nq;         // queue entries published
+    __shared__ volatile int s_done;            // producer finished
     __shared__ double s_drive[11];
     __shared__ signed char s_bp[121][5][2];
     __shared__ uint4 s_pathm[121];
@@ -624,178 +611,205 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_tile_kernel(const __grid
     for (int k = threadIdx.x; k < 121; k += blockDim.x)
         s_pathm[k] = make_uint4(c_pathmask[k][0], c_pathmask[k][1], c_pathmask[k][2], c_pathmask[k][3]);
     const PlanCommon& a = A.c;
-    const uint64_t step = (uint64_t)a.sc->step;
-    // list entry of fetch number i, or -1 past the end
-    auto fetch_entry = [&](int i) {
-        for (int p = 0, k = i; p < A.passes; ++p) {
-            const int lo = (int)A.deal[p * gridDim.x + blockIdx.x], hi = (int)A.deal[p * gridDim.x + blockIdx.x + 1];
-            if (k < hi - lo) return lo + k;
-            k -= hi - lo;
-        }
-        return -1;
-    };
-    // fetch number i into slot i % PLAN_SLOTS (one thread)
-    auto fetch = [&](int i) {
-        const int slot = i % PLAN_SLOTS;
-        s_gen[slot] = -1;  // seqlock: readers that raced with this refill see a changed generation
-        __threadfence_block();
-        // fetch i of this CTA is the i-th entry of its ranges (one per pass, bucket.cu
-        // tile_deal_kernel) taken in order, so fetch numbers map monotonically onto the list and
-        // an exhausted fetch ends every later one (refills complete out of order)
-        const int t = fetch_entry(i);
-#ifdef FP_PLAN_DEBUG
-        if (blockIdx.x == 5 && i < 256) g_plan_dbg[i] = globaltimer_p();
-#endif
-        if (t >= 0) {
-            const uint32_t tile = A.tile_list[t];
-            const int tx = (int)(tile % (uint32_t)A.tiles_x), ty = (int)(tile / (uint32_t)A.tiles_x);
-            const int x0 = tx * A.tile_w, y0 = ty * A.tile_h;
-            s_tile[slot] = (int)tile;
-            s_cnt[slot] = (int)A.tile_cnt[tile];
-            s_off[slot] = (int)A.tile_off[tile];
-            s_x0[slot] = x0;
-            s_y0[slot] = y0;
-            s_done[slot] = 0;
-            if (A.use_tma) {
-                const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&bars[slot], tx_bytes);
-                tma_load_2d(smem + slot * box_stride, &tmap, &bars[slot], x0 - 8 + FP_XPAD_W, y0 - FP_HALO);
-                tma_load_2d(smem + PLAN_SLOTS * box_stride + slot * occ_stride, &tmap_occ, &bars[slot], gws,
-                            y0 - FP_HALO);
-                tma_load_2d(smem + PLAN_SLOTS * box_stride + (PLAN_SLOTS + slot) * occ_stride, &tmap_wall,
-                            &bars[slot], gws, y0 - FP_HALO);
-            }
-        } else {
-            s_tile[slot] = -1;
-        }
-        __threadfence_block();
-        s_gen[slot] = i;
-    };
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < PLAN_SLOTS; ++s) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < PLAN_SLOTS; ++s) s_gen[s] = -1;
-    }
     if (threadIdx.x < 11) {
         s_drive[threadIdx.x] = (a.potential == FP_POTENTIAL_DRIVE_X)
                                    ? (double)drive_weight_f(a.k_s, a.drive_gradient, (int)threadIdx.x - 5)
                                    : 0.0;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-#ifdef FP_PLAN_DEBUG
-        if (blockIdx.x < 256) {
-            g_plan_cta[blockIdx.x] = globaltimer_p();
-            g_plan_cta[256 + blockIdx.x] = 0;
-        }
-#endif
-        for (int s = 0; s < PLAN_SLOTS; ++s) fetch(s);
+    if (threadIdx.x < RING_SLOTS) {
+        s_gen[threadIdx.x] = 0;
+        s_ref[threadIdx.x] = 0;
     }
-    for (int i = 0;; ++i) {
-        const int slot = i % PLAN_SLOTS;
-        // bounded wait: a scheduling bug must surface as an error flag, never as a hung GPU
-        // (-1 while a refill is being published; a generation past i means fetch i already
-        // completed without this thread -- it had no agent there -- and the slot moved on)
-        // (exponential backoff: idle threads must not steal issue slots from the computing warps)
-        int gen;
-        unsigned nap = 32;
-        for (long long spin = 0; (gen = s_gen[slot]) < i; ++spin) {
-            __nanosleep(nap);
-            nap = min(nap * 2u, (unsigned)FP_PLAN_NAP_MAX);
-            if (spin > (1ll << 22)) {
-                atomicOr(&a.sc->err, 1ull);
-                return;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < RING_SLOTS; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_next = 0;
+        s_pub = 0;
+        s_done = 0;
+        s_nq = 0;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows_chunks = (a.g.H + CHUNK_ROWS - 1) / CHUNK_ROWS;  // chunks with rows in the grid
+    const unsigned tx_bytes = (unsigned)(CHUNK_ROWS * (A.boxw + 2 * OCCW)) * 4u;
+    const uint32_t n_items = (uint32_t)a.sc->n_plan_items;
+    if (warp == 0) {
+        // ---------------- producer
+        bool ok = true;
+        unsigned pub = 0, nq = 0;
+        int half = 0;  // ring half of the next item (items alternate halves: double buffering)
+        while (ok) {
+            uint32_t i = 0;
+            if (lane == 0) i = (uint32_t)atomicAdd(&a.sc->tile_next, 1ull);
+            i = __shfl_sync(0xffffffffu, i, 0);
+            if (i >= n_items) break;
+            const uint4 it = __ldg(&A.items[i]);
+            const uint32_t gf = it.x;
+            const int nk = (int)it.y + 1;
+            const uint32_t a0 = it.z, a1 = it.w;
+            const int s = (int)(gf / (uint32_t)A.cps), kf = (int)(gf % (uint32_t)A.cps);
+            // agents of the item in chunk kf + lane
+            uint32_t c = 0;
+            if (lane < nk) {
+                const uint32_t off = __ldg(&A.coff[gf + lane]), cnt = __ldg(&A.ccnt[gf + lane]);
+                const uint32_t lo = max(off, a0), hi = min(off + cnt, a1);
+                c = hi > lo ? hi - lo : 0u;
             }
+            const int kk = kf - 1 + lane;  // the slot this lane looks after
+            uint32_t refs = 0;             // agents of the item whose ball reaches slot kk
+#pragma unroll
+            for (int d = -1; d <= 1; ++d) {
+                const int j = lane - 1 + d;  // item chunk index of chunk kk + d
+                const uint32_t cj = __shfl_sync(0xffffffffu, c, j & 31);
+                if (j >= 0 && j < nk) refs += cj;
+            }
+            const int p = half * RING_HALF + lane;
+            if (lane < nk + 2 && refs != 0 && kk >= 0 && kk < rows_chunks) {
+                for (long long spin = 0; *((volatile int*)&s_ref[p]) != 0; ++spin) {
+                    __nanosleep(64);
+                    if (spin > (1ll << 24)) {
+                        atomicOr(&a.sc->err, 4ull);
+                        ok = false;
+                        break;
+                    }
+                }
+                if (ok) {
+                    s_gen[p] = s_gen[p] + 1;
+                    const int x0 = s * A.tile_w;
+                    const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&bars[p], tx_bytes);
+                    tma_load_2d(ringw + p * CHUNK_ROWS * A.boxw, &tmap_w, &bars[p], x0 - 8 + FP_XPAD_W, kk * CHUNK_ROWS);
+                    tma_load_2d(ringo + p * CHUNK_ROWS * OCCW, &tmap_o, &bars[p], gws, kk * CHUNK_ROWS);
+                    tma_load_2d(ringl + p * CHUNK_ROWS * OCCW, &tmap_l, &bars[p], gws, kk * CHUNK_ROWS);
+                    atomicAdd(&s_ref[p], (int)refs);
+                }
+            }
+            ok = __all_sync(0xffffffffu, ok);
+            if (lane == 0 && ok) {
+                s_qv[nq % PLAN_QUEUE] = pub;
+                s_qa[nq % PLAN_QUEUE] = a0;
+                s_qs[nq % PLAN_QUEUE] = half | (kf << 1);
+                ++nq;
+                pub += a1 - a0;
+                __threadfence_block();
+                s_nq = nq;
+                __threadfence_block();
+                s_pub = pub;
+            }
+            half ^= 1;
         }
-        if (gen > i) continue;
-        const int tile = s_tile[slot];
-        const int cnt = s_cnt[slot], off = s_off[slot], x0 = s_x0[slot], y0 = s_y0[slot];
-        __threadfence_block();
-        // validate the snapshot before acting on any of it (including the end-of-list marker:
-        // a refill racing with these reads may already have written tile = -1 for fetch i+2)
-        if (s_gen[slot] != i) continue;  // fetch i already completed without this thread's help
-        if (tile < 0) {
-#ifdef FP_PLAN_DEBUG
-            if (blockIdx.x < 256 && (threadIdx.x & 31) == 0) {
-                atomicMax(&g_plan_cta[256 + blockIdx.x], globaltimer_p());
-                g_plan_cta[512 + blockIdx.x] = i;
-            }
-#endif
-            break;
-        }
-        // agent slot of this thread's lane group (the rotation keeps groups P-aligned)
-        int k = (((int)threadIdx.x - i * A.rot) & (PLAN_THREADS - 1)) / P;
-        if (k >= cnt) continue;  // no agent of this fetch for this thread
-        uint32_t* buf = smem + slot * box_stride;
-        uint32_t* occs = smem + PLAN_SLOTS * box_stride + slot * occ_stride;
-        uint32_t* walls = smem + PLAN_SLOTS * box_stride + (PLAN_SLOTS + slot) * occ_stride;
-        const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
-        const int osh0 = x0 - 8 + FP_XPAD_BITS - gws * 32;  // staged-occupancy bit of box column 0
-        if (A.use_tma) {
-            if (!mbar_wait(&bars[slot], (unsigned)(i / PLAN_SLOTS) & 1u)) {
-                atomicOr(&a.sc->err, 2ull);
-                return;
-            }
-#ifdef FP_PLAN_DEBUG
-            if (blockIdx.x == 5 && i < 256 && g_plan_dbg[256 + i] < g_plan_dbg[i]) g_plan_dbg[256 + i] = globaltimer_p();
-#endif
-        } else if (true) {
-            // comparison path: each thread fills what it reads (slow; debugging only)
-            const int gx0 = x0 - 8 + FP_XPAD_W, gy0 = y0 - FP_HALO;
-            for (int e = 0; e < box_words; ++e) {
-                const int r = e / A.boxw, cidx = e % A.boxw;
-                const int gy = gy0 + r, gx = gx0 + cidx;
-                buf[e] = (gy >= 0 && gy < a.g.H && gx < A.PW) ? A.plane[(size_t)gy * A.PW + gx] : 0u;
-            }
-            for (int e = 0; e < occ_words; ++e) {
-                const int r = e / A.occw, wcol = e % A.occw;
-                const int gy = gy0 + r, gw = gws + wcol;
-                const bool in = gy >= 0 && gy < a.g.H && gw < a.g.P;
-                occs[e] = in ? a.occ[(size_t)gy * a.g.P + gw] : 0u;
-                walls[e] = in ? a.g.wall[(size_t)gy * a.g.P + gw] : 0u;
-            }
-        }
-        int mine = 0;
-        const bool lead = (threadIdx.x & (P - 1)) == 0;
-        for (; k < cnt; k += PLAN_THREADS / P) {
-            const uint4 br = __ldcg(&A.brec[off + k]);  // (id, wrapped x, y, v_max), bucket.cu
-            const uint32_t id = br.x;
-            const int px = (int)br.y, py = (int)br.z;
-            const int v = (int)br.w;
-            const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
-            int cx = 0, cy = 0;
-            const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
-                               ? plan_fast_v<true, P>(v, A, buf, occs, walls, s_pathm, osh0, x0, y0, px, py, u,
-                                                      s_drive, &cx, &cy)
-                               : plan_fast_v<false, P>(v, A, buf, occs, walls, s_pathm, osh0, x0, y0, px, py, u,
-                                                       s_drive, &cx, &cy);
-            if (!lead) {
-                // the group's other lanes: nothing to write
-            } else if (st == 1) {
-                a.dx[id] = cx;
-                a.dy[id] = cy;
-                if (A.emit)  // the motion's walk record, walls from the staged plane
-                    A.rec0[off + k] = record_of_tile(a.g, a.occ, A.tile_exit[tile], buf, A.boxw, px - (x0 - 8),
-                                                     py - (y0 - FP_HALO), id, px, py, cx, cy, v, s_bp);
-            } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
-                A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, (uint32_t)(off + k));
-            }
-            ++mine;
-        }
-        // release: this thread's reads of the slot happen before its count lands (without the
-        // fence the compiler may sink shared loads below the relaxed atomic and the refill
-        // TMA would overwrite data still being read); the last finisher acquires, then refills
-        __threadfence_block();
-        if (atomicAdd(&s_done[slot], mine) + mine == cnt * P) {  // last lane of fetch i
+        if (lane == 0) {
             __threadfence_block();
-#ifdef FP_PLAN_DEBUG
-            if (blockIdx.x == 5 && i < 256) {
-                g_plan_dbg[512 + i] = globaltimer_p();
-                g_plan_dbg[768 + i] = cnt;
-            }
+            s_done = 1;
+        }
+        return;
+    }
+    // ---------------- consumers
+    // warps sharing the producer's scheduler (warp id mod 4) may stay idle so the producer is
+    // never starved of issue slots (FP_PLAN_SKIP_SCHED0)
+#ifndef FP_PLAN_SKIP_SCHED0
+#define FP_PLAN_SKIP_SCHED0 0
 #endif
-            fetch(i + PLAN_SLOTS);
+    if (FP_PLAN_SKIP_SCHED0 && (warp & 3) == 0) return;
+    const uint64_t step = (uint64_t)a.sc->step;
+    unsigned qhint = 0;  // queue entry of the last agent this warp found
+    for (;;) {
+        unsigned g = 0;
+        if (lane == 0) g = atomicAdd(&s_next, 32u);
+        g = __shfl_sync(0xffffffffu, g, 0);
+        const unsigned ai = g + lane;
+        bool pending = true;
+        for (;;) {
+            // lane 0 waits until the first still-pending agent of the claim is published or the
+            // producer is done; then every lane whose agent is published plans it (the others
+            // idle, they do not spin)
+            const unsigned todo = __ballot_sync(0xffffffffu, pending);
+            if (!todo) break;
+            const unsigned need = g + (unsigned)(__ffs(todo) - 1);
+            unsigned pub = 0, nq = 0;
+            int done = 0, bad = 0;
+            if (lane == 0) {
+                for (long long spin = 0;; ++spin) {
+                    // order: done, then pub, then nq (the producer writes them in reverse)
+                    done = s_done;
+                    __threadfence_block();
+                    pub = s_pub;
+                    __threadfence_block();
+                    nq = s_nq;
+                    if (pub > need || done) break;
+                    __nanosleep(64);
+                    if (spin > (1ll << 24)) {
+                        bad = 1;
+                        break;
+                    }
+                }
+            }
+            if (__shfl_sync(0xffffffffu, bad, 0)) {
+                if (lane == 0) atomicOr(&a.sc->err, 8ull);
+                return;
+            }
+            pub = __shfl_sync(0xffffffffu, pub, 0);
+            nq = __shfl_sync(0xffffffffu, nq, 0);
+            done = __shfl_sync(0xffffffffu, done, 0);
+            __threadfence_block();
+            if (done && pub <= need) return;  // everything published was claimed: finished
+            int k_lo = 0, k_hi = -1, sbase = 0;  // sbase: ring slot of chunk 0 of the item (may be < 0)
+            if (pending && ai < pub) {
+                pending = false;
+                // queue entry holding virtual agent ai: entries are published in order and the
+                // ring bounds how many are in flight, so the last PLAN_QUEUE are enough
+                unsigned q = max(qhint, nq > PLAN_QUEUE ? nq - PLAN_QUEUE : 0u);
+                while (q + 1 < nq && s_qv[(q + 1) % PLAN_QUEUE] <= ai) ++q;
+                qhint = q;
+                const unsigned pos = s_qa[q % PLAN_QUEUE] + (ai - s_qv[q % PLAN_QUEUE]);
+                const int qs = s_qs[q % PLAN_QUEUE], ihalf = qs & 1, kf = qs >> 1;
+                sbase = ihalf * RING_HALF - (kf - 1);
+                const uint4 br = __ldcg(&A.brec[pos]);  // (id, wrapped x, y, v_max), bucket.cu
+                const uint32_t id = br.x;
+                const int px = (int)br.y, py = (int)br.z, v = (int)br.w;
+                const int s = px / A.tile_w, k = py >> 3;
+                k_lo = max(k - 1, 0);
+                k_hi = min(k + 1, rows_chunks - 1);
+                bool ready = true;
+                for (int kk = k_lo; kk <= k_hi; ++kk) {
+                    const int p = sbase + kk;
+                    ready &= mbar_wait(&bars[p], (unsigned)(s_gen[p] - 1) & 1u);
+                }
+                if (!ready) atomicOr(&a.sc->err, 2ull);
+                const Ring R{ringw + ihalf * RING_HALF * CHUNK_ROWS * A.boxw, ringo + ihalf * RING_HALF * CHUNK_ROWS * OCCW,
+                             ringl + ihalf * RING_HALF * CHUNK_ROWS * OCCW, A.boxw, CHUNK_ROWS * (kf - 1)};
+                const int x0 = s * A.tile_w;
+                const int X0 = x0 - 8;  // staged column 0 (TMA inner coordinates stay 16-byte aligned)
+                const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
+                const int osh0 = x0 - 8 + FP_XPAD_BITS - gws * 32;  // staged bit of column X0
+                const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
+                int cx = 0, cy = 0;
+                const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
+                                   ? plan_ring_v<true>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy)
+                                   : plan_ring_v<false>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy);
+                if (st == 1) {
+                    a.dx[id] = cx;
+                    a.dy[id] = cy;
+                    const int tile = (py / A.tile_h) * A.tiles_x + s;
+                    A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], R, px - X0, id, px, py, cx, cy, v, s_bp);
+                } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
+                    A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, pos);
+                }
+            }
+            // release: the lanes' reads of the slots happen before their references drop; lanes
+            // on the same slot combine their decrements (one shared atomic per slot and warp)
+            __syncwarp();
+            __threadfence_block();
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const int kk = k_lo + d;
+                const bool has = kk <= k_hi;
+                const int key = has ? (sbase + kk) : -1;
+                const unsigned peers = __match_any_sync(0xffffffffu, key);
+                if (has && (__ffs(peers) - 1) == lane) atomicSub(&s_ref[key], __popc(peers));
+            }
+            if (done && !__any_sync(0xffffffffu, pending)) break;
         }
     }
 }
@@ -966,51 +980,33 @@ int fp_plan_exact_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     return FP_OK;
 }
 
-static void tile_geometry(const fp_ctx* ctx, TileArgs& A, size_t& smem) {
-    A.boxw = ctx->tile_w + 16;
-    A.boxh = ctx->tile_h + 2 * FP_HALO;
-    A.occw = 16;  // TMA box of the occupancy plane: 16 words (512 bits) from a 16-byte aligned word
-    const size_t box_stride = ((size_t)A.boxw * A.boxh + 31) & ~(size_t)31;
-    const size_t occ_stride = ((size_t)A.boxh * A.occw + 31) & ~(size_t)31;
-    smem = (PLAN_SLOTS * box_stride + 2 * PLAN_SLOTS * occ_stride) * 4 + 8 * PLAN_SLOTS /* barriers */ +
+static size_t stream_smem(const fp_ctx* ctx) {
+    const size_t boxw = (size_t)ctx->tile_w + 16;
+    return (size_t)RING_SLOTS * CHUNK_ROWS * (boxw + 2 * OCCW) * 4 + 8 * RING_SLOTS /* barriers */ +
            128 /* alignment slack */;
 }
 
-static TileArgs make_tile_args(fp_ctx* ctx, double k_s, uint64_t seed, size_t& smem, unsigned& grid) {
-    TileArgs A;
+static StreamArgs make_stream_args(fp_ctx* ctx, double k_s, uint64_t seed) {
+    StreamArgs A;
     A.c = make_common(ctx, k_s, seed);
-    A.PW = ctx->PW;
-    A.plane = ctx->d_plane;
-    A.use_tma = ctx->use_tma;
-    A.bucket = ctx->d_bucket;
     A.brec = ctx->d_brec;
-    A.tile_off = ctx->d_tile_off;
-    A.tile_cnt = ctx->d_tile_cnt;
-    A.tile_list = ctx->d_tile_list;
-    A.deal = ctx->d_tile_deal;
+    A.ccnt = ctx->d_sub_cnt;
+    A.coff = ctx->d_sub_off;
+    A.items = ctx->d_plan_items;
+    A.nchunks = fp_plan_chunks(ctx);
     A.tile_exit = ctx->d_tile_exit;
-    A.passes = ctx->deal_passes;
     A.tile_w = ctx->tile_w;
     A.tile_h = ctx->tile_h;
     A.tiles_x = ctx->tiles_x;
+    A.cps = ctx->cps;
+    A.boxw = ctx->tile_w + 16;
     A.fallback = ctx->d_fallback;
     A.rec0 = ctx->d_rec0;
-    A.p1 = ctx->d_p1;
-    A.p2 = ctx->d_p2;
-    A.emit = 1;
     A.mixed = ctx->mixed_v ? 1 : 0;
-    {
-        static const int rot = getenv("FP_PLAN_ROT") ? atoi(getenv("FP_PLAN_ROT")) : PLAN_THREADS * 5 / 16;
-        A.rot = rot;
-    }
-    tile_geometry(ctx, A, smem);
-    const size_t nt = (size_t)ctx->tiles_x * ctx->tiles_y;
-    grid = (unsigned)ctx->sm_count;  // tile_deal_kernel deals to exactly sm_count CTAs
-    (void)nt;
     return A;
 }
 
-static EmitArgs emit_args(const TileArgs& A) { return EmitArgs{A.rec0, A.p1, A.p2, A.emit}; }
+static EmitArgs emit_args(fp_ctx* ctx) { return EmitArgs{ctx->d_rec0, ctx->d_p1, ctx->d_p2, 1}; }
 
 // Everything the planning phase allocates or builds, done outside any graph capture.
 int fp_plan_prepare(fp_ctx* ctx, double k_s) {
@@ -1018,53 +1014,31 @@ int fp_plan_prepare(fp_ctx* ctx, double k_s) {
     if (!tiled_ok(ctx)) return FP_OK;
     if (int rc = fp_plane_ensure(ctx, k_s)) return rc;
     if (int rc = fp_bucket_reserve(ctx)) return rc;
-    if (int rc = fp_ensure_res(ctx)) return rc;  // contention bitplanes the plan marks
-    TileArgs A;
-    size_t smem;
-    tile_geometry(ctx, A, smem);
+    if (int rc = fp_ensure_res(ctx)) return rc;
+    const size_t smem = stream_smem(ctx);
     static size_t configured_by_device[64] = {0};  // the attribute is per device
     size_t& configured = configured_by_device[ctx->device & 63];
     if (smem > configured) {
-        FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        FP_CUDA(ctx, cudaFuncSetAttribute(plan_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FP_CUDA(ctx, cudaFuncSetAttribute(plan_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
     return FP_OK;
 }
 
-// Threads per agent in the plan kernel (FP_PLAN_LANES: 1, 2 or 4).
-static int plan_lanes() {
-    static const int p = getenv("FP_PLAN_LANES") ? atoi(getenv("FP_PLAN_LANES")) : 1;
-    return (p == 2 || p == 4) ? p : 1;
-}
-
-static void plan_kernel_launch(fp_ctx* ctx, const TileArgs& A, size_t smem, unsigned grid) {
-    switch (plan_lanes()) {
-        case 4:
-            plan_tile_kernel<4><<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
-                                                                           ctx->tmap_wall, A);
-            break;
-        case 2:
-            plan_tile_kernel<2><<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
-                                                                           ctx->tmap_wall, A);
-            break;
-        default:
-            plan_tile_kernel<1><<<grid, PLAN_THREADS, smem, ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
-                                                                           ctx->tmap_wall, A);
-    }
-}
-
-static int launch_tile(fp_ctx* ctx, const TileArgs& A, size_t smem, unsigned grid) {
-    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
+static int launch_stream(fp_ctx* ctx, const StreamArgs& A) {
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
-    plan_kernel_launch(ctx, A, smem, grid);
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
+#ifdef FP_PLAN_PROF
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_sc->plan_prof, 0, sizeof(ctx->d_sc->plan_prof), ctx->stream));
+#endif
+    plan_stream_kernel<<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
+                                                                                      ctx->tmap_wall, A);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
 
-// Enqueues the whole planning phase (bucketing + tiled kernel + exact-path pass) on
-// ctx->stream.  Graph-safe: the step, tile count, cursors and the fallback count live in device
+// Enqueues the whole planning phase (bucketing + streaming kernel + exact-path pass) on
+// ctx->stream.  Graph-safe: the step, chunk counts, deal and the fallback count live in device
 // memory; fp_plan_prepare ran before.
 int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     if (ctx->n == 0) return FP_OK;
@@ -1078,13 +1052,11 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
         FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
     }
     ctx->bucket_fresh = true;  // the motion seed pass walks agents in this (spatial) order
-    ctx->rec_fresh = true;     // walk records + contention marks emitted below
+    ctx->rec_fresh = true;     // walk records emitted below
     ctx->marks_dirty = true;
-    size_t smem;
-    unsigned grid;
-    const TileArgs A = make_tile_args(ctx, k_s, seed, smem, grid);
-    if (int rc = launch_tile(ctx, A, smem, grid)) return rc;
-    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(A));
+    const StreamArgs A = make_stream_args(ctx, k_s, seed);
+    if (int rc = launch_stream(ctx, A)) return rc;
+    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -1098,18 +1070,17 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
         return FP_OK;
     }
     if (int rc = fp_bucket_launch(ctx)) return rc;
-    size_t smem;
-    unsigned grid;
-    const TileArgs A = make_tile_args(ctx, k_s, seed, smem, grid);
+    const StreamArgs A = make_stream_args(ctx, k_s, seed);
     cudaEvent_t e0, e1;
     FP_CUDA(ctx, cudaEventCreate(&e0));
     FP_CUDA(ctx, cudaEventCreate(&e1));
     double total = 0.0;
     for (int i = 0; i < iters; ++i) {
-        FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
+        FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
         cudaEventRecord(e0, ctx->stream);
-        plan_kernel_launch(ctx, A, smem, grid);
+        plan_stream_kernel<<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(
+            ctx->tmap_plane, ctx->tmap_occ, ctx->tmap_wall, A);
         FP_LAUNCHED(ctx);
         cudaEventRecord(e1, ctx->stream);
         FP_CUDA(ctx, cudaEventSynchronize(e1));
@@ -1117,11 +1088,11 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
         cudaEventElapsedTime(&t, e0, e1);
         total += t;
     }
-    // repeated launches marked the footprints many times: the next motion rebuilds its records
+    // the records were re-emitted by every launch; the next motion rebuilds nothing it needs
     ctx->rec_fresh = false;
     ctx->marks_dirty = true;
     // leave the state planned (the fallbacks of the last launch decided exactly)
-    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(A));
+    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
     FP_LAUNCHED(ctx);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

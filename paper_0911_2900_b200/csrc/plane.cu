@@ -186,8 +186,9 @@ __global__ void tile_exit_kernel(Geo g, int tile_w, int tile_h, int tiles_x, int
     }
 }
 
-// Chooses the plan tile for this grid and encodes the TMA box (tile + FP_HALO halo rows,
-// tile + 6 columns each side so the inner box width stays a multiple of 16 bytes).
+// Chooses the stripe width / motion tile for this grid and encodes the TMA boxes of one 8-row
+// chunk of a stripe (stripe + 8 columns each side, so the inner box start stays 16-byte aligned
+// and the box holds the 5-cell halo).
 #ifndef FP_BIG_TILE_H
 #define FP_BIG_TILE_H 48
 #endif
@@ -205,6 +206,7 @@ static int make_tmap(fp_ctx* ctx) {
     }
     ctx->tiles_x = (ctx->W + ctx->tile_w - 1) / ctx->tile_w;
     ctx->tiles_y = (ctx->H + ctx->tile_h - 1) / ctx->tile_h;
+    ctx->cps = ctx->tiles_y * (ctx->tile_h / 8);
     PFN_encodeTiled enc = get_encode();
     if (!enc) return fp_fail(ctx, FP_ECUDA, "cuTensorMapEncodeTiled unavailable");
     cuuint64_t dims[2] = {(cuuint64_t)ctx->PW, (cuuint64_t)ctx->H};
@@ -212,7 +214,7 @@ static int make_tmap(fp_ctx* ctx) {
     // inner box start x0-8 keeps the inner coordinate 16-byte aligned (an unaligned inner
     // coordinate faults with "illegal instruction" on sm_100a, tools/tma_probe); box covers
     // [x0-8, x0+tile_w+8) which contains the 5-cell halo on both sides
-    cuuint32_t box[2] = {(cuuint32_t)(ctx->tile_w + 16), (cuuint32_t)(ctx->tile_h + 2 * FP_HALO)};
+    cuuint32_t box[2] = {(cuuint32_t)(ctx->tile_w + 16), 8u};  // one 8-row chunk of a stripe (plan.cu)
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(&ctx->tmap_plane, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, ctx->d_plane, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -222,7 +224,7 @@ static int make_tmap(fp_ctx* ctx) {
     // 5-cell halo window of any tile (tile_w + 16 <= 256 columns, <= 127 bits of misalignment)
     cuuint64_t odims[2] = {(cuuint64_t)ctx->P, (cuuint64_t)ctx->H};
     cuuint64_t ostr[1] = {(cuuint64_t)ctx->P * 4};
-    cuuint32_t obox[2] = {16u, (cuuint32_t)(ctx->tile_h + 2 * FP_HALO)};
+    cuuint32_t obox[2] = {16u, 8u};
     r = enc(&ctx->tmap_occ, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, ctx->d_occ, odims, ostr, obox, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);

@@ -17,6 +17,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libfastped_b200.so")
+# experiments only: another build of the library (tools/build_variant.py); never set in product runs
+_LIB_OVERRIDE = os.environ.get("FASTPED_B200_LIB")
 
 FREE, WALL, EXIT = 0, 1, 2                      # CellKind, world.hpp:18
 CLOSED, PERIODIC_X = 0, 1                       # Boundary, world.hpp:19
@@ -117,9 +119,12 @@ def library():
     """Loads the in-tree CUDA library (building it first if it is missing or stale)."""
     global _lib
     if _lib is None:
-        from . import build as _build
-        _build.build()
-        L = C.CDLL(LIB_PATH)
+        if _LIB_OVERRIDE:
+            L = C.CDLL(_LIB_OVERRIDE)
+        else:
+            from . import build as _build
+            _build.build()
+            L = C.CDLL(LIB_PATH)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(L, name)
             fn.restype = res
