@@ -438,7 +438,7 @@ def ours_arm(args):
     a_start, a_end = b0 / (kernel_ms0 * 1e-3) / 1e9, b1 / (kernel_ms1 * 1e-3) / 1e9
     achieved = 0.5 * (a_start + a_end)
     t0_, t1_ = plan_traffic(args.config, "start"), plan_traffic(args.config, "end")
-    roof = {"kernel": "plan_tile_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+    roof = {"kernel": "plan_stream_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
             "unit": "GB/s", "frac": achieved / peak,
             "traffic": (0.5 * (t0_ + t1_)) if (t0_ and t1_) else None,
             "bytes_per_launch": 0.5 * (b0 + b1),

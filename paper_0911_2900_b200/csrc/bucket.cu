@@ -10,7 +10,8 @@
 //   bucket / brec           agent id and its planner record (id, x, y, v_max) per position
 //   tile_cnt / tile_off     per tile (row-major id), tile_list = the non-empty tiles,
 //   items                   motion seed work items (tile-list entry, chunk of SEED_ITEM agents)
-//   deal                    the plan kernel's per-CTA chunk ranges (equal cost)
+//   plan items              the plan kernel's work units: <= PLAN_ITEM_CHUNKS chunks of one
+//                           stripe and <= PLAN_ITEM_AGENTS of their agents
 // All passes are this file's kernels (no library primitives in the step).
 #include "internal.cuh"
 

@@ -4,10 +4,11 @@
 //            -> enumerate_candidates (planning.hpp:23-57), line_of_sight (world.hpp:181-191),
 //               potential_drop (planning.hpp:76-80), std::exp, sample_index (:63-73).
 //
-// Production path (plan_tile_kernel): a persistent CTA per SM walks the non-empty plan tiles.
-// For each tile, TMA brings the tile + 5-cell halo of the weight plane (plane.cu, 4 B/cell)
-// into shared memory (double-buffered, mbarrier completion) while the previous tile computes;
-// the occupancy bits of the same window are staged beside it.  One thread plans one agent:
+// Production path (plan_stream_kernel): a persistent, warp-specialised CTA per SM.  A producer
+// warp streams 8-row chunks of 240-column stripes of the weight plane (plane.cu, 4 B/cell), the
+// occupancy and the wall bitplanes into a shared-memory ring with TMA (mbarrier completion),
+// taking plan items (bucket.cu) from a global cursor; consumer warps plan one agent per lane as
+// soon as the rows its ball spans have landed:
 //   pass 1  rows centre-out, so the line-of-sight test of a cell only needs the wall bits of
 //           rows already seen (ball wall mask, 121 bits) AND a per-offset Bresenham path mask
 //           (constant memory); each valid candidate's weight m_c*2^(C_p-C_c) is built from the
@@ -260,7 +261,12 @@ __device__ __forceinline__ float drive_weight_f(double k_s, double g, int dx) {
 // Ring of RING_SLOTS 8-row chunks of one stripe (tile_w columns + 8 each side): weight-plane
 // words, occupancy bits and wall bits, staged by TMA.  Chunk k of the stripe lives in ring slot
 // k % RING_SLOTS.
+#ifndef PLAN_THREADS
 #define PLAN_THREADS 512
+#endif
+#ifndef FP_PLAN_NAP_MAX
+#define FP_PLAN_NAP_MAX 512  // ns, longest back-off of a waiting warp
+#endif
 #ifndef RING_SLOTS
 #define RING_SLOTS 24
 #endif
@@ -665,8 +671,10 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
             }
             const int p = half * RING_HALF + lane;
             if (lane < nk + 2 && refs != 0 && kk >= 0 && kk < rows_chunks) {
+                unsigned nap = 32;
                 for (long long spin = 0; *((volatile int*)&s_ref[p]) != 0; ++spin) {
-                    __nanosleep(64);
+                    __nanosleep(nap);
+                    nap = min(nap * 2u, (unsigned)FP_PLAN_NAP_MAX);
                     if (spin > (1ll << 24)) {
                         atomicOr(&a.sc->err, 4ull);
                         ok = false;
@@ -730,6 +738,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
             unsigned pub = 0, nq = 0;
             int done = 0, bad = 0;
             if (lane == 0) {
+                unsigned nap = 32;
                 for (long long spin = 0;; ++spin) {
                     // order: done, then pub, then nq (the producer writes them in reverse)
                     done = s_done;
@@ -738,7 +747,8 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                     __threadfence_block();
                     nq = s_nq;
                     if (pub > need || done) break;
-                    __nanosleep(64);
+                    __nanosleep(nap);  // backoff: idle lanes must not steal issue slots
+                    nap = min(nap * 2u, (unsigned)FP_PLAN_NAP_MAX);
                     if (spin > (1ll << 24)) {
                         bad = 1;
                         break;
