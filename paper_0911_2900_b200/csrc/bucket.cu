@@ -14,11 +14,10 @@
 //                           stripe and <= PLAN_ITEM_AGENTS of their agents
 // All passes are this file's kernels (no library primitives in the step).
 #include "internal.cuh"
+#include "scan.cuh"
 
-#define SCAN_BLOCK 1024
 #define PLAN_ITEM_CHUNKS 10   // chunks per plan item (plan.cu's ring holds two items of <= 12 slots)
 #define PLAN_ITEM_AGENTS 512  // agents per plan item at most
-#define SCAN_PER 4  // elements per thread in the scan passes
 
 __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* alive,
                                     const uint8_t* owned, uint32_t n, int tile_w, uint32_t cps, uint32_t* cnt,
@@ -38,87 +37,6 @@ __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, c
         chunk_of[i] = c;
         slot[i] = atomicAdd(&cnt[c], 1u);
     }
-}
-
-// Block-wide exclusive scan of one value per thread; *total = the block's sum.
-__device__ __forceinline__ uint32_t block_scan_excl(uint32_t v, uint32_t* s_warp, uint32_t* total) {
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    uint32_t incl = v;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    __syncthreads();  // s_warp free
-    if (lane == 31) s_warp[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-        const uint32_t wv = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0u;
-        uint32_t wi = wv;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += t;
-        }
-        s_warp[lane] = wi - wv;
-        if (lane == 31) s_warp[32] = wi;
-    }
-    __syncthreads();
-    const uint32_t r = s_warp[w] + incl - v;
-    *total = s_warp[32];
-    return r;
-}
-
-// Exclusive scan in three passes: per-block sums, one block scanning them, the block offsets
-// applied.  n <= SCAN_BLOCK * SCAN_PER * SCAN_BLOCK (4M chunks).
-__global__ void __launch_bounds__(SCAN_BLOCK) scan_sums_kernel(const uint32_t* in, uint32_t n, uint32_t* sums) {
-    __shared__ uint32_t s_warp[33];
-    const uint32_t base = blockIdx.x * SCAN_BLOCK * SCAN_PER + threadIdx.x * SCAN_PER;
-    uint32_t v = 0;
-#pragma unroll
-    for (int k = 0; k < SCAN_PER; ++k) v += base + k < n ? in[base + k] : 0u;
-    uint32_t total;
-    block_scan_excl(v, s_warp, &total);
-    if (threadIdx.x == 0) sums[blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(SCAN_BLOCK) scan_top_kernel(uint32_t* sums, uint32_t nb) {
-    __shared__ uint32_t s_warp[33];
-    const uint32_t v = threadIdx.x < nb ? sums[threadIdx.x] : 0u;
-    uint32_t total;
-    const uint32_t e = block_scan_excl(v, s_warp, &total);
-    if (threadIdx.x < nb) sums[threadIdx.x] = e;
-}
-
-__global__ void __launch_bounds__(SCAN_BLOCK) scan_apply_kernel(const uint32_t* in, uint32_t n, const uint32_t* sums,
-                                                                uint32_t* out) {
-    __shared__ uint32_t s_warp[33];
-    const uint32_t base = blockIdx.x * SCAN_BLOCK * SCAN_PER + threadIdx.x * SCAN_PER;
-    uint32_t v[SCAN_PER], t = 0;
-#pragma unroll
-    for (int k = 0; k < SCAN_PER; ++k) {
-        v[k] = base + k < n ? in[base + k] : 0u;
-        t += v[k];
-    }
-    uint32_t total;
-    uint32_t e = block_scan_excl(t, s_warp, &total) + sums[blockIdx.x];
-#pragma unroll
-    for (int k = 0; k < SCAN_PER; ++k) {
-        if (base + k < n) out[base + k] = e;
-        e += v[k];
-    }
-}
-
-static int exclusive_scan(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* sums) {
-    cudaStream_t s = ctx->stream;
-    const uint32_t per = SCAN_BLOCK * SCAN_PER;
-    const uint32_t nb = std::max<uint32_t>(1, (n + per - 1) / per);
-    if (nb > SCAN_BLOCK) return fp_fail(ctx, FP_ERUNTIME, "bucket: too many plan chunks for the scan");
-    scan_sums_kernel<<<nb, SCAN_BLOCK, 0, s>>>(in, n, sums);
-    FP_LAUNCHED(ctx);
-    scan_top_kernel<<<1, SCAN_BLOCK, 0, s>>>(sums, nb);
-    FP_LAUNCHED(ctx);
-    scan_apply_kernel<<<nb, SCAN_BLOCK, 0, s>>>(in, n, sums, out);
-    FP_LAUNCHED(ctx);
-    return FP_OK;
 }
 
 // Also writes the planner's record of the agent, (id, wrapped x, y, v_max), so the plan kernel
@@ -236,7 +154,7 @@ int fp_bucket_reserve(fp_ctx* ctx) {
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_cnt, nt * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_off, nt * 4));
         FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_list, nt * 4));
-        FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums, SCAN_BLOCK * 4));
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums, FP_SCAN_SUMS * 4));
         ctx->n_tiles_alloc = nt;
         ctx->n_chunks_alloc = nch;
         ctx->graph_valid = false;
@@ -274,7 +192,7 @@ int fp_bucket_launch(fp_ctx* ctx) {
                                           ctx->st.on ? ctx->st.d_owned : nullptr, n, ctx->tile_w, ctx->cps,
                                           ctx->d_sub_cnt, ctx->d_flags, ctx->d_cursor_b, &ctx->d_sc->n_planned);
     FP_LAUNCHED(ctx);
-    if (int rc = exclusive_scan(ctx, ctx->d_sub_cnt, ctx->d_sub_off, nch, ctx->d_scan_sums)) return rc;
+    if (int rc = fp_scan_u32(ctx, ctx->d_sub_cnt, ctx->d_sub_off, nch, ctx->d_scan_sums, s)) return rc;
     tile_sums_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s>>>(
         ctx->d_sub_cnt, ctx->d_sub_off, ctx->tiles_x, ctx->tiles_y, ctx->cps, ctx->tile_h / 8, ctx->d_tile_cnt,
         ctx->d_tile_off, ctx->d_tile_list, &ctx->d_sc->n_tiles);

@@ -234,6 +234,7 @@ struct fp_ctx {
     size_t n_tiles_alloc = 0;
     size_t n_chunks_alloc = 0;
     uint32_t* d_scan_sums = nullptr;  // block sums of the chunk scan (bucket.cu)
+    uint32_t* d_scan_sums2 = nullptr; // block sums of the order's scans (order.cu, stream2)
     uint4* d_plan_items = nullptr;     // plan kernel work items (bucket.cu)
     size_t plan_items_alloc = 0;
     uint2* d_seed_items = nullptr;    // (tile-list entry, chunk) per motion seed work item
@@ -345,6 +346,10 @@ int fp_plan_prepare(fp_ctx* ctx, double k_s);                         // plan.cu
 bool fp_plan_tiled(const fp_ctx* ctx);
 int fp_bucket_reserve(fp_ctx* ctx);                                   // bucket.cu
 uint32_t fp_plan_chunks(const fp_ctx* ctx);
+int fp_scan_u32(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* sums,
+                cudaStream_t s);                                      // scan.cu
+int fp_select_alive(fp_ctx* ctx, const uint8_t* alive, uint32_t n, uint32_t* ids, unsigned long long* count,
+                    uint32_t* sums, cudaStream_t s);
 int fp_exits_sort_launch(fp_ctx* ctx);                                // move.cu
 int fp_strip_reserve(fp_ctx* ctx);                                    // strip.cu
 int fp_strip_begin_launch(fp_ctx* ctx);

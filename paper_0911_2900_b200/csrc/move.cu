@@ -24,7 +24,6 @@
 // many agents are pending, then block 0 finishes the last TAIL_MAX alone in shared memory
 // while the other blocks zero the contention bitplanes for the next phase.
 #include <cooperative_groups.h>
-#include <cub/cub.cuh>
 
 #include "motion_rec.cuh"
 
@@ -1379,16 +1378,33 @@ int fp_exits_sort_launch(fp_ctx* ctx) {
     return FP_OK;
 }
 
-// Sorts the exit records of the last phase by rank (processing order) for fp_get_exited.
+// Exit records are (rank << 32 | id) with distinct ranks in [0, n_alive): a rank flag array,
+// its exclusive scan, and a scatter put them in processing order.
+__global__ void exits_flag_kernel(const unsigned long long* exits, uint32_t ne, uint32_t* flag) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ne) flag[(uint32_t)(exits[i] >> 32)] = 1u;
+}
+
+__global__ void exits_place_kernel(const unsigned long long* exits, uint32_t ne, const uint32_t* pos,
+                                   unsigned long long* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ne) out[pos[(uint32_t)(exits[i] >> 32)]] = exits[i];
+}
+
+// Sorts the exit records of the last phase by rank (processing order) for fp_get_exited, when
+// there were too many for the motion graph's one-block sort (host path, after the step's sync;
+// the order scratch d_cnt / d_off is free until the next step).
 int fp_exits_finish(fp_ctx* ctx) {
     const uint32_t ne = ctx->n_exits;
     if (ne <= 1 || ctx->h_sc->exits_sorted) return FP_OK;  // sorted in the motion graph
-    size_t need = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, need, ctx->d_exits, ctx->d_exits_sorted, (int)ne, 0, 64, ctx->stream);
-    if (int rc = fp_ensure_temp(ctx, need)) return rc;
-    FP_CUDA(ctx, cub::DeviceRadixSort::SortKeys(ctx->d_temp, need, ctx->d_exits, ctx->d_exits_sorted, (int)ne, 0, 64,
-                                                ctx->stream));
-    ctx->ctr.kernel_launches += 4;
+    const uint32_t na = std::max<uint32_t>(ctx->n_order, 1);
+    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 1024 * 4));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, (size_t)na * 4, ctx->stream));
+    exits_flag_kernel<<<fp_blocks(ne, 256), 256, 0, ctx->stream>>>(ctx->d_exits, ne, ctx->d_cnt);
+    FP_LAUNCHED(ctx);
+    if (int rc = fp_scan_u32(ctx, ctx->d_cnt, ctx->d_off, na, ctx->d_scan_sums2, ctx->stream)) return rc;
+    exits_place_kernel<<<fp_blocks(ne, 256), 256, 0, ctx->stream>>>(ctx->d_exits, ne, ctx->d_off, ctx->d_exits_sorted);
+    FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaMemcpyAsync(ctx->d_exits, ctx->d_exits_sorted, ne * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToDevice, ctx->stream));
     return FP_OK;

@@ -14,9 +14,6 @@
 // Work is O(n) with counting-sort buckets (expected |L_q| ~ ln(n/q)); chains are short.
 // The alive count comes from device memory, so the whole sequence is graph-capturable.
 // Pinned against the sequential loop by tests (oracle.movement_order, n up to 10^7).
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-
 #include "internal.cuh"
 
 #define GS_LOOP(i, n) for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += gridDim.x * blockDim.x)
@@ -106,11 +103,6 @@ __global__ void fy_final_kernel(const unsigned long long* pn, const uint32_t* j,
     }
 }
 
-struct IsAlive {
-    const uint8_t* alive;
-    __device__ __forceinline__ bool operator()(uint32_t i) const { return alive[i] != 0; }
-};
-
 int fp_ensure_temp(fp_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->temp_bytes) return FP_OK;
     if (ctx->d_temp) {
@@ -136,11 +128,7 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cursor, 0, sizeof(uint32_t) * cap, s));
     fy_targets_kernel<<<G, 256, 0, s>>>(n_dev, seed, step_dev, ctx->d_j, ctx->d_cnt);
     FP_LAUNCHED(ctx);
-    size_t need = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, need, ctx->d_cnt, ctx->d_off, (int)cap, s);
-    if (need > ctx->temp_bytes) return fp_fail(ctx, FP_ERUNTIME, "order: scratch not reserved");
-    FP_CUDA(ctx, cub::DeviceScan::ExclusiveSum(ctx->d_temp, need, ctx->d_cnt, ctx->d_off, (int)cap, s));
-    ctx->ctr.kernel_launches += 2;
+    if (int rc = fp_scan_u32(ctx, ctx->d_cnt, ctx->d_off, cap, ctx->d_scan_sums2, s)) return rc;
     fy_scatter_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_j, ctx->d_cursor, ctx->d_off, ctx->d_fy_bucket);
     FP_LAUNCHED(ctx);
     fy_link_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_off, ctx->d_cnt, ctx->d_fy_bucket, ctx->d_succ, ctx->d_nxt);
@@ -152,16 +140,11 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
     return FP_OK;
 }
 
-// Reserves the CUB scratch of the order + bucketing stages (outside any graph capture).
+// Reserves the order stage's scratch (outside any graph capture).
 int fp_order_reserve(fp_ctx* ctx) {
     const uint32_t n = std::max<uint32_t>(ctx->n, 1);
-    if (ctx->order_reserved_n == n && ctx->d_temp) return FP_OK;
-    size_t a = 0, b = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, a, ctx->d_cnt, ctx->d_off, (int)n, ctx->stream);
-    thrust::counting_iterator<uint32_t> it(0);
-    cub::DeviceSelect::If(nullptr, b, it, ctx->d_alive_ids, &ctx->d_sc->n_alive, (int)n, IsAlive{ctx->d_alive},
-                          ctx->stream);
-    if (int rc = fp_ensure_temp(ctx, std::max(a, b) * 2 + 4096)) return rc;
+    if (ctx->order_reserved_n == n && ctx->d_scan_sums2) return FP_OK;
+    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 1024 * 4));
     ctx->order_reserved_n = n;
     return FP_OK;
 }
@@ -180,14 +163,7 @@ int fp_order_positions(fp_ctx* ctx, uint32_t n, uint64_t seed, int64_t step, uin
 int fp_order_launch(fp_ctx* ctx, uint64_t seed, cudaStream_t s) {
     const uint32_t n = ctx->n;
     if (n == 0) return FP_OK;
-    thrust::counting_iterator<uint32_t> it(0);
-    size_t need = 0;
-    cub::DeviceSelect::If(nullptr, need, it, ctx->d_alive_ids, &ctx->d_sc->n_alive, (int)n, IsAlive{ctx->d_alive}, s);
-    if (need > ctx->temp_bytes / 2) return fp_fail(ctx, FP_ERUNTIME, "order: scratch not reserved");
-    // select uses the upper half of the scratch so it never aliases the scan's
-    void* t2 = (char*)ctx->d_temp + ctx->temp_bytes / 2;
-    FP_CUDA(ctx, cub::DeviceSelect::If(t2, need, it, ctx->d_alive_ids, &ctx->d_sc->n_alive, (int)n,
-                                       IsAlive{ctx->d_alive}, s));
-    ctx->ctr.kernel_launches += 2;
+    if (int rc = fp_select_alive(ctx, ctx->d_alive, n, ctx->d_alive_ids, &ctx->d_sc->n_alive, ctx->d_scan_sums2, s))
+        return rc;
     return fy_run(ctx, s, &ctx->d_sc->n_alive, n, seed, &ctx->d_sc->step, ctx->d_alive_ids, ctx->d_order, ctx->d_rank);
 }

@@ -1,0 +1,23 @@
+"""Motion-phase breakdown (device globaltimer counters of fp_counters) along a plaza run."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_0911_2900_b200 import fastped as fp, scenarios  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "plaza"
+wl = scenarios.build(cfg)
+st = fp.SimState(wl.grid, None, wl.roster)
+if wl.potential:
+    st.set_potential(wl.potential, wl.drive_gradient)
+p = fp.SimParams(k_s=wl.k_s, seed=wl.seed, steps=1)
+marks = {1, 10, 50, 100, 150, 200, 250, 300, 350, 395}
+tot = 0.0
+for s in range(396):
+    fp.step(st, p)
+    if s in marks:
+        c = st.counters()
+        us = lambda k: c[k] / 1e3  # noqa: E731
+        print(f"step {s:3d}: alive {st.alive} contended {c['motion_contended']:7d} | mark {us('motion_mark_ns'):6.1f} "
+              f"seed {us('motion_seed_ns'):6.1f} prep {us('motion_prep_ns'):6.1f} grid {us('motion_grid_ns'):6.1f} "
+              f"({c['motion_grid_rounds']} rounds) tail {us('motion_tail_ns'):6.1f} us", flush=True)
