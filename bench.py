@@ -356,6 +356,7 @@ def ours_arm(args):
     with Clocks(local) as clk:
         rs = fp.run(st, params)
     torch.cuda.synchronize()
+    run_dx = st.run_dx
     c1 = st.counters()
     # max over ranks of the device time; the agent-updates are the simulation's (global on every
     # strip rank, so rank 0's count is the job's)
@@ -465,6 +466,12 @@ def ours_arm(args):
                    "sample": f"first {r['steps']} of {args.steps} steps of {args.config} ({n} agents), "
                              f"{r['seconds']:.1f} s, reference run() on {cores} physical cores, {cpu_model()}"}
 
+    fd = None
+    if wl.potential == fp.DRIVE_X:  # fundamental-diagram sampling (bench.hpp:244-305), fused in the motion
+        free_area = float(wl.grid.free_cell_count()) * wl.grid.cell_size ** 2
+        speed = run_dx * wl.grid.cell_size / max(float(rs.agent_updates), 1.0)  # dt = 1 s
+        fd = {"density_per_m2": n / free_area, "mean_speed_mps": speed, "flow_per_m_s": n / free_area * speed,
+              "note": "sum of segment_dx per step, reduced in the motion kernel (timed run)"}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": wall / max(rs.steps, 1) * 1e3, "higher_is_better": True,
            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -474,7 +481,7 @@ def ours_arm(args):
                           else "single",
            "phases_ms": {"plan": rs.plan_time_s * 1e3, "move": rs.move_time_s * 1e3, "total": rs.wall_time_s * 1e3},
            "full_run": full, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-           "realtime_capacity": capacity,
+           "realtime_capacity": capacity, "fundamental_diagram": fd,
            "gpu_launches": int(c1["kernel_launches"] - c0["kernel_launches"]),
            "motion_rounds_per_step": (c1["motion_rounds"] - c0["motion_rounds"]) / max(rs.steps, 1),
            "plan_fallbacks_per_step": (c1["plan_fallbacks"] - c0["plan_fallbacks"]) / max(rs.steps, 1)}

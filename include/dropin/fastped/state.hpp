@@ -38,10 +38,17 @@ struct Mirror {
     std::int64_t step = -1;
     int potential = -1;
     double gradient = 0.0;
+    // ScheduleParams::gpus > 1: one strip context per GPU, driven from this thread (fp_strips_*)
+    std::vector<fp_ctx*> strips;
     Mirror() = default;
     Mirror(const Mirror&) = delete;
     Mirror& operator=(const Mirror&) = delete;
+    void drop_strips() {
+        for (fp_ctx* c : strips) fp_destroy(c);
+        strips.clear();
+    }
     ~Mirror() {
+        drop_strips();
         if (ctx) fp_destroy(ctx);
     }
 };
@@ -104,6 +111,75 @@ struct SimState {
             b200::check(fp_set_desired(m.ctx, dx.data(), dy.data()), m.ctx);
         }
         return m.ctx;
+    }
+
+    /// The strip set for `gpus` x-strips (rank r on device (device() + r) % device count; one
+    /// GPU gives virtual strips), loaded with the host state.  Rebuilt when the count changes.
+    fp_ctx* const* strips_for(int gpus) const {
+        b200::Mirror& m = *dev;
+        if ((int)m.strips.size() != gpus) {
+            m.drop_strips();
+            const fp_grid_desc d = b200::desc_of(*grid);
+            const std::vector<std::uint8_t> cells = b200::cells_of(*grid);
+            int ndev = 1;
+            if (fp_device_count(&ndev) != FP_OK || ndev < 1) ndev = 1;
+            for (int r = 0; r < gpus; ++r) {
+                fp_ctx* c = nullptr;
+                b200::check(fp_create(&d, cells.data(), field->s.data(), (b200::device() + r) % ndev, &c));
+                m.strips.push_back(c);
+                std::int32_t lo = 0, hi = 0;
+                b200::check(fp_strip_bounds(grid->width(), r, gpus, &lo, &hi));
+                const std::size_t n = agents.size();
+                std::vector<std::int32_t> x(n ? n : 1), y(n ? n : 1), v(n ? n : 1);
+                std::vector<std::uint8_t> a(n ? n : 1);
+                for (std::size_t i = 0; i < n; ++i) {
+                    x[i] = agents[i].pos.x, y[i] = agents[i].pos.y, v[i] = agents[i].v_max;
+                    a[i] = agents[i].alive ? 1 : 0;
+                }
+                b200::check(fp_set_agents(c, static_cast<std::uint32_t>(n), x.data(), y.data(), v.data(), a.data(), step), c);
+                b200::check(fp_strip_config(c, r, gpus, lo, hi, 0, 0), c);
+            }
+        }
+        // the host state (the reference's authoritative fields) onto every rank
+        const std::size_t n = agents.size();
+        std::vector<std::int32_t> x(n ? n : 1), y(n ? n : 1), v(n ? n : 1);
+        std::vector<std::uint8_t> a(n ? n : 1);
+        for (std::size_t i = 0; i < n; ++i) {
+            x[i] = agents[i].pos.x, y[i] = agents[i].pos.y, v[i] = agents[i].v_max;
+            a[i] = agents[i].alive ? 1 : 0;
+        }
+        for (fp_ctx* c : m.strips) {
+            b200::check(fp_set_agents(c, static_cast<std::uint32_t>(n), x.data(), y.data(), v.data(), a.data(), step), c);
+            b200::check(fp_set_potential(c, static_cast<int>(potential), drive_gradient), c);
+        }
+        return m.strips.data();
+    }
+
+    /// Strip ranks -> host: every agent from the rank that owns it, occupancy, counters.
+    void pull_strips() {
+        b200::Mirror& m = *dev;
+        const std::size_t n = agents.size();
+        std::vector<std::int32_t> x(n ? n : 1), y(n ? n : 1);
+        std::vector<std::uint8_t> a(n ? n : 1), o(n ? n : 1);
+        for (std::size_t r = 0; r < m.strips.size(); ++r) {
+            fp_ctx* c = m.strips[r];
+            b200::check(fp_get_agents(c, x.data(), y.data(), a.data()), c);
+            b200::check(fp_strip_get_owned(c, o.data()), c);
+            // rank 0 first for everyone (agents nobody owns -- exited in a resolved walk, or dead from
+            // the start -- are identical on every rank), then each agent from the rank owning it
+            for (std::size_t i = 0; i < n; ++i)
+                if (r == 0 || o[i]) {
+                    agents[i].pos = Cell{x[i], y[i]};
+                    agents[i].alive = a[i] != 0;
+                }
+        }
+        occupancy.assign(static_cast<std::size_t>(grid->width()) * grid->height(), kEmpty);
+        for (std::size_t i = 0; i < n; ++i)
+            if (agents[i].alive) occupancy[grid->index(grid->normalize(agents[i].pos))] = static_cast<std::int32_t>(i);
+        b200::check(fp_get_alive_count(m.strips[0], &alive), m.strips[0]);
+        b200::check(fp_get_step(m.strips[0], &step), m.strips[0]);
+        m.step = -1;  // the single-device mirror is stale now
+        m.x.clear();
     }
 
     /// Device -> host: desired cells only (after plan_phase).

@@ -89,6 +89,8 @@ typedef struct {
 } fp_counters;
 
 const char* fp_version(void);
+/* CUDA devices visible to the library (strip placement). */
+int fp_device_count(int* n);
 const char* fp_last_error(const fp_ctx* ctx);
 
 /* compute_blocksize(number_of_agents, cores) -- engine.hpp:27-33 (host arithmetic). */
@@ -121,6 +123,8 @@ int fp_get_alive_count(const fp_ctx* ctx, int64_t* alive);
  * each step of run): the per-step x displacement fundamental_diagram accumulates on the host
  * from positions (bench.hpp:291-302), reduced on the device during the walks instead. */
 int fp_get_last_dx(const fp_ctx* ctx, int64_t* dx);
+/* The same sum over every step of the last fp_run (the fundamental diagram's flow over a run). */
+int fp_get_run_dx(const fp_ctx* ctx, int64_t* dx);
 /* SimState::potential / drive_gradient -- state.hpp:32-33 */
 int fp_set_potential(fp_ctx* ctx, int kind, double drive_gradient);
 /* SimState::desired (scratch between phases); injected by motion-only tests. */

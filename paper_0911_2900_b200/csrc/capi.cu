@@ -35,6 +35,14 @@ extern "C" const char* fp_last_error(const fp_ctx* ctx) {
     return ctx ? ctx->err.c_str() : g_error.c_str();
 }
 
+extern "C" int fp_device_count(int* n) {
+    if (!n) return fail(nullptr, FP_EINVAL, "null argument");
+    *n = 0;
+    cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) return fail(nullptr, FP_ECUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    return FP_OK;
+}
+
 extern "C" int fp_compute_blocksize(int64_t agents, int cores, int32_t* out) {
     if (cores < 1) return fail(nullptr, FP_EINVAL, "compute_blocksize: cores must be >= 1");
     if (agents < 0) return fail(nullptr, FP_EINVAL, "compute_blocksize: agent count must be >= 0");
@@ -445,6 +453,11 @@ extern "C" int fp_get_last_dx(const fp_ctx* c, int64_t* dx) {
     *dx = c->last_dx;
     return FP_OK;
 }
+extern "C" int fp_get_run_dx(const fp_ctx* c, int64_t* dx) {
+    if (!c || !dx) return fail(nullptr, FP_EINVAL, "null argument");
+    *dx = (int64_t)c->h_sc->tot_dx;
+    return FP_OK;
+}
 extern "C" int fp_get_alive_count(const fp_ctx* c, int64_t* a) {
     if (!c || !a) return fail(nullptr, FP_EINVAL, "null argument");
     *a = c->alive;
@@ -655,6 +668,7 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
 __global__ void run_begin_kernel(DevScalars* sc) {
     sc->tot_exits = 0;
     sc->tot_disp = 0;
+    sc->tot_dx = 0;
     sc->tot_updates = 0;
 }
 

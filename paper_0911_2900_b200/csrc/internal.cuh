@@ -117,6 +117,7 @@ struct DevScalars {
     long long step_dx;            // sum of segment_dx(start, end) over the last move phase
     unsigned long long tot_exits; // accumulated over a run
     unsigned long long tot_disp;  // accumulated over a run
+    long long tot_dx;             // sum of segment_dx over the run (fundamental-diagram flow)
     unsigned long long tot_updates;  // sum of alive counts entering each step
     unsigned long long fallbacks; // exact-path re-samples
     unsigned long long n_tiles;   // non-empty plan tiles this step

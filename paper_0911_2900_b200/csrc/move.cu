@@ -30,6 +30,9 @@
 namespace cg = cooperative_groups;
 
 #define MOVE_THREADS 512
+#ifndef FP_MOVE_BLOCKS_PER_SM
+#define FP_MOVE_BLOCKS_PER_SM 2  // cooperative CTAs per SM (bounded by occupancy)
+#endif
 
 __constant__ signed char c_bpath[121][5][2];
 static bool g_bpath_ready[64] = {false};
@@ -1200,6 +1203,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
         const unsigned long long d = a.sc->disp;
         a.sc->disp = d & 0xFFFFFFFFull;
         a.sc->step_dx = (long long)(int)(unsigned)(d >> 32);
+        a.sc->tot_dx += a.sc->step_dx;
         a.sc->tot_disp += d & 0xFFFFFFFFull;
     }
 }
@@ -1305,7 +1309,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
         int per_sm = 0;
         FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS,
                                                                    MOVE_DYN_SMEM));
-        move_blocks = std::max(1, std::min(per_sm, 2)) * ctx->sm_count;
+        move_blocks = std::max(1, std::min(per_sm, FP_MOVE_BLOCKS_PER_SM)) * ctx->sm_count;
     }
     MoveArgs a;
     a.g = fp_geo(ctx);
@@ -1398,7 +1402,7 @@ int fp_exits_finish(fp_ctx* ctx) {
     const uint32_t ne = ctx->n_exits;
     if (ne <= 1 || ctx->h_sc->exits_sorted) return FP_OK;  // sorted in the motion graph
     const uint32_t na = std::max<uint32_t>(ctx->n_order, 1);
-    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 1024 * 4));
+    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 8192 * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, (size_t)na * 4, ctx->stream));
     exits_flag_kernel<<<fp_blocks(ne, 256), 256, 0, ctx->stream>>>(ctx->d_exits, ne, ctx->d_cnt);
     FP_LAUNCHED(ctx);

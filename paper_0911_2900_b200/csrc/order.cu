@@ -144,7 +144,7 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
 int fp_order_reserve(fp_ctx* ctx) {
     const uint32_t n = std::max<uint32_t>(ctx->n, 1);
     if (ctx->order_reserved_n == n && ctx->d_scan_sums2) return FP_OK;
-    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 1024 * 4));
+    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 8192 * 4));
     ctx->order_reserved_n = n;
     return FP_OK;
 }

@@ -16,14 +16,27 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_sums_kernel(const uint32_t
     if (threadIdx.x == 0) sums[blockIdx.x] = total;
 }
 
-// Exclusive scan of the tile sums in place; the grand total to *total_out (when given).
+// Exclusive scan of the tile sums in place (up to FP_SCAN_SUMS: 8 per thread); the grand total
+// to *total_out (when given).
 __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_top_kernel(uint32_t* sums, uint32_t nb,
                                                                   unsigned long long* total_out) {
     __shared__ uint32_t s_warp[33];
-    const uint32_t v = threadIdx.x < nb ? sums[threadIdx.x] : 0u;
+    constexpr int PER = FP_SCAN_SUMS / FP_SCAN_BLOCK;
+    uint32_t v[PER], t = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint32_t i = threadIdx.x * PER + k;
+        v[k] = i < nb ? sums[i] : 0u;
+        t += v[k];
+    }
     uint32_t total;
-    const uint32_t e = block_scan_excl(v, s_warp, &total);
-    if (threadIdx.x < nb) sums[threadIdx.x] = e;
+    uint32_t e = block_scan_excl(t, s_warp, &total);
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const uint32_t i = threadIdx.x * PER + k;
+        if (i < nb) sums[i] = e;
+        e += v[k];
+    }
     if (threadIdx.x == 0 && total_out) *total_out = total;
 }
 
@@ -78,7 +91,7 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_scatter_kernel(const uin
 
 int fp_scan_u32(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* sums, cudaStream_t s) {
     const uint32_t nb = std::max<uint32_t>(1, (n + FP_SCAN_TILE - 1) / FP_SCAN_TILE);
-    if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "scan: more than 16M elements");
+    if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "scan: more than 134M elements");
     scan_sums_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(in, n, sums);
     FP_LAUNCHED(ctx);
     scan_top_kernel<<<1, FP_SCAN_BLOCK, 0, s>>>(sums, nb, nullptr);
@@ -91,7 +104,7 @@ int fp_scan_u32(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint
 int fp_select_alive(fp_ctx* ctx, const uint8_t* alive, uint32_t n, uint32_t* ids, unsigned long long* count,
                     uint32_t* sums, cudaStream_t s) {
     const uint32_t nb = std::max<uint32_t>(1, (n + FP_SCAN_TILE - 1) / FP_SCAN_TILE);
-    if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "select: more than 16M agents");
+    if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "select: more than 134M agents");
     select_sums_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(alive, n, sums);
     FP_LAUNCHED(ctx);
     scan_top_kernel<<<1, FP_SCAN_BLOCK, 0, s>>>(sums, nb, count);

@@ -6,7 +6,7 @@
 
 #define FP_SCAN_BLOCK 1024
 #define FP_SCAN_PER 16                           // elements per thread in the scan passes
-#define FP_SCAN_SUMS 1024                        // block sums: n <= 1024 * 1024 * 16
+#define FP_SCAN_SUMS 8192                        // tile sums: n <= 8192 * 16384 (134M)
 #define FP_SCAN_TILE (FP_SCAN_BLOCK * FP_SCAN_PER)
 
 // Block-wide exclusive scan of one value per thread; *total = the block's sum.  s_warp: 33

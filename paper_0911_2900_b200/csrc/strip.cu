@@ -448,7 +448,9 @@ __global__ void __launch_bounds__(1024) strip_finish_kernel(const unsigned char*
         const unsigned long long all_hops = hops + (rh & 0xFFFFFFFFull);
         sc->tot_disp += all_hops - sc->disp;
         sc->disp = all_hops;
+        const long long local_dx = sc->step_dx;
         sc->step_dx = (long long)dx + (long long)(int)(unsigned)(rh >> 32);
+        sc->tot_dx += sc->step_dx - local_dx;
         sc->strip_rexits = 0;
         sc->strip_nc = 0;
         sc->exits_sorted = 0;

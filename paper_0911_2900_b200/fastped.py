@@ -67,6 +67,7 @@ _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 SIGNATURES = {
     "fp_version": (C.c_char_p, []),
     "fp_last_error": (C.c_char_p, [C.c_void_p]),
+    "fp_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "fp_compute_blocksize": (C.c_int, [C.c_int64, C.c_int, C.POINTER(C.c_int32)]),
     "fp_create": (C.c_int, [C.POINTER(_Grid), _u8p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]),
     "fp_destroy": (None, [C.c_void_p]),
@@ -78,6 +79,7 @@ SIGNATURES = {
     "fp_get_step": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "fp_get_alive_count": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "fp_get_last_dx": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "fp_get_run_dx": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
     "fp_set_potential": (C.c_int, [C.c_void_p, C.c_int, C.c_double]),
     "fp_set_desired": (C.c_int, [C.c_void_p, _i32p, _i32p]),
     "fp_plan": (C.c_int, [C.c_void_p, C.c_double, C.c_uint64]),
@@ -407,6 +409,13 @@ class SimState:
         """Sum of segment_dx(x before, x after) over all agents in the last move phase."""
         v = C.c_int64()
         _check(library().fp_get_last_dx(self._ctx, C.byref(v)), self._ctx)
+        return v.value
+
+    @property
+    def run_dx(self) -> int:
+        """Sum of segment_dx over every step of the last run()."""
+        v = C.c_int64()
+        _check(library().fp_get_run_dx(self._ctx, C.byref(v)), self._ctx)
         return v.value
 
     # -- dumps

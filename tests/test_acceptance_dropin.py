@@ -54,3 +54,19 @@ def test_reference_acceptance_suite_on_device():
     assert sorted(res) == list(range(1, 10)), out
     failed = [k for k in MUST_PASS if res[k] != "PASS"]
     assert not failed, out
+
+
+STRIPS = os.path.join(ROOT, "tests", "native", "_bin", "strips_dropin_check")
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("gpus", [2, 3])
+def test_dropin_schedule_gpus_equals_one_gpu(gpus):
+    """The reference's API (make_plaza / make_scenario / spawn_agents from its own
+    scenario_io.hpp) through the overlay with ScheduleParams{cores, gpus}: x strips driven from
+    one thread (virtual strips on one GPU) equal gpus = 1 at every step and over run()."""
+    if not os.path.exists(STRIPS):
+        pytest.skip("strips_dropin_check not built (reference headers absent at build time)")
+    p = subprocess.run([STRIPS, str(gpus), "40"], capture_output=True, text=True, timeout=550)
+    assert p.returncode == 0 and p.stdout.startswith("ok"), p.stdout + p.stderr

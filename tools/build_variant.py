@@ -1,5 +1,5 @@
 """Builds the library with extra nvcc defines into another path (A/B experiments):
-python tools/build_variant.py exp/lib_s4h32.so -DPLAN_SLOTS=4 -DFP_BIG_TILE_H=32"""
+python tools/build_variant.py exp/lib_t640.so -DPLAN_THREADS=640"""
 import os
 import sys
 
