@@ -71,10 +71,12 @@ struct MoveArgs {
     unsigned npos_cap;             // bucket positions: <= 6 per contended agent
     unsigned* bcnt;                // per bucket: entries counted (zero between phases)
     unsigned* bbase;               // per bucket: its first position
-    unsigned* bcur;                // per bucket: position of its current earliest agent
+    unsigned* bown;                // per bucket: position of the agent standing on the cell, BK_NIL if none
+    uint8_t* bocc0;                // per bucket: the cell's occupancy when the rounds begin
     uint2* brank;                  // per position (placement order): (rank, agent * 8 + cell)
     unsigned* long_list;           // buckets longer than BK_SORT_REG (ranked by warps)
-    uint8_t* bdone;                // per position (rank order): that agent has walked
+    uint8_t* bdone;                // per position (rank order): 0 pending, 1 walked, 2 walked and stopped here
+    uint8_t* eoff;                 // 8 per contended agent: offset of its position in each bucket
     uint2* entry;                  // 6 per contended agent: (slot, then position; bucket) per
                                    // footprint cell; BK_NIL/BK_NIL for an uncontended cell
     // contended-index pending lists (ping-pong), carved from rec[0] (free after step 2)
@@ -219,18 +221,28 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
 // ------------------------------------------------------------------ grid-wide reservation rounds
 // Every contended cell (covered by two or more footprints, P2) is numbered densely (p2_number)
 // and holds a bucket: the contended agents whose footprint has the cell, in rank (processing)
-// order, at positions [bbase[b], bbase[b] + n_b) of one array.  Agents leave a bucket in rank
-// order -- an agent walks only as the earliest pending agent of every contended cell it has --
-// so bcur[b], the position of the cell's current earliest agent, only ever steps by one: the
-// agent at position p owns the cell iff bcur[b] == p, and after its walk it sets bcur[b] = p + 1
-// and bdone[p].  A blocked agent at p waits for bdone[p - 1]: its predecessor in the bucket
-// walks only after everyone before it, so one byte says when the cell is its own.  cur and done
-// are a few MB and stay in L2 through the rounds.  Built per phase by
-//   bk_count  per contended agent: its slot k in each of its buckets (one atomic counter each)
+// order, at positions [bbase[b], bbase[b] + n_b) of one array.  When an agent walks
+// (engine.hpp:116-129) a path cell c blocks it iff c is occupied at its turn, and for a contended
+// cell that is decided by the bucket alone:
+//   * the agent standing on c at the start (bown) has not walked yet -- it comes later in the
+//     order -- or it is earlier and stayed;
+//   * a static occupant (bocc0 without bown: nobody stands there who will move);
+//   * an earlier agent of the bucket stopped on c.
+// So an agent at position p resolves c as soon as the done bytes of the positions before p say
+// so: a 2 there (an earlier agent ended its walk on c) blocks it whatever the pending ones do;
+// all of them 1 (walked, left or passed) frees it; otherwise it waits for the first pending one.
+// An agent walks once every path cell up to the one that stops it is resolved -- the cells
+// behind that, and its own start cell, never make it wait -- and then writes its done bytes:
+// 2 on the cell it ends on (its start if it stays), 1 on the others.  Nothing else of its walk
+// is read by the other contended agents during the phase (an uncontended cell is only ever
+// touched by its one agent), so no fence orders the occupancy updates before the done bytes.
+// bbase, bown and done are a few MB and stay in L2 through the rounds.  Built per phase by
+//   bk_count  per contended agent: its slot k in each of its buckets (one atomic counter each),
+//             the cells' occupancy (bocc0)
 //   bk_scan   bbase = exclusive prefix of the bucket sizes (two passes like p2_number)
 //   bk_place  brank[bbase + k] = (rank, agent * 8 + cell)
 //   bk_sort   per bucket: each entry's position = bbase + #{ranks below its own}, handed to its
-//             agent; bcur = bbase; the bucket's done flags cleared
+//             agent; bown; the bucket's done flags cleared
 #define BK_EMPTY 0xFFFFFFFFu
 // Release/acquire is all the walk -> advanced-cell handoff needs (MEMBAR.ALL.GPU, not the
 // sequentially consistent MEMBAR.SC.GPU that __threadfence() emits).
@@ -254,14 +266,18 @@ __device__ __forceinline__ unsigned bucket_of(const MoveArgs& a, int x, int y) {
 // Buckets of a record's footprint cells: [0] start, [1..mf] path (motion_rec.cuh), BK_NIL for
 // cells no other footprint covers; returns mf.
 __device__ __forceinline__ int footprint(const MoveArgs& a, const uint4& r, const signed char (*bp)[5][2],
-                                         unsigned* cell) {
+                                         unsigned* cell, bool* occ = nullptr) {
     int cx[5], cy[5];
     path_of(a, r, bp, cx, cy);
     const int m = rec_mf(r);
     cell[0] = bucket_of(a, rec_x(r), rec_y(r));
+    if (occ) occ[0] = true;  // its own agent stands there
 #pragma unroll
     for (int j = 0; j < 5; ++j)
-        if (j < m) cell[j + 1] = bucket_of(a, cx[j], cy[j]);
+        if (j < m) {
+            cell[j + 1] = bucket_of(a, cx[j], cy[j]);
+            if (occ) occ[j + 1] = occ_test(a, cx[j], cy[j]);
+        }
     return m;
 }
 
@@ -292,9 +308,10 @@ __device__ __forceinline__ void bk_count(const MoveArgs& a, const unsigned* ci, 
 #pragma unroll
     for (int b = 0; b < B; ++b) r[b] = ok[b] ? __ldcg(&a.crec[ci[b]]) : make_uint4(0, 0, 0, 0);
     unsigned cell[B][6];
+    bool occ[B][6];
     int m[B];
 #pragma unroll
-    for (int b = 0; b < B; ++b) m[b] = ok[b] ? footprint(a, r[b], bp, cell[b]) : -1;
+    for (int b = 0; b < B; ++b) m[b] = ok[b] ? footprint(a, r[b], bp, cell[b], occ[b]) : -1;
 #pragma unroll
     for (int b = 0; b < B; ++b) {
         if (!ok[b]) continue;
@@ -304,6 +321,9 @@ __device__ __forceinline__ void bk_count(const MoveArgs& a, const unsigned* ci, 
             c6[j] = j <= m[b] ? cell[b][j] : BK_NIL;
             slot[j] = c6[j] != BK_NIL ? atomicAdd(&a.bcnt[c6[j]], 1u) : BK_NIL;
         }
+#pragma unroll
+        for (int j = 0; j < 6; ++j)
+            if (c6[j] != BK_NIL) a.bocc0[c6[j]] = occ[b][j];  // every writer of a cell agrees
         store_pairs(a, ci[b], slot, c6);
         a.alist[0][ci[b]] = make_uint2(ci[b], BK_NOWATCH);
     }
@@ -384,20 +404,21 @@ __device__ __forceinline__ void bk_place(const MoveArgs& a, const unsigned* ci, 
 // longer buckets are handed to warps (bk_sort_long).
 #define BK_SORT_REG 16
 #define BK_SORT_MAX 128  // a cell is covered by at most 121 footprints
-// An agent behind others in a bucket starts the rounds watching its predecessor there instead
-// of being checked in round 0 (any blocked bucket's predecessor is a valid watch: it only
-// schedules the next check; concurrent writers from different buckets may pick any of them).
-__device__ __forceinline__ void bk_hand_out(const MoveArgs& a, uint2 e, unsigned pos, unsigned base) {
-    const unsigned ci = e.y >> 3;
-    a.entry[(size_t)ci * 6 + (e.y & 7u)].x = pos;
+// An agent behind others in the bucket of its first path cell starts the rounds watching its
+// predecessor there instead of being checked in round 0 (a watch only schedules the next check).
+__device__ __forceinline__ void bk_hand_out(const MoveArgs& a, uint2 e, unsigned pos, unsigned base, unsigned b) {
+    const unsigned ci = e.y >> 3, j = e.y & 7u;
+    a.entry[(size_t)ci * 6 + j].x = pos;
+    a.eoff[(size_t)ci * 8 + j] = (uint8_t)(pos - base);  // < BK_SORT_MAX
     a.bdone[pos] = 0;
-    if (pos > base) a.alist[0][ci].y = pos - 1;
+    if (j == 0) a.bown[b] = pos;
+    if (j == 1 && pos > base) a.alist[0][ci].y = pos - 1;
 }
 
 __device__ void bk_sort(const MoveArgs& a, unsigned nbu, unsigned gtid, unsigned nthreads) {
     for (unsigned b = gtid; b < nbu; b += nthreads) {
         const unsigned base = __ldcg(&a.bbase[b]), n = __ldcg(&a.bcnt[b]);
-        a.bcur[b] = base;
+        a.bown[b] = BK_NIL;
         if (n > BK_SORT_REG) {
             a.long_list[atomicAdd(&a.pcount[7], 1u)] = b;
             continue;
@@ -411,7 +432,7 @@ __device__ void bk_sort(const MoveArgs& a, unsigned nbu, unsigned gtid, unsigned
             unsigned below = 0;
 #pragma unroll
             for (int k = 0; k < BK_SORT_REG; ++k) below += e[k].x < e[i].x;
-            bk_hand_out(a, e[i], base + below, base);
+            bk_hand_out(a, e[i], base + below, base, b);
         }
     }
 }
@@ -430,49 +451,165 @@ __device__ void bk_sort_long(const MoveArgs& a, unsigned* scratch) {
             const uint2 e = __ldcg(&a.brank[base + i]);
             unsigned below = 0;
             for (unsigned k = 0; k < n; ++k) below += srk[k] < e.x;
-            bk_hand_out(a, e, base + below, base);
+            bk_hand_out(a, e, base + below, base, b);
         }
         __syncwarp();
     }
 }
 
-// Full check of pending agent ci (its watched predecessor, if any, has walked): it owns every
-// contended cell it has when each cell's current position is its own.  Holding them all it
-// walks, then advances each cell and marks its positions done (release fence between), so a
-// later agent that sees them may walk in the same round: its acquire fence orders its
-// occupancy reads after this walk.  Otherwise returns the predecessor position to watch.
+// The done bytes of positions [lo, hi) of one bucket (the agents before hi there): 2 if one of
+// them stopped on the cell, else 1 if all of them walked, else 0 with *q = the first pending.
+// v holds the 32 bytes from lo & ~15 (loaded by the caller); longer ranges load the rest.
+__device__ __forceinline__ void bk_word(unsigned w, unsigned wa, unsigned lo, unsigned hi, bool& stop, unsigned& first) {
+    unsigned in = 0xFFFFFFFFu;  // bytes of the word inside [lo, hi)
+    if (wa < lo) in = lo - wa >= 4 ? 0u : in << (8 * (lo - wa));
+    if (wa + 4 > hi) in = hi <= wa ? 0u : in & (0xFFFFFFFFu >> (8 * (wa + 4 - hi)));
+    stop |= (w & in & 0x02020202u) != 0u;
+    const unsigned z = ~(w | (w >> 1)) & in & 0x01010101u;
+    if (z && first == BK_NIL) first = wa + (unsigned)((__ffs(z) - 1) >> 3);
+}
+
+__device__ __forceinline__ int bk_before(const MoveArgs& a, unsigned lo, unsigned hi, const uint4* v, unsigned* q) {
+    unsigned first = BK_NIL;
+    bool stop = false;
+    const unsigned c0 = lo & ~15u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) bk_word((&v[k >> 2].x)[k & 3], c0 + 4 * k, lo, hi, stop, first);
+    for (unsigned c = c0 + 32; c < hi && !stop; c += 16) {
+        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) bk_word((&u.x)[k], c + 4 * k, lo, hi, stop, first);
+    }
+    if (stop) return 2;
+    if (first == BK_NIL) return 1;
+    *q = first;
+    return 0;
+}
+
+// Check of pending agent ci: its path cells in walk order, each free, blocking or undecided
+// (see the bucket notes).  Decided up to the cell that stops it, it walks and writes its done
+// bytes; otherwise returns the pending position to watch.
 __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2],
                                          unsigned long long* hops, unsigned* watch) {
-    // the record and the (position, bucket) pairs in one trip, the cells' current positions in
-    // the next
+    // the record and the (position, bucket) pairs in one trip, the buckets' bases and occupants
+    // (or an uncontended cell's occupancy) in the next, then the done bytes
     const uint4 r = __ldcg(&a.crec[ci]);
-    unsigned pos[6], cell[6], cur[6];
+    unsigned pos[6], cell[6];
     load_pairs(a, ci, pos, cell);
+    const uint2 ko = __ldcg(reinterpret_cast<const uint2*>(a.eoff + (size_t)ci * 8));
+    int cx[5], cy[5];
+    const int m = path_of(a, r, bp, cx, cy);
+    unsigned base[5], own[5];
+    bool occ0[5];
+    uint4 dv[5][2];
 #pragma unroll
-    for (int j = 0; j < 6; ++j) cur[j] = cell[j] != BK_NIL ? __ldcg(&a.bcur[cell[j]]) : 0u;
-    unsigned behind = 0, w = BK_NOWATCH;
+    for (int i = 0; i < 5; ++i) {
+        base[i] = 0;
+        own[i] = BK_NIL;
+        occ0[i] = false;
+        dv[i][0] = dv[i][1] = make_uint4(0, 0, 0, 0);
+        if (i >= m) continue;
+        const unsigned b = cell[i + 1];
+        if (b != BK_NIL) {
+            const unsigned k = ((i + 1 < 4 ? ko.x >> (8 * (i + 1)) : ko.y >> (8 * (i - 3))) & 0xFFu);
+            base[i] = pos[i + 1] - k;
+            own[i] = __ldcg(&a.bown[b]);
+            occ0[i] = __ldcg(&a.bocc0[b]);
+            const unsigned c0 = base[i] & ~15u;
+            if (k) dv[i][0] = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c0));
+            if (c0 + 16 < pos[i + 1]) dv[i][1] = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c0 + 16));
+        } else {
+            occ0[i] = occ_test(a, cx[i], cy[i]);  // only this agent's footprint has the cell
+        }
+    }
+    int h = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        if (i >= m || h != i) continue;
+        const unsigned b = cell[i + 1], p = pos[i + 1];
+        if (b == BK_NIL) {
+            if (!occ0[i]) h = i + 1;
+            continue;
+        }
+        if (own[i] != BK_NIL ? own[i] > p : occ0[i]) continue;  // its occupant has not left
+        unsigned q = 0;
+        const int st = bk_before(a, base[i], p, dv[i], &q);
+        if (st == 2) continue;  // an earlier agent stopped here
+        if (st == 0) {
+            *watch = q;
+            return false;
+        }
+        h = i + 1;
+    }
+    bool blocked[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) blocked[i] = i >= h;
+    walk_apply(a, r, cx, cy, m, blocked, hops);
+    const bool exited = (h == m) && (r.z & 0x80000000u);
+    const int jf = exited ? -1 : h;  // footprint index of the cell it ends on (0: it stays)
 #pragma unroll
     for (int j = 0; j < 6; ++j)
-        if (cell[j] != BK_NIL && cur[j] != pos[j] && (w == BK_NOWATCH || pos[j] - cur[j] > behind)) {
-            behind = pos[j] - cur[j];  // wait where the most agents are still ahead
-            w = pos[j] - 1;
-        }
-    if (w != BK_NOWATCH) {
-        *watch = w;
-        return false;
-    }
-    fence_acq_rel_gpu();  // acquire: the walks of the earlier agents on these cells are visible
-    int cx[5], cy[5];
-    const int mw = path_of(a, r, bp, cx, cy);  // the walk covers the whole path (m >= mf)
-    walk_owned(a, r, cx, cy, mw, hops);
-    fence_acq_rel_gpu();  // release: this walk before the advanced cells
-#pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        if (cell[j] == BK_NIL) continue;
-        a.bcur[cell[j]] = pos[j] + 1;
-        a.bdone[pos[j]] = 1;
-    }
+        if (cell[j] != BK_NIL) a.bdone[pos[j]] = j == jf ? 2 : 1;
     return true;
+}
+
+// The late rounds, asynchronously: once at most MOVE_ASYNC_K pending agents per thread remain,
+// each thread owns its share of the list (entry k of the list goes to thread k mod nthreads) and
+// polls the done flag each agent watches, re-checking the agent as soon as it is set -- a chain
+// advances one link per poll instead of one per grid round, and no barrier separates the links.
+// An agent is only ever checked by its owner, so no two checks of one agent overlap; the globally
+// earliest pending agent can always walk, and every owner stays resident (cooperative launch),
+// so the phase finishes.  The entries live in the (then unused) dynamic shared memory.
+#ifndef MOVE_ASYNC_K
+#define MOVE_ASYNC_K 4
+#endif
+#ifndef MOVE_ASYNC_NAP
+#define MOVE_ASYNC_NAP 128
+#endif
+__device__ void async_walk(const MoveArgs& a, const uint2* list, unsigned np, unsigned gtid, unsigned nthreads,
+                           uint2* mine, const signed char (*bp)[5][2], unsigned long long* hops) {
+    unsigned live = 0;
+#pragma unroll
+    for (int j = 0; j < MOVE_ASYNC_K; ++j) {
+        const unsigned k = gtid + j * nthreads;
+        if (k < np) {
+            mine[j * blockDim.x] = __ldcg(&list[k]);
+            live |= 1u << j;
+        }
+    }
+    unsigned nap = 32;
+    long long idle = 0;
+    while (live) {
+        unsigned v[MOVE_ASYNC_K];
+#pragma unroll
+        for (int j = 0; j < MOVE_ASYNC_K; ++j) {
+            const unsigned w = ((live >> j) & 1u) ? mine[j * blockDim.x].y : BK_NOWATCH;
+            v[j] = w != BK_NOWATCH ? __ldcg(&a.bdone[w]) : ((live >> j) & 1u);
+        }
+        bool prog = false;
+#pragma unroll 1
+        for (int j = 0; j < MOVE_ASYNC_K; ++j) {
+            if (!v[j]) continue;
+            const uint2 e = mine[j * blockDim.x];
+            unsigned w;
+            if (bk_check(a, e.x, bp, hops, &w)) {
+                live &= ~(1u << j);
+            } else {
+                mine[j * blockDim.x].y = w;
+            }
+            prog = true;
+        }
+        if (prog) {
+            nap = 32;
+            continue;
+        }
+        __nanosleep(nap);
+        nap = min(nap * 2u, (unsigned)MOVE_ASYNC_NAP);
+        if (++idle > (1ll << 24)) {
+            atomicOr(&a.sc->err, 32ull);
+            return;
+        }
+    }
 }
 
 // Adds the group's hop counts to the phase displacement.  Every thread of the group calls it.
@@ -517,6 +654,8 @@ struct TailSmem {
 #define MOVE_DYN_SMEM (sizeof(TailSmem) > QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) \
                            ? sizeof(TailSmem) : QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned))
 static_assert((MOVE_THREADS / 32) * BK_SORT_MAX * sizeof(unsigned) <= MOVE_DYN_SMEM, "long-bucket ranking");
+static_assert(MOVE_ASYNC_K * MOVE_THREADS * sizeof(uint2) <= MOVE_DYN_SMEM, "async entries");
+static_assert(MOVE_ASYNC_K >= 1 && MOVE_ASYNC_K <= 32, "async entries per thread");
 
 __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y) {
     const unsigned cell = (unsigned)y * (unsigned)a.g.W + (unsigned)x;
@@ -1081,7 +1220,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                 a.sc->t_round[r] = globaltimer();
                 a.sc->n_round[r] = np;
             }
-            if (np <= TAIL_MAX) break;  // every block reads the same np
+            if (np <= TAIL_MAX || np <= (unsigned)MOVE_ASYNC_K * nthreads) break;  // every block reads the same np
             if (gtid == 0) a.pcount[4 + (r + 2) % 3] = 0;
             uint2* next = a.alist[(r + 1) & 1];
             unsigned int* ncount = &a.pcount[4 + (r + 1) % 3];
@@ -1178,6 +1317,13 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
             for (unsigned i = threadIdx.x; i < nq; i += blockDim.x) next[s_q[2] + i] = qp[i];
             grid.sync();
         }
+        if (MOVE_ASYNC_K) {
+            unsigned long long hops = 0;
+            async_walk(a, list, np, gtid, nthreads, reinterpret_cast<uint2*>(s_dyn) + threadIdx.x, s_bp, &hops);
+            flush_hops(B, a.sc, hops);
+            np = 0;  // nothing left for the tail
+            grid.sync();
+        }
     }
     if (gridDim.x > 1 && blockIdx.x != 0) {
         zero_marks(a, nbu, blockIdx.x - 1, gridDim.x - 1);
@@ -1264,7 +1410,7 @@ int fp_ensure_res(fp_ctx* ctx) {
 static int g_move_blocks[64] = {0};
 
 // Buckets: per contended cell (<= 3 per contended agent: every contended cell is covered by >= 2
-// of the <= 6-cell footprints) a counter, a base and a current position; per position (<= 6 per
+// of the <= 6-cell footprints) a counter, a base and its standing agent; per position (<= 6 per
 // contended agent) a rank and a done flag; the per-agent (position, bucket) pairs; the scan
 // counts.  Counters zero between phases.
 static int ensure_buckets(fp_ctx* ctx) {
@@ -1278,8 +1424,8 @@ static int ensure_buckets(fp_ctx* ctx) {
         if (p) cudaFree(p);
     FP_CUDA(ctx, cudaMalloc(&ctx->d_bkt, words * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0, words * 4, ctx->stream));
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_bdone, npos));
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * 6 * sizeof(uint2)));
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_bdone, npos + 16 + nb));  // done bytes (+ 16: whole-chunk reads), bocc0
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * (6 * sizeof(uint2) + 8)));  // + eoff
     ctx->bk_nb_cap = (unsigned)nb;
     ctx->bk_npos_cap = (unsigned)npos;
     ctx->bk_agent_cap = ctx->cap;
@@ -1344,11 +1490,13 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.pw = ctx->d_pw;
     a.bcnt = ctx->d_bkt;
     a.bbase = ctx->d_bkt + ctx->bk_nb_cap;
-    a.bcur = ctx->d_bkt + 2 * (size_t)ctx->bk_nb_cap;
     a.brank = reinterpret_cast<uint2*>(ctx->d_bkt + 3 * (size_t)ctx->bk_nb_cap);
     a.scan = reinterpret_cast<unsigned*>(a.brank + ctx->bk_npos_cap);
     a.bdone = ctx->d_bdone;
+    a.bocc0 = ctx->d_bdone + ctx->bk_npos_cap + 16;
+    a.bown = ctx->d_bkt + 2 * (size_t)ctx->bk_nb_cap;
     a.entry = ctx->d_entry;
+    a.eoff = reinterpret_cast<uint8_t*>(ctx->d_entry + (size_t)ctx->cap * 6);
     uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
     a.alist[0] = lists;
     a.alist[1] = lists + ctx->cap;
