@@ -69,59 +69,58 @@ __global__ void tile_sums_kernel(const uint32_t* ccnt, const uint32_t* coff, int
     }
 }
 
-// One block: the motion's seed work items (tile-list entry, chunk of <= SEED_ITEM agents).
-__global__ void __launch_bounds__(1024) motion_items_kernel(const uint32_t* list, const uint32_t* cnt,
-                                                             const unsigned long long* n_tiles_p, uint2* items,
-                                                             unsigned long long* n_items) {
-    __shared__ uint32_t s_warp[33];
-    const uint32_t n = (uint32_t)*n_tiles_p;
-    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
-    const uint32_t e0 = min(n, threadIdx.x * per), e1 = min(n, e0 + per);
-    uint32_t mine = 0;
-    for (uint32_t e = e0; e < e1; ++e) mine += (cnt[list[e]] + SEED_ITEM - 1) / SEED_ITEM;
-    uint32_t total;
-    uint32_t ib = block_scan_excl(mine, s_warp, &total);
-    for (uint32_t e = e0; e < e1; ++e) {
-        const unsigned k = (cnt[list[e]] + SEED_ITEM - 1) / SEED_ITEM;
-        for (unsigned c = 0; c < k; ++c) items[ib++] = make_uint2(e, c);
+// Warp-aggregated reservation of k consecutive slots of a list counted by *n: the warp's
+// lanes get consecutive ranges in lane order (one atomic per warp).  Every lane calls it.
+__device__ __forceinline__ uint32_t warp_reserve(uint32_t k, unsigned long long* n) {
+    const int lane = threadIdx.x & 31;
+    uint32_t incl = k;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
     }
-    if (threadIdx.x == 0) *n_items = total;
+    const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t base = 0;
+    if (lane == 0 && tot) base = (uint32_t)atomicAdd(n, (unsigned long long)tot);
+    return __shfl_sync(0xffffffffu, base, 0) + incl - k;
 }
 
-// One block: the plan kernel's work items.  Each stripe is cut into batches of PLAN_ITEM_CHUNKS
-// consecutive chunks; a batch's agents (one contiguous bucket run) are split into
-// ceil(agents / PLAN_ITEM_AGENTS) equal items.  Item = (first chunk touched, chunks touched - 1,
-// first agent, end agent); empty batches give none.
-__global__ void __launch_bounds__(1024) plan_items_kernel(const uint32_t* ccnt, const uint32_t* coff, uint32_t cps,
-                                                          uint32_t tiles_x, const unsigned long long* n_planned_p,
-                                                          uint4* items, unsigned long long* n_items) {
-    __shared__ uint32_t s_warp[33];
+// The motion's seed work items (tile-list entry, chunk of <= SEED_ITEM agents); *n_items is
+// zero on entry.  Item order is free: the seed passes deal them out dynamically.
+__global__ void motion_items_kernel(const uint32_t* list, const uint32_t* cnt, const unsigned long long* n_tiles_p,
+                                    uint2* items, unsigned long long* n_items) {
+    const uint32_t n = (uint32_t)*n_tiles_p;
+    for (uint32_t e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
+        const uint32_t e = e0 + threadIdx.x;
+        const uint32_t k = e < n ? (cnt[list[e]] + SEED_ITEM - 1) / SEED_ITEM : 0u;
+        const uint32_t ib = warp_reserve(k, n_items);
+        for (uint32_t c = 0; c < k; ++c) items[ib + c] = make_uint2(e, c);
+    }
+}
+
+// The plan kernel's work items.  Each stripe is cut into batches of PLAN_ITEM_CHUNKS consecutive
+// chunks; a batch's agents (one contiguous bucket run) are split into ceil(agents /
+// PLAN_ITEM_AGENTS) equal items.  Item = (first chunk touched, chunks touched - 1, first agent,
+// end agent); empty batches give none; *n_items is zero on entry.  Items are claimed in list
+// order, which follows the batches warp by warp (results never depend on it).
+__global__ void plan_items_kernel(const uint32_t* ccnt, const uint32_t* coff, uint32_t cps, uint32_t tiles_x,
+                                  const unsigned long long* n_planned_p, uint4* items, unsigned long long* n_items) {
     const uint32_t nch = cps * tiles_x;
     const uint32_t n_planned = (uint32_t)*n_planned_p;
     const uint32_t bps = (cps + PLAN_ITEM_CHUNKS - 1) / PLAN_ITEM_CHUNKS;
     const uint32_t nb = bps * tiles_x;
-    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
-    const uint32_t e0 = min(nb, threadIdx.x * per), e1 = min(nb, e0 + per);
-    auto batch = [&](uint32_t b, uint32_t& g0, uint32_t& g1, uint32_t& a0, uint32_t& a1) {
-        const uint32_t s = b / bps, j = b % bps;
-        g0 = s * cps + j * PLAN_ITEM_CHUNKS;
-        g1 = min(g0 + PLAN_ITEM_CHUNKS, (s + 1) * cps);
-        a0 = coff[g0];
-        a1 = g1 < nch ? coff[g1] : n_planned;
-    };
-    uint32_t mine = 0;
-    for (uint32_t b = e0; b < e1; ++b) {
-        uint32_t g0, g1, a0, a1;
-        batch(b, g0, g1, a0, a1);
-        mine += (a1 - a0 + PLAN_ITEM_AGENTS - 1) / PLAN_ITEM_AGENTS;
-    }
-    uint32_t total;
-    uint32_t ib = block_scan_excl(mine, s_warp, &total);
-    for (uint32_t b = e0; b < e1; ++b) {
-        uint32_t g0, g1, a0, a1;
-        batch(b, g0, g1, a0, a1);
+    for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < nb; b0 += gridDim.x * blockDim.x) {
+        const uint32_t b = b0 + threadIdx.x;
+        uint32_t g0 = 0, g1 = 0, a0 = 0, a1 = 0, k = 0;
+        if (b < nb) {
+            const uint32_t s = b / bps, j = b % bps;
+            g0 = s * cps + j * PLAN_ITEM_CHUNKS;
+            g1 = min(g0 + PLAN_ITEM_CHUNKS, (s + 1) * cps);
+            a0 = coff[g0];
+            a1 = g1 < nch ? coff[g1] : n_planned;
+            k = (a1 - a0 + PLAN_ITEM_AGENTS - 1) / PLAN_ITEM_AGENTS;
+        }
+        uint32_t ib = warp_reserve(k, n_items);
         const uint32_t A = a1 - a0;
-        const uint32_t k = (A + PLAN_ITEM_AGENTS - 1) / PLAN_ITEM_AGENTS;
         for (uint32_t t = 0; t < k; ++t) {
             const uint32_t lo = a0 + (uint32_t)((unsigned long long)t * A / k);
             const uint32_t hi = a0 + (uint32_t)((unsigned long long)(t + 1) * A / k);
@@ -134,7 +133,6 @@ __global__ void __launch_bounds__(1024) plan_items_kernel(const uint32_t* ccnt, 
             items[ib++] = make_uint4(gf, gl - gf, lo, hi);
         }
     }
-    if (threadIdx.x == 0) *n_items = total;
 }
 
 uint32_t fp_plan_chunks(const fp_ctx* ctx) { return (uint32_t)ctx->tiles_x * (uint32_t)ctx->cps; }
@@ -197,14 +195,18 @@ int fp_bucket_launch(fp_ctx* ctx) {
         ctx->d_sub_cnt, ctx->d_sub_off, ctx->tiles_x, ctx->tiles_y, ctx->cps, ctx->tile_h / 8, ctx->d_tile_cnt,
         ctx->d_tile_off, ctx->d_tile_list, &ctx->d_sc->n_tiles);
     FP_LAUNCHED(ctx);
-    motion_items_kernel<<<1, 1024, 0, s>>>(ctx->d_tile_list, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->d_seed_items,
-                                           &ctx->d_sc->n_items);
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_items, 0, 8, s));
+    motion_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nt, 256)), 256, 0, s>>>(
+        ctx->d_tile_list, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->d_seed_items, &ctx->d_sc->n_items);
     FP_LAUNCHED(ctx);
     bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, n, ctx->d_flags,
                                             ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket, ctx->d_brec);
     FP_LAUNCHED(ctx);
-    plan_items_kernel<<<1, 1024, 0, s>>>(ctx->d_sub_cnt, ctx->d_sub_off, (uint32_t)ctx->cps, (uint32_t)ctx->tiles_x,
-                                         &ctx->d_sc->n_planned, ctx->d_plan_items, &ctx->d_sc->n_plan_items);
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_plan_items, 0, 8, s));
+    const uint32_t nbatch = (uint32_t)((ctx->cps + PLAN_ITEM_CHUNKS - 1) / PLAN_ITEM_CHUNKS) * (uint32_t)ctx->tiles_x;
+    plan_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nbatch, 128)), 128, 0, s>>>(
+        ctx->d_sub_cnt, ctx->d_sub_off, (uint32_t)ctx->cps, (uint32_t)ctx->tiles_x, &ctx->d_sc->n_planned,
+        ctx->d_plan_items, &ctx->d_sc->n_plan_items);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }

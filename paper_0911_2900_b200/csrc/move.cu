@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include "motion_rec.cuh"
+#include "scan.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -1083,6 +1084,7 @@ __device__ __forceinline__ bool classify(const MoveArgs& a, uint4& rec, const si
     return true;
 }
 
+template <int PART>
 __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a) {
     cg::grid_group grid = cg::this_grid();
     __shared__ signed char s_bp[121][5][2];
@@ -1102,61 +1104,63 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     const unsigned nthreads = gridDim.x * blockDim.x;
     const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t n = (uint32_t)cta_load(&a.sc->n_alive);
-    if (gtid == 0) a.sc->t_motion[0] = globaltimer();
-    const uint4* cand = a.rec0;
-    unsigned ncand = n;
-    if (!a.premade) {
-        // step 1 here: records of every mover, footprints marked
-        for (uint32_t base = 0; base < n; base += nthreads) {
-            const uint32_t k = base + gtid;
-            uint4 rec = make_uint4(0, 0, 0, 0);
-            bool take = false;
-            if (k < n) {
-                const uint32_t id = a.seed_list[k];
-                const int tx = a.g.wrap(a.dx[id]), ty = a.dy[id];
-                rec = record_of(a.g, a.occ, id, a.g.wrap(a.x[id]), a.y[id], tx, ty, a.v[id], s_bp);
-                take = rec_m(rec) > 0;
-                if (take) mark_record(a.p1, a.p2, a.g, rec, s_bp, tx, ty);
+    if (PART == 1) {  // steps 1 and 2
+        if (gtid == 0) a.sc->t_motion[0] = globaltimer();
+        const uint4* cand = a.rec0;
+        unsigned ncand = n;
+        if (!a.premade) {
+            // step 1 here: records of every mover, footprints marked
+            for (uint32_t base = 0; base < n; base += nthreads) {
+                const uint32_t k = base + gtid;
+                uint4 rec = make_uint4(0, 0, 0, 0);
+                bool take = false;
+                if (k < n) {
+                    const uint32_t id = a.seed_list[k];
+                    const int tx = a.g.wrap(a.dx[id]), ty = a.dy[id];
+                    rec = record_of(a.g, a.occ, id, a.g.wrap(a.x[id]), a.y[id], tx, ty, a.v[id], s_bp);
+                    take = rec_m(rec) > 0;
+                    if (take) mark_record(a.p1, a.p2, a.g, rec, s_bp, tx, ty);
+                }
+                append(B, &a.pcount[0], a.rec[0], take, rec);
             }
-            append(B, &a.pcount[0], a.rec[0], take, rec);
+            grid.sync();
+            p2_count(a, s_red);
+            cand = a.rec[0];
+            ncand = cta_load(&a.pcount[0]);
+        } else {
+            // steps 1 and 2 tile by tile over the plan's records
+            const int nwmax = seed_ww(a.tile_w) * (a.tile_h + 10);
+            uint32_t* win = reinterpret_cast<uint32_t*>(s_dyn) + (threadIdx.x / SEED_GROUP) * 2 * nwmax;
+            seed_mark(a, win, s_bp);
+            grid.sync();
+            if (gtid == 0) a.sc->t_marked = globaltimer();
+            p2_count(a, s_red);
+            unsigned long long hops = 0;
+            seed_classify(a, Gs, win, s_bp, &hops);
+            flush_hops(B, a.sc, hops);
+            ncand = 0;  // step 2 done
+        }
+        if (!a.premade && gtid == 0) a.sc->t_marked = globaltimer();
+        // step 2
+        {
+            unsigned long long hops = 0;
+            for (unsigned base = 0; base < ncand; base += nthreads) {
+                const unsigned k = base + gtid;
+                bool contended = false;
+                uint4 rec = make_uint4(0, 0, 0, 0);
+                if (k < ncand) {
+                    rec = __ldcg(&cand[k]);
+                    if (rec_m(rec)) contended = classify(a, rec, s_bp, &hops);
+                }
+                append(B, &a.pcount[1], a.rec[1], contended, rec);
+            }
+            flush_hops(B, a.sc, hops);
         }
         grid.sync();
-        p2_count(a, s_red);
-        cand = a.rec[0];
-        ncand = cta_load(&a.pcount[0]);
-    } else {
-        // steps 1 and 2 tile by tile over the plan's records
-        const int nwmax = seed_ww(a.tile_w) * (a.tile_h + 10);
-        uint32_t* win = reinterpret_cast<uint32_t*>(s_dyn) + (threadIdx.x / SEED_GROUP) * 2 * nwmax;
-        seed_mark(a, win, s_bp);
-        grid.sync();
-        if (gtid == 0) a.sc->t_marked = globaltimer();
-        p2_count(a, s_red);
-        unsigned long long hops = 0;
-        seed_classify(a, Gs, win, s_bp, &hops);
-        flush_hops(B, a.sc, hops);
-        ncand = 0;  // step 2 done
-    }
-    if (!a.premade && gtid == 0) a.sc->t_marked = globaltimer();
-    // step 2
-    {
-        unsigned long long hops = 0;
-        for (unsigned base = 0; base < ncand; base += nthreads) {
-            const unsigned k = base + gtid;
-            bool contended = false;
-            uint4 rec = make_uint4(0, 0, 0, 0);
-            if (k < ncand) {
-                rec = __ldcg(&cand[k]);
-                if (rec_m(rec)) contended = classify(a, rec, s_bp, &hops);
-            }
-            append(B, &a.pcount[1], a.rec[1], contended, rec);
+        if (gtid == 0) {
+            a.sc->t_motion[1] = globaltimer();
+            a.sc->contended = __ldcg(&a.pcount[1]);
         }
-        flush_hops(B, a.sc, hops);
-    }
-    grid.sync();
-    if (gtid == 0) {
-        a.sc->t_motion[1] = globaltimer();
-        a.sc->contended = __ldcg(&a.pcount[1]);
     }
     // step 3: bucket rounds while many are pending, then block 0 alone in shared memory while
     // the other blocks clean up (contention bitplanes, overflow chunks)
@@ -1165,46 +1169,12 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     unsigned r = 0, nbu = 0;
     const uint2* list = nullptr;  // null: the tail takes crec[0, np) directly
     unsigned np = nc;
+    if (PART == 1) {  // the buckets are built by the prep kernels between the two parts
+        if (rounds) p2_number(a, s_red);
+        return;
+    }
     if (rounds) {
-        p2_number(a, s_red);
-        grid.sync();
-        for (unsigned base = gtid; base < nc; base += BK_PREP_BATCH * nthreads) {
-            unsigned ci[BK_PREP_BATCH];
-            bool ok[BK_PREP_BATCH];
-#pragma unroll
-            for (int b = 0; b < BK_PREP_BATCH; ++b) {
-                ci[b] = base + b * nthreads;
-                ok[b] = ci[b] < nc;
-            }
-            bk_count<BK_PREP_BATCH>(a, ci, ok, s_bp);
-        }
-        if (gtid == 0) {
-            // pending counts rotate over pcount[4..6]: round r reads its own, fills the next and
-            // zeroes the one last read in round r-1
-            a.pcount[4] = nc;
-            a.pcount[5] = a.pcount[6] = 0;
-        }
-        grid.sync();
         nbu = cta_load(&a.scan[gridDim.x]);  // buckets (p2_number)
-        bk_scan_count(a, nbu, s_red);
-        grid.sync();
-        bk_scan_base(a, nbu, s_red);
-        grid.sync();
-        for (unsigned base = gtid; base < nc; base += BK_PREP_BATCH * nthreads) {
-            unsigned ci[BK_PREP_BATCH];
-            bool ok[BK_PREP_BATCH];
-#pragma unroll
-            for (int b = 0; b < BK_PREP_BATCH; ++b) {
-                ci[b] = base + b * nthreads;
-                ok[b] = ci[b] < nc;
-            }
-            bk_place<BK_PREP_BATCH>(a, ci, ok);
-        }
-        grid.sync();
-        bk_sort(a, nbu, gtid, nthreads);
-        grid.sync();
-        bk_sort_long(a, reinterpret_cast<unsigned*>(s_dyn));
-        grid.sync();
         if (gtid == 0) a.sc->t_prep = globaltimer();
         // Per round and CTA, in the (now free) dynamic shared memory: a queue of agents whose
         // watched blocker has walked (full check) and a queue of still-pending (agent, watch)
@@ -1354,6 +1324,76 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     }
 }
 
+// ------------------------------------------------------------------ bucket prep kernels
+// Between the two parts of the motion: plain launches at full occupancy (the cooperative parts
+// hold one 512-thread CTA per SM), each a latency-bound pass that wants many loads in flight.
+// Each returns at once when the phase has too few contended agents for the rounds.
+#define PREP_THREADS 256
+__global__ void __launch_bounds__(PREP_THREADS) bk_count_kernel(MoveArgs a) {
+    __shared__ signed char s_bp[121][5][2];
+    for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
+    const unsigned nc = cta_load(&a.pcount[1]);  // (its barriers also publish s_bp)
+    if (nc <= TAIL_MAX) return;
+    const unsigned nthreads = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (unsigned base = gtid; base < nc; base += BK_PREP_BATCH * nthreads) {
+        unsigned ci[BK_PREP_BATCH];
+        bool ok[BK_PREP_BATCH];
+#pragma unroll
+        for (int b = 0; b < BK_PREP_BATCH; ++b) {
+            ci[b] = base + b * nthreads;
+            ok[b] = ci[b] < nc;
+        }
+        bk_count<BK_PREP_BATCH>(a, ci, ok, s_bp);
+    }
+    if (gtid == 0) {
+        // pending counts rotate over pcount[4..6]: round r reads its own, fills the next and
+        // zeroes the one last read in round r-1
+        a.pcount[4] = nc;
+        a.pcount[5] = a.pcount[6] = 0;
+    }
+}
+
+// bbase = exclusive prefix of the bucket sizes: per-CTA sums, then each CTA's slice (both
+// launched with the same grid).
+__global__ void __launch_bounds__(MOVE_THREADS) bk_scan_count_kernel(MoveArgs a, unsigned g1) {
+    __shared__ unsigned s_red[32];
+    if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
+    bk_scan_count(a, cta_load(&a.scan[g1]), s_red);
+}
+
+__global__ void __launch_bounds__(MOVE_THREADS) bk_scan_base_kernel(MoveArgs a, unsigned g1) {
+    __shared__ unsigned s_red[32];
+    if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
+    bk_scan_base(a, cta_load(&a.scan[g1]), s_red);
+}
+
+__global__ void __launch_bounds__(PREP_THREADS) bk_place_kernel(MoveArgs a) {
+    const unsigned nc = cta_load(&a.pcount[1]);
+    if (nc <= TAIL_MAX) return;
+    const unsigned nthreads = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (unsigned base = gtid; base < nc; base += BK_PREP_BATCH * nthreads) {
+        unsigned ci[BK_PREP_BATCH];
+        bool ok[BK_PREP_BATCH];
+#pragma unroll
+        for (int b = 0; b < BK_PREP_BATCH; ++b) {
+            ci[b] = base + b * nthreads;
+            ok[b] = ci[b] < nc;
+        }
+        bk_place<BK_PREP_BATCH>(a, ci, ok);
+    }
+}
+
+__global__ void __launch_bounds__(PREP_THREADS) bk_sort_kernel(MoveArgs a, unsigned g1) {
+    if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
+    bk_sort(a, cta_load(&a.scan[g1]), blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
+__global__ void __launch_bounds__(PREP_THREADS) bk_sort_long_kernel(MoveArgs a) {
+    __shared__ unsigned s_rank[(PREP_THREADS / 32) * BK_SORT_MAX];
+    if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
+    bk_sort_long(a, s_rank);
+}
+
 // The phase's exit records (rank << 32 | id) into processing order on the device when they are
 // few (the usual case: a handful per step); more than EXITS_SMEM are left to the host's radix sort.
 #define EXITS_SMEM 4096
@@ -1408,6 +1448,7 @@ int fp_ensure_res(fp_ctx* ctx) {
 // per device: the raised shared-memory limit and the occupancy are attributes of the device's
 // function instance, so a process driving several devices configures each one
 static int g_move_blocks[64] = {0};
+static int g_prep_blocks[64] = {0};
 
 // Buckets: per contended cell (<= 3 per contended agent: every contended cell is covered by >= 2
 // of the <= 6-cell footprints) a counter, a base and its standing agent; per position (<= 6 per
@@ -1450,13 +1491,24 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     }
     int& move_blocks = g_move_blocks[ctx->device & 63];
     if (!move_blocks) {
-        FP_CUDA(ctx, cudaFuncSetAttribute(move_rounds_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)MOVE_DYN_SMEM));
-        int per_sm = 0;
-        FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, move_rounds_kernel, MOVE_THREADS,
-                                                                   MOVE_DYN_SMEM));
+        int per_sm = 1 << 30;
+        for (const void* k : {(const void*)move_rounds_kernel<1>, (const void*)move_rounds_kernel<2>}) {
+            FP_CUDA(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVE_DYN_SMEM));
+            int c = 0;
+            FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k, MOVE_THREADS, MOVE_DYN_SMEM));
+            per_sm = std::min(per_sm, c);
+        }
         move_blocks = std::max(1, std::min(per_sm, FP_MOVE_BLOCKS_PER_SM)) * ctx->sm_count;
+        int pc = 0;  // the prep kernels: as many CTAs as fit on every SM (grid-stride loops)
+        for (const void* k : {(const void*)bk_count_kernel, (const void*)bk_place_kernel, (const void*)bk_sort_kernel,
+                              (const void*)bk_sort_long_kernel}) {
+            int c = 0;
+            FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k, PREP_THREADS, 0));
+            pc = pc ? std::min(pc, c) : c;
+        }
+        g_prep_blocks[ctx->device & 63] = std::max(1, pc) * ctx->sm_count;
     }
+    const unsigned prep_blocks = (unsigned)g_prep_blocks[ctx->device & 63];
     MoveArgs a;
     a.g = fp_geo(ctx);
     a.occ = ctx->d_occ;
@@ -1515,7 +1567,22 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel, a));
+    FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<1>, a));
+    ctx->ctr.kernel_launches++;
+    const unsigned pg = prep_blocks;
+    bk_count_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+    FP_LAUNCHED(ctx);
+    bk_scan_count_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a, blocks);
+    FP_LAUNCHED(ctx);
+    bk_scan_base_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a, blocks);
+    FP_LAUNCHED(ctx);
+    bk_place_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+    FP_LAUNCHED(ctx);
+    bk_sort_kernel<<<pg, PREP_THREADS, 0, s>>>(a, blocks);
+    FP_LAUNCHED(ctx);
+    bk_sort_long_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+    FP_LAUNCHED(ctx);
+    FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<2>, a));
     ctx->ctr.kernel_launches++;
     exits_sort_kernel<<<1, 1024, 0, s>>>(ctx->d_exits, ctx->d_sc);
     FP_LAUNCHED(ctx);
@@ -1550,7 +1617,7 @@ int fp_exits_finish(fp_ctx* ctx) {
     const uint32_t ne = ctx->n_exits;
     if (ne <= 1 || ctx->h_sc->exits_sorted) return FP_OK;  // sorted in the motion graph
     const uint32_t na = std::max<uint32_t>(ctx->n_order, 1);
-    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 8192 * 4));
+    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, FP_SCAN_SUMS * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, (size_t)na * 4, ctx->stream));
     exits_flag_kernel<<<fp_blocks(ne, 256), 256, 0, ctx->stream>>>(ctx->d_exits, ne, ctx->d_cnt);
     FP_LAUNCHED(ctx);

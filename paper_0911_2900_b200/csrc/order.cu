@@ -15,6 +15,7 @@
 // The alive count comes from device memory, so the whole sequence is graph-capturable.
 // Pinned against the sequential loop by tests (oracle.movement_order, n up to 10^7).
 #include "internal.cuh"
+#include "scan.cuh"
 
 #define GS_LOOP(i, n) for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += gridDim.x * blockDim.x)
 
@@ -144,7 +145,7 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
 int fp_order_reserve(fp_ctx* ctx) {
     const uint32_t n = std::max<uint32_t>(ctx->n, 1);
     if (ctx->order_reserved_n == n && ctx->d_scan_sums2) return FP_OK;
-    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, 8192 * 4));
+    if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, FP_SCAN_SUMS * 4));
     ctx->order_reserved_n = n;
     return FP_OK;
 }

@@ -5,38 +5,72 @@
 #include "internal.cuh"
 #include "scan.cuh"
 
+// FP_SCAN_PER consecutive words of `in` from element base (16-byte loads when the run is whole).
+__device__ __forceinline__ void load_run(const uint32_t* in, uint32_t n, uint32_t base, uint32_t* v) {
+    if (base + FP_SCAN_PER <= n) {
+#pragma unroll
+        for (int q = 0; q < FP_SCAN_PER / 4; ++q) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(in + base) + q);
+            v[4 * q] = u.x;
+            v[4 * q + 1] = u.y;
+            v[4 * q + 2] = u.z;
+            v[4 * q + 3] = u.w;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < FP_SCAN_PER; ++k) v[k] = base + k < n ? in[base + k] : 0u;
+    }
+}
+
+// FP_SCAN_PER consecutive alive flags as a bit mask.
+__device__ __forceinline__ uint32_t load_flags(const uint8_t* alive, uint32_t n, uint32_t base) {
+    uint32_t f = 0;
+    if (base + FP_SCAN_PER <= n) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(alive + base));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int k = 0; k < FP_SCAN_PER; ++k) f |= (((w[k >> 2] >> (8 * (k & 3))) & 0xFFu) != 0u ? 1u : 0u) << k;
+    } else {
+#pragma unroll
+        for (int k = 0; k < FP_SCAN_PER; ++k) f |= (base + k < n && alive[base + k] ? 1u : 0u) << k;
+    }
+    return f;
+}
+
 __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_sums_kernel(const uint32_t* in, uint32_t n, uint32_t* sums) {
     __shared__ uint32_t s_warp[33];
-    const uint32_t base = blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER;
-    uint32_t v = 0;
+    uint32_t v[FP_SCAN_PER], t = 0;
+    load_run(in, n, blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER, v);
 #pragma unroll
-    for (int k = 0; k < FP_SCAN_PER; ++k) v += base + k < n ? in[base + k] : 0u;
+    for (int k = 0; k < FP_SCAN_PER; ++k) t += v[k];
     uint32_t total;
-    block_scan_excl(v, s_warp, &total);
+    block_scan_excl(t, s_warp, &total);
     if (threadIdx.x == 0) sums[blockIdx.x] = total;
 }
 
-// Exclusive scan of the tile sums in place (up to FP_SCAN_SUMS: 8 per thread); the grand total
-// to *total_out (when given).
-__global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_top_kernel(uint32_t* sums, uint32_t nb,
-                                                                  unsigned long long* total_out) {
+// Exclusive scan of the tile sums in place (up to FP_SCAN_SUMS: FP_SCAN_SUMS / FP_SCAN_TOP
+// per thread); the grand total to *total_out (when given).
+__global__ void __launch_bounds__(FP_SCAN_TOP) scan_top_kernel(uint32_t* sums, uint32_t nb,
+                                                               unsigned long long* total_out) {
     __shared__ uint32_t s_warp[33];
-    constexpr int PER = FP_SCAN_SUMS / FP_SCAN_BLOCK;
-    uint32_t v[PER], t = 0;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        const uint32_t i = threadIdx.x * PER + k;
-        v[k] = i < nb ? sums[i] : 0u;
-        t += v[k];
+    constexpr int PER = FP_SCAN_SUMS / FP_SCAN_TOP;
+    const uint32_t per = (nb + FP_SCAN_TOP - 1) / FP_SCAN_TOP;  // <= PER
+    uint32_t t = 0;
+    for (uint32_t k = 0; k < per; ++k) {
+        const uint32_t i = threadIdx.x * per + k;
+        t += i < nb ? sums[i] : 0u;
     }
     uint32_t total;
     uint32_t e = block_scan_excl(t, s_warp, &total);
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        const uint32_t i = threadIdx.x * PER + k;
-        if (i < nb) sums[i] = e;
-        e += v[k];
+    for (uint32_t k = 0; k < per; ++k) {
+        const uint32_t i = threadIdx.x * per + k;
+        if (i < nb) {
+            const uint32_t v = sums[i];
+            sums[i] = e;
+            e += v;
+        }
     }
+    (void)PER;
     if (threadIdx.x == 0 && total_out) *total_out = total;
 }
 
@@ -45,27 +79,32 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_apply_kernel(const uint32_
     __shared__ uint32_t s_warp[33];
     const uint32_t base = blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER;
     uint32_t v[FP_SCAN_PER], t = 0;
+    load_run(in, n, base, v);
 #pragma unroll
-    for (int k = 0; k < FP_SCAN_PER; ++k) {
-        v[k] = base + k < n ? in[base + k] : 0u;
-        t += v[k];
-    }
+    for (int k = 0; k < FP_SCAN_PER; ++k) t += v[k];
     uint32_t total;
     uint32_t e = block_scan_excl(t, s_warp, &total) + sums[blockIdx.x];
+    uint32_t o[FP_SCAN_PER];
 #pragma unroll
     for (int k = 0; k < FP_SCAN_PER; ++k) {
-        if (base + k < n) out[base + k] = e;
+        o[k] = e;
         e += v[k];
+    }
+    if (base + FP_SCAN_PER <= n) {
+#pragma unroll
+        for (int q = 0; q < FP_SCAN_PER / 4; ++q)
+            reinterpret_cast<uint4*>(out + base)[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < FP_SCAN_PER; ++k)
+            if (base + k < n) out[base + k] = o[k];
     }
 }
 
 // Compaction of the alive flags: per-tile counts, then ascending ids written from the offsets.
 __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_sums_kernel(const uint8_t* alive, uint32_t n, uint32_t* sums) {
     __shared__ uint32_t s_warp[33];
-    const uint32_t base = blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER;
-    uint32_t v = 0;
-#pragma unroll
-    for (int k = 0; k < FP_SCAN_PER; ++k) v += (base + k < n && alive[base + k]) ? 1u : 0u;
+    const uint32_t v = __popc(load_flags(alive, n, blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER));
     uint32_t total;
     block_scan_excl(v, s_warp, &total);
     if (threadIdx.x == 0) sums[blockIdx.x] = total;
@@ -75,18 +114,14 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_scatter_kernel(const uin
                                                                        const uint32_t* sums, uint32_t* ids) {
     __shared__ uint32_t s_warp[33];
     const uint32_t base = blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER;
-    uint32_t f = 0, t = 0;
-#pragma unroll
-    for (int k = 0; k < FP_SCAN_PER; ++k) {
-        const bool a = base + k < n && alive[base + k];
-        f |= (uint32_t)a << k;
-        t += a;
-    }
+    uint32_t f = load_flags(alive, n, base);
     uint32_t total;
-    uint32_t e = block_scan_excl(t, s_warp, &total) + sums[blockIdx.x];
-#pragma unroll
-    for (int k = 0; k < FP_SCAN_PER; ++k)
-        if ((f >> k) & 1u) ids[e++] = base + k;
+    uint32_t e = block_scan_excl(__popc(f), s_warp, &total) + sums[blockIdx.x];
+    while (f) {
+        const int k = __ffs(f) - 1;
+        f &= f - 1;
+        ids[e++] = base + (uint32_t)k;
+    }
 }
 
 int fp_scan_u32(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* sums, cudaStream_t s) {
@@ -94,7 +129,7 @@ int fp_scan_u32(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint
     if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "scan: more than 134M elements");
     scan_sums_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(in, n, sums);
     FP_LAUNCHED(ctx);
-    scan_top_kernel<<<1, FP_SCAN_BLOCK, 0, s>>>(sums, nb, nullptr);
+    scan_top_kernel<<<1, FP_SCAN_TOP, 0, s>>>(sums, nb, nullptr);
     FP_LAUNCHED(ctx);
     scan_apply_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(in, n, sums, out);
     FP_LAUNCHED(ctx);
@@ -107,7 +142,7 @@ int fp_select_alive(fp_ctx* ctx, const uint8_t* alive, uint32_t n, uint32_t* ids
     if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "select: more than 134M agents");
     select_sums_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(alive, n, sums);
     FP_LAUNCHED(ctx);
-    scan_top_kernel<<<1, FP_SCAN_BLOCK, 0, s>>>(sums, nb, count);
+    scan_top_kernel<<<1, FP_SCAN_TOP, 0, s>>>(sums, nb, count);
     FP_LAUNCHED(ctx);
     select_scatter_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(alive, n, sums, ids);
     FP_LAUNCHED(ctx);

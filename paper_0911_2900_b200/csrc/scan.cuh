@@ -4,10 +4,11 @@
 
 #include <stdint.h>
 
-#define FP_SCAN_BLOCK 1024
-#define FP_SCAN_PER 16                           // elements per thread in the scan passes
-#define FP_SCAN_SUMS 8192                        // tile sums: n <= 8192 * 16384 (134M)
+#define FP_SCAN_BLOCK 256                        // the per-tile passes: many small CTAs fill every SM
+#define FP_SCAN_PER 16                           // elements per thread (four 16-byte loads)
 #define FP_SCAN_TILE (FP_SCAN_BLOCK * FP_SCAN_PER)
+#define FP_SCAN_TOP 1024                         // the one-block pass over the tile sums
+#define FP_SCAN_SUMS 32768                       // tile sums: n <= 32768 * 4096 (134M)
 
 // Block-wide exclusive scan of one value per thread; *total = the block's sum.  s_warp: 33
 // words of shared memory.
