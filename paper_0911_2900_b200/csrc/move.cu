@@ -1169,10 +1169,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     unsigned r = 0, nbu = 0;
     const uint2* list = nullptr;  // null: the tail takes crec[0, np) directly
     unsigned np = nc;
-    if (PART == 1) {  // the buckets are built by the prep kernels between the two parts
-        if (rounds) p2_number(a, s_red);
-        return;
-    }
+    if (PART == 1) return;  // (mode B) the buckets are built by the prep kernels between the parts
     if (rounds) {
         nbu = cta_load(&a.scan[gridDim.x]);  // buckets (p2_number)
         if (gtid == 0) a.sc->t_prep = globaltimer();
@@ -1324,6 +1321,61 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     }
 }
 
+// ------------------------------------------------------------------ seed kernels (mode A)
+// Steps 1 and 2 of a phase whose records the plan kernel emitted, as two plain launches (marks,
+// then classification) so every SM holds as many seed workers as fit instead of one
+// cooperative CTA's four; then the contended-cell numbering (p2_count / p2_number, both on the
+// motion's grid, whose slices they share).
+#ifndef SEED_MARK_MINB
+#define SEED_MARK_MINB 3
+#endif
+__global__ void __launch_bounds__(MOVE_THREADS, SEED_MARK_MINB) seed_mark_kernel(MoveArgs a) {
+    __shared__ signed char s_bp[121][5][2];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.sc->t_motion[0] = globaltimer();
+    __syncthreads();
+    const int nwmax = seed_ww(a.tile_w) * (a.tile_h + 10);
+    seed_mark(a, reinterpret_cast<uint32_t*>(s_dyn) + (threadIdx.x / SEED_GROUP) * 2 * nwmax, s_bp);
+}
+
+#ifndef SEED_CLASSIFY_MINB
+#define SEED_CLASSIFY_MINB 2
+#endif
+__global__ void __launch_bounds__(MOVE_THREADS, SEED_CLASSIFY_MINB) seed_classify_kernel(MoveArgs a) {
+    __shared__ signed char s_bp[121][5][2];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    __shared__ unsigned int s_app[2 + 2 * SEED_GROUPS];
+    __shared__ unsigned long long s_hops[1 + SEED_GROUPS];
+    for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
+    if (threadIdx.x < 2 + 2 * SEED_GROUPS) s_app[threadIdx.x] = 0;
+    if (threadIdx.x < 1 + SEED_GROUPS) s_hops[threadIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.sc->t_marked = globaltimer();
+    __syncthreads();
+    const Group B{0, (int)blockDim.x, threadIdx.x == 0, &s_app[0], &s_hops[0]};
+    const unsigned sg = threadIdx.x / SEED_GROUP;
+    const Group Gs{1 + (int)sg, SEED_GROUP, threadIdx.x % SEED_GROUP == 0, &s_app[2 + 2 * sg], &s_hops[1 + sg]};
+    const int nwmax = seed_ww(a.tile_w) * (a.tile_h + 10);
+    unsigned long long hops = 0;
+    seed_classify(a, Gs, reinterpret_cast<uint32_t*>(s_dyn) + sg * 2 * nwmax, s_bp, &hops);
+    flush_hops(B, a.sc, hops);
+}
+
+__global__ void __launch_bounds__(MOVE_THREADS) p2_count_kernel(MoveArgs a) {
+    __shared__ unsigned s_red[32];
+    p2_count(a, s_red);
+}
+
+__global__ void __launch_bounds__(MOVE_THREADS) p2_number_kernel(MoveArgs a) {
+    __shared__ unsigned s_red[32];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a.sc->t_motion[1] = globaltimer();
+        a.sc->contended = __ldcg(&a.pcount[1]);
+    }
+    if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
+    p2_number(a, s_red);
+}
+
 // ------------------------------------------------------------------ bucket prep kernels
 // Between the two parts of the motion: plain launches at full occupancy (the cooperative parts
 // hold one 512-thread CTA per SM), each a latency-bound pass that wants many loads in flight.
@@ -1449,6 +1501,8 @@ int fp_ensure_res(fp_ctx* ctx) {
 // function instance, so a process driving several devices configures each one
 static int g_move_blocks[64] = {0};
 static int g_prep_blocks[64] = {0};
+static int g_seed_per_sm[64] = {0};
+static int g_seed_smem[64] = {0};
 
 // Buckets: per contended cell (<= 3 per contended agent: every contended cell is covered by >= 2
 // of the <= 6-cell footprints) a counter, a base and its standing agent; per position (<= 6 per
@@ -1509,6 +1563,21 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
         g_prep_blocks[ctx->device & 63] = std::max(1, pc) * ctx->sm_count;
     }
     const unsigned prep_blocks = (unsigned)g_prep_blocks[ctx->device & 63];
+    int& seed_per_sm = g_seed_per_sm[ctx->device & 63];
+    int& seed_smem_at = g_seed_smem[ctx->device & 63];
+    const int smem = SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4;
+    if (premade && (seed_per_sm == 0 || seed_smem_at != smem)) {  // seed CTAs per SM for this window size
+        seed_smem_at = smem;
+        int c = 1 << 30;
+        for (const void* k : {(const void*)seed_mark_kernel, (const void*)seed_classify_kernel}) {
+            FP_CUDA(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MOVE_DYN_SMEM));
+            int o = 0;
+            FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k, MOVE_THREADS, smem));
+            c = std::min(c, o);
+        }
+        seed_per_sm = std::max(1, c);
+    }
+    const unsigned seed_blocks = (unsigned)std::max(1, seed_per_sm) * (unsigned)ctx->sm_count;
     MoveArgs a;
     a.g = fp_geo(ctx);
     a.occ = ctx->d_occ;
@@ -1567,8 +1636,21 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<1>, a));
-    ctx->ctr.kernel_launches++;
+    const size_t seed_smem = (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4;
+    if (premade) {  // steps 1 and 2 over the plan's records: two plain launches
+        const unsigned sb = std::min(seed_blocks, std::max(1u, (unsigned)fp_blocks(ctx->n, SEED_ITEM)));
+        seed_mark_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
+        FP_LAUNCHED(ctx);
+        p2_count_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a);
+        FP_LAUNCHED(ctx);
+        seed_classify_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
+        FP_LAUNCHED(ctx);
+    } else {
+        FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<1>, a));
+        ctx->ctr.kernel_launches++;
+    }
+    p2_number_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a);
+    FP_LAUNCHED(ctx);
     const unsigned pg = prep_blocks;
     bk_count_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
     FP_LAUNCHED(ctx);
