@@ -78,6 +78,7 @@ struct MoveArgs {
     unsigned* long_list;           // buckets longer than BK_SORT_REG (ranked by warps)
     uint8_t* bdone;                // per position (rank order): 0 pending, 1 walked, 2 walked and stopped here
     uint8_t* eoff;                 // 8 per contended agent: offset of its position in each bucket
+    uint4* ck;                     // 2 per contended agent: what a check reads (bk_final_kernel)
     uint2* entry;                  // 6 per contended agent: (slot, then position; bucket) per
                                    // footprint cell; BK_NIL/BK_NIL for an uncontended cell
     // contended-index pending lists (ping-pong), carved from rec[0] (free after step 2)
@@ -460,7 +461,8 @@ __device__ void bk_sort_long(const MoveArgs& a, unsigned* scratch) {
 
 // The done bytes of positions [lo, hi) of one bucket (the agents before hi there): 2 if one of
 // them stopped on the cell, else 1 if all of them walked, else 0 with *q = the first pending.
-// v holds the 32 bytes from lo & ~15 (loaded by the caller); longer ranges load the rest.
+// v holds the 32 bytes from lo & ~15 (loaded by the caller); longer ranges (at most 120
+// positions before hi, so lo & ~15 + 144 covers them) load the rest at once.
 __device__ __forceinline__ void bk_word(unsigned w, unsigned wa, unsigned lo, unsigned hi, bool& stop, unsigned& first) {
     unsigned in = 0xFFFFFFFFu;  // bytes of the word inside [lo, hi)
     if (wa < lo) in = lo - wa >= 4 ? 0u : in << (8 * (lo - wa));
@@ -476,10 +478,17 @@ __device__ __forceinline__ int bk_before(const MoveArgs& a, unsigned lo, unsigne
     const unsigned c0 = lo & ~15u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) bk_word((&v[k >> 2].x)[k & 3], c0 + 4 * k, lo, hi, stop, first);
-    for (unsigned c = c0 + 32; c < hi && !stop; c += 16) {
-        const uint4 u = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c));
+    if (c0 + 32 < hi && !stop) {  // a long bucket: the rest (<= 112 more bytes) in one trip
+        uint4 u[7];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) bk_word((&u.x)[k], c + 4 * k, lo, hi, stop, first);
+        for (int h = 0; h < 7; ++h) {
+            const unsigned c = c0 + 32 + 16 * h;
+            u[h] = c < hi ? __ldcg(reinterpret_cast<const uint4*>(a.bdone + c)) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int h = 0; h < 7; ++h)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) bk_word((&u[h].x)[k], c0 + 32 + 16 * h + 4 * k, lo, hi, stop, first);
     }
     if (stop) return 2;
     if (first == BK_NIL) return 1;
@@ -487,58 +496,55 @@ __device__ __forceinline__ int bk_before(const MoveArgs& a, unsigned lo, unsigne
     return 0;
 }
 
+// What a check of a contended agent reads, prepared once per phase after the buckets are sorted
+// (bk_final_kernel), so a check is two trips (this, then the done bytes) instead of four.
+// ck[2ci] = positions of footprint cells 0..3, ck[2ci+1] = (positions of cells 4, 5; bucket
+// offsets of path cells 0..3 as bytes; offset of path cell 4 | codes << 8).  A position is BK_NIL
+// for an uncontended cell.  Path cell i (footprint cell i + 1) has a 2-bit code: CK_FREE and
+// CK_BLOCK are decided for the whole phase (an uncontended cell's occupancy; a static occupant
+// or a start occupant later in the order), CK_DYN by the done bytes before its position.
+#define CK_FREE 0u
+#define CK_BLOCK 1u
+#define CK_DYN 2u
+
 // Check of pending agent ci: its path cells in walk order, each free, blocking or undecided
 // (see the bucket notes).  Decided up to the cell that stops it, it walks and writes its done
 // bytes; otherwise returns the pending position to watch.
 __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const signed char (*bp)[5][2],
                                          unsigned long long* hops, unsigned* watch) {
-    // the record and the (position, bucket) pairs in one trip, the buckets' bases and occupants
-    // (or an uncontended cell's occupancy) in the next, then the done bytes
     const uint4 r = __ldcg(&a.crec[ci]);
-    unsigned pos[6], cell[6];
-    load_pairs(a, ci, pos, cell);
-    const uint2 ko = __ldcg(reinterpret_cast<const uint2*>(a.eoff + (size_t)ci * 8));
+    const uint4 k0 = __ldcg(&a.ck[2 * (size_t)ci]), k1 = __ldcg(&a.ck[2 * (size_t)ci + 1]);
+    const unsigned pos[6] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y};
+    const unsigned codes = k1.w >> 8;
     int cx[5], cy[5];
     const int m = path_of(a, r, bp, cx, cy);
-    unsigned base[5], own[5];
-    bool occ0[5];
+    unsigned base[5];
     uint4 dv[5][2];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
         base[i] = 0;
-        own[i] = BK_NIL;
-        occ0[i] = false;
         dv[i][0] = dv[i][1] = make_uint4(0, 0, 0, 0);
-        if (i >= m) continue;
-        const unsigned b = cell[i + 1];
-        if (b != BK_NIL) {
-            const unsigned k = ((i + 1 < 4 ? ko.x >> (8 * (i + 1)) : ko.y >> (8 * (i - 3))) & 0xFFu);
-            base[i] = pos[i + 1] - k;
-            own[i] = __ldcg(&a.bown[b]);
-            occ0[i] = __ldcg(&a.bocc0[b]);
-            const unsigned c0 = base[i] & ~15u;
-            if (k) dv[i][0] = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c0));
-            if (c0 + 16 < pos[i + 1]) dv[i][1] = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c0 + 16));
-        } else {
-            occ0[i] = occ_test(a, cx[i], cy[i]);  // only this agent's footprint has the cell
-        }
+        if (i >= m || ((codes >> (2 * i)) & 3u) != CK_DYN) continue;
+        const unsigned k = (i < 4 ? k1.z >> (8 * i) : k1.w) & 0xFFu;
+        base[i] = pos[i + 1] - k;
+        const unsigned c0 = base[i] & ~15u;
+        if (k) dv[i][0] = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c0));
+        if (c0 + 16 < pos[i + 1]) dv[i][1] = __ldcg(reinterpret_cast<const uint4*>(a.bdone + c0 + 16));
     }
     int h = 0;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
         if (i >= m || h != i) continue;
-        const unsigned b = cell[i + 1], p = pos[i + 1];
-        if (b == BK_NIL) {
-            if (!occ0[i]) h = i + 1;
-            continue;
-        }
-        if (own[i] != BK_NIL ? own[i] > p : occ0[i]) continue;  // its occupant has not left
-        unsigned q = 0;
-        const int st = bk_before(a, base[i], p, dv[i], &q);
-        if (st == 2) continue;  // an earlier agent stopped here
-        if (st == 0) {
-            *watch = q;
-            return false;
+        const unsigned c = (codes >> (2 * i)) & 3u;
+        if (c == CK_BLOCK) continue;
+        if (c == CK_DYN) {
+            unsigned q = 0;
+            const int st = bk_before(a, base[i], pos[i + 1], dv[i], &q);
+            if (st == 2) continue;  // an earlier agent stopped here
+            if (st == 0) {
+                *watch = q;
+                return false;
+            }
         }
         h = i + 1;
     }
@@ -550,7 +556,7 @@ __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const s
     const int jf = exited ? -1 : h;  // footprint index of the cell it ends on (0: it stays)
 #pragma unroll
     for (int j = 0; j < 6; ++j)
-        if (cell[j] != BK_NIL) a.bdone[pos[j]] = j == jf ? 2 : 1;
+        if (pos[j] != BK_NIL) a.bdone[pos[j]] = j == jf ? 2 : 1;
     return true;
 }
 
@@ -1446,6 +1452,59 @@ __global__ void __launch_bounds__(PREP_THREADS) bk_sort_long_kernel(MoveArgs a) 
     bk_sort_long(a, s_rank);
 }
 
+// Per contended agent, once every bucket is sorted: its check record (see bk_check).
+__global__ void __launch_bounds__(PREP_THREADS) bk_final_kernel(MoveArgs a) {
+    __shared__ signed char s_bp[121][5][2];
+    for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
+    const unsigned nc = cta_load(&a.pcount[1]);  // (its barriers also publish s_bp)
+    if (nc <= TAIL_MAX) return;
+    const unsigned nthreads = gridDim.x * blockDim.x;
+    for (unsigned ci = blockIdx.x * blockDim.x + threadIdx.x; ci < nc; ci += nthreads) {
+        const uint4 r = __ldcg(&a.crec[ci]);
+        unsigned pos[6], cell[6];
+        load_pairs(a, ci, pos, cell);
+        const uint2 ko = __ldcg(reinterpret_cast<const uint2*>(a.eoff + (size_t)ci * 8));
+        int cx[5], cy[5];
+        const int m = path_of(a, r, s_bp, cx, cy);
+        unsigned own[5];
+        bool occ0[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            own[i] = BK_NIL;
+            occ0[i] = false;
+            if (i >= m) continue;
+            const unsigned b = cell[i + 1];
+            if (b != BK_NIL) {
+                own[i] = __ldcg(&a.bown[b]);
+                occ0[i] = __ldcg(&a.bocc0[b]);
+            } else {
+                occ0[i] = occ_test(a, cx[i], cy[i]);  // only this agent's footprint has the cell
+            }
+        }
+        unsigned codes = 0, offs = 0, off4 = 0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            if (i >= m) continue;
+            const unsigned b = cell[i + 1], p = pos[i + 1];
+            unsigned c;
+            if (b == BK_NIL) c = occ0[i] ? CK_BLOCK : CK_FREE;
+            else if (own[i] != BK_NIL ? own[i] > p : occ0[i]) c = CK_BLOCK;  // its occupant has not left
+            else c = CK_DYN;
+            codes |= c << (2 * i);
+            if (b != BK_NIL) {
+                const unsigned k = ((i + 1 < 4 ? ko.x >> (8 * (i + 1)) : ko.y >> (8 * (i - 3))) & 0xFFu);
+                if (i < 4) offs |= k << (8 * i);
+                else off4 = k;
+            }
+        }
+        unsigned pj[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) pj[j] = cell[j] != BK_NIL ? pos[j] : BK_NIL;
+        a.ck[2 * (size_t)ci] = make_uint4(pj[0], pj[1], pj[2], pj[3]);
+        a.ck[2 * (size_t)ci + 1] = make_uint4(pj[4], pj[5], offs, off4 | (codes << 8));
+    }
+}
+
 // The phase's exit records (rank << 32 | id) into processing order on the device when they are
 // few (the usual case: a handful per step); more than EXITS_SMEM are left to the host's radix sort.
 #define EXITS_SMEM 4096
@@ -1520,7 +1579,7 @@ static int ensure_buckets(fp_ctx* ctx) {
     FP_CUDA(ctx, cudaMalloc(&ctx->d_bkt, words * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_bkt, 0, words * 4, ctx->stream));
     FP_CUDA(ctx, cudaMalloc(&ctx->d_bdone, npos + 16 + nb));  // done bytes (+ 16: whole-chunk reads), bocc0
-    FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * (6 * sizeof(uint2) + 8)));  // + eoff
+    FP_CUDA(ctx, cudaMalloc(&ctx->d_entry, (size_t)ctx->cap * (6 * sizeof(uint2) + 8 + 2 * sizeof(uint4)) + 16));  // + eoff, ck
     ctx->bk_nb_cap = (unsigned)nb;
     ctx->bk_npos_cap = (unsigned)npos;
     ctx->bk_agent_cap = ctx->cap;
@@ -1555,7 +1614,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
         move_blocks = std::max(1, std::min(per_sm, FP_MOVE_BLOCKS_PER_SM)) * ctx->sm_count;
         int pc = 0;  // the prep kernels: as many CTAs as fit on every SM (grid-stride loops)
         for (const void* k : {(const void*)bk_count_kernel, (const void*)bk_place_kernel, (const void*)bk_sort_kernel,
-                              (const void*)bk_sort_long_kernel}) {
+                              (const void*)bk_sort_long_kernel, (const void*)bk_final_kernel}) {
             int c = 0;
             FP_CUDA(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k, PREP_THREADS, 0));
             pc = pc ? std::min(pc, c) : c;
@@ -1618,6 +1677,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.bown = ctx->d_bkt + 2 * (size_t)ctx->bk_nb_cap;
     a.entry = ctx->d_entry;
     a.eoff = reinterpret_cast<uint8_t*>(ctx->d_entry + (size_t)ctx->cap * 6);
+    a.ck = reinterpret_cast<uint4*>(ctx->d_entry + (((size_t)ctx->cap * 7 + 1) & ~(size_t)1));  // 16-byte aligned
     uint2* lists = reinterpret_cast<uint2*>(ctx->d_rec_a);  // 16 B per agent: two uint2 lists
     a.alist[0] = lists;
     a.alist[1] = lists + ctx->cap;
@@ -1663,6 +1723,8 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     bk_sort_kernel<<<pg, PREP_THREADS, 0, s>>>(a, blocks);
     FP_LAUNCHED(ctx);
     bk_sort_long_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+    FP_LAUNCHED(ctx);
+    bk_final_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
     FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<2>, a));
     ctx->ctr.kernel_launches++;
