@@ -16,8 +16,12 @@
 #include "internal.cuh"
 #include "scan.cuh"
 
+#ifndef PLAN_ITEM_CHUNKS
 #define PLAN_ITEM_CHUNKS 10   // chunks per plan item (plan.cu's ring holds two items of <= 12 slots)
+#endif
+#ifndef PLAN_ITEM_AGENTS
 #define PLAN_ITEM_AGENTS 512  // agents per plan item at most
+#endif
 
 __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* alive,
                                     const uint8_t* owned, uint32_t n, int tile_w, uint32_t cps, uint32_t* cnt,

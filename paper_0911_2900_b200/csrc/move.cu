@@ -237,7 +237,9 @@ __device__ __forceinline__ void walk_owned(const MoveArgs& a, const uint4& r, co
 // behind that, and its own start cell, never make it wait -- and then writes its done bytes:
 // 2 on the cell it ends on (its start if it stays), 1 on the others.  Nothing else of its walk
 // is read by the other contended agents during the phase (an uncontended cell is only ever
-// touched by its one agent), so no fence orders the occupancy updates before the done bytes.
+// touched by its one agent); the one write that can collide is a later agent setting the
+// occupancy bit of a start cell this agent cleared, so a release fence orders that clear before
+// the done bytes when the agent leaves a contended start cell.
 // bbase, bown and done are a few MB and stay in L2 through the rounds.  Built per phase by
 //   bk_count  per contended agent: its slot k in each of its buckets (one atomic counter each),
 //             the cells' occupancy (bocc0)
@@ -552,6 +554,10 @@ __device__ __forceinline__ bool bk_check(const MoveArgs& a, unsigned ci, const s
 #pragma unroll
     for (int i = 0; i < 5; ++i) blocked[i] = i >= h;
     walk_apply(a, r, cx, cy, m, blocked, hops);
+    // A later agent may end its walk on the start cell this one left (only if that cell is
+    // contended): the cleared occupancy bit must be performed before the done bytes let it in,
+    // or its set bit could be wiped.
+    if (h > 0 && pos[0] != BK_NIL) fence_acq_rel_gpu();
     const bool exited = (h == m) && (r.z & 0x80000000u);
     const int jf = exited ? -1 : h;  // footprint index of the cell it ends on (0: it stays)
 #pragma unroll

@@ -590,7 +590,10 @@ __device__ __forceinline__ unsigned long long globaltimer_p() {
 //     then release those slots.
 // The ring holds two items, so the TMA of the next item overlaps the planning of the current one.
 #define PLAN_QUEUE 64  // published items a CTA remembers (the ring bounds the ones in flight)
-#define RING_HALF (RING_SLOTS / 2)  // slots per item (>= PLAN_ITEM_CHUNKS + 2, bucket.cu)
+#ifndef RING_PARTS
+#define RING_PARTS 2  // items in flight per CTA (the ring's parts; 2 = double buffering)
+#endif
+#define RING_HALF (RING_SLOTS / RING_PARTS)  // slots per item (>= PLAN_ITEM_CHUNKS + 2, bucket.cu)
 
 __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __grid_constant__ CUtensorMap tmap_w,
                                                                       const __grid_constant__ CUtensorMap tmap_o,
@@ -605,7 +608,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
     __shared__ int s_ref[RING_SLOTS];
     __shared__ unsigned s_qv[PLAN_QUEUE];      // published item q: first virtual agent index
     __shared__ unsigned s_qa[PLAN_QUEUE];      //   its first bucket position
-    __shared__ int s_qs[PLAN_QUEUE];           //   its ring half | first chunk << 1
+    __shared__ int s_qs[PLAN_QUEUE];           //   its ring part | first chunk << 2
     __shared__ unsigned s_next;                // consumers' claim cursor (virtual agents)
     __shared__ volatile unsigned s_pub;        // virtual agents published
     __shared__ volatile unsigned s_nq;         // queue entries published
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
         // ---------------- producer
         bool ok = true;
         unsigned pub = 0, nq = 0;
-        int half = 0;  // ring half of the next item (items alternate halves: double buffering)
+        int half = 0;  // ring part of the next item (items take the parts in turn)
         while (ok) {
             uint32_t i = 0;
             if (lane == 0) i = (uint32_t)atomicAdd(&a.sc->tile_next, 1ull);
@@ -697,7 +700,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
             if (lane == 0 && ok) {
                 s_qv[nq % PLAN_QUEUE] = pub;
                 s_qa[nq % PLAN_QUEUE] = a0;
-                s_qs[nq % PLAN_QUEUE] = half | (kf << 1);
+                s_qs[nq % PLAN_QUEUE] = half | (kf << 2);
                 ++nq;
                 pub += a1 - a0;
                 __threadfence_block();
@@ -705,7 +708,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                 __threadfence_block();
                 s_pub = pub;
             }
-            half ^= 1;
+            half = half + 1 == RING_PARTS ? 0 : half + 1;
         }
         if (lane == 0) {
             __threadfence_block();
@@ -773,7 +776,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                 while (q + 1 < nq && s_qv[(q + 1) % PLAN_QUEUE] <= ai) ++q;
                 qhint = q;
                 const unsigned pos = s_qa[q % PLAN_QUEUE] + (ai - s_qv[q % PLAN_QUEUE]);
-                const int qs = s_qs[q % PLAN_QUEUE], ihalf = qs & 1, kf = qs >> 1;
+                const int qs = s_qs[q % PLAN_QUEUE], ihalf = qs & 3, kf = qs >> 2;
                 sbase = ihalf * RING_HALF - (kf - 1);
                 const uint4 br = __ldcg(&A.brec[pos]);  // (id, wrapped x, y, v_max), bucket.cu
                 const uint32_t id = br.x;
