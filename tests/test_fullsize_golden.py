@@ -119,3 +119,19 @@ def test_run_matches_reference(name):
     assert r.displacement_cells == int(f["displacement"].sum())
     assert r.alive == int(f["alive"][-1])
     assert fp.state_hash(st) == int(f["state_hash"][-1])
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(1800)
+@pytest.mark.parametrize("name", ["room_v5", "plaza"])
+def test_repeated_runs_are_identical(name):
+    """Race probe for the lock-free motion and plan pipelines: the same run repeated on fresh
+    contexts always ends on the reference's final state (a lost occupancy update or a stale ring
+    slot would show up as a divergent run, as a rare one did before the start-cell fence)."""
+    f = fixture(name)
+    wl = workload(f)
+    steps = int(f["steps"])
+    for rep in range(4):
+        st = fresh(wl)
+        fp.run(st, fp.SimParams(k_s=float(f["k_s"]), seed=int(f["seed"]), steps=steps))
+        assert fp.state_hash(st) == int(f["state_hash"][-1]), f"repetition {rep} diverged"
