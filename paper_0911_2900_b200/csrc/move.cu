@@ -66,6 +66,7 @@ struct MoveArgs {
     // reservation rounds (see the bucket notes below)
     const uint4* crec;             // contended records (= rec[1]), rank in .y
     uint2* pw;                     // per bitplane word: (contended cells before it, its P2 bits)
+    unsigned p2g;                  // G: the grid of p2_count / p2_number (<= BK_SCAN2 - 1)
     unsigned* scan;                // [0, G) per-CTA contended cells, [G] their total;
                                    // [BK_SCAN2, BK_SCAN2 + G) per-CTA bucket entries, + G total
     unsigned nb_cap;               // buckets (contended cells): <= 3 per contended agent
@@ -1136,7 +1137,6 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                 append(B, &a.pcount[0], a.rec[0], take, rec);
             }
             grid.sync();
-            p2_count(a, s_red);
             cand = a.rec[0];
             ncand = cta_load(&a.pcount[0]);
         } else {
@@ -1146,7 +1146,6 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
             seed_mark(a, win, s_bp);
             grid.sync();
             if (gtid == 0) a.sc->t_marked = globaltimer();
-            p2_count(a, s_red);
             unsigned long long hops = 0;
             seed_classify(a, Gs, win, s_bp, &hops);
             flush_hops(B, a.sc, hops);
@@ -1183,7 +1182,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
     unsigned np = nc;
     if (PART == 1) return;  // (mode B) the buckets are built by the prep kernels between the parts
     if (rounds) {
-        nbu = cta_load(&a.scan[gridDim.x]);  // buckets (p2_number)
+        nbu = cta_load(&a.scan[a.p2g]);  // buckets (p2_number)
         if (gtid == 0) a.sc->t_prep = globaltimer();
         // Per round and CTA, in the (now free) dynamic shared memory: a queue of agents whose
         // watched blocker has walked (full check) and a queue of still-pending (agent, watch)
@@ -1678,6 +1677,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.bbase = ctx->d_bkt + ctx->bk_nb_cap;
     a.brank = reinterpret_cast<uint2*>(ctx->d_bkt + 3 * (size_t)ctx->bk_nb_cap);
     a.scan = reinterpret_cast<unsigned*>(a.brank + ctx->bk_npos_cap);
+    a.p2g = (unsigned)std::min(BK_SCAN2 - 1, 4 * ctx->sm_count);
     a.bdone = ctx->d_bdone;
     a.bocc0 = ctx->d_bdone + ctx->bk_npos_cap + 16;
     a.bown = ctx->d_bkt + 2 * (size_t)ctx->bk_nb_cap;
@@ -1703,11 +1703,12 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const size_t seed_smem = (size_t)SEED_GROUPS * 2 * seed_ww(ctx->tile_w) * (ctx->tile_h + 10) * 4;
-    if (premade) {  // steps 1 and 2 over the plan's records: two plain launches
+    // a roster the shared-memory tail always takes whole (<= TAIL_MAX agents) needs no buckets:
+    // one cooperative launch for steps 1 and 2, no prep launches (launch-bound small configs)
+    const bool tiny = ctx->n <= TAIL_MAX;
+    if (premade && !tiny) {  // steps 1 and 2 over the plan's records: two plain launches
         const unsigned sb = std::min(seed_blocks, std::max(1u, (unsigned)fp_blocks(ctx->n, SEED_ITEM)));
         seed_mark_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
-        FP_LAUNCHED(ctx);
-        p2_count_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a);
         FP_LAUNCHED(ctx);
         seed_classify_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
         FP_LAUNCHED(ctx);
@@ -1715,23 +1716,27 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
         FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<1>, a));
         ctx->ctr.kernel_launches++;
     }
-    p2_number_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a);
-    FP_LAUNCHED(ctx);
-    const unsigned pg = prep_blocks;
-    bk_count_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
-    FP_LAUNCHED(ctx);
-    bk_scan_count_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a, blocks);
-    FP_LAUNCHED(ctx);
-    bk_scan_base_kernel<<<blocks, MOVE_THREADS, 0, s>>>(a, blocks);
-    FP_LAUNCHED(ctx);
-    bk_place_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
-    FP_LAUNCHED(ctx);
-    bk_sort_kernel<<<pg, PREP_THREADS, 0, s>>>(a, blocks);
-    FP_LAUNCHED(ctx);
-    bk_sort_long_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
-    FP_LAUNCHED(ctx);
-    bk_final_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
-    FP_LAUNCHED(ctx);
+    if (!tiny) {
+        p2_count_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a);
+        FP_LAUNCHED(ctx);
+        p2_number_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a);
+        FP_LAUNCHED(ctx);
+        const unsigned pg = prep_blocks;
+        bk_count_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        FP_LAUNCHED(ctx);
+        bk_scan_count_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a, a.p2g);
+        FP_LAUNCHED(ctx);
+        bk_scan_base_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a, a.p2g);
+        FP_LAUNCHED(ctx);
+        bk_place_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        FP_LAUNCHED(ctx);
+        bk_sort_kernel<<<pg, PREP_THREADS, 0, s>>>(a, a.p2g);
+        FP_LAUNCHED(ctx);
+        bk_sort_long_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        FP_LAUNCHED(ctx);
+        bk_final_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        FP_LAUNCHED(ctx);
+    }
     FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<2>, a));
     ctx->ctr.kernel_launches++;
     exits_sort_kernel<<<1, 1024, 0, s>>>(ctx->d_exits, ctx->d_sc);

@@ -609,6 +609,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
     __shared__ unsigned s_qv[PLAN_QUEUE];      // published item q: first virtual agent index
     __shared__ unsigned s_qa[PLAN_QUEUE];      //   its first bucket position
     __shared__ int s_qs[PLAN_QUEUE];           //   its ring part | first chunk << 2
+    __shared__ int s_qx[PLAN_QUEUE];           //   its stripe
     __shared__ unsigned s_next;                // consumers' claim cursor (virtual agents)
     __shared__ volatile unsigned s_pub;        // virtual agents published
     __shared__ volatile unsigned s_nq;         // queue entries published
@@ -701,6 +702,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                 s_qv[nq % PLAN_QUEUE] = pub;
                 s_qa[nq % PLAN_QUEUE] = a0;
                 s_qs[nq % PLAN_QUEUE] = half | (kf << 2);
+                s_qx[nq % PLAN_QUEUE] = s;
                 ++nq;
                 pub += a1 - a0;
                 __threadfence_block();
@@ -781,7 +783,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                 const uint4 br = __ldcg(&A.brec[pos]);  // (id, wrapped x, y, v_max), bucket.cu
                 const uint32_t id = br.x;
                 const int px = (int)br.y, py = (int)br.z, v = (int)br.w;
-                const int s = px / A.tile_w, k = py >> 3;
+                const int s = s_qx[q % PLAN_QUEUE], k = py >> 3;  // the item's stripe (= px / tile_w)
                 k_lo = max(k - 1, 0);
                 k_hi = min(k + 1, rows_chunks - 1);
                 bool ready = true;
