@@ -4,8 +4,8 @@
 //   wall / exit / occupancy : 1-bit planes, P u32 words per row covering x in [-32, 32*P-32);
 //                             for periodic-x grids the ghost bits mirror the wrapped columns
 //   weight plane            : u32 per cell, pitch PW covering x in [-8, PW-8): the static
-//                             planning data of a cell for one (k_s, potential) -- wall flag,
-//                             unreachable flag, and the fp32-mantissa / integer-exponent split of
+//                             planning data of a cell for one (k_s, potential) -- an exact-path
+//                             flag and the fp32-mantissa / integer-exponent split of
 //                             2^(-k_s*log2(e)*S) (plane.cu).  Read by the plan kernel via TMA.
 //   field                   : fp64 per cell (StaticField::s), read only by the exact path
 //   motion scratch          : P1/P2 contention bitplanes (like occupancy); a 32-byte rank
@@ -32,8 +32,7 @@
 // weight-plane word encoding (plane.cu)
 #define FP_W_WALL 0xFFFFFFFFu
 #define FP_W_UNREACH 0x80000000u
-#define FP_W_SPECIAL 0x80000000u
-#define FP_W_UNSAFE 0x40000000u
+#define FP_W_FLAG 0x80000000u  // the exact path plans an agent standing here
 
 struct Geo {
     int W, H, boundary, P;

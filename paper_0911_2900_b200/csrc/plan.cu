@@ -241,16 +241,20 @@ __global__ void plan_exact_kernel(PlanCommon a) {
 // ------------------------------------------------------------------------------ fast weights
 enum { MODE_EXIT = 0, MODE_ONES = 1, MODE_DRIVE = 2 };
 
+// The agent's exponent offset A_p = ((C_p + 127) mod 256) << 23 from its own plane word
+// (bits 30..23 hold (-C_p) mod 256, plane.cu).
+__device__ __forceinline__ uint32_t plane_offset(uint32_t own) { return ((127u - (own >> 23)) & 255u) << 23; }
+
+// Weight of a reachable candidate word relative to the agent (offset ap): m_c * 2^(C_p - C_c),
+// an exact fp32 number (|C_p - C_c| <= 60 on cells the fast path plans, plane.cu).
+__device__ __forceinline__ float plane_weight(uint32_t w, uint32_t ap) { return fabsf(__uint_as_float(w + ap)); }
+
 // Weight of a non-wall candidate word, as an exact fp64 value (an fp32-precision weight).
-__device__ __forceinline__ double fast_weight(uint32_t w, int Cp, int mode, double drive_w) {
+__device__ __forceinline__ double fast_weight(uint32_t w, uint32_t ap, int mode, double drive_w, bool unreach) {
     if (mode == MODE_ONES) return 1.0;
     if (mode == MODE_DRIVE) return drive_w;
-    if (w & FP_W_SPECIAL) return 0.0;  // unreachable (walls never get here)
-    const int d = ((int)((uint32_t)(Cp - (int)((w >> 23) & 0x7Fu)) << 25)) >> 25;
-    const uint32_t mant = w & 0x7FFFFFu;
-    const int hi = ((1023 + d) << 20) | (int)(mant >> 3);
-    const int lo = (int)((mant & 7u) << 29);
-    return __hiloint2double(hi, lo);
+    if (unreach) return 0.0;
+    return (double)plane_weight(w, ap);
 }
 
 __device__ __forceinline__ float drive_weight_f(double k_s, double g, int dx) {
@@ -351,15 +355,6 @@ __device__ __forceinline__ void mask_or_row(Mask121& m, uint32_t rowbits, int B)
     if (B + 11 > 64) m.hi |= (B >= 64) ? ((unsigned long long)rowbits << (B - 64)) : ((unsigned long long)rowbits >> (64 - B));
 }
 
-// Weight of a reachable plane word in ExitDistance mode as an exact fp64 number:
-// m_c * 2^(C_p - C_c), with (C_p - C_c) recovered mod 128 (|d| <= 60 on safe cells).
-__device__ __forceinline__ double exit_weight(uint32_t w, int cp_biased /* C_p + 64 (+128) */) {
-    const uint32_t t = (uint32_t)(cp_biased - (int)(w >> 23)) & 127u;  // d + 64
-    const int hi = (int)((t << 20) + (959u << 20)) | (int)((w >> 3) & 0xFFFFFu);
-    const int lo = (int)(w << 29);
-    return __hiloint2double(hi, lo);
-}
-
 // Path mask test against the shared-memory copy of c_pathmask (lanes index it divergently).
 __device__ __forceinline__ bool path_blocked_s(const uint4* pm, const Mask121& m, int o) {
     const uint4 q = pm[o];
@@ -368,30 +363,31 @@ __device__ __forceinline__ bool path_blocked_s(const uint4* pm, const Mask121& m
     return ((m.lo & plo) | (m.hi & phi)) != 0ull;
 }
 
-// The same weight as an fp32 number -- exact: the plane keeps a 23-bit mantissa and
-// |C_p - C_c| <= 60 stays inside the fp32 exponent range.
-__device__ __forceinline__ float exit_weight32(uint32_t w, int cp_biased) {
-    const uint32_t t = (uint32_t)(cp_biased - (int)(w >> 23)) & 127u;  // d + 64
-    return __uint_as_float(((t + 63u) << 23) | (w & 0x7FFFFFu));
-}
-
-// Pairwise fp32 sum of x[0..N) (depth ceil(log2 N): the error bound the guard band assumes).
+// Pairwise fp32 sum of |x[0..N)| (depth ceil(log2 N): the error bound the guard band assumes;
+// the |.| is an operand modifier of the adds, see plane_weight).
 template <int N>
 __device__ __forceinline__ float pairwise_sum(const float* x) {
     if constexpr (N == 1) {
-        return x[0];
+        return fabsf(x[0]);
     } else {
         constexpr int H = (N + 1) / 2;
         return pairwise_sum<H>(x) + pairwise_sum<N - H>(x + H);
     }
 }
 
+// Bits [osh, osh + 32) of a staged bitplane row.
+__device__ __forceinline__ uint32_t row_bits(const uint32_t* row, int osh) {
+    return __funnelshift_r(row[osh >> 5], row[(osh >> 5) + 1], osh & 31);
+}
+
 // Plans one agent from the staged stripe (V = its v_max, DRIVE = DriveX potential).  Returns 1
 // when the fast path decided (result in *ox, *oy), 2 when the exact path must decide.
 //   walls   the ball's wall bits (staged wall bitplane, one word pair per row)
-//   pass 1  rows centre-out: valid candidates (not Wall/unreachable, not occupied by another
-//           agent, visible) contribute their exact fp32 weight to a pairwise fp32 row sum; the
-//           row sums are accumulated in fp64
+//   pass 1  rows centre-out: candidates (in the grid, not Wall, not occupied by another agent,
+//           visible) contribute their exact fp32 weight -- one integer add on the plane word,
+//           plane.cu -- to a pairwise fp32 row sum; the row sums are accumulated in fp64.
+//           Unreachable free cells never reach this path: their word and every centre within
+//           Chebyshev 5 of them carry the exact-path flag (plane.cu)
 //   pass 2  u*total picks the row; the row is replayed in list order (wrapped-x sorted at a
 //           periodic seam) to find the first cumulative weight > threshold; guard band.
 // MASKED: one radius-V code path for every v_max <= V (mixed rosters): rows and columns beyond
@@ -404,21 +400,21 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
                                            int vr = V) {
     constexpr int D = 2 * V + 1;
     const PlanCommon& a = A.c;
-    const uint32_t colmask = MASKED ? (((1u << (2 * vr + 1)) - 1u) << (V - vr)) : ((1u << D) - 1u);
-    const int lx = px - X0;
-    int cpb = 0;
-    if (!DRIVE) {
-        const uint32_t own = R.wrow(py)[lx];
-        if (own & (FP_W_SPECIAL | FP_W_UNSAFE)) return 2;  // "ones" pocket / unsafe centre
-        cpb = (int)((own >> 23) & 0x7Fu) + 64 + 128;
+    uint32_t colmask = MASKED ? (((1u << (2 * vr + 1)) - 1u) << (V - vr)) : ((1u << D) - 1u);
+    if (a.g.boundary != FP_BOUNDARY_PERIODIC_X) {  // columns outside [0, W) (planning.hpp:39-41)
+        if (px < V) colmask &= ~0u << (V - px);
+        if (px + V >= a.g.W) colmask &= (1u << (a.g.W - px + V)) - 1u;
     }
+    const int lx = px - X0;
+    const uint32_t own = R.wrow(py)[lx];
+    if (own >> 31) return 2;  // flagged centre: unreachable pocket, steep field, unreachable neighbour
+    const uint32_t ap = DRIVE ? 0u : plane_offset(own);
     const int osh = osh0 + lx - V;  // staged bitplane bit of dx = -V
     Mask121 wm{0ull, 0ull};
 #pragma unroll
     for (int dy = -V; dy <= V; ++dy) {
         if ((unsigned)(py + dy) >= (unsigned)a.g.H) continue;
-        const uint32_t* wrow = R.lrow(py + dy);
-        const uint32_t wb = __funnelshift_r(wrow[osh >> 5], wrow[(osh >> 5) + 1], osh & 31) & ((1u << D) - 1u);
+        const uint32_t wb = row_bits(R.lrow(py + dy), osh) & ((1u << D) - 1u);
         mask_or_row(wm, wb, (dy + 5) * 11 + 5 - V);
     }
     const bool anywall = (wm.lo | wm.hi) != 0ull;
@@ -431,18 +427,10 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
         const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);  // centre-out: 0, -1, 1, -2, 2, ...
         const bool rowok = (unsigned)(py + dy) < (unsigned)a.g.H;
         const uint32_t* row = R.wrow(py + dy) + lx - V;
-        uint32_t wv[D];
-        uint32_t spec = 0u;
-#pragma unroll
-        for (int k = 0; k < D; ++k) {
-            wv[k] = row[k];
-            spec |= (wv[k] >> 31) << k;
-        }
-        const uint32_t* orow = R.orow(py + dy);
-        uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
+        uint32_t occ = row_bits(R.orow(py + dy), osh) | row_bits(R.lrow(py + dy), osh);
         if (dy == 0) occ &= ~(1u << V);  // the own cell stays a candidate (planning.hpp:45-46)
         const bool inball = !MASKED || (dy <= vr && -dy <= vr);
-        uint32_t valid = (rowok && inball) ? (~(spec | occ) & colmask) : 0u;
+        uint32_t valid = (rowok && inball) ? (~occ & colmask) : 0u;
         if (anywall) {
 #pragma unroll
             for (int k = 0; k < D; ++k)
@@ -450,8 +438,10 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
         }
         float w[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k)
-            w[k] = ((valid >> k) & 1u) ? (DRIVE ? dw[k] : exit_weight32(wv[k], cpb)) : 0.0f;
+        for (int k = 0; k < D; ++k) {
+            if (DRIVE) w[k] = ((valid >> k) & 1u) ? dw[k] : 0.0f;
+            else w[k] = __uint_as_float(((valid >> k) & 1u) ? row[k] + ap : 0u);
+        }
         rso[t] = pairwise_sum<D>(w);
     }
     double rs[D];  // row sums, indexed by dy + V
@@ -476,9 +466,9 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
     if (rstar < 0) return 2;  // u*total rounded up to total
     const int dy = rstar - V;
     const uint32_t* row = R.wrow(py + dy) + lx;
-    const uint32_t* orow = R.orow(py + dy);
-    uint32_t occ = __funnelshift_r(orow[osh >> 5], orow[(osh >> 5) + 1], osh & 31);
+    uint32_t occ = row_bits(R.orow(py + dy), osh) | row_bits(R.lrow(py + dy), osh);
     if (dy == 0) occ &= ~(1u << V);
+    const uint32_t valid = ~occ & colmask;
     const int Rr = MASKED ? vr : V;  // the agent's radius
     int a0 = -Rr, a1 = Rr, b0 = 0, b1 = -1;
     if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {  // wrapped-x order at the seam (planning.hpp:50-53)
@@ -494,11 +484,9 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
     for (int seg = 0; seg < 2 && !found; ++seg) {
         const int lo = seg ? b0 : a0, hi = seg ? b1 : a1;
         for (int dx = lo; dx <= hi; ++dx) {
-            const uint32_t w = row[dx];
-            if (w >> 31) continue;                 // wall / unreachable (weight 0)
-            if ((occ >> (dx + V)) & 1u) continue;  // occupied by another agent
+            if (!((valid >> (dx + V)) & 1u)) continue;  // outside the grid, Wall, occupied
             if (anywall && path_blocked_s(pathm, wm, (dy + 5) * 11 + dx + 5)) continue;
-            const double wt = DRIVE ? drive_tab[dx + 5] : exit_weight(w, cpb);
+            const double wt = DRIVE ? drive_tab[dx + 5] : (double)plane_weight(row[dx], ap);
             const double next = prefix + wt;
             if (next > theta) {
                 lower = prefix;
@@ -523,10 +511,10 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
 }
 
 // record_of (motion_rec.cuh) for a fast-path decision inside the staged stripe: the target lies in
-// the ball, the Wall test reads the staged plane words, and the Exit test (global bitplane) runs
+// the ball, the Wall test reads the staged wall bits, and the Exit test (global bitplane) runs
 // only in tiles whose window holds an Exit.
 __device__ __forceinline__ uint4 record_of_ring(const Geo& g, const uint32_t* occ, bool tile_exit, const Ring& R,
-                                                int lx, uint32_t id, int sx, int sy, int tx, int ty, int v,
+                                                int lbit, uint32_t id, int sx, int sy, int tx, int ty, int v,
                                                 const signed char (*bp)[5][2]) {
     const int ddx = g.segment_dx(sx, tx), ddy = ty - sy;
     const int o = (ddy + 5) * 11 + ddx + 5;
@@ -535,7 +523,8 @@ __device__ __forceinline__ uint4 record_of_ring(const Geo& g, const uint32_t* oc
     bool ex = false;
     for (int j = 0; j < len; ++j) {
         const int ox = bp[o][j][0], oy = bp[o][j][1];
-        if (R.wrow(sy + oy)[lx + ox] == FP_W_WALL) break;
+        const int b = lbit + ox;
+        if ((R.lrow(sy + oy)[b >> 5] >> (b & 31)) & 1u) break;  // Wall
         ++m;
         if (tile_exit) {
             const int x = g.wrap(sx + ox), y = sy + oy;
@@ -807,7 +796,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                     a.dx[id] = cx;
                     a.dy[id] = cy;
                     const int tile = (py / A.tile_h) * A.tiles_x + s;
-                    A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], R, px - X0, id, px, py, cx, cy, v, s_bp);
+                    A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], R, osh0 + px - X0, id, px, py, cx, cy, v, s_bp);
                 } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
                     A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, pos);
                 }
@@ -933,10 +922,10 @@ __global__ void choice_kernel(PlanCommon a, const uint32_t* plane, int PW, uint3
     const int py = a.y[i];
     const ExactWeight wf = make_weight(a, px, py);
     const uint32_t own = plane ? plane[(size_t)py * PW + px + FP_XPAD_W] : 0u;
-    int mode = MODE_EXIT, Cp = 0;
+    int mode = MODE_EXIT;
     if (a.potential == FP_POTENTIAL_DRIVE_X) mode = MODE_DRIVE;
-    else if (own == FP_W_UNREACH) mode = MODE_ONES;
-    else Cp = (int)((own >> 23) & 0x7Fu);
+    else if (wf.ones) mode = MODE_ONES;
+    const uint32_t ap = plane_offset(own);
     uint32_t n = 0;
     double fast_total = 0.0;
     for_each_candidate(a, px, py, a.v[i], [&](int x, int y) {
@@ -947,7 +936,8 @@ __global__ void choice_kernel(PlanCommon a, const uint32_t* plane, int PW, uint3
         if (plane) {
             const int dxs = a.g.segment_dx(px, x);
             const uint32_t word = plane[(size_t)y * PW + px + dxs + FP_XPAD_W];
-            fw = fast_weight(word, Cp, mode, (double)drive_weight_f(a.k_s, a.drive_gradient, dxs));
+            fw = fast_weight(word, ap, mode, (double)drive_weight_f(a.k_s, a.drive_gradient, dxs),
+                             mode == MODE_EXIT && isinf(a.field[(size_t)y * a.g.W + x]));
         } else {
             fw = w[n];
         }

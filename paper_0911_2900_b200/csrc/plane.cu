@@ -2,15 +2,20 @@
 //
 // The reference weighs candidate c of an agent at p by w = exp(k_s * (S(p) - S(c)))
 // (planning.hpp:102).  With K = k_s*log2(e) and y = K*S, w = 2^(y_p - y_c).  Per cell we store
-// the split 2^(-y_c) = m_c * 2^(-C_c), C_c = ceil(y_c), m_c = 2^(C_c - y_c) in [1, 2), as one u32:
-//     bit 31      special (Wall = 0xFFFFFFFF, unreachable free cell = 0x80000000)
-//     bit 30      "unsafe centre": some reachable cell within Chebyshev 5 has |C - C_c| > 60
-//     bits 29..23 C_c mod 128
+// the split 2^(-y_c) = m_c * 2^(-C_c), C_c = ceil(y_c), m_c = 2^(C_c - y_c) in [1, 2), as one u32
+// laid out like an fp32 number:
+//     bit 31      "exact" flag: Wall (0xFFFFFFFF), unreachable free cell, or a centre the fast
+//                 path must not plan -- some reachable cell within Chebyshev 5 has
+//                 |C - C_c| > 60, or an unreachable free cell lies within Chebyshev 5
+//     bits 30..23 (-C_c) mod 256
 //     bits 22..0  23-bit mantissa of m_c (relative rounding error <= 2^-24)
-// An agent at p then weighs c by m_c * 2^(C_p - C_c) -- the reference weight times the common
-// factor 2^(C_p - y_p) -- so sampling (which is scale invariant, planning.hpp:60-62) sees the
-// reference weights to 2^-24 relative; the plan kernel's guard band turns that into bit-exact
-// decisions (plan.cu).  4 bytes per cell instead of the fp64 field's 8.
+// An agent at p weighs c by m_c * 2^(C_p - C_c) -- the reference weight times the common factor
+// 2^(C_p - y_p) -- so sampling (scale invariant, planning.hpp:60-62) sees the reference weights
+// to 2^-24 relative; the plan kernel's guard band turns that into bit-exact decisions (plan.cu).
+// That weight is ONE integer add away from the word: w_c + ((C_p + 127) mod 256) << 23 has
+// exponent field (C_p - C_c + 127) mod 256 and c's mantissa, i.e. it is +-m_c * 2^(C_p - C_c)
+// as an fp32 number (the carry out of the exponent lands in the sign bit, which the kernel's
+// |x| operand modifier drops).  4 bytes per cell instead of the fp64 field's 8.
 // DriveX: the plane only carries walls (weights depend on dx alone, plan.cu table).
 #include <limits.h>
 #include <math.h>
@@ -42,6 +47,7 @@ __global__ void plane_build_kernel(Geo g, int PW, const double* field, int poten
             const double s = field[(size_t)y * g.W + x];
             if (isinf(s)) {
                 w = FP_W_UNREACH;
+                c = INT_MIN + 1;  // unreachable free cell (flags every centre within Chebyshev 5)
             } else {
                 const double yv = K * s;
                 double C = ceil(yv);
@@ -53,7 +59,7 @@ __global__ void plane_build_kernel(Geo g, int PW, const double* field, int poten
                 }
                 const long long Ci = (long long)C;
                 c = (int)Ci;
-                w = ((uint32_t)(Ci & 0x7F) << 23) | (uint32_t)mant;
+                w = ((uint32_t)(-Ci & 0xFF) << 23) | (uint32_t)mant;
             }
         }
         plane[i] = w;
@@ -61,7 +67,8 @@ __global__ void plane_build_kernel(Geo g, int PW, const double* field, int poten
     }
 }
 
-// Row pass of the radius-5 min/max of C (INT_MIN marks non-normal cells).
+// Row pass of the radius-5 min/max of C (cval: INT_MIN wall / outside, INT_MIN + 1 unreachable
+// free cell; a window holding an unreachable cell gets rmin = INT_MIN).
 __global__ void plane_rowminmax_kernel(int PW, int H, const int* cval, int* rmin, int* rmax) {
     const size_t total = (size_t)PW * H;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -73,6 +80,10 @@ __global__ void plane_rowminmax_kernel(int PW, int H, const int* cval, int* rmin
             if (q < 0 || q >= PW) continue;
             const int c = cval[row + q];
             if (c == INT_MIN) continue;
+            if (c == INT_MIN + 1) {
+                mn = INT_MIN;
+                continue;
+            }
             mn = min(mn, c);
             mx = max(mx, c);
         }
@@ -86,7 +97,7 @@ __global__ void plane_unsafe_kernel(int PW, int H, const int* cval, const int* r
     const size_t total = (size_t)PW * H;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int c = cval[i];
-        if (c == INT_MIN) continue;
+        if (c == INT_MIN || c == INT_MIN + 1) continue;  // walls / unreachable cells carry the flag already
         const int xp = (int)(i % PW), y = (int)(i / PW);
         int mn = INT_MAX, mx = INT_MIN;
         for (int d = -FP_HALO; d <= FP_HALO; ++d) {
@@ -95,8 +106,8 @@ __global__ void plane_unsafe_kernel(int PW, int H, const int* cval, const int* r
             mn = min(mn, rmin[(size_t)yy * PW + xp]);
             mx = max(mx, rmax[(size_t)yy * PW + xp]);
         }
-        if (mx - c > 60 || c - mn > 60) {
-            plane[i] |= FP_W_UNSAFE;
+        if (mn == INT_MIN || mx - c > 60 || c - mn > 60) {
+            plane[i] |= FP_W_FLAG;
             atomicAdd(n_unsafe, 1ull);
         }
     }
