@@ -11,7 +11,9 @@
 //   tile_cnt / tile_off     per tile (row-major id), tile_list = the non-empty tiles,
 //   items                   motion seed work items (tile-list entry, chunk of SEED_ITEM agents)
 //   plan items              the plan kernel's work units: <= PLAN_ITEM_CHUNKS chunks of one
-//                           stripe and <= PLAN_ITEM_AGENTS of their agents
+//                           stripe and <= PLAN_ITEM_AGENTS of their agents; 64 B each: (first
+//                           chunk, chunks - 1, first agent, end agent) + u16 reference count
+//                           per ring slot
 // All passes are this file's kernels (no library primitives in the step).
 #include "internal.cuh"
 #include "scan.cuh"
@@ -134,7 +136,30 @@ __global__ void plan_items_kernel(const uint32_t* ccnt, const uint32_t* coff, ui
                 if (c && o <= lo && lo < o + c) gf = g;
                 if (c && o <= hi - 1 && hi - 1 < o + c) gl = g;
             }
-            items[ib++] = make_uint4(gf, gl - gf, lo, hi);
+            // the item's agents per chunk, and per ring slot j (chunk gf - 1 + j) the agents
+            // whose ball reaches it (chunks gf - 2 + j .. gf + j): the producer's reference counts
+            uint32_t ca[PLAN_ITEM_CHUNKS];
+            for (uint32_t g = gf; g <= gl; ++g) {
+                const uint32_t o = coff[g], c = ccnt[g];
+                const uint32_t l = max(o, lo), h = min(o + c, hi);
+                ca[g - gf] = h > l ? h - l : 0u;
+            }
+            uint4* rec = items + 4 * (size_t)ib++;
+            rec[0] = make_uint4(gf, gl - gf, lo, hi);
+            uint16_t refs[24] = {0};
+            const int nk = (int)(gl - gf) + 1;
+            for (int j = 0; j < nk + 2 && j < 24; ++j) {
+                uint32_t r = 0;
+                for (int d = -1; d <= 1; ++d) {
+                    const int e = j - 1 + d;  // item chunk index
+                    if (e >= 0 && e < nk) r += ca[e];
+                }
+                refs[j] = (uint16_t)r;
+            }
+            const uint4* rv = reinterpret_cast<const uint4*>(refs);
+            rec[1] = rv[0];
+            rec[2] = rv[1];
+            rec[3] = rv[2];
         }
     }
 }
@@ -164,7 +189,7 @@ int fp_bucket_reserve(fp_ctx* ctx) {
     const size_t pitems = nch / PLAN_ITEM_CHUNKS + ctx->tiles_x + (size_t)ctx->cap / PLAN_ITEM_AGENTS + 16;
     if (pitems > ctx->plan_items_alloc) {
         if (ctx->d_plan_items) cudaFree(ctx->d_plan_items);
-        FP_CUDA(ctx, cudaMalloc(&ctx->d_plan_items, pitems * sizeof(uint4)));
+        FP_CUDA(ctx, cudaMalloc(&ctx->d_plan_items, pitems * 4 * sizeof(uint4)));  // 64 B per item
         ctx->plan_items_alloc = pitems;
         ctx->graph_valid = false;
     }

@@ -286,7 +286,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
         if (S.ev) cudaEventDestroy(S.ev);
     }
     void* ptrs[] = {c->d_wall, c->d_exit, c->d_occ, c->d_field, c->d_counters, c->d_temp, c->d_temp_b,
-                    c->d_plane, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal, c->d_tile_exit, c->d_seed_items, c->d_plan_items, c->d_scan_sums, c->d_scan_sums2,
+                    c->d_plane, c->d_plane_t, c->d_tile_cnt, c->d_tile_off, c->d_tile_list, c->d_sub_cnt, c->d_sub_off, c->d_tile_deal, c->d_tile_exit, c->d_seed_items, c->d_plan_items, c->d_scan_sums, c->d_scan_sums2,
                     c->d_sc,
                     c->d_p1, c->d_p2,
                     c->d_bkt, c->d_bdone, c->d_pw};

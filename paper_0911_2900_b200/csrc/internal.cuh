@@ -196,6 +196,7 @@ struct fp_ctx {
 
     // weight plane (plane.cu), valid for (plane_ks, plane_potential, plane_gradient)
     uint32_t* d_plane = nullptr;
+    uint32_t* d_plane_t = nullptr;   // the same words chunk-tiled: [stripe][chunk][8 rows][tile_w + 16]
     int PW = 0;
     bool plane_valid = false;
     double plane_ks = 0.0;

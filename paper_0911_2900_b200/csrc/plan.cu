@@ -282,13 +282,15 @@ struct StreamArgs {
     const uint4* brec;          // (id, wrapped x, y, v_max) per bucket position (bucket.cu)
     const uint32_t* ccnt;       // agents per chunk
     const uint32_t* coff;       // first bucket position per chunk
-    const uint4* items;         // plan items (bucket.cu): (first chunk, chunks - 1, first agent, end agent)
+    const uint4* items;         // plan items (bucket.cu), 4 x uint4 each: (first chunk, chunks - 1,
+                                //   first agent, end agent), then u16 references per ring slot
     uint32_t nchunks;
     const uint8_t* tile_exit;   // an Exit within the tile's window
     int tile_w, tile_h, tiles_x, cps, boxw;
     uint2* fallback;            // (id, bucket position) handed to plan_exact_list_kernel
     uint4* rec0;                // walk records in bucket order (motion_rec.cuh)
     int mixed;                  // roster has more than one v_max: the masked radius-5 variant
+    const uint32_t* plane_t;    // chunk-tiled weight plane (plane.cu plane_tile_kernel)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -320,6 +322,15 @@ __device__ __forceinline__ bool mbar_wait(uint64_t* bar, unsigned parity) {
         if (ok) return true;
     }
     return false;
+}
+
+
+// One contiguous run of global memory into shared memory (cp.async.bulk, mbarrier completion).
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int cx, int cy) {
@@ -547,6 +558,9 @@ __device__ __forceinline__ int plan_ring_v(int v, const StreamArgs& A, const Rin
                                            int X0, int px, int py, double u, const double* drive_tab, int* ox,
                                            int* oy) {
 #define FP_PLAN_ARGS A, R, pathm, osh0, X0, px, py, u, drive_tab, ox, oy
+#ifdef FP_PLAN_ONLY_V4  // SASS inspection builds: one instantiation
+    return plan_ring_t<4, DRIVE>(FP_PLAN_ARGS);
+#endif
     if (A.mixed)  // one instruction stream for a mixed-v roster (see plan_ring_t)
         return plan_ring_t<5, DRIVE, true>(FP_PLAN_ARGS, v);
     switch (v) {
@@ -637,31 +651,44 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
         bool ok = true;
         unsigned pub = 0, nq = 0;
         int half = 0;  // ring part of the next item (items take the parts in turn)
+        // Items flow through a two-stage pipeline so no global-memory latency sits between two
+        // items: while item j stages, item j+1's record (descriptor + per-slot reference counts,
+        // bucket.cu) is in flight and item j+2's index is being claimed.
+        const uint16_t* refs_base = reinterpret_cast<const uint16_t*>(A.items);
+        auto load_rec = [&](uint32_t i, uint4& d, uint32_t& r) {
+            if (i < n_items) {
+                d = __ldg(&A.items[4 * (size_t)i]);
+                r = (lane < 24) ? __ldg(&refs_base[32 * (size_t)i + 8 + lane]) : 0u;
+            }
+        };
+        uint32_t claim_b = 0;  // lane 0: index of the item after next (atomic in flight)
+        uint32_t i_cur = 0;
+        if (lane == 0) {
+            i_cur = (uint32_t)atomicAdd(&a.sc->tile_next, 1ull);
+            claim_b = (uint32_t)atomicAdd(&a.sc->tile_next, 1ull);
+        }
+        i_cur = __shfl_sync(0xffffffffu, i_cur, 0);
+        uint4 d_cur = make_uint4(0, 0, 0, 0);
+        uint32_t r_cur = 0;
+        load_rec(i_cur, d_cur, r_cur);
         while (ok) {
-            uint32_t i = 0;
-            if (lane == 0) i = (uint32_t)atomicAdd(&a.sc->tile_next, 1ull);
-            i = __shfl_sync(0xffffffffu, i, 0);
+            const uint32_t i = i_cur;
             if (i >= n_items) break;
-            const uint4 it = __ldg(&A.items[i]);
+            const uint32_t i_nx = __shfl_sync(0xffffffffu, claim_b, 0);
+            if (lane == 0) claim_b = (uint32_t)atomicAdd(&a.sc->tile_next, 1ull);
+            uint4 d_nx = make_uint4(0, 0, 0, 0);
+            uint32_t r_nx = 0;
+            load_rec(i_nx, d_nx, r_nx);
+            const uint4 it = d_cur;
+            const uint32_t refs = r_cur;  // agents of the item whose ball reaches slot kk
+            i_cur = i_nx;
+            d_cur = d_nx;
+            r_cur = r_nx;
             const uint32_t gf = it.x;
             const int nk = (int)it.y + 1;
             const uint32_t a0 = it.z, a1 = it.w;
             const int s = (int)(gf / (uint32_t)A.cps), kf = (int)(gf % (uint32_t)A.cps);
-            // agents of the item in chunk kf + lane
-            uint32_t c = 0;
-            if (lane < nk) {
-                const uint32_t off = __ldg(&A.coff[gf + lane]), cnt = __ldg(&A.ccnt[gf + lane]);
-                const uint32_t lo = max(off, a0), hi = min(off + cnt, a1);
-                c = hi > lo ? hi - lo : 0u;
-            }
             const int kk = kf - 1 + lane;  // the slot this lane looks after
-            uint32_t refs = 0;             // agents of the item whose ball reaches slot kk
-#pragma unroll
-            for (int d = -1; d <= 1; ++d) {
-                const int j = lane - 1 + d;  // item chunk index of chunk kk + d
-                const uint32_t cj = __shfl_sync(0xffffffffu, c, j & 31);
-                if (j >= 0 && j < nk) refs += cj;
-            }
             const int p = half * RING_HALF + lane;
             if (lane < nk + 2 && refs != 0 && kk >= 0 && kk < rows_chunks) {
                 unsigned nap = 32;
@@ -680,7 +707,9 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                     const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(&bars[p], tx_bytes);
-                    tma_load_2d(ringw + p * CHUNK_ROWS * A.boxw, &tmap_w, &bars[p], x0 - 8 + FP_XPAD_W, kk * CHUNK_ROWS);
+                    bulk_load(ringw + p * CHUNK_ROWS * A.boxw,
+                              A.plane_t + ((size_t)s * rows_chunks + kk) * (CHUNK_ROWS * A.boxw),
+                              (unsigned)(CHUNK_ROWS * A.boxw) * 4u, &bars[p]);
                     tma_load_2d(ringo + p * CHUNK_ROWS * OCCW, &tmap_o, &bars[p], gws, kk * CHUNK_ROWS);
                     tma_load_2d(ringl + p * CHUNK_ROWS * OCCW, &tmap_l, &bars[p], gws, kk * CHUNK_ROWS);
                     atomicAdd(&s_ref[p], (int)refs);
@@ -708,112 +737,106 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
         return;
     }
     // ---------------- consumers
-    // warps sharing the producer's scheduler (warp id mod 4) may stay idle so the producer is
-    // never starved of issue slots (FP_PLAN_SKIP_SCHED0)
-#ifndef FP_PLAN_SKIP_SCHED0
-#define FP_PLAN_SKIP_SCHED0 0
-#endif
-    if (FP_PLAN_SKIP_SCHED0 && (warp & 3) == 0) return;
+    // A warp claims up to 32 consecutive agents of ONE published item (compare-and-swap on the
+    // claim cursor, bounded by the item's end and the published count), so every claim is planned
+    // in one pass with the item's staging parameters uniform across the warp.
     const uint64_t step = (uint64_t)a.sc->step;
-    unsigned qhint = 0;  // queue entry of the last agent this warp found
+    unsigned qhint = 0;  // queue entry of this warp's last claim (claims only move forward)
     for (;;) {
-        unsigned g = 0;
-        if (lane == 0) g = atomicAdd(&s_next, 32u);
+        unsigned g = 0, k = 0, q = 0;
+        int bad = 0;
+        if (lane == 0) {
+            unsigned nap = 32;
+            for (long long spin = 0;; ++spin) {
+                // order: done, then pub, then nq (the producer writes them in reverse)
+                const int done = s_done;
+                __threadfence_block();
+                const unsigned pub = s_pub;
+                __threadfence_block();
+                const unsigned nq = s_nq;
+                g = *((volatile unsigned*)&s_next);
+                if (g < pub) {
+                    q = max(qhint, nq > PLAN_QUEUE ? nq - PLAN_QUEUE : 0u);
+                    while (q + 1 < nq && s_qv[(q + 1) % PLAN_QUEUE] <= g) ++q;
+                    const unsigned end = (q + 1 < nq) ? s_qv[(q + 1) % PLAN_QUEUE] : pub;
+                    k = min(32u, end - g);
+                    if (atomicCAS(&s_next, g, g + k) == g) break;
+                    k = 0;
+                    continue;  // another warp claimed first: retry at once
+                }
+                if (done) break;  // k = 0: everything published was claimed
+                __nanosleep(nap);  // backoff: idle warps must not steal issue slots
+                nap = min(nap * 2u, (unsigned)FP_PLAN_NAP_MAX);
+                if (spin > (1ll << 24)) {
+                    bad = 1;
+                    break;
+                }
+            }
+        }
+        if (__shfl_sync(0xffffffffu, bad, 0)) {
+            if (lane == 0) atomicOr(&a.sc->err, 8ull);
+            return;
+        }
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k == 0) return;
         g = __shfl_sync(0xffffffffu, g, 0);
-        const unsigned ai = g + lane;
-        bool pending = true;
-        for (;;) {
-            // lane 0 waits until the first still-pending agent of the claim is published or the
-            // producer is done; then every lane whose agent is published plans it (the others
-            // idle, they do not spin)
-            const unsigned todo = __ballot_sync(0xffffffffu, pending);
-            if (!todo) break;
-            const unsigned need = g + (unsigned)(__ffs(todo) - 1);
-            unsigned pub = 0, nq = 0;
-            int done = 0, bad = 0;
-            if (lane == 0) {
-                unsigned nap = 32;
-                for (long long spin = 0;; ++spin) {
-                    // order: done, then pub, then nq (the producer writes them in reverse)
-                    done = s_done;
-                    __threadfence_block();
-                    pub = s_pub;
-                    __threadfence_block();
-                    nq = s_nq;
-                    if (pub > need || done) break;
-                    __nanosleep(nap);  // backoff: idle lanes must not steal issue slots
-                    nap = min(nap * 2u, (unsigned)FP_PLAN_NAP_MAX);
-                    if (spin > (1ll << 24)) {
-                        bad = 1;
-                        break;
-                    }
-                }
+        q = __shfl_sync(0xffffffffu, q, 0);
+        qhint = q;
+        __threadfence_block();
+        const unsigned qi = q % PLAN_QUEUE;
+        const int qs = s_qs[qi], ihalf = qs & 3, kf = qs >> 2;
+        const int sbase = ihalf * RING_HALF - (kf - 1);  // ring slot of chunk 0 of the item (may be < 0)
+        const int s = s_qx[qi];                          // the item's stripe (= px / tile_w)
+        const Ring R{ringw + ihalf * RING_HALF * CHUNK_ROWS * A.boxw, ringo + ihalf * RING_HALF * CHUNK_ROWS * OCCW,
+                     ringl + ihalf * RING_HALF * CHUNK_ROWS * OCCW, A.boxw, CHUNK_ROWS * (kf - 1)};
+        const int x0 = s * A.tile_w;
+        const int X0 = x0 - 8;  // staged column 0 (TMA inner coordinates stay 16-byte aligned)
+        const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
+        const int osh0 = x0 - 8 + FP_XPAD_BITS - gws * 32;  // staged bit of column X0
+        int k_lo = 0, k_hi = -1;
+        if ((unsigned)lane < k) {
+            const unsigned pos = s_qa[qi] + (g + lane - s_qv[qi]);
+            const uint4 br = __ldcg(&A.brec[pos]);  // (id, wrapped x, y, v_max), bucket.cu
+            const uint32_t id = br.x;
+            const int px = (int)br.y, py = (int)br.z, v = (int)br.w;
+            const int kc = py >> 3;
+            k_lo = max(kc - 1, 0);
+            k_hi = min(kc + 1, rows_chunks - 1);
+            bool ready = true;
+            for (int kk = k_lo; kk <= k_hi; ++kk) {
+                const int p = sbase + kk;
+                ready &= mbar_wait(&bars[p], (unsigned)(s_gen[p] - 1) & 1u);
             }
-            if (__shfl_sync(0xffffffffu, bad, 0)) {
-                if (lane == 0) atomicOr(&a.sc->err, 8ull);
-                return;
+            if (!ready) atomicOr(&a.sc->err, 2ull);
+            const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
+            int cx = 0, cy = 0;
+#ifdef FP_PLAN_NOCOMPUTE  // A/B experiments only: the staging pipeline without the planning work
+            const int st = (u < 0.0) ? 1 : 3;
+#else
+            const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
+                               ? plan_ring_v<true>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy)
+                               : plan_ring_v<false>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy);
+#endif
+            if (st == 1) {
+                a.dx[id] = cx;
+                a.dy[id] = cy;
+                const int tile = (py / A.tile_h) * A.tiles_x + s;
+                A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], R, osh0 + px - X0, id, px, py, cx, cy, v, s_bp);
+            } else if (st == 2) {  // decided by the exact path after the sweep (plan_exact_list_kernel)
+                A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, pos);
             }
-            pub = __shfl_sync(0xffffffffu, pub, 0);
-            nq = __shfl_sync(0xffffffffu, nq, 0);
-            done = __shfl_sync(0xffffffffu, done, 0);
-            __threadfence_block();
-            if (done && pub <= need) return;  // everything published was claimed: finished
-            int k_lo = 0, k_hi = -1, sbase = 0;  // sbase: ring slot of chunk 0 of the item (may be < 0)
-            if (pending && ai < pub) {
-                pending = false;
-                // queue entry holding virtual agent ai: entries are published in order and the
-                // ring bounds how many are in flight, so the last PLAN_QUEUE are enough
-                unsigned q = max(qhint, nq > PLAN_QUEUE ? nq - PLAN_QUEUE : 0u);
-                while (q + 1 < nq && s_qv[(q + 1) % PLAN_QUEUE] <= ai) ++q;
-                qhint = q;
-                const unsigned pos = s_qa[q % PLAN_QUEUE] + (ai - s_qv[q % PLAN_QUEUE]);
-                const int qs = s_qs[q % PLAN_QUEUE], ihalf = qs & 3, kf = qs >> 2;
-                sbase = ihalf * RING_HALF - (kf - 1);
-                const uint4 br = __ldcg(&A.brec[pos]);  // (id, wrapped x, y, v_max), bucket.cu
-                const uint32_t id = br.x;
-                const int px = (int)br.y, py = (int)br.z, v = (int)br.w;
-                const int s = s_qx[q % PLAN_QUEUE], k = py >> 3;  // the item's stripe (= px / tile_w)
-                k_lo = max(k - 1, 0);
-                k_hi = min(k + 1, rows_chunks - 1);
-                bool ready = true;
-                for (int kk = k_lo; kk <= k_hi; ++kk) {
-                    const int p = sbase + kk;
-                    ready &= mbar_wait(&bars[p], (unsigned)(s_gen[p] - 1) & 1u);
-                }
-                if (!ready) atomicOr(&a.sc->err, 2ull);
-                const Ring R{ringw + ihalf * RING_HALF * CHUNK_ROWS * A.boxw, ringo + ihalf * RING_HALF * CHUNK_ROWS * OCCW,
-                             ringl + ihalf * RING_HALF * CHUNK_ROWS * OCCW, A.boxw, CHUNK_ROWS * (kf - 1)};
-                const int x0 = s * A.tile_w;
-                const int X0 = x0 - 8;  // staged column 0 (TMA inner coordinates stay 16-byte aligned)
-                const int gws = ((x0 - 8 + FP_XPAD_BITS) >> 5) & ~3;
-                const int osh0 = x0 - 8 + FP_XPAD_BITS - gws * 32;  // staged bit of column X0
-                const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
-                int cx = 0, cy = 0;
-                const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
-                                   ? plan_ring_v<true>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy)
-                                   : plan_ring_v<false>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy);
-                if (st == 1) {
-                    a.dx[id] = cx;
-                    a.dy[id] = cy;
-                    const int tile = (py / A.tile_h) * A.tiles_x + s;
-                    A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], R, osh0 + px - X0, id, px, py, cx, cy, v, s_bp);
-                } else {  // decided by the exact path after the sweep (plan_exact_list_kernel)
-                    A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, pos);
-                }
-            }
-            // release: the lanes' reads of the slots happen before their references drop; lanes
-            // on the same slot combine their decrements (one shared atomic per slot and warp)
-            __syncwarp();
-            __threadfence_block();
+        }
+        // release: the lanes' reads of the slots happen before their references drop; lanes
+        // on the same slot combine their decrements (one shared atomic per slot and warp)
+        __syncwarp();
+        __threadfence_block();
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const int kk = k_lo + d;
-                const bool has = kk <= k_hi;
-                const int key = has ? (sbase + kk) : -1;
-                const unsigned peers = __match_any_sync(0xffffffffu, key);
-                if (has && (__ffs(peers) - 1) == lane) atomicSub(&s_ref[key], __popc(peers));
-            }
-            if (done && !__any_sync(0xffffffffu, pending)) break;
+        for (int d = 0; d < 3; ++d) {
+            const int kk = k_lo + d;
+            const bool has = kk <= k_hi;
+            const int key = has ? (sbase + kk) : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, key);
+            if (has && (__ffs(peers) - 1) == lane) atomicSub(&s_ref[key], __popc(peers));
         }
     }
 }
@@ -1008,6 +1031,7 @@ static StreamArgs make_stream_args(fp_ctx* ctx, double k_s, uint64_t seed) {
     A.fallback = ctx->d_fallback;
     A.rec0 = ctx->d_rec0;
     A.mixed = ctx->mixed_v ? 1 : 0;
+    A.plane_t = ctx->d_plane_t;
     return A;
 }
 

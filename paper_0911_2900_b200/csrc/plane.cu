@@ -67,6 +67,25 @@ __global__ void plane_build_kernel(Geo g, int PW, const double* field, int poten
     }
 }
 
+// Chunk-tiled copy of the plane for the plan kernel's producer: block (stripe s, chunk k) holds
+// rows 8k..8k+7, columns s*tile_w - 8 .. s*tile_w + tile_w + 8 (the stripe and its halo) as one
+// contiguous 8 * boxw-word run, and the chunks of a stripe follow each other -- a plan item's
+// rows are one contiguous range of HBM (long DRAM bursts instead of 1 KB row pieces 80 KB apart).
+// Words outside the plane (rows >= H, columns past the pitch) read as Wall.
+__global__ void plane_tile_kernel(const uint32_t* plane, int PW, int H, int tile_w, int boxw, int rows_chunks,
+                                  size_t total, uint32_t* out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % boxw);
+        const size_t rb = i / boxw;  // (stripe * rows_chunks + chunk) * 8 + row
+        const int r = (int)(rb % 8);
+        const size_t b = rb / 8;
+        const int k = (int)(b % rows_chunks), st = (int)(b / rows_chunks);
+        const int y = 8 * k + r;
+        const int xp = st * tile_w - 8 + c + FP_XPAD_W;  // plane column
+        out[i] = (y < H && xp >= 0 && xp < PW) ? plane[(size_t)y * PW + xp] : FP_W_WALL;
+    }
+}
+
 // Row pass of the radius-5 min/max of C (cval: INT_MIN wall / outside, INT_MIN + 1 unreachable
 // free cell; a window holding an unreachable cell gets rmin = INT_MIN).
 __global__ void plane_rowminmax_kernel(int PW, int H, const int* cval, int* rmin, int* rmax) {
@@ -279,6 +298,13 @@ int fp_plane_ensure(fp_ctx* ctx, double k_s) {
         FP_LAUNCHED(ctx);
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->pad[0], 0, 8, s));
         plane_unsafe_kernel<<<G, 256, 0, s>>>(ctx->PW, ctx->H, cval, rmin, rmax, ctx->d_plane, &ctx->d_sc->pad[0]);
+        FP_LAUNCHED(ctx);
+    }
+    {
+        const int boxw = ctx->tile_w + 16, rc = (ctx->H + 7) / 8;
+        const size_t tot = (size_t)ctx->tiles_x * rc * 8 * boxw;
+        if (!ctx->d_plane_t) FP_CUDA(ctx, cudaMalloc(&ctx->d_plane_t, tot * 4));
+        plane_tile_kernel<<<G, 256, 0, s>>>(ctx->d_plane, ctx->PW, ctx->H, ctx->tile_w, boxw, rc, tot, ctx->d_plane_t);
         FP_LAUNCHED(ctx);
     }
     FP_CUDA(ctx, cudaFreeAsync(cval, s));
