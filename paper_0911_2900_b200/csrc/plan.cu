@@ -592,6 +592,10 @@ __device__ __forceinline__ unsigned long long globaltimer_p() {
 //     published and the (at most three) slots its ball spans have landed, one agent per lane,
 //     then release those slots.
 // The ring holds two items, so the TMA of the next item overlaps the planning of the current one.
+#ifndef PLAN_MIN_CLAIM
+#define PLAN_MIN_CLAIM 32 // smallest claim of a consumer warp (agents)
+#endif
+#define PLAN_CONSUMERS (PLAN_THREADS / 32 - 1)
 #define PLAN_QUEUE 64  // published items a CTA remembers (the ring bounds the ones in flight)
 #ifndef RING_PARTS
 #define RING_PARTS 2  // items in flight per CTA (the ring's parts; 2 = double buffering)
@@ -614,6 +618,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
     __shared__ int s_qs[PLAN_QUEUE];           //   its ring part | first chunk << 2
     __shared__ int s_qx[PLAN_QUEUE];           //   its stripe
     __shared__ unsigned s_next;                // consumers' claim cursor (virtual agents)
+    __shared__ volatile unsigned s_qcur;       // queue entry of a recent claim (search hint)
     __shared__ volatile unsigned s_pub;        // virtual agents published
     __shared__ volatile unsigned s_nq;         // queue entries published
     __shared__ volatile int s_done;            // producer finished
@@ -637,6 +642,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
         for (int s = 0; s < RING_SLOTS; ++s) mbar_init(&bars[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         s_next = 0;
+        s_qcur = 0;
         s_pub = 0;
         s_done = 0;
         s_nq = 0;
@@ -756,11 +762,18 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                 const unsigned nq = s_nq;
                 g = *((volatile unsigned*)&s_next);
                 if (g < pub) {
-                    q = max(qhint, nq > PLAN_QUEUE ? nq - PLAN_QUEUE : 0u);
+                    // s_qcur: the entry of some earlier claim (a lower bound for g's entry)
+                    q = max(max(qhint, *((volatile unsigned*)&s_qcur)), nq > PLAN_QUEUE ? nq - PLAN_QUEUE : 0u);
                     while (q + 1 < nq && s_qv[(q + 1) % PLAN_QUEUE] <= g) ++q;
+                    const unsigned beg = s_qv[q % PLAN_QUEUE];
                     const unsigned end = (q + 1 < nq) ? s_qv[(q + 1) % PLAN_QUEUE] : pub;
-                    k = min(32u, end - g);
-                    if (atomicCAS(&s_next, g, g + k) == g) break;
+                    // sparse items are spread over more warps (shorter claims, more in flight)
+                    const unsigned share = (end - beg + PLAN_CONSUMERS - 1) / PLAN_CONSUMERS;
+                    k = min(min(32u, max((unsigned)PLAN_MIN_CLAIM, share)), end - g);
+                    if (atomicCAS(&s_next, g, g + k) == g) {
+                        s_qcur = q;
+                        break;
+                    }
                     k = 0;
                     continue;  // another warp claimed first: retry at once
                 }
