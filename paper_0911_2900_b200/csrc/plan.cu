@@ -854,12 +854,13 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
     }
 }
 
-// The exact path for the agents the tiled kernel could not decide: one warp per agent.  Lanes
-// own candidate slots of the ball in list order (row-major, wrapped-x sorted at the seam),
-// test them against the global bitplanes (walls, occupancy, Bresenham line of sight) and compute
-// the exact weights (restated glibc exp); lane 0 then folds the weights serially in list order
-// (sample_index, planning.hpp:63-73).  Narrow periodic grids (2v+1 > W-?) use choose_exact.
-#define EXACT_WARPS 4
+// The exact path for the agents the tiled kernel could not decide: one CTA per agent, one thread
+// per candidate slot of the ball in list order (row-major, wrapped-x sorted at the seam): each
+// tests its cell against the global bitplanes (walls, occupancy, Bresenham line of sight) and
+// computes the exact weight (restated glibc exp) in parallel; thread 0 then folds the weights
+// serially in list order (sample_index, planning.hpp:63-73).  Narrow periodic grids
+// (2v+1 >= W) use choose_exact.
+#define EXACT_THREADS 128  // >= 121 candidate slots (v_max <= 5)
 struct EmitArgs {
     uint4* rec0;
     uint32_t* p1;
@@ -873,26 +874,27 @@ __device__ __forceinline__ void emit_record(const PlanCommon& a, const EmitArgs&
     E.rec0[pos] = record_of(a.g, a.occ, id, px, py, cx, cy, v, c_bpath_p);
 }
 
-__global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanCommon a, const uint2* list,
-                                                                           EmitArgs E) {
-    __shared__ double s_w[EXACT_WARPS][121];
-    __shared__ int s_c[EXACT_WARPS][121];
+__global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanCommon a, const uint2* list,
+                                                                        EmitArgs E) {
+    __shared__ double s_w[EXACT_THREADS];
+    __shared__ int s_c[EXACT_THREADS];
     const unsigned n = (unsigned)a.sc->fb_count;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = threadIdx.x;
     const uint64_t step = (uint64_t)a.sc->step;
-    for (unsigned e = blockIdx.x * EXACT_WARPS + warp; e < n; e += gridDim.x * EXACT_WARPS) {
+    for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
         const uint2 ent = list[e];
         const uint32_t id = ent.x;
         const int px = a.g.wrap(a.x[id]), py = a.y[id], v = a.v[id];
         const int D = 2 * v + 1;
         if (a.g.boundary == FP_BOUNDARY_PERIODIC_X && D >= a.g.W) {
-            if (lane == 0) {
+            if (t == 0) {
                 int cx, cy;
                 choose_exact(a, id, step, &cx, &cy);
                 a.dx[id] = cx;
                 a.dy[id] = cy;
                 emit_record(a, E, id, ent.y, px, py, cx, cy, v);
             }
+            __syncthreads();
             continue;
         }
         // list-order column -> dx (wrapped-x sort at the periodic seam, planning.hpp:50-53)
@@ -904,9 +906,9 @@ __global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanC
                 a0 = -px; na = v - a0 + 1; b0 = -v;
             }
         }
-        const ExactWeight wf = make_weight(a, px, py);
-        for (int k = lane; k < D * D; k += 32) {
-            const int r = k / D, c = k % D;
+        if (t < D * D) {
+            const ExactWeight wf = make_weight(a, px, py);
+            const int r = t / D, c = t % D;
             const int y = py - v + r;
             const int dx = c < na ? a0 + c : b0 + (c - na);
             int x = px + dx;
@@ -916,36 +918,36 @@ __global__ void __launch_bounds__(EXACT_WARPS * 32) plan_exact_list_kernel(PlanC
             ok = ok && !a.g.is_wall(x, y);
             ok = ok && !(occ_bit(a.occ, a.g, x, y) && !(x == px && y == py));
             ok = ok && los(a.g, px, py, x, y);
-            s_w[warp][k] = ok ? wf(x, y) : -1.0;
-            s_c[warp][k] = ok ? (y * a.g.W + x) : -1;
+            s_w[t] = ok ? wf(x, y) : -1.0;
+            s_c[t] = ok ? (y * a.g.W + x) : -1;
         }
-        __syncwarp();
-        if (lane == 0) {
+        __syncthreads();
+        if (t == 0) {
             double total = 0.0;
             int last = -1;
             for (int k = 0; k < D * D; ++k)
-                if (s_c[warp][k] >= 0) {
-                    total = FPX_ADD(total, s_w[warp][k]);
+                if (s_c[k] >= 0) {
+                    total = FPX_ADD(total, s_w[k]);
                     last = k;
                 }
             const double threshold = FPX_MUL(fp_unit_interval(fp_rng_u64(a.seed, id, step, 0)), total);
             double cum = 0.0;
             int pick = last;
             for (int k = 0; k < D * D; ++k)
-                if (s_c[warp][k] >= 0) {
-                    cum = FPX_ADD(cum, s_w[warp][k]);
+                if (s_c[k] >= 0) {
+                    cum = FPX_ADD(cum, s_w[k]);
                     if (cum > threshold) {
                         pick = k;
                         break;
                     }
                 }
-            const int cell = s_c[warp][pick];
+            const int cell = s_c[pick];
             const int cx = cell % a.g.W, cy = cell / a.g.W;
             a.dx[id] = cx;
             a.dy[id] = cy;
             emit_record(a, E, id, ent.y, px, py, cx, cy, v);
         }
-        __syncwarp();
+        __syncthreads();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) a.sc->fallbacks += n;
 }
@@ -1098,7 +1100,7 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     ctx->marks_dirty = true;
     const StreamArgs A = make_stream_args(ctx, k_s, seed);
     if (int rc = launch_stream(ctx, A)) return rc;
-    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
+    plan_exact_list_kernel<<<ctx->sm_count * 4, EXACT_THREADS, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -1134,7 +1136,7 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
     ctx->rec_fresh = false;
     ctx->marks_dirty = true;
     // leave the state planned (the fallbacks of the last launch decided exactly)
-    plan_exact_list_kernel<<<ctx->sm_count, EXACT_WARPS * 32, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
+    plan_exact_list_kernel<<<ctx->sm_count * 4, EXACT_THREADS, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
     FP_LAUNCHED(ctx);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
