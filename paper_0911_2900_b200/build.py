@@ -14,7 +14,7 @@ OUT = os.path.join(HERE, "libfastped_b200.so")
 SOURCES = ["capi.cu", "plan.cu", "order.cu", "move.cu", "field.cu", "plane.cu", "bucket.cu", "strip.cu", "scan.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--fmad=false",
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "--fmad=false",
          "-Xcompiler", "-ffp-contract=off"]
 
 

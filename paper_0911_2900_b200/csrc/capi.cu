@@ -603,12 +603,17 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     int rc = FP_OK;
     if (strip) rc = fp_strip_begin_launch(c);
+#ifdef FP_ORDER_SERIAL  // A/B experiments: the movement order after the plan, same stream
+    if (rc == FP_OK) rc = fp_plan_launch(c, k_s, seed);
+    if (rc == FP_OK) rc = fp_order_launch(c, seed, c->stream);
+#else
     cudaEventRecord(c->ev_fork, c->stream);
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
     if (rc == FP_OK) rc = fp_order_launch(c, seed, c->stream2);
     cudaEventRecord(c->ev_join, c->stream2);
     if (rc == FP_OK) rc = fp_plan_launch(c, k_s, seed);
     cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+#endif
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     if (rc != FP_OK) {
         if (g) cudaGraphDestroy(g);

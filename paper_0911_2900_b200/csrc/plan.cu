@@ -40,28 +40,38 @@
 __constant__ signed char c_bpath_p[121][5][2];
 
 // Bresenham path masks over the 11x11 offset frame (bit (dy+5)*11 + dx+5): the cells strictly
-// between (0,0) and (dx,dy) on the segment (world.hpp:143-167).
+// between (0,0) and (dx,dy) on the segment (world.hpp:143-167).  Built at compile time: the plan
+// kernel's unrolled candidate loops fold them into instruction immediates (k_pathmask_dev); the
+// runtime-indexed users read the constant-memory copy (c_pathmask) or a shared-memory one.
+struct PathMasks {
+    uint32_t m[121][4];
+};
+constexpr PathMasks make_pathmasks() {
+    PathMasks P{};
+    for (int dy = -5; dy <= 5; ++dy)
+        for (int dx = -5; dx <= 5; ++dx) {
+            const int adx = dx < 0 ? -dx : dx, sx = 0 < dx ? 1 : -1;
+            const int ady = -(dy < 0 ? -dy : dy), sy = 0 < dy ? 1 : -1;
+            int err = adx + ady, x = 0, y = 0;
+            while (!(x == dx && y == dy)) {
+                const int e2 = 2 * err;
+                if (e2 >= ady) { err += ady; x += sx; }
+                if (e2 <= adx) { err += adx; y += sy; }
+                if (x == dx && y == dy) break;
+                const int b = (y + 5) * 11 + x + 5;
+                P.m[(dy + 5) * 11 + dx + 5][b >> 5] |= 1u << (b & 31);
+            }
+        }
+    return P;
+}
+static constexpr PathMasks k_pathmask_host = make_pathmasks();
+__device__ constexpr PathMasks k_pathmask_dev = make_pathmasks();
 __constant__ uint32_t c_pathmask[121][4];
 static bool g_pathmask_ready[64] = {false};
 
 static void host_pathmasks(uint32_t out[121][4]) {
-    for (int dy = -5; dy <= 5; ++dy)
-        for (int dx = -5; dx <= 5; ++dx) {
-            uint32_t* m = out[(dy + 5) * 11 + dx + 5];
-            m[0] = m[1] = m[2] = m[3] = 0;
-            const int tx = dx, ty = dy;
-            const int adx = abs(tx), sx = 0 < tx ? 1 : -1;
-            const int ady = -abs(ty), sy = 0 < ty ? 1 : -1;
-            int err = adx + ady, x = 0, y = 0;
-            while (!(x == tx && y == ty)) {
-                const int e2 = 2 * err;
-                if (e2 >= ady) { err += ady; x += sx; }
-                if (e2 <= adx) { err += adx; y += sy; }
-                if (x == tx && y == ty) break;
-                const int b = (y + 5) * 11 + x + 5;
-                m[b >> 5] |= 1u << (b & 31);
-            }
-        }
+    for (int o = 0; o < 121; ++o)
+        for (int j = 0; j < 4; ++j) out[o][j] = k_pathmask_host.m[o][j];
 }
 
 static int ensure_pathmasks(fp_ctx* ctx) {
@@ -366,6 +376,13 @@ __device__ __forceinline__ void mask_or_row(Mask121& m, uint32_t rowbits, int B)
     if (B + 11 > 64) m.hi |= (B >= 64) ? ((unsigned long long)rowbits << (B - 64)) : ((unsigned long long)rowbits >> (64 - B));
 }
 
+// Path mask test for an offset o known at compile time (unrolled loops): immediates, no loads.
+__device__ __forceinline__ bool path_blocked_c(const Mask121& m, int o) {
+    const unsigned long long plo = ((unsigned long long)k_pathmask_dev.m[o][1] << 32) | k_pathmask_dev.m[o][0];
+    const unsigned long long phi = ((unsigned long long)k_pathmask_dev.m[o][3] << 32) | k_pathmask_dev.m[o][2];
+    return ((m.lo & plo) | (m.hi & phi)) != 0ull;
+}
+
 // Path mask test against the shared-memory copy of c_pathmask (lanes index it divergently).
 __device__ __forceinline__ bool path_blocked_s(const uint4* pm, const Mask121& m, int o) {
     const uint4 q = pm[o];
@@ -445,7 +462,7 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
         if (anywall) {
 #pragma unroll
             for (int k = 0; k < D; ++k)
-                if (path_blocked_s(pathm, wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
+                if (path_blocked_c(wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
         }
         float w[D];
 #pragma unroll
