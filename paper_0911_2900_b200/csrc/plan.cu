@@ -450,6 +450,7 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
 #pragma unroll
     for (int k = 0; k < D; ++k) dw[k] = DRIVE ? (float)drive_tab[k - V + 5] : 0.0f;
     float rso[D];
+    Mask121 vm{0ull, 0ull};  // the candidates (in frame bits, like wm)
 #pragma unroll
     for (int t = 0; t < D; ++t) {
         const int dy = (t & 1) ? -((t + 1) >> 1) : (t >> 1);  // centre-out: 0, -1, 1, -2, 2, ...
@@ -464,6 +465,7 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
             for (int k = 0; k < D; ++k)
                 if (path_blocked_c(wm, (dy + 5) * 11 + k - V + 5)) valid &= ~(1u << k);
         }
+        mask_or_row(vm, valid, (dy + 5) * 11 + 5 - V);  // kept for the row replay
         float w[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
@@ -494,9 +496,12 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
     if (rstar < 0) return 2;  // u*total rounded up to total
     const int dy = rstar - V;
     const uint32_t* row = R.wrow(py + dy) + lx;
-    uint32_t occ = row_bits(R.orow(py + dy), osh) | row_bits(R.lrow(py + dy), osh);
-    if (dy == 0) occ &= ~(1u << V);
-    const uint32_t valid = ~occ & colmask;
+    uint32_t valid;  // the row's candidates, bit dx + V (pass 1's masks)
+    {
+        const int b = (dy + 5) * 11 + 5 - V;
+        const unsigned long long w64 = b < 64 ? ((vm.lo >> b) | (b ? (vm.hi << (64 - b)) : 0ull)) : (vm.hi >> (b - 64));
+        valid = (uint32_t)w64 & ((1u << D) - 1u);
+    }
     const int Rr = MASKED ? vr : V;  // the agent's radius
     int a0 = -Rr, a1 = Rr, b0 = 0, b1 = -1;
     if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {  // wrapped-x order at the seam (planning.hpp:50-53)
@@ -512,8 +517,7 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
     for (int seg = 0; seg < 2 && !found; ++seg) {
         const int lo = seg ? b0 : a0, hi = seg ? b1 : a1;
         for (int dx = lo; dx <= hi; ++dx) {
-            if (!((valid >> (dx + V)) & 1u)) continue;  // outside the grid, Wall, occupied
-            if (anywall && path_blocked_s(pathm, wm, (dy + 5) * 11 + dx + 5)) continue;
+            if (!((valid >> (dx + V)) & 1u)) continue;  // outside the grid, Wall, occupied, hidden
             const double wt = DRIVE ? drive_tab[dx + 5] : (double)plane_weight(row[dx], ap);
             const double next = prefix + wt;
             if (next > theta) {

@@ -1,3 +1,3 @@
-bash tools/variants.sh j
-timeout 600 python tools/plan_timing.py plaza 396 > gpurun_out/plan_timing_j.txt 2>&1; cat gpurun_out/plan_timing_j.txt
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_fullsize_golden.py -x -q -m gpu > gpurun_out/pytest_j.log 2>&1; tail -2 gpurun_out/pytest_j.log
+bash tools/variants.sh l
+timeout 600 python tools/plan_timing.py plaza 396 > gpurun_out/plan_timing_l.txt 2>&1; cat gpurun_out/plan_timing_l.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_fullsize_golden.py -x -q -m gpu > gpurun_out/pytest_l.log 2>&1; tail -2 gpurun_out/pytest_l.log
