@@ -539,13 +539,14 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
     else if (cx >= a.g.W) cx -= a.g.W;
     *ox = cx;
     *oy = py + dy;
-    return 1;
+    return anywall ? 5 : 1;  // bit 2: the ball holds a Wall (record_of_ring walks the path)
 }
 
 // record_of (motion_rec.cuh) for a fast-path decision inside the staged stripe: the target lies in
 // the ball, the Wall test reads the staged wall bits, and the Exit test (global bitplane) runs
 // only in tiles whose window holds an Exit.
-__device__ __forceinline__ uint4 record_of_ring(const Geo& g, const uint32_t* occ, bool tile_exit, const Ring& R,
+__device__ __forceinline__ uint4 record_of_ring(const Geo& g, const uint32_t* occ, bool tile_exit, bool ball_wall,
+                                                const Ring& R,
                                                 int lbit, uint32_t id, int sx, int sy, int tx, int ty, int v,
                                                 const signed char (*bp)[5][2]) {
     const int ddx = g.segment_dx(sx, tx), ddy = ty - sy;
@@ -553,7 +554,8 @@ __device__ __forceinline__ uint4 record_of_ring(const Geo& g, const uint32_t* oc
     const int len = min(max(abs(ddx), abs(ddy)), v);
     int m = 0, ex_x = 0, ex_y = 0;
     bool ex = false;
-    for (int j = 0; j < len; ++j) {
+    if (!ball_wall && !tile_exit) m = len;  // nothing on the path can stop the walk early
+    else for (int j = 0; j < len; ++j) {
         const int ox = bp[o][j][0], oy = bp[o][j][1];
         const int b = lbit + ox;
         if ((R.lrow(sy + oy)[b >> 5] >> (b & 31)) & 1u) break;  // Wall
@@ -851,11 +853,12 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                                ? plan_ring_v<true>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy)
                                : plan_ring_v<false>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy);
 #endif
-            if (st == 1) {
+            if ((st & 3) == 1) {
                 a.dx[id] = cx;
                 a.dy[id] = cy;
                 const int tile = (py / A.tile_h) * A.tiles_x + s;
-                A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], R, osh0 + px - X0, id, px, py, cx, cy, v, s_bp);
+                A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], st & 4, R, osh0 + px - X0, id, px, py, cx,
+                                             cy, v, s_bp);
             } else if (st == 2) {  // decided by the exact path after the sweep (plan_exact_list_kernel)
                 A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, pos);
             }
