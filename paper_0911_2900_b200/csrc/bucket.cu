@@ -19,7 +19,7 @@
 #include "scan.cuh"
 
 #ifndef PLAN_ITEM_CHUNKS
-#define PLAN_ITEM_CHUNKS 10   // chunks per plan item (plan.cu's ring holds two items of <= 12 slots)
+#define PLAN_ITEM_CHUNKS 6    // chunks per plan item (plan.cu's ring holds three items of <= 8 slots)
 #endif
 #ifndef PLAN_ITEM_AGENTS
 #define PLAN_ITEM_AGENTS 512  // agents per plan item at most

@@ -514,7 +514,20 @@ __device__ __forceinline__ int plan_ring_t(const StreamArgs& A, const Ring& R, c
     double prefix = before, lower = 0.0, upper = 0.0;
     int kx = 0;
     bool found = false;
-    for (int seg = 0; seg < 2 && !found; ++seg) {
+    if (b1 < b0) {  // no seam: list order is dx ascending -- one branch-free pass over the row
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const bool ok = (valid >> k) & 1u;
+            const double wk = DRIVE ? drive_tab[k - V + 5] : (double)plane_weight(row[k - V], ap);
+            const double next = prefix + (ok ? wk : 0.0);
+            const bool hit = ok && !found && next > theta;
+            lower = hit ? prefix : lower;
+            upper = hit ? next : upper;
+            kx = hit ? k - V : kx;
+            found = found || hit;
+            prefix = next;
+        }
+    } else for (int seg = 0; seg < 2 && !found; ++seg) {
         const int lo = seg ? b0 : a0, hi = seg ? b1 : a1;
         for (int dx = lo; dx <= hi; ++dx) {
             if (!((valid >> (dx + V)) & 1u)) continue;  // outside the grid, Wall, occupied, hidden
@@ -614,14 +627,15 @@ __device__ __forceinline__ unsigned long long globaltimer_p() {
 //   consumers (the other warps): claim 32 virtual agents at a time, plan each once it is
 //     published and the (at most three) slots its ball spans have landed, one agent per lane,
 //     then release those slots.
-// The ring holds two items, so the TMA of the next item overlaps the planning of the current one.
+// The ring holds RING_PARTS items, so the TMA of the next items overlaps the planning of the
+// current one; an item is published before its part drains, so its agents are claimed early.
 #ifndef PLAN_MIN_CLAIM
 #define PLAN_MIN_CLAIM 32 // smallest claim of a consumer warp (agents)
 #endif
 #define PLAN_CONSUMERS (PLAN_THREADS / 32 - 1)
 #define PLAN_QUEUE 64  // published items a CTA remembers (the ring bounds the ones in flight)
 #ifndef RING_PARTS
-#define RING_PARTS 2  // items in flight per CTA (the ring's parts; 2 = double buffering)
+#define RING_PARTS 3  // items in flight per CTA (the ring's parts)
 #endif
 #define RING_HALF (RING_SLOTS / RING_PARTS)  // slots per item (>= PLAN_ITEM_CHUNKS + 2, bucket.cu)
 
@@ -640,6 +654,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
     __shared__ unsigned s_qa[PLAN_QUEUE];      //   its first bucket position
     __shared__ int s_qs[PLAN_QUEUE];           //   its ring part | first chunk << 2
     __shared__ int s_qx[PLAN_QUEUE];           //   its stripe
+    __shared__ unsigned s_qp[PLAN_QUEUE];      //   barrier parity per slot of its part (bit i: slot i)
     __shared__ unsigned s_next;                // consumers' claim cursor (virtual agents)
     __shared__ volatile unsigned s_qcur;       // queue entry of a recent claim (search hint)
     __shared__ volatile unsigned s_pub;        // virtual agents published
@@ -719,7 +734,25 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
             const int s = (int)(gf / (uint32_t)A.cps), kf = (int)(gf % (uint32_t)A.cps);
             const int kk = kf - 1 + lane;  // the slot this lane looks after
             const int p = half * RING_HALF + lane;
-            if (lane < nk + 2 && refs != 0 && kk >= 0 && kk < rows_chunks) {
+            const bool mine = lane < nk + 2 && refs != 0 && kk >= 0 && kk < rows_chunks;
+            // Publish first: consumers claim the item's agents (and load their records) while its
+            // part drains and its rows stream in; they wait for the rows on the slot barriers.
+            // Slot p has had s_gen[p] loads, so this one completes phase s_gen[p]: parity bit.
+            const unsigned pbits = __ballot_sync(0xffffffffu, mine && (s_gen[p] & 1));
+            if (lane == 0) {
+                s_qv[nq % PLAN_QUEUE] = pub;
+                s_qa[nq % PLAN_QUEUE] = a0;
+                s_qs[nq % PLAN_QUEUE] = half | (kf << 2);
+                s_qx[nq % PLAN_QUEUE] = s;
+                s_qp[nq % PLAN_QUEUE] = pbits;
+                ++nq;
+                pub += a1 - a0;
+                __threadfence_block();
+                s_nq = nq;
+                __threadfence_block();
+                s_pub = pub;
+            }
+            if (mine) {
                 unsigned nap = 32;
                 for (long long spin = 0; *((volatile int*)&s_ref[p]) != 0; ++spin) {
                     __nanosleep(nap);
@@ -745,18 +778,6 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                 }
             }
             ok = __all_sync(0xffffffffu, ok);
-            if (lane == 0 && ok) {
-                s_qv[nq % PLAN_QUEUE] = pub;
-                s_qa[nq % PLAN_QUEUE] = a0;
-                s_qs[nq % PLAN_QUEUE] = half | (kf << 2);
-                s_qx[nq % PLAN_QUEUE] = s;
-                ++nq;
-                pub += a1 - a0;
-                __threadfence_block();
-                s_nq = nq;
-                __threadfence_block();
-                s_pub = pub;
-            }
             half = half + 1 == RING_PARTS ? 0 : half + 1;
         }
         if (lane == 0) {
@@ -821,6 +842,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
         __threadfence_block();
         const unsigned qi = q % PLAN_QUEUE;
         const int qs = s_qs[qi], ihalf = qs & 3, kf = qs >> 2;
+        const unsigned qpar = s_qp[qi];
         const int sbase = ihalf * RING_HALF - (kf - 1);  // ring slot of chunk 0 of the item (may be < 0)
         const int s = s_qx[qi];                          // the item's stripe (= px / tile_w)
         const Ring R{ringw + ihalf * RING_HALF * CHUNK_ROWS * A.boxw, ringo + ihalf * RING_HALF * CHUNK_ROWS * OCCW,
@@ -839,10 +861,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
             k_lo = max(kc - 1, 0);
             k_hi = min(kc + 1, rows_chunks - 1);
             bool ready = true;
-            for (int kk = k_lo; kk <= k_hi; ++kk) {
-                const int p = sbase + kk;
-                ready &= mbar_wait(&bars[p], (unsigned)(s_gen[p] - 1) & 1u);
-            }
+            for (int kk = k_lo; kk <= k_hi; ++kk) ready &= mbar_wait(&bars[sbase + kk], (qpar >> (kk - (kf - 1))) & 1u);
             if (!ready) atomicOr(&a.sc->err, 2ull);
             const double u = fp_unit_interval(fp_rng_u64(a.seed, id, step, 0));
             int cx = 0, cy = 0;
