@@ -411,8 +411,10 @@ extern "C" int fp_set_agents(fp_ctx* c, uint32_t n, const int32_t* x, const int3
         if (v_max[i] < 1 || v_max[i] > 5) return fail(c, FP_EINVAL, "make_state: v_max must be in [1,5]");
         mixed |= v_max[i] != v_max[0];
     }
-    if (mixed != c->mixed_v) c->graph_valid = false;  // the plan kernel variant changes
+    const int vu = (n && !mixed) ? v_max[0] : 5;
+    if (mixed != c->mixed_v || vu != c->v_uniform) c->graph_valid = false;  // the plan kernel variant changes
     c->mixed_v = mixed;
+    c->v_uniform = vu;
     cudaSetDevice(c->device);
     if (int rc = ensure_agents(c, n)) return rc;
     c->n = n;

@@ -30,6 +30,8 @@
 // tiled path does not cover, and test-mode dumps.  There is no CPU fallback.
 #include <math.h>
 
+#include <vector>
+
 #include "fp_exp.h"
 #include "internal.cuh"
 #include "motion_rec.cuh"
@@ -639,6 +641,10 @@ __device__ __forceinline__ unsigned long long globaltimer_p() {
 #endif
 #define RING_HALF (RING_SLOTS / RING_PARTS)  // slots per item (>= PLAN_ITEM_CHUNKS + 2, bucket.cu)
 
+// KV = 0: any roster and potential (runtime dispatch over v_max and the potential); KV = 1..5:
+// one code path for a uniform-v_max roster (KMIXED: the masked radius-5 path of a mixed roster)
+// and one potential -- a smaller kernel body for the instruction cache.
+template <int KV, bool KDRIVE, bool KMIXED>
 __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __grid_constant__ CUtensorMap tmap_w,
                                                                       const __grid_constant__ CUtensorMap tmap_o,
                                                                       const __grid_constant__ CUtensorMap tmap_l,
@@ -868,9 +874,13 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
 #ifdef FP_PLAN_NOCOMPUTE  // A/B experiments only: the staging pipeline without the planning work
             const int st = (u < 0.0) ? 1 : 3;
 #else
-            const int st = (a.potential == FP_POTENTIAL_DRIVE_X)
-                               ? plan_ring_v<true>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy)
-                               : plan_ring_v<false>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy);
+            int st;
+            if constexpr (KV > 0)
+                st = plan_ring_t<KV, KDRIVE, KMIXED>(A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy, v);
+            else
+                st = (a.potential == FP_POTENTIAL_DRIVE_X)
+                         ? plan_ring_v<true>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy)
+                         : plan_ring_v<false>(v, A, R, s_pathm, osh0, X0, px, py, u, s_drive, &cx, &cy);
 #endif
             if ((st & 3) == 1) {
                 a.dx[id] = cx;
@@ -1095,6 +1105,36 @@ static StreamArgs make_stream_args(fp_ctx* ctx, double k_s, uint64_t seed) {
 
 static EmitArgs emit_args(fp_ctx* ctx) { return EmitArgs{ctx->d_rec0, ctx->d_p1, ctx->d_p2, 1}; }
 
+#define FP_STREAM_VARIANTS(X)                                                                                \
+    X(0, false, false) X(1, false, false) X(2, false, false) X(3, false, false) X(4, false, false)        \
+    X(5, false, false) X(1, true, false) X(2, true, false) X(3, true, false) X(4, true, false)              \
+    X(5, true, false) X(5, false, true) X(5, true, true)
+
+static std::vector<const void*> stream_kernels() {
+    std::vector<const void*> v;
+#define FP_SK(V, D, M) v.push_back((const void*)plan_stream_kernel<V, D, M>);
+    FP_STREAM_VARIANTS(FP_SK)
+#undef FP_SK
+    return v;
+}
+
+// The plan kernel variant for this context's roster and potential (plan_stream_kernel).
+static void launch_stream_kernel(fp_ctx* ctx, const StreamArgs& A) {
+    const bool drive = ctx->potential == FP_POTENTIAL_DRIVE_X;
+    const int v = ctx->mixed_v ? 5 : ctx->v_uniform;
+    const bool mixed = ctx->mixed_v;
+#define FP_SK(V, D, M)                                                                                         \
+    if (V > 0 && v == V && drive == D && mixed == M) {                                                         \
+        plan_stream_kernel<V, D, M><<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(           \
+            ctx->tmap_plane, ctx->tmap_occ, ctx->tmap_wall, A);                                                \
+        return;                                                                                                \
+    }
+    FP_STREAM_VARIANTS(FP_SK)
+#undef FP_SK
+    plan_stream_kernel<0, false, false><<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(
+        ctx->tmap_plane, ctx->tmap_occ, ctx->tmap_wall, A);
+}
+
 // Everything the planning phase allocates or builds, done outside any graph capture.
 int fp_plan_prepare(fp_ctx* ctx, double k_s) {
     if (int rc = ensure_pathmasks(ctx)) return rc;
@@ -1106,7 +1146,8 @@ int fp_plan_prepare(fp_ctx* ctx, double k_s) {
     static size_t configured_by_device[64] = {0};  // the attribute is per device
     size_t& configured = configured_by_device[ctx->device & 63];
     if (smem > configured) {
-        FP_CUDA(ctx, cudaFuncSetAttribute(plan_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        for (const void* k : stream_kernels())
+            FP_CUDA(ctx, cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         configured = smem;
     }
     return FP_OK;
@@ -1118,8 +1159,7 @@ static int launch_stream(fp_ctx* ctx, const StreamArgs& A) {
 #ifdef FP_PLAN_PROF
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_sc->plan_prof, 0, sizeof(ctx->d_sc->plan_prof), ctx->stream));
 #endif
-    plan_stream_kernel<<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(ctx->tmap_plane, ctx->tmap_occ,
-                                                                                      ctx->tmap_wall, A);
+    launch_stream_kernel(ctx, A);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -1166,8 +1206,7 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
         cudaEventRecord(e0, ctx->stream);
-        plan_stream_kernel<<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(
-            ctx->tmap_plane, ctx->tmap_occ, ctx->tmap_wall, A);
+        launch_stream_kernel(ctx, A);
         FP_LAUNCHED(ctx);
         cudaEventRecord(e1, ctx->stream);
         FP_CUDA(ctx, cudaEventSynchronize(e1));
