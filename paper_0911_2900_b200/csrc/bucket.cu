@@ -28,11 +28,14 @@
 __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* alive,
                                     const uint8_t* owned, uint32_t n, int tile_w, uint32_t cps, uint32_t* cnt,
                                     uint32_t* chunk_of, uint32_t* slot, unsigned long long* n_planned) {
+    __shared__ unsigned s_taken;  // agents this block takes (one global atomic per block)
+    if (threadIdx.x == 0) s_taken = 0;
+    __syncthreads();
     for (uint32_t i0 = blockIdx.x * blockDim.x; i0 < n; i0 += gridDim.x * blockDim.x) {
         const uint32_t i = i0 + threadIdx.x;
         const bool take = i < n && alive[i] && (!owned || owned[i]);
         const unsigned b = __ballot_sync(0xffffffffu, take);
-        if ((threadIdx.x & 31) == 0 && b) atomicAdd(n_planned, (unsigned long long)__popc(b));
+        if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_taken, (unsigned)__popc(b));
         if (i >= n) continue;
         if (!take) {
             chunk_of[i] = FP_NONE;
@@ -43,6 +46,8 @@ __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, c
         chunk_of[i] = c;
         slot[i] = atomicAdd(&cnt[c], 1u);
     }
+    __syncthreads();
+    if (threadIdx.x == 0 && s_taken) atomicAdd(n_planned, (unsigned long long)s_taken);
 }
 
 // Also writes the planner's record of the agent, (id, wrapped x, y, v_max), so the plan kernel
@@ -64,14 +69,22 @@ __global__ void bucket_scatter_kernel(Geo g, const int32_t* x, const int32_t* y,
 __global__ void tile_sums_kernel(const uint32_t* ccnt, const uint32_t* coff, int tiles_x, int tiles_y, uint32_t cps,
                                  int cpt, uint32_t* cnt, uint32_t* off, uint32_t* list, unsigned long long* n_tiles) {
     const uint32_t nt = (uint32_t)tiles_x * (uint32_t)tiles_y;
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
-        const uint32_t tx = t % (uint32_t)tiles_x, ty = t / (uint32_t)tiles_x;
-        const uint32_t g0 = tx * cps + ty * (uint32_t)cpt;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t t0 = blockIdx.x * blockDim.x; t0 < nt; t0 += gridDim.x * blockDim.x) {
+        const uint32_t t = t0 + threadIdx.x;
         uint32_t c = 0;
-        for (int k = 0; k < cpt; ++k) c += ccnt[g0 + k];
-        cnt[t] = c;
-        off[t] = coff[g0];
-        if (c) list[atomicAdd(n_tiles, 1ull)] = t;
+        if (t < nt) {
+            const uint32_t tx = t % (uint32_t)tiles_x, ty = t / (uint32_t)tiles_x;
+            const uint32_t g0 = tx * cps + ty * (uint32_t)cpt;
+            for (int k = 0; k < cpt; ++k) c += ccnt[g0 + k];
+            cnt[t] = c;
+            off[t] = coff[g0];
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, c != 0);  // one list reservation per warp
+        uint32_t base = 0;
+        if (lane == 0 && b) base = (uint32_t)atomicAdd(n_tiles, (unsigned long long)__popc(b));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (c) list[base + __popc(b & ((1u << lane) - 1u))] = t;
     }
 }
 
@@ -219,7 +232,13 @@ int fp_bucket_launch(fp_ctx* ctx) {
                                           ctx->st.on ? ctx->st.d_owned : nullptr, n, ctx->tile_w, ctx->cps,
                                           ctx->d_sub_cnt, ctx->d_flags, ctx->d_cursor_b, &ctx->d_sc->n_planned);
     FP_LAUNCHED(ctx);
+#ifdef FP_STAGE_BUCKET
+    FP_STAMP(ctx, s, 4);
+#endif
     if (int rc = fp_scan_u32(ctx, ctx->d_sub_cnt, ctx->d_sub_off, nch, ctx->d_scan_sums, s)) return rc;
+#ifdef FP_STAGE_BUCKET
+    FP_STAMP(ctx, s, 5);
+#endif
     tile_sums_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s>>>(
         ctx->d_sub_cnt, ctx->d_sub_off, ctx->tiles_x, ctx->tiles_y, ctx->cps, ctx->tile_h / 8, ctx->d_tile_cnt,
         ctx->d_tile_off, ctx->d_tile_list, &ctx->d_sc->n_tiles);
@@ -228,6 +247,9 @@ int fp_bucket_launch(fp_ctx* ctx) {
     motion_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nt, 256)), 256, 0, s>>>(
         ctx->d_tile_list, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->d_seed_items, &ctx->d_sc->n_items);
     FP_LAUNCHED(ctx);
+#ifdef FP_STAGE_BUCKET
+    FP_STAMP(ctx, s, 6);
+#endif
     bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, n, ctx->d_flags,
                                             ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket, ctx->d_brec);
     FP_LAUNCHED(ctx);

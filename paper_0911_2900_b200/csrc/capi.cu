@@ -613,8 +613,15 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     cudaStreamWaitEvent(c->stream2, c->ev_fork, 0);
     if (rc == FP_OK) rc = fp_order_launch(c, seed, c->stream2);
     cudaEventRecord(c->ev_join, c->stream2);
+    // the order branch runs beside bucketing + plan kernel and joins before the motion (joining
+    // before the plan kernel instead was measured slower: the branch takes ~140 us)
+#ifdef FP_ORDER_JOIN_EARLY
+    if (rc == FP_OK) rc = fp_plan_launch(c, k_s, seed, c->ev_join);
+#else
     if (rc == FP_OK) rc = fp_plan_launch(c, k_s, seed);
+#endif
     cudaStreamWaitEvent(c->stream, c->ev_join, 0);
+    FP_STAMP(c, c->stream, 7);
 #endif
     cudaError_t e = cudaStreamEndCapture(c->stream, &g);
     if (rc != FP_OK) {

@@ -100,6 +100,13 @@ __host__ __device__ __forceinline__ uint64_t fp_rng_u64(uint64_t seed, uint64_t 
 __host__ __device__ __forceinline__ double fp_unit_interval(uint64_t x) {
     return (double)(x >> 11) * 0x1.0p-53;
 }
+// FP_STAGE_TIMING builds: globaltimer stamps between the plan-graph stages (diagnostics).
+#ifdef FP_STAGE_TIMING
+__global__ void fp_stamp_kernel(unsigned long long* t);
+#define FP_STAMP(ctx, strm, slot) fp_stamp_kernel<<<1, 1, 0, (strm)>>>(&(ctx)->d_sc->plan_prof[slot])
+#else
+#define FP_STAMP(ctx, strm, slot) ((void)0)
+#endif
 #define FP_MOVE_ORDER_STREAM (1ULL << 63)
 #define FP_SPAWN_STREAM ((1ULL << 63) + 1)
 
@@ -329,7 +336,8 @@ int fp_plane_ensure(fp_ctx* ctx, double k_s);                         // plane.c
 int fp_ghost_occ(fp_ctx* ctx);                                        // plane.cu
 int fp_ghost_static(fp_ctx* ctx);                                     // plane.cu
 int fp_bucket_launch(fp_ctx* ctx);                                    // bucket.cu
-int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed);           // plan.cu
+// plan.cu; wait_before_kernel: an event the stream kernel waits for (the movement order branch)
+int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed, cudaEvent_t wait_before_kernel = nullptr);
 int fp_plan_exact_launch(fp_ctx* ctx, double k_s, uint64_t seed);     // plan.cu
 int fp_order_launch(fp_ctx* ctx, uint64_t seed, cudaStream_t s);     // order.cu
 int fp_motion_launch(fp_ctx* ctx, bool spatial);                      // move.cu

@@ -164,7 +164,18 @@ int fp_order_positions(fp_ctx* ctx, uint32_t n, uint64_t seed, int64_t step, uin
 int fp_order_launch(fp_ctx* ctx, uint64_t seed, cudaStream_t s) {
     const uint32_t n = ctx->n;
     if (n == 0) return FP_OK;
+#ifndef FP_STAGE_BUCKET
+    FP_STAMP(ctx, s, 4);
+#endif
     if (int rc = fp_select_alive(ctx, ctx->d_alive, n, ctx->d_alive_ids, &ctx->d_sc->n_alive, ctx->d_scan_sums2, s))
         return rc;
-    return fy_run(ctx, s, &ctx->d_sc->n_alive, n, seed, &ctx->d_sc->step, ctx->d_alive_ids, ctx->d_order, ctx->d_rank);
+#ifndef FP_STAGE_BUCKET
+    FP_STAMP(ctx, s, 5);
+#endif
+    const int rc = fy_run(ctx, s, &ctx->d_sc->n_alive, n, seed, &ctx->d_sc->step, ctx->d_alive_ids, ctx->d_order,
+                          ctx->d_rank);
+#ifndef FP_STAGE_BUCKET
+    FP_STAMP(ctx, s, 6);
+#endif
+    return rc;
 }

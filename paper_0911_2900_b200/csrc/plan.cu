@@ -1164,15 +1164,25 @@ static int launch_stream(fp_ctx* ctx, const StreamArgs& A) {
     return FP_OK;
 }
 
+#ifdef FP_STAGE_TIMING
+__global__ void fp_stamp_kernel(unsigned long long* t) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    *t = v;
+}
+#endif
+
 // Enqueues the whole planning phase (bucketing + streaming kernel + exact-path pass) on
 // ctx->stream.  Graph-safe: the step, chunk counts, deal and the fallback count live in device
 // memory; fp_plan_prepare ran before.
-int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
+int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed, cudaEvent_t wait_before_kernel) {
     if (ctx->n == 0) return FP_OK;
     if (!tiled_ok(ctx)) return fp_plan_exact_launch(ctx, k_s, seed);
     if (!ctx->plane_valid || ctx->plane_ks != k_s || ctx->plane_potential != ctx->potential)
         return fp_fail(ctx, FP_ERUNTIME, "plan: weight plane not prepared for this k_s");
+    FP_STAMP(ctx, ctx->stream, 0);
     if (int rc = fp_bucket_launch(ctx)) return rc;
+    FP_STAMP(ctx, ctx->stream, 1);
     if (ctx->marks_dirty) {  // marks of an earlier plan no motion phase consumed
         const size_t nwords = (size_t)ctx->P * ctx->H;
         FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
@@ -1182,9 +1192,13 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     ctx->rec_fresh = true;     // walk records emitted below
     ctx->marks_dirty = true;
     const StreamArgs A = make_stream_args(ctx, k_s, seed);
+    // the persistent stream kernel takes every SM: work that must not queue behind it joins first
+    if (wait_before_kernel) FP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, wait_before_kernel, 0));
     if (int rc = launch_stream(ctx, A)) return rc;
+    FP_STAMP(ctx, ctx->stream, 2);
     plan_exact_list_kernel<<<ctx->sm_count * 4, EXACT_THREADS, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
     FP_LAUNCHED(ctx);
+    FP_STAMP(ctx, ctx->stream, 3);
     return FP_OK;
 }
 
