@@ -239,25 +239,31 @@ int fp_bucket_launch(fp_ctx* ctx) {
 #ifdef FP_STAGE_BUCKET
     FP_STAMP(ctx, s, 5);
 #endif
-    tile_sums_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s>>>(
+    // after the scan: the tile lists and the plan items (side branch) beside the scatter
+    cudaStream_t s3 = ctx->stream3;
+    FP_CUDA(ctx, cudaEventRecord(ctx->ev_bfork, s));
+    FP_CUDA(ctx, cudaStreamWaitEvent(s3, ctx->ev_bfork, 0));
+    tile_sums_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s3>>>(
         ctx->d_sub_cnt, ctx->d_sub_off, ctx->tiles_x, ctx->tiles_y, ctx->cps, ctx->tile_h / 8, ctx->d_tile_cnt,
         ctx->d_tile_off, ctx->d_tile_list, &ctx->d_sc->n_tiles);
     FP_LAUNCHED(ctx);
-    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_items, 0, 8, s));
-    motion_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nt, 256)), 256, 0, s>>>(
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_items, 0, 8, s3));
+    motion_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nt, 256)), 256, 0, s3>>>(
         ctx->d_tile_list, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->d_seed_items, &ctx->d_sc->n_items);
     FP_LAUNCHED(ctx);
+    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_plan_items, 0, 8, s3));
+    const uint32_t nbatch = (uint32_t)((ctx->cps + PLAN_ITEM_CHUNKS - 1) / PLAN_ITEM_CHUNKS) * (uint32_t)ctx->tiles_x;
+    plan_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nbatch, 128)), 128, 0, s3>>>(
+        ctx->d_sub_cnt, ctx->d_sub_off, (uint32_t)ctx->cps, (uint32_t)ctx->tiles_x, &ctx->d_sc->n_planned,
+        ctx->d_plan_items, &ctx->d_sc->n_plan_items);
+    FP_LAUNCHED(ctx);
+    FP_CUDA(ctx, cudaEventRecord(ctx->ev_bjoin, s3));
 #ifdef FP_STAGE_BUCKET
     FP_STAMP(ctx, s, 6);
 #endif
     bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, n, ctx->d_flags,
                                             ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket, ctx->d_brec);
     FP_LAUNCHED(ctx);
-    FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_plan_items, 0, 8, s));
-    const uint32_t nbatch = (uint32_t)((ctx->cps + PLAN_ITEM_CHUNKS - 1) / PLAN_ITEM_CHUNKS) * (uint32_t)ctx->tiles_x;
-    plan_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nbatch, 128)), 128, 0, s>>>(
-        ctx->d_sub_cnt, ctx->d_sub_off, (uint32_t)ctx->cps, (uint32_t)ctx->tiles_x, &ctx->d_sc->n_planned,
-        ctx->d_plan_items, &ctx->d_sc->n_plan_items);
-    FP_LAUNCHED(ctx);
+    FP_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_bjoin, 0));
     return FP_OK;
 }

@@ -218,8 +218,18 @@ extern "C" int fp_create(const fp_grid_desc* g, const uint8_t* cells, const doub
         fp_destroy(c);
         return rc;
     };
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+    // the critical path (bucketing, plan kernel, motion) outranks the movement-order branch,
+    // which fills the gaps beside it (stream priorities carry into the captured graphs)
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+#ifdef FP_NO_STREAM_PRIORITY
+    prio_hi = prio_lo;
+#endif
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->stream3, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_bfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_bjoin, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)
         return bail(fp_cuda_fail(c, cudaGetLastError(), "cudaStreamCreate"));
@@ -270,6 +280,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     free_agents(c);
     if (c->stream2) cudaStreamSynchronize(c->stream2);
+    if (c->stream3) cudaStreamSynchronize(c->stream3);
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
     if (c->st.graph_fin) cudaGraphExecDestroy(c->st.graph_fin);
@@ -299,6 +310,9 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream2) cudaStreamDestroy(c->stream2);
+    if (c->stream3) cudaStreamDestroy(c->stream3);
+    if (c->ev_bfork) cudaEventDestroy(c->ev_bfork);
+    if (c->ev_bjoin) cudaEventDestroy(c->ev_bjoin);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

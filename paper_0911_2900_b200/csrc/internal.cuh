@@ -189,6 +189,8 @@ struct fp_ctx {
     int sm_count = 148;
     cudaStream_t stream = nullptr;   // main stream
     cudaStream_t stream2 = nullptr;  // order (Fisher-Yates) branch
+    cudaStream_t stream3 = nullptr;  // bucketing side branch (tile lists, plan items)
+    cudaEvent_t ev_bfork = nullptr, ev_bjoin = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
 

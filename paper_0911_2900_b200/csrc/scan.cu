@@ -124,7 +124,49 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_scatter_kernel(const uin
     }
 }
 
+// One CTA over the whole array in FP_SCAN_TOP * FP_SCAN_PER-element rounds with a running carry:
+// one launch instead of three for short arrays (the per-step chunk counts).
+#define FP_SCAN_SMALL_ROUND (FP_SCAN_TOP * FP_SCAN_PER)
+#define FP_SCAN_SMALL_MAX (16 * FP_SCAN_SMALL_ROUND)
+#ifndef FP_SCAN_USE_SMALL
+#define FP_SCAN_USE_SMALL 0
+#endif
+__global__ void __launch_bounds__(FP_SCAN_TOP) scan_small_kernel(const uint32_t* in, uint32_t n, uint32_t* out) {
+    __shared__ uint32_t s_warp[33];
+    uint32_t carry = 0;
+    for (uint32_t r0 = 0; r0 < n; r0 += FP_SCAN_SMALL_ROUND) {
+        const uint32_t base = r0 + threadIdx.x * FP_SCAN_PER;
+        uint32_t v[FP_SCAN_PER], t = 0;
+        load_run(in, n, base, v);
+#pragma unroll
+        for (int k = 0; k < FP_SCAN_PER; ++k) t += v[k];
+        uint32_t total;
+        uint32_t e = block_scan_excl(t, s_warp, &total) + carry;
+        carry += total;
+        uint32_t o[FP_SCAN_PER];
+#pragma unroll
+        for (int k = 0; k < FP_SCAN_PER; ++k) {
+            o[k] = e;
+            e += v[k];
+        }
+        if (base + FP_SCAN_PER <= n) {
+#pragma unroll
+            for (int q = 0; q < FP_SCAN_PER / 4; ++q)
+                reinterpret_cast<uint4*>(out + base)[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < FP_SCAN_PER; ++k)
+                if (base + k < n) out[base + k] = o[k];
+        }
+    }
+}
+
 int fp_scan_u32(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* sums, cudaStream_t s) {
+    if (FP_SCAN_USE_SMALL && n <= FP_SCAN_SMALL_MAX) {  // measured slower than the 3-pass scan
+        scan_small_kernel<<<1, FP_SCAN_TOP, 0, s>>>(in, n, out);
+        FP_LAUNCHED(ctx);
+        return FP_OK;
+    }
     const uint32_t nb = std::max<uint32_t>(1, (n + FP_SCAN_TILE - 1) / FP_SCAN_TILE);
     if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "scan: more than 134M elements");
     scan_sums_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(in, n, sums);
