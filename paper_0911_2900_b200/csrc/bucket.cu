@@ -18,6 +18,9 @@
 #include "internal.cuh"
 #include "scan.cuh"
 
+#ifndef FP_BUCKET_CTAS_PER_SM
+#define FP_BUCKET_CTAS_PER_SM 16  // grid of the counting / scatter passes (per SM)
+#endif
 #ifndef PLAN_ITEM_CHUNKS
 #define PLAN_ITEM_CHUNKS 6    // chunks per plan item (plan.cu's ring holds three items of <= 8 slots)
 #endif
@@ -227,7 +230,7 @@ int fp_bucket_launch(fp_ctx* ctx) {
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_sub_cnt, 0, (size_t)nch * 4, s));
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_planned, 0, 8, s));
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_tiles, 0, 8, s));
-    const unsigned G = (unsigned)std::min<size_t>(fp_blocks(n, 256), (size_t)ctx->sm_count * 16);
+    const unsigned G = (unsigned)std::min<size_t>(fp_blocks(n, 256), (size_t)ctx->sm_count * FP_BUCKET_CTAS_PER_SM);
     bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_alive,
                                           ctx->st.on ? ctx->st.d_owned : nullptr, n, ctx->tile_w, ctx->cps,
                                           ctx->d_sub_cnt, ctx->d_flags, ctx->d_cursor_b, &ctx->d_sc->n_planned);

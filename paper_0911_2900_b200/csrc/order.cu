@@ -17,6 +17,9 @@
 #include "internal.cuh"
 #include "scan.cuh"
 
+#ifndef FP_ORDER_CTAS_PER_SM
+#define FP_ORDER_CTAS_PER_SM 8  // grid of the order's grid-stride kernels (per SM)
+#endif
 #define GS_LOOP(i, n) for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += gridDim.x * blockDim.x)
 
 __global__ void fy_targets_kernel(const unsigned long long* pn, uint64_t seed, const long long* pstep, uint32_t* j,
@@ -124,7 +127,7 @@ int fp_ensure_temp(fp_ctx* ctx, size_t bytes) {
 static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, uint32_t cap, uint64_t seed,
                   const long long* step_dev, const uint32_t* ids, uint32_t* out, uint32_t* rank) {
     if (cap == 0) return FP_OK;
-    const unsigned G = (unsigned)std::min<size_t>(fp_blocks(cap, 256), (size_t)ctx->sm_count * 8);
+    const unsigned G = (unsigned)std::min<size_t>(fp_blocks(cap, 256), (size_t)ctx->sm_count * FP_ORDER_CTAS_PER_SM);
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, sizeof(uint32_t) * cap, s));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cursor, 0, sizeof(uint32_t) * cap, s));
     fy_targets_kernel<<<G, 256, 0, s>>>(n_dev, seed, step_dev, ctx->d_j, ctx->d_cnt);

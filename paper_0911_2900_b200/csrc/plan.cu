@@ -927,19 +927,28 @@ __device__ __forceinline__ void emit_record(const PlanCommon& a, const EmitArgs&
     E.rec0[pos] = record_of(a.g, a.occ, id, px, py, cx, cy, v, c_bpath_p);
 }
 
+// 11 bits of a global bitplane row: columns x0 .. x0 + 10 (ghost columns at the edges).
+__device__ __forceinline__ uint32_t bits11(const uint32_t* plane, const Geo& g, int x0, int y) {
+    const int b = x0 + FP_XPAD_BITS;
+    const size_t w = (size_t)y * g.P + (size_t)(b >> 5);
+    return __funnelshift_r(__ldg(&plane[w]), __ldg(&plane[w + 1]), b & 31) & 0x7FFu;
+}
+
 __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanCommon a, const uint2* list,
                                                                         EmitArgs E) {
     __shared__ double s_w[EXACT_THREADS];
     __shared__ int s_c[EXACT_THREADS];
+    __shared__ uint32_t s_wr[11], s_er[11];  // the ball's wall / exit bits (frame rows and columns -5..5)
     const unsigned n = (unsigned)a.sc->fb_count;
     const int t = threadIdx.x;
     const uint64_t step = (uint64_t)a.sc->step;
+    const Geo& g = a.g;
     for (unsigned e = blockIdx.x; e < n; e += gridDim.x) {
         const uint2 ent = list[e];
         const uint32_t id = ent.x;
-        const int px = a.g.wrap(a.x[id]), py = a.y[id], v = a.v[id];
+        const int px = g.wrap(a.x[id]), py = a.y[id], v = a.v[id];
         const int D = 2 * v + 1;
-        if (a.g.boundary == FP_BOUNDARY_PERIODIC_X && D >= a.g.W) {
+        if (g.boundary == FP_BOUNDARY_PERIODIC_X && D >= g.W) {
             if (t == 0) {
                 int cx, cy;
                 choose_exact(a, id, step, &cx, &cy);
@@ -950,29 +959,66 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
             __syncthreads();
             continue;
         }
+        // every load of the agent in one round: the ball's wall / exit rows, and per candidate
+        // slot its occupancy word and field value
+        if (t < 11) {
+            const int y = py - 5 + t;
+            const bool in = y >= 0 && y < g.H;
+            s_wr[t] = in ? bits11(g.wall, g, px - 5, y) : 0u;
+            s_er[t] = in ? bits11(g.exitb, g, px - 5, y) : 0u;
+        }
         // list-order column -> dx (wrapped-x sort at the periodic seam, planning.hpp:50-53)
         int a0 = -v, na = D, b0 = 0;
-        if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) {
-            if (px + v >= a.g.W) {
-                a0 = a.g.W - px; na = v - a0 + 1; b0 = -v;
+        if (g.boundary == FP_BOUNDARY_PERIODIC_X) {
+            if (px + v >= g.W) {
+                a0 = g.W - px; na = v - a0 + 1; b0 = -v;
             } else if (px - v < 0) {
                 a0 = -px; na = v - a0 + 1; b0 = -v;
             }
         }
+        const ExactWeight wf = make_weight(a, px, py);
+        bool ok = false;
+        int x = 0, y = 0, dx = 0, dy = 0;
+        double sc = 0.0;
+        uint32_t occw = 0;
         if (t < D * D) {
-            const ExactWeight wf = make_weight(a, px, py);
             const int r = t / D, c = t % D;
-            const int y = py - v + r;
-            const int dx = c < na ? a0 + c : b0 + (c - na);
-            int x = px + dx;
-            bool ok = y >= 0 && y < a.g.H;
-            if (a.g.boundary == FP_BOUNDARY_PERIODIC_X) x = a.g.wrap(x);
-            else ok = ok && x >= 0 && x < a.g.W;
-            ok = ok && !a.g.is_wall(x, y);
-            ok = ok && !(occ_bit(a.occ, a.g, x, y) && !(x == px && y == py));
-            ok = ok && los(a.g, px, py, x, y);
-            s_w[t] = ok ? wf(x, y) : -1.0;
-            s_c[t] = ok ? (y * a.g.W + x) : -1;
+            dy = r - v;
+            y = py + dy;
+            dx = c < na ? a0 + c : b0 + (c - na);
+            x = px + dx;
+            ok = y >= 0 && y < g.H;
+            if (g.boundary == FP_BOUNDARY_PERIODIC_X) x = g.wrap(x);
+            else ok = ok && x >= 0 && x < g.W;
+            if (ok) {
+                occw = __ldg(&a.occ[g.word(x, y)]);
+                if (wf.exitd && !wf.ones) sc = __ldg(&a.field[(size_t)y * g.W + x]);
+            }
+        }
+        __syncthreads();
+        if (t < D * D) {
+            if (ok) {
+                const bool wall = (s_wr[dy + 5] >> (dx + 5)) & 1u;
+                const bool occ = (occw >> (x & 31)) & 1u;
+                ok = !wall && !(occ && !(x == px && y == py));
+            }
+            if (ok) {  // line of sight (world.hpp:181-191): no Wall strictly between (walls inside the ball)
+                Mask121 wm{0ull, 0ull};
+#pragma unroll
+                for (int rr = 0; rr < 11; ++rr) mask_or_row(wm, s_wr[rr], rr * 11);
+                const int o = (dy + 5) * 11 + dx + 5;
+                const unsigned long long plo = ((unsigned long long)c_pathmask[o][1] << 32) | c_pathmask[o][0];
+                const unsigned long long phi = ((unsigned long long)c_pathmask[o][3] << 32) | c_pathmask[o][2];
+                ok = ((wm.lo & plo) | (wm.hi & phi)) == 0ull;
+            }
+            double wt = 0.0;
+            if (ok) {
+                if (wf.ones) wt = 1.0;
+                else if (wf.exitd) wt = isinf(sc) ? 0.0 : fpx_exp(FPX_MUL(wf.k_s, FPX_SUB(wf.sp, sc)));
+                else wt = fpx_exp(FPX_MUL(wf.k_s, FPX_MUL(wf.g, (double)g.segment_dx(px, x))));
+            }
+            s_w[t] = ok ? wt : -1.0;
+            s_c[t] = ok ? (y * g.W + x) : -1;
         }
         __syncthreads();
         if (t == 0) {
@@ -995,10 +1041,32 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
                     }
                 }
             const int cell = s_c[pick];
-            const int cx = cell % a.g.W, cy = cell / a.g.W;
+            const int cx = cell % g.W, cy = cell / g.W;
             a.dx[id] = cx;
             a.dy[id] = cy;
-            emit_record(a, E, id, ent.y, px, py, cx, cy, v);
+            if (E.emit) {  // record_of (motion_rec.cuh) from the staged rows
+                const int ddx = g.segment_dx(px, cx), ddy = cy - py;
+                const int o = (ddy + 5) * 11 + ddx + 5;
+                const int len = min(max(abs(ddx), abs(ddy)), v);
+                int m = 0, ex_x = 0, ex_y = 0;
+                bool ex = false;
+                for (int j = 0; j < len; ++j) {
+                    const int ox = c_bpath_p[o][j][0], oy = c_bpath_p[o][j][1];
+                    if ((s_wr[oy + 5] >> (ox + 5)) & 1u) break;
+                    ++m;
+                    if ((s_er[oy + 5] >> (ox + 5)) & 1u) {
+                        ex = true;
+                        ex_x = g.wrap(px + ox);
+                        ex_y = py + oy;
+                        break;
+                    }
+                }
+                const bool exit_free = ex && !((__ldcg(&a.occ[g.word(ex_x, ex_y)]) >> (ex_x & 31)) & 1u);
+                E.rec0[ent.y] = make_uint4(id, 0u,
+                                           (uint32_t)px | (exit_free ? REC_EXIT_FREE : 0u) | ((uint32_t)m << 28) |
+                                               (ex ? 0x80000000u : 0u),
+                                           (uint32_t)py | ((uint32_t)o << 24));
+            }
         }
         __syncthreads();
     }
