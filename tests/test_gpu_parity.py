@@ -303,3 +303,37 @@ def test_plaza_sampled_plan_and_invariants():
     occ = dev.occupancy()
     assert (occ[y1[al], x1[al]] == np.nonzero(al)[0]).all()
     assert (occ >= 0).sum() == al.sum()
+
+
+def _pocket_grid(r, w=120, h=90):
+    """Closed rooms with exits, plus walled pockets (enclosed free cells: unreachable, S = inf)
+    scattered through them; thin (1-cell) pocket walls so reachable agents see pocket cells inside
+    their balls."""
+    c = random_grid(r, w, h, 0.05, 3)
+    for _ in range(25):
+        pw, ph = int(r.integers(2, 7)), int(r.integers(2, 7))
+        x0, y0 = int(r.integers(2, w - pw - 3)), int(r.integers(2, h - ph - 3))
+        c[y0 - 1:y0 + ph + 1, x0 - 1:x0 + pw + 1] = WALL
+        c[y0:y0 + ph, x0:x0 + pw] = FREE
+    return c
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_plan_flagged_centres(case):
+    """The weight plane's exact-path flag (plane.cu): agents inside unreachable pockets (all
+    weights 1), agents with pocket cells within Chebyshev 5 (zero-weight candidates), and steep
+    fields (k_s = 8: weights spanning > 2^60 in a ball) -- every decision equal to the oracle's."""
+    r = np.random.default_rng(7100 + case)
+    cells = _pocket_grid(r)
+    free = np.argwhere(cells == FREE)
+    pick = r.choice(len(free), size=min(1500, len(free) // 3), replace=False)
+    y, x = free[pick, 0].astype(np.int32), free[pick, 1].astype(np.int32)
+    v = r.integers(1, 6, len(x)).astype(np.int32) if case % 2 else np.full(len(x), 5, np.int32)
+    dev, orc = pair(cells, x, y, v, step=int(r.integers(0, 300)))
+    f = O.static_field(cells, 0)
+    assert np.isinf(f[y, x]).any(), "no agent inside a pocket"
+    for k_s, seed in ((1.2, 3), (8.0, 77), (20.0, 5)):
+        fp.plan_phase(dev, fp.SimParams(k_s=k_s, seed=seed))
+        orc.plan(k_s, seed)
+        dx, dy = dev.desired()
+        assert (dx == orc.dx).all() and (dy == orc.dy).all(), (k_s, seed)
