@@ -231,6 +231,7 @@ struct fp_ctx {
     int64_t step = 0;
     int64_t alive = 0;
     bool mixed_v = false;
+    bool plan_marked = false;        // the last plan marked its movers' footprints in P1/P2
     int v_uniform = 1;               // the roster's v_max when not mixed (plan kernel variant)
     bool poisoned = false;  // a failed upload left the device roster inconsistent (capi.cu)
     int vmax_all = 1;

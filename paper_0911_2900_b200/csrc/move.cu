@@ -51,6 +51,7 @@ struct MoveArgs {
     const uint32_t* seed_list;     // mode B: alive ids to build records from
     const uint4* rec0;             // mode A: records emitted by the plan kernel (n_alive of them)
     int premade;                   // 1: mode A, 0: mode B
+    int premarked;                 // mode A with the footprints already marked by the plan
     uint4* rec[2];                 // pending records, ping-pong
     unsigned int* pcount;          // [0..1] list counts, [4..6] round pending counts, [7] long buckets (zero between phases)
     DevScalars* sc;
@@ -1143,7 +1144,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
             // steps 1 and 2 tile by tile over the plan's records
             const int nwmax = seed_ww(a.tile_w) * (a.tile_h + 10);
             uint32_t* win = reinterpret_cast<uint32_t*>(s_dyn) + (threadIdx.x / SEED_GROUP) * 2 * nwmax;
-            seed_mark(a, win, s_bp);
+            if (!a.premarked) seed_mark(a, win, s_bp);
             grid.sync();
             if (gtid == 0) a.sc->t_marked = globaltimer();
             unsigned long long hops = 0;
@@ -1534,6 +1535,7 @@ __global__ void __launch_bounds__(1024) exits_sort_kernel(unsigned long long* ex
 __global__ void move_begin_kernel(DevScalars* sc) {
     for (int r = threadIdx.x; r < 64; r += blockDim.x) sc->chk_max[r] = sc->chk_cnt[r] = sc->p1_max[r] = 0;
     if (threadIdx.x) return;
+    sc->t_motion[0] = globaltimer();  // (the marking pass, when it runs, restamps its start)
     sc->n_exits = 0;
     sc->exits_sorted = 0;
     sc->disp = 0;
@@ -1655,6 +1657,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.seed_list = spatial ? ctx->d_bucket : ctx->d_order;
     a.rec0 = ctx->d_rec0;
     a.premade = premade ? 1 : 0;
+    a.premarked = (premade && ctx->plan_marked) ? 1 : 0;
     a.rec[0] = ctx->d_rec_a;
     a.rec[1] = ctx->d_rec_b;
     a.pcount = (unsigned int*)ctx->d_counters;  // [0], [1] as u32 (kept zero between phases)
@@ -1708,8 +1711,10 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     const bool tiny = ctx->n <= TAIL_MAX;
     if (premade && !tiny) {  // steps 1 and 2 over the plan's records: two plain launches
         const unsigned sb = std::min(seed_blocks, std::max(1u, (unsigned)fp_blocks(ctx->n, SEED_ITEM)));
-        seed_mark_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
-        FP_LAUNCHED(ctx);
+        if (!ctx->plan_marked) {  // (else the plan kernels marked the footprints as they emitted them)
+            seed_mark_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
+            FP_LAUNCHED(ctx);
+        }
         seed_classify_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
         FP_LAUNCHED(ctx);
     } else {
@@ -1743,6 +1748,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     FP_LAUNCHED(ctx);
     ctx->rec_fresh = false;
     ctx->marks_dirty = false;
+    ctx->plan_marked = false;
     return fp_ghost_occ(ctx);
 }
 

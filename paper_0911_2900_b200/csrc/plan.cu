@@ -37,6 +37,10 @@
 #include "motion_rec.cuh"
 
 #define FP_GUARD 8e-7  // see the guard-band note above
+#ifndef FP_PLAN_MARKS
+#define FP_PLAN_MARKS 0  // 1: the plan marks footprints in P1/P2 and move.cu skips seed_mark_kernel
+                         // (measured: plan kernel +84 us for the global fetch-ORs, motion -40 us)
+#endif
 
 // Walk records (motion_rec.cuh): the plan emits them for the motion phase.
 __constant__ signed char c_bpath_p[121][5][2];
@@ -303,6 +307,8 @@ struct StreamArgs {
     uint4* rec0;                // walk records in bucket order (motion_rec.cuh)
     int mixed;                  // roster has more than one v_max: the masked radius-5 variant
     const uint32_t* plane_t;    // chunk-tiled weight plane (plane.cu plane_tile_kernel)
+    uint32_t* p1;               // non-null: mark each mover's footprint in the motion's contention
+    uint32_t* p2;               //   bitplanes as its record is emitted (mark_record, motion_rec.cuh)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -886,8 +892,10 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                 a.dx[id] = cx;
                 a.dy[id] = cy;
                 const int tile = (py / A.tile_h) * A.tiles_x + s;
-                A.rec0[pos] = record_of_ring(a.g, a.occ, A.tile_exit[tile], st & 4, R, osh0 + px - X0, id, px, py, cx,
-                                             cy, v, s_bp);
+                const uint4 rec = record_of_ring(a.g, a.occ, A.tile_exit[tile], st & 4, R, osh0 + px - X0, id, px,
+                                                 py, cx, cy, v, s_bp);
+                A.rec0[pos] = rec;
+                if (A.p1 && rec_m(rec)) mark_record(A.p1, A.p2, a.g, rec, s_bp, cx, cy);
             } else if (st == 2) {  // decided by the exact path after the sweep (plan_exact_list_kernel)
                 A.fallback[atomicAdd(&a.sc->fb_count, 1ull)] = make_uint2(id, pos);
             }
@@ -924,7 +932,9 @@ struct EmitArgs {
 __device__ __forceinline__ void emit_record(const PlanCommon& a, const EmitArgs& E, uint32_t id, uint32_t pos, int px,
                                             int py, int cx, int cy, int v) {
     if (!E.emit) return;
-    E.rec0[pos] = record_of(a.g, a.occ, id, px, py, cx, cy, v, c_bpath_p);
+    const uint4 rec = record_of(a.g, a.occ, id, px, py, cx, cy, v, c_bpath_p);
+    E.rec0[pos] = rec;
+    if (E.p1 && rec_m(rec)) mark_record(E.p1, E.p2, a.g, rec, c_bpath_p, cx, cy);
 }
 
 // 11 bits of a global bitplane row: columns x0 .. x0 + 10 (ghost columns at the edges).
@@ -1062,10 +1072,12 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
                     }
                 }
                 const bool exit_free = ex && !((__ldcg(&a.occ[g.word(ex_x, ex_y)]) >> (ex_x & 31)) & 1u);
-                E.rec0[ent.y] = make_uint4(id, 0u,
-                                           (uint32_t)px | (exit_free ? REC_EXIT_FREE : 0u) | ((uint32_t)m << 28) |
-                                               (ex ? 0x80000000u : 0u),
-                                           (uint32_t)py | ((uint32_t)o << 24));
+                const uint4 rec = make_uint4(id, 0u,
+                                             (uint32_t)px | (exit_free ? REC_EXIT_FREE : 0u) | ((uint32_t)m << 28) |
+                                                 (ex ? 0x80000000u : 0u),
+                                             (uint32_t)py | ((uint32_t)o << 24));
+                E.rec0[ent.y] = rec;
+                if (E.p1 && rec_m(rec)) mark_record(E.p1, E.p2, g, rec, c_bpath_p, cx, cy);
             }
         }
         __syncthreads();
@@ -1150,6 +1162,8 @@ static size_t stream_smem(const fp_ctx* ctx) {
            128 /* alignment slack */;
 }
 
+static bool plan_marks(const fp_ctx* ctx);
+
 static StreamArgs make_stream_args(fp_ctx* ctx, double k_s, uint64_t seed) {
     StreamArgs A;
     A.c = make_common(ctx, k_s, seed);
@@ -1168,10 +1182,19 @@ static StreamArgs make_stream_args(fp_ctx* ctx, double k_s, uint64_t seed) {
     A.rec0 = ctx->d_rec0;
     A.mixed = ctx->mixed_v ? 1 : 0;
     A.plane_t = ctx->d_plane_t;
+    A.p1 = plan_marks(ctx) ? ctx->d_p1 : nullptr;
+    A.p2 = plan_marks(ctx) ? ctx->d_p2 : nullptr;
     return A;
 }
 
-static EmitArgs emit_args(fp_ctx* ctx) { return EmitArgs{ctx->d_rec0, ctx->d_p1, ctx->d_p2, 1}; }
+// The plan marks the movers' footprints itself (the motion then skips its marking pass) on
+// single-GPU contexts; strip ranks mark after the deferral (strip.cu).
+static bool plan_marks(const fp_ctx* ctx) { return FP_PLAN_MARKS && !ctx->st.on; }
+
+static EmitArgs emit_args(fp_ctx* ctx) {
+    const bool mk = plan_marks(ctx);
+    return EmitArgs{ctx->d_rec0, mk ? ctx->d_p1 : nullptr, mk ? ctx->d_p2 : nullptr, 1};
+}
 
 #define FP_STREAM_VARIANTS(X)                                                                                \
     X(0, false, false) X(1, false, false) X(2, false, false) X(3, false, false) X(4, false, false)        \
@@ -1259,6 +1282,7 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed, cudaEvent_t wait_befo
     ctx->bucket_fresh = true;  // the motion seed pass walks agents in this (spatial) order
     ctx->rec_fresh = true;     // walk records emitted below
     ctx->marks_dirty = true;
+    ctx->plan_marked = plan_marks(ctx);  // ... with their footprints marked
     const StreamArgs A = make_stream_args(ctx, k_s, seed);
     // the persistent stream kernel takes every SM: work that must not queue behind it joins first
     if (wait_before_kernel) FP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, wait_before_kernel, 0));
@@ -1284,9 +1308,14 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
     FP_CUDA(ctx, cudaEventCreate(&e0));
     FP_CUDA(ctx, cudaEventCreate(&e1));
     double total = 0.0;
+    const size_t nwords = (size_t)ctx->P * ctx->H;
     for (int i = 0; i < iters; ++i) {
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->fb_count, 0, 8, ctx->stream));
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->tile_next, 0, 8, ctx->stream));
+        if (A.p1) {  // each launch marks afresh (outside the timed region)
+            FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p1, 0, nwords * 4, ctx->stream));
+            FP_CUDA(ctx, cudaMemsetAsync(ctx->d_p2, 0, nwords * 4, ctx->stream));
+        }
         cudaEventRecord(e0, ctx->stream);
         launch_stream_kernel(ctx, A);
         FP_LAUNCHED(ctx);
