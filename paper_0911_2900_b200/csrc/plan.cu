@@ -949,6 +949,7 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
     __shared__ double s_w[EXACT_THREADS];
     __shared__ int s_c[EXACT_THREADS];
     __shared__ uint32_t s_wr[11], s_er[11];  // the ball's wall / exit bits (frame rows and columns -5..5)
+    __shared__ int s_last;                    // the last candidate slot in list order
     const unsigned n = (unsigned)a.sc->fb_count;
     const int t = threadIdx.x;
     const uint64_t step = (uint64_t)a.sc->step;
@@ -957,18 +958,7 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
         const uint2 ent = list[e];
         const uint32_t id = ent.x;
         const int px = g.wrap(a.x[id]), py = a.y[id], v = a.v[id];
-        const int D = 2 * v + 1;
-        if (g.boundary == FP_BOUNDARY_PERIODIC_X && D >= g.W) {
-            if (t == 0) {
-                int cx, cy;
-                choose_exact(a, id, step, &cx, &cy);
-                a.dx[id] = cx;
-                a.dy[id] = cy;
-                emit_record(a, E, id, ent.y, px, py, cx, cy, v);
-            }
-            __syncthreads();
-            continue;
-        }
+        const int D = 2 * v + 1;  // (2v+1 < W: the tiled path runs on periodic grids of W >= 16)
         // every load of the agent in one round: the ball's wall / exit rows, and per candidate
         // slot its occupancy word and field value
         if (t < 11) {
@@ -977,6 +967,7 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
             s_wr[t] = in ? bits11(g.wall, g, px - 5, y) : 0u;
             s_er[t] = in ? bits11(g.exitb, g, px - 5, y) : 0u;
         }
+        if (t == 0) s_last = -1;
         // list-order column -> dx (wrapped-x sort at the periodic seam, planning.hpp:50-53)
         int a0 = -v, na = D, b0 = 0;
         if (g.boundary == FP_BOUNDARY_PERIODIC_X) {
@@ -1027,29 +1018,29 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
                 else if (wf.exitd) wt = isinf(sc) ? 0.0 : fpx_exp(FPX_MUL(wf.k_s, FPX_SUB(wf.sp, sc)));
                 else wt = fpx_exp(FPX_MUL(wf.k_s, FPX_MUL(wf.g, (double)g.segment_dx(px, x))));
             }
-            s_w[t] = ok ? wt : -1.0;
+            // non-candidates add +0.0: the serial sums keep every intermediate value, and the
+            // running sum can only cross the threshold at a candidate
+            s_w[t] = ok ? wt : 0.0;
             s_c[t] = ok ? (y * g.W + x) : -1;
+            if (ok) atomicMax(&s_last, t);
         }
         __syncthreads();
         if (t == 0) {
             double total = 0.0;
-            int last = -1;
-            for (int k = 0; k < D * D; ++k)
-                if (s_c[k] >= 0) {
-                    total = FPX_ADD(total, s_w[k]);
-                    last = k;
-                }
+#pragma unroll 8
+            for (int k = 0; k < D * D; ++k) total = FPX_ADD(total, s_w[k]);  // loads off the add chain
+            const int last = s_last;
             const double threshold = FPX_MUL(fp_unit_interval(fp_rng_u64(a.seed, id, step, 0)), total);
             double cum = 0.0;
             int pick = last;
-            for (int k = 0; k < D * D; ++k)
-                if (s_c[k] >= 0) {
-                    cum = FPX_ADD(cum, s_w[k]);
-                    if (cum > threshold) {
-                        pick = k;
-                        break;
-                    }
+#pragma unroll 4
+            for (int k = 0; k < D * D; ++k) {
+                cum = FPX_ADD(cum, s_w[k]);
+                if (cum > threshold) {
+                    pick = k;
+                    break;
                 }
+            }
             const int cell = s_c[pick];
             const int cx = cell % g.W, cy = cell / g.W;
             a.dx[id] = cx;
