@@ -182,6 +182,8 @@ static int ensure_agents(fp_ctx* c, uint32_t n) {
                          &c->d_cursor, &c->d_bucket, &c->d_succ, &c->d_nxt, &c->d_V, &c->d_pend_a,
                          &c->d_pend_b, &c->d_fy_bucket, &c->d_flags, &c->d_cursor_b};
     for (uint32_t** p : u32s) FP_CUDA(c, cudaMalloc(p, m * 4));
+    FP_CUDA(c, cudaMemsetAsync(c->d_cnt, 0, m * 4, c->stream));     // order.cu: zero between shuffles
+    FP_CUDA(c, cudaMemsetAsync(c->d_cursor, 0, m * 4, c->stream));
     FP_CUDA(c, cudaMalloc(&c->d_exits, m * 8));
     FP_CUDA(c, cudaMalloc(&c->d_exits_sorted, m * 8));
     FP_CUDA(c, cudaMalloc(&c->d_rec_a, m * sizeof(uint4)));
@@ -228,6 +230,9 @@ extern "C" int fp_create(const fp_grid_desc* g, const uint8_t* cells, const doub
     if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->stream2, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&c->stream3, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&c->stream4, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_sfork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_sjoin, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_bfork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_bjoin, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -281,6 +286,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
     free_agents(c);
     if (c->stream2) cudaStreamSynchronize(c->stream2);
     if (c->stream3) cudaStreamSynchronize(c->stream3);
+    if (c->stream4) cudaStreamSynchronize(c->stream4);
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
     if (c->st.graph_fin) cudaGraphExecDestroy(c->st.graph_fin);
@@ -311,6 +317,10 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream2) cudaStreamDestroy(c->stream2);
     if (c->stream3) cudaStreamDestroy(c->stream3);
+    if (c->stream4) cudaStreamDestroy(c->stream4);
+    if (c->ev_sfork) cudaEventDestroy(c->ev_sfork);
+    if (c->ev_sjoin) cudaEventDestroy(c->ev_sjoin);
+    if (c->d_scan_sums3) cudaFree(c->d_scan_sums3);
     if (c->ev_bfork) cudaEventDestroy(c->ev_bfork);
     if (c->ev_bjoin) cudaEventDestroy(c->ev_bjoin);
     if (c->stream) cudaStreamDestroy(c->stream);

@@ -191,6 +191,8 @@ struct fp_ctx {
     cudaStream_t stream2 = nullptr;  // order (Fisher-Yates) branch
     cudaStream_t stream3 = nullptr;  // bucketing side branch (tile lists, plan items)
     cudaEvent_t ev_bfork = nullptr, ev_bjoin = nullptr;
+    cudaStream_t stream4 = nullptr;  // alive compaction beside the shuffle (order.cu)
+    cudaEvent_t ev_sfork = nullptr, ev_sjoin = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
 
@@ -247,6 +249,7 @@ struct fp_ctx {
     size_t n_chunks_alloc = 0;
     uint32_t* d_scan_sums = nullptr;  // block sums of the chunk scan (bucket.cu)
     uint32_t* d_scan_sums2 = nullptr; // block sums of the order's scans (order.cu, stream2)
+    uint32_t* d_scan_sums3 = nullptr; // block sums of the alive compaction beside it (stream4)
     uint4* d_plan_items = nullptr;     // plan kernel work items (bucket.cu)
     size_t plan_items_alloc = 0;
     uint2* d_seed_items = nullptr;    // (tile-list entry, chunk) per motion seed work item

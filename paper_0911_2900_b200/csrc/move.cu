@@ -1787,5 +1787,6 @@ int fp_exits_finish(fp_ctx* ctx) {
     FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaMemcpyAsync(ctx->d_exits, ctx->d_exits_sorted, ne * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToDevice, ctx->stream));
+    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, (size_t)na * 4, ctx->stream));  // the order's zero invariant
     return FP_OK;
 }

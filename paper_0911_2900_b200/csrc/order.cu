@@ -17,6 +17,9 @@
 #include "internal.cuh"
 #include "scan.cuh"
 
+#ifndef FP_ORDER_SELECT_BESIDE
+#define FP_ORDER_SELECT_BESIDE 1  // alive compaction on its own branch beside the shuffle
+#endif
 #ifndef FP_ORDER_CTAS_PER_SM
 #define FP_ORDER_CTAS_PER_SM 8  // grid of the order's grid-stride kernels (per SM)
 #endif
@@ -86,10 +89,15 @@ __global__ void fy_chain_kernel(const unsigned long long* pn, const uint32_t* nx
 }
 
 // A[p] -> out (positions) or, with ids != null, order/rank of agent ids.
+// Also zeroes the target counters and cursors of slot p for the next shuffle (every target of
+// this one is < n; fy_run starts from zero arrays without a memset).
 __global__ void fy_final_kernel(const unsigned long long* pn, const uint32_t* j, const uint32_t* succ,
-                                const uint32_t* V, const uint32_t* ids, uint32_t* out, uint32_t* rank) {
+                                const uint32_t* V, const uint32_t* ids, uint32_t* out, uint32_t* rank,
+                                uint32_t* cnt, uint32_t* cursor) {
     const uint32_t n = (uint32_t)*pn;
     GS_LOOP(p, n) {
+        cnt[p] = 0;
+        cursor[p] = 0;
         uint32_t a;
         if (p == 0) {
             a = V[0];
@@ -125,11 +133,12 @@ int fp_ensure_temp(fp_ctx* ctx, size_t bytes) {
 // Positions permutation A (ids == null) or the id order + ranks; n_dev holds the count,
 // cap bounds it (sizes the scan).  Uses d_temp + its second half for scratch.
 static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, uint32_t cap, uint64_t seed,
-                  const long long* step_dev, const uint32_t* ids, uint32_t* out, uint32_t* rank) {
+                  const long long* step_dev, const uint32_t* ids, uint32_t* out, uint32_t* rank,
+                  cudaEvent_t wait_before_final = nullptr) {
     if (cap == 0) return FP_OK;
     const unsigned G = (unsigned)std::min<size_t>(fp_blocks(cap, 256), (size_t)ctx->sm_count * FP_ORDER_CTAS_PER_SM);
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, sizeof(uint32_t) * cap, s));
-    FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cursor, 0, sizeof(uint32_t) * cap, s));
+    // d_cnt / d_cursor are zero here: zeroed at allocation, re-zeroed by fy_final_kernel and by
+    // the exits sort that borrows d_cnt (move.cu fp_exits_finish)
     fy_targets_kernel<<<G, 256, 0, s>>>(n_dev, seed, step_dev, ctx->d_j, ctx->d_cnt);
     FP_LAUNCHED(ctx);
     if (int rc = fp_scan_u32(ctx, ctx->d_cnt, ctx->d_off, cap, ctx->d_scan_sums2, s)) return rc;
@@ -139,7 +148,9 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
     FP_LAUNCHED(ctx);
     fy_chain_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_nxt, ctx->d_V);
     FP_LAUNCHED(ctx);
-    fy_final_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_j, ctx->d_succ, ctx->d_V, ids, out, rank);
+    if (wait_before_final) FP_CUDA(ctx, cudaStreamWaitEvent(s, wait_before_final, 0));  // ids ready
+    fy_final_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_j, ctx->d_succ, ctx->d_V, ids, out, rank, ctx->d_cnt,
+                                      ctx->d_cursor);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -147,8 +158,9 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
 // Reserves the order stage's scratch (outside any graph capture).
 int fp_order_reserve(fp_ctx* ctx) {
     const uint32_t n = std::max<uint32_t>(ctx->n, 1);
-    if (ctx->order_reserved_n == n && ctx->d_scan_sums2) return FP_OK;
+    if (ctx->order_reserved_n == n && ctx->d_scan_sums2 && ctx->d_scan_sums3) return FP_OK;
     if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, FP_SCAN_SUMS * 4));
+    if (!ctx->d_scan_sums3) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums3, FP_SCAN_SUMS * 4));
     ctx->order_reserved_n = n;
     return FP_OK;
 }
@@ -170,6 +182,23 @@ int fp_order_launch(fp_ctx* ctx, uint64_t seed, cudaStream_t s) {
 #ifndef FP_STAGE_BUCKET
     FP_STAMP(ctx, s, 4);
 #endif
+    if (!ctx->st.on && FP_ORDER_SELECT_BESIDE) {
+        // the shuffle's positions depend only on the alive count, which the device already
+        // holds (DevScalars::alive): the compaction of the alive ids runs beside it and joins
+        // before the ids are mapped (fy_final_kernel)
+        FP_CUDA(ctx, cudaEventRecord(ctx->ev_sfork, s));
+        FP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream4, ctx->ev_sfork, 0));
+        if (int rc = fp_select_alive(ctx, ctx->d_alive, n, ctx->d_alive_ids, &ctx->d_sc->n_alive, ctx->d_scan_sums3,
+                                     ctx->stream4))
+            return rc;
+        FP_CUDA(ctx, cudaEventRecord(ctx->ev_sjoin, ctx->stream4));
+        const int rc = fy_run(ctx, s, &ctx->d_sc->alive, n, seed, &ctx->d_sc->step, ctx->d_alive_ids, ctx->d_order,
+                              ctx->d_rank, ctx->ev_sjoin);
+#ifndef FP_STAGE_BUCKET
+        FP_STAMP(ctx, s, 6);
+#endif
+        return rc;
+    }
     if (int rc = fp_select_alive(ctx, ctx->d_alive, n, ctx->d_alive_ids, &ctx->d_sc->n_alive, ctx->d_scan_sums2, s))
         return rc;
 #ifndef FP_STAGE_BUCKET
