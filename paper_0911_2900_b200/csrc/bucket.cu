@@ -62,7 +62,7 @@ __global__ void bucket_scatter_kernel(Geo g, const int32_t* x, const int32_t* y,
         const uint32_t c = chunk_of[i];
         if (c == FP_NONE) continue;
         const uint32_t p = off[c] + slot[i];
-        bucket[p] = i;
+        if (bucket) bucket[p] = i;
         brec[p] = make_uint4(i, (uint32_t)g.wrap(x[i]), (uint32_t)y[i], v[i]);
     }
 }
@@ -265,7 +265,7 @@ int fp_bucket_launch(fp_ctx* ctx) {
     FP_STAMP(ctx, s, 6);
 #endif
     bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, n, ctx->d_flags,
-                                            ctx->d_cursor_b, ctx->d_sub_off, ctx->d_bucket, ctx->d_brec);
+                                            ctx->d_cursor_b, ctx->d_sub_off, nullptr /* ids: brec.x */, ctx->d_brec);
     FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_bjoin, 0));
     return FP_OK;

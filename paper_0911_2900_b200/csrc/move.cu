@@ -1654,7 +1654,8 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     a.v = ctx->d_v;
     a.alive = ctx->d_alive;
     a.rank = ctx->d_rank;
-    a.seed_list = spatial ? ctx->d_bucket : ctx->d_order;
+    a.seed_list = ctx->d_order;  // mode B only (any order: the motion is order-independent)
+    (void)spatial;
     a.rec0 = ctx->d_rec0;
     a.premade = premade ? 1 : 0;
     a.premarked = (premade && ctx->plan_marked) ? 1 : 0;
