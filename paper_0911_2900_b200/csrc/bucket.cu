@@ -31,6 +31,7 @@
 __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* alive,
                                     const uint8_t* owned, uint32_t n, int tile_w, uint32_t cps, uint32_t* cnt,
                                     uint32_t* chunk_of, uint32_t* slot, unsigned long long* n_planned) {
+    FP_PDL_WAIT();
     __shared__ unsigned s_taken;  // agents this block takes (one global atomic per block)
     if (threadIdx.x == 0) s_taken = 0;
     __syncthreads();
@@ -58,6 +59,7 @@ __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, c
 __global__ void bucket_scatter_kernel(Geo g, const int32_t* x, const int32_t* y, const uint8_t* v, uint32_t n,
                                       const uint32_t* chunk_of, const uint32_t* slot, const uint32_t* off,
                                       uint32_t* bucket, uint4* brec) {
+    FP_PDL_WAIT();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t c = chunk_of[i];
         if (c == FP_NONE) continue;
@@ -71,6 +73,7 @@ __global__ void bucket_scatter_kernel(Geo g, const int32_t* x, const int32_t* y,
 // the compacted list of non-empty tiles (order irrelevant to the motion).
 __global__ void tile_sums_kernel(const uint32_t* ccnt, const uint32_t* coff, int tiles_x, int tiles_y, uint32_t cps,
                                  int cpt, uint32_t* cnt, uint32_t* off, uint32_t* list, unsigned long long* n_tiles) {
+    FP_PDL_WAIT();
     const uint32_t nt = (uint32_t)tiles_x * (uint32_t)tiles_y;
     const int lane = threadIdx.x & 31;
     for (uint32_t t0 = blockIdx.x * blockDim.x; t0 < nt; t0 += gridDim.x * blockDim.x) {
@@ -110,6 +113,7 @@ __device__ __forceinline__ uint32_t warp_reserve(uint32_t k, unsigned long long*
 // zero on entry.  Item order is free: the seed passes deal them out dynamically.
 __global__ void motion_items_kernel(const uint32_t* list, const uint32_t* cnt, const unsigned long long* n_tiles_p,
                                     uint2* items, unsigned long long* n_items) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)*n_tiles_p;
     for (uint32_t e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
         const uint32_t e = e0 + threadIdx.x;
@@ -126,6 +130,7 @@ __global__ void motion_items_kernel(const uint32_t* list, const uint32_t* cnt, c
 // order, which follows the batches warp by warp (results never depend on it).
 __global__ void plan_items_kernel(const uint32_t* ccnt, const uint32_t* coff, uint32_t cps, uint32_t tiles_x,
                                   const unsigned long long* n_planned_p, uint4* items, unsigned long long* n_items) {
+    FP_PDL_WAIT();
     const uint32_t nch = cps * tiles_x;
     const uint32_t n_planned = (uint32_t)*n_planned_p;
     const uint32_t bps = (cps + PLAN_ITEM_CHUNKS - 1) / PLAN_ITEM_CHUNKS;
@@ -231,7 +236,7 @@ int fp_bucket_launch(fp_ctx* ctx) {
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_planned, 0, 8, s));
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_tiles, 0, 8, s));
     const unsigned G = (unsigned)std::min<size_t>(fp_blocks(n, 256), (size_t)ctx->sm_count * FP_BUCKET_CTAS_PER_SM);
-    bucket_count_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_alive,
+    fp_launch(bucket_count_kernel, G, 256, 0, s, fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_alive,
                                           ctx->st.on ? ctx->st.d_owned : nullptr, n, ctx->tile_w, ctx->cps,
                                           ctx->d_sub_cnt, ctx->d_flags, ctx->d_cursor_b, &ctx->d_sc->n_planned);
     FP_LAUNCHED(ctx);
@@ -246,17 +251,17 @@ int fp_bucket_launch(fp_ctx* ctx) {
     cudaStream_t s3 = ctx->stream3;
     FP_CUDA(ctx, cudaEventRecord(ctx->ev_bfork, s));
     FP_CUDA(ctx, cudaStreamWaitEvent(s3, ctx->ev_bfork, 0));
-    tile_sums_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s3>>>(
+    fp_launch(tile_sums_kernel, (unsigned)std::min<size_t>(fp_blocks(nt, 256), (size_t)ctx->sm_count * 8), 256, 0, s3,
         ctx->d_sub_cnt, ctx->d_sub_off, ctx->tiles_x, ctx->tiles_y, ctx->cps, ctx->tile_h / 8, ctx->d_tile_cnt,
         ctx->d_tile_off, ctx->d_tile_list, &ctx->d_sc->n_tiles);
     FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_items, 0, 8, s3));
-    motion_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nt, 256)), 256, 0, s3>>>(
+    fp_launch(motion_items_kernel, (unsigned)std::max<size_t>(1, fp_blocks(nt, 256)), 256, 0, s3,
         ctx->d_tile_list, ctx->d_tile_cnt, &ctx->d_sc->n_tiles, ctx->d_seed_items, &ctx->d_sc->n_items);
     FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->n_plan_items, 0, 8, s3));
     const uint32_t nbatch = (uint32_t)((ctx->cps + PLAN_ITEM_CHUNKS - 1) / PLAN_ITEM_CHUNKS) * (uint32_t)ctx->tiles_x;
-    plan_items_kernel<<<(unsigned)std::max<size_t>(1, fp_blocks(nbatch, 128)), 128, 0, s3>>>(
+    fp_launch(plan_items_kernel, (unsigned)std::max<size_t>(1, fp_blocks(nbatch, 128)), 128, 0, s3,
         ctx->d_sub_cnt, ctx->d_sub_off, (uint32_t)ctx->cps, (uint32_t)ctx->tiles_x, &ctx->d_sc->n_planned,
         ctx->d_plan_items, &ctx->d_sc->n_plan_items);
     FP_LAUNCHED(ctx);
@@ -264,7 +269,7 @@ int fp_bucket_launch(fp_ctx* ctx) {
 #ifdef FP_STAGE_BUCKET
     FP_STAMP(ctx, s, 6);
 #endif
-    bucket_scatter_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, n, ctx->d_flags,
+    fp_launch(bucket_scatter_kernel, G, 256, 0, s, fp_geo(ctx), ctx->d_x, ctx->d_y, ctx->d_v, n, ctx->d_flags,
                                             ctx->d_cursor_b, ctx->d_sub_off, nullptr /* ids: brec.x */, ctx->d_brec);
     FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_bjoin, 0));

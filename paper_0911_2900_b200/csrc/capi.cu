@@ -15,6 +15,14 @@
 
 static thread_local std::string g_error;
 
+bool fp_pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("FASTPED_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 void fp_set_global_error(const std::string& s) { g_error = s; }
 
 static int fail(fp_ctx* ctx, int code, const std::string& msg) {
@@ -85,6 +93,7 @@ static int validate_grid(const fp_grid_desc* g, const uint8_t* cells) {
 
 // ------------------------------------------------------------------------ bitplanes
 __global__ void pack_planes_kernel(const uint8_t* cells, int W, int H, int P, uint32_t* wall, uint32_t* ex) {
+    FP_PDL_WAIT();
     const size_t nw = (size_t)P * H;
     for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < nw; w += (size_t)gridDim.x * blockDim.x) {
         const int y = (int)(w / P), x0 = (int)(w % P) * 32 - FP_XPAD_BITS;
@@ -102,15 +111,18 @@ __global__ void pack_planes_kernel(const uint8_t* cells, int W, int H, int P, ui
 }
 
 __global__ void sc_set_kernel(DevScalars* sc, long long step, unsigned long long alive) {
+    FP_PDL_WAIT();
     sc->step = step;
     sc->alive = alive;
 }
 
-__global__ void sc_step_kernel(DevScalars* sc) { sc->step += 1; }
+__global__ void sc_step_kernel(DevScalars* sc) {
+    FP_PDL_WAIT(); sc->step += 1; }
 
 // occupancy from alive positions + make_state checks (state.hpp:46-70)
 __global__ void build_occ_kernel(const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
                                  Geo g, uint32_t* occ, unsigned long long* errs) {
+    FP_PDL_WAIT();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = i < n && alive[i];
     const unsigned cnt = __popc(__ballot_sync(0xffffffffu, live));  // alive count -> errs[3]
@@ -132,12 +144,14 @@ __global__ void build_occ_kernel(const int32_t* x, const int32_t* y, const uint8
 
 __global__ void occ_dump_kernel(const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
                                 Geo g, int32_t* out) {
+    FP_PDL_WAIT();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || !alive[i]) return;
     out[(size_t)y[i] * g.W + g.wrap(x[i])] = (int32_t)i;
 }
 
 __global__ void u8_from_i32_kernel(const int32_t* in, uint8_t* out, uint32_t n) {
+    FP_PDL_WAIT();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = (uint8_t)in[i];
 }
@@ -261,7 +275,7 @@ extern "C" int fp_create(const fp_grid_desc* g, const uint8_t* cells, const doub
     cudaMemcpyAsync(d_cells, cells, ncell, cudaMemcpyHostToDevice, c->stream);
     cudaMemsetAsync(c->d_sc, 0, sizeof(DevScalars), c->stream);
     cudaMemsetAsync(c->d_counters, 0, 16 * sizeof(unsigned long long), c->stream);
-    pack_planes_kernel<<<1184, 256, 0, c->stream>>>(d_cells, c->W, c->H, c->P, c->d_wall, c->d_exit);
+    fp_launch(pack_planes_kernel, 1184, 256, 0, c->stream, d_cells, c->W, c->H, c->P, c->d_wall, c->d_exit);
     c->ctr.kernel_launches++;
     fp_ghost_static(c);
     cudaMemsetAsync(c->d_occ, 0, nwords * 4, c->stream);
@@ -348,7 +362,7 @@ extern "C" int fp_get_field(const fp_ctx* cc, double* out) {
 // last read_scalars or sync_scalars left them there and the host has not changed them since)
 static int sync_scalars(fp_ctx* c) {
     if (c->dev_step == c->step && c->dev_alive == c->alive) return FP_OK;
-    sc_set_kernel<<<1, 1, 0, c->stream>>>(c->d_sc, (long long)c->step, (unsigned long long)c->alive);
+    fp_launch(sc_set_kernel, 1, 1, 0, c->stream, c->d_sc, (long long)c->step, (unsigned long long)c->alive);
     FP_LAUNCHED(c);
     c->dev_step = c->step;
     c->dev_alive = c->alive;
@@ -402,7 +416,7 @@ static int upload_agents(fp_ctx* c, const int32_t* x, const int32_t* y, const ui
     FP_CUDA(c, cudaMemsetAsync(c->d_counters + 8, 0xFF, 3 * 8, s));
     FP_CUDA(c, cudaMemsetAsync(c->d_counters + 11, 0, 8, s));
     if (n) {
-        build_occ_kernel<<<fp_blocks(n, 256), 256, 0, s>>>(c->d_x, c->d_y, c->d_alive, n, geo_of(c), c->d_occ,
+        fp_launch(build_occ_kernel, fp_blocks(n, 256), 256, 0, s, c->d_x, c->d_y, c->d_alive, n, geo_of(c), c->d_occ,
                                                             c->d_counters + 8);
         FP_LAUNCHED(c);
     }
@@ -448,7 +462,7 @@ extern "C" int fp_set_agents(fp_ctx* c, uint32_t n, const int32_t* x, const int3
     if (n) {
         int32_t* d_tmp = c->d_dx;  // stage v_max as i32, convert to u8
         FP_CUDA(c, cudaMemcpyAsync(d_tmp, v_max, (size_t)n * 4, cudaMemcpyHostToDevice, c->stream));
-        u8_from_i32_kernel<<<fp_blocks(n, 256), 256, 0, c->stream>>>(d_tmp, c->d_v, n);
+        fp_launch(u8_from_i32_kernel, fp_blocks(n, 256), 256, 0, c->stream, d_tmp, c->d_v, n);
         FP_LAUNCHED(c);
     }
     if (int rc = upload_agents(c, x, y, alive)) return rc;
@@ -663,7 +677,7 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     c->bucket_fresh = false;
     if (rc == FP_OK && strip) rc = fp_strip_pack_launch(c);
     if (rc == FP_OK && !strip) {
-        sc_step_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+        fp_launch(sc_step_kernel, 1, 1, 0, c->stream, c->d_sc);
         c->ctr.kernel_launches++;
     }
     e = cudaStreamEndCapture(c->stream, &g);
@@ -682,7 +696,7 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
         if (rc == FP_OK) rc = fp_exits_sort_launch(c);
         if (rc == FP_OK) rc = fp_ghost_occ(c);
         if (rc == FP_OK) {
-            sc_step_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+            fp_launch(sc_step_kernel, 1, 1, 0, c->stream, c->d_sc);
             c->ctr.kernel_launches++;
         }
         e = cudaStreamEndCapture(c->stream, &g);
@@ -704,6 +718,7 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
 }
 
 __global__ void run_begin_kernel(DevScalars* sc) {
+    FP_PDL_WAIT();
     sc->tot_exits = 0;
     sc->tot_disp = 0;
     sc->tot_dx = 0;
@@ -721,7 +736,7 @@ extern "C" int fp_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_ru
     if (!c->graph_valid || c->graph_ks != k_s || c->graph_seed != seed)
         if (int rc = capture(c, k_s, seed)) return rc;
     if (int rc = sync_scalars(c)) return rc;
-    run_begin_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+    fp_launch(run_begin_kernel, 1, 1, 0, c->stream, c->d_sc);
     FP_LAUNCHED(c);
     const int64_t launches_per_step = 0;  // counted at capture; see fp_counters note
     (void)launches_per_step;
@@ -877,7 +892,7 @@ static int strip_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_run
     if (c->st.transport != FP_STRIP_NCCL && c->st.transport != FP_STRIP_HOST)
         return fail(c, FP_EINVAL, "strip run: no exchange transport");
     if (int rc = strip_ready(c, k_s, seed)) return rc;
-    run_begin_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+    fp_launch(run_begin_kernel, 1, 1, 0, c->stream, c->d_sc);
     FP_LAUNCHED(c);
     std::vector<cudaEvent_t> ev((size_t)2 * steps + 1);
     for (auto& e : ev) FP_CUDA(c, cudaEventCreate(&e));
@@ -1015,7 +1030,7 @@ extern "C" int fp_strips_run(fp_ctx* const* cs, int n, double k_s, uint64_t seed
         fp_ctx* c = cs[r];
         cudaSetDevice(c->device);
         if (int rc = strip_ready(c, k_s, seed)) return rc;
-        run_begin_kernel<<<1, 1, 0, c->stream>>>(c->d_sc);
+        fp_launch(run_begin_kernel, 1, 1, 0, c->stream, c->d_sc);
         FP_LAUNCHED(c);
         FP_CUDA(c, cudaEventCreate(&e0[r]));
         FP_CUDA(c, cudaEventCreate(&e1[r]));
@@ -1092,7 +1107,7 @@ extern "C" int fp_get_occupancy(const fp_ctx* cc, int32_t* occ) {
     FP_CUDA(c, cudaMalloc(&d, ncell * 4));
     cudaMemsetAsync(d, 0xFF, ncell * 4, c->stream);
     if (c->n) {
-        occ_dump_kernel<<<fp_blocks(c->n, 256), 256, 0, c->stream>>>(c->d_x, c->d_y, c->d_alive, c->n, geo_of(c), d);
+        fp_launch(occ_dump_kernel, fp_blocks(c->n, 256), 256, 0, c->stream, c->d_x, c->d_y, c->d_alive, c->n, geo_of(c), d);
         c->ctr.kernel_launches++;
     }
     cudaMemcpyAsync(occ, d, ncell * 4, cudaMemcpyDeviceToHost, c->stream);

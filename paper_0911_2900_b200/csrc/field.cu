@@ -25,6 +25,7 @@ struct FieldArgs {
 };
 
 __global__ void field_init_kernel(FieldArgs a, size_t n) {
+    FP_PDL_WAIT();
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
         const bool ex = a.cells[i] == FP_CELL_EXIT;
         a.s[i] = ex ? 0ull : 0x7ff0000000000000ull;
@@ -45,6 +46,7 @@ __device__ __forceinline__ int wrapx(const FieldArgs& a, int x) {
 }
 
 __global__ void field_relax_kernel(FieldArgs a, int k) {
+    FP_PDL_WAIT();
     const int cur = k % 3;
     const unsigned cnt = a.counts[cur];
     const uint32_t* list = a.lists[cur];
@@ -111,13 +113,13 @@ int fp_field_compute(fp_ctx* ctx, const uint8_t* d_cells) {
     if (e != cudaSuccess) rc = fp_cuda_fail(ctx, e, "cudaMallocHost");
     if (rc == FP_OK) {
         cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned int), s);
-        field_init_kernel<<<1184, 256, 0, s>>>(a, n);
+        fp_launch(field_init_kernel, 1184, 256, 0, s, a, n);
         ctx->ctr.kernel_launches++;
         // Process buckets; check for an empty window every `batch` buckets.
         const int batch = 16;
         for (int k = 0;; k += batch) {
             for (int b = k; b < k + batch; ++b) {
-                field_relax_kernel<<<1184, 256, 0, s>>>(a, b);
+                fp_launch(field_relax_kernel, 1184, 256, 0, s, a, b);
                 ctx->ctr.kernel_launches++;
                 // bucket b is drained; it is reused for b+3
                 cudaMemsetAsync(counts + (b % 3), 0, sizeof(unsigned int), s);

@@ -22,6 +22,37 @@
 
 #include "../../include/fastped_b200.h"
 
+// Programmatic dependent launch.  Every kernel is launched through fp_launch with programmatic
+// stream serialisation, so the next kernel of a stream (or captured graph branch) is dispatched
+// while its predecessor drains instead of after it; every kernel body opens with FP_PDL_WAIT
+// (griddepcontrol.wait: blocks until the predecessor grid has completed and its memory is
+// visible; returns at once for a kernel launched without the attribute).  Nothing runs before
+// the wait, so ordering is exactly that of plain launches.  FP_PDL_TRIGGER builds additionally
+// release the dependent launch right after the wait (its CTAs are then resident and parked
+// while this grid runs).  FASTPED_PDL=0 in the environment launches without the attribute.
+#ifdef FP_PDL_TRIGGER
+#define FP_PDL_WAIT() asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+#else
+#define FP_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#endif
+
+bool fp_pdl_enabled();  // capi.cu
+
+template <typename... KArgs, typename... Args>
+inline void fp_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = fp_pdl_enabled() ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kernel, args...);  // errors surface through cudaGetLastError
+}
+
 #define FP_NONE 0xFFFFFFFFu
 #define FP_XPAD_BITS 32  // ghost columns left of x = 0 in the bitplanes
 #define FP_XPAD_W 8      // ghost columns left of x = 0 in the weight plane
@@ -103,7 +134,7 @@ __host__ __device__ __forceinline__ double fp_unit_interval(uint64_t x) {
 // FP_STAGE_TIMING builds: globaltimer stamps between the plan-graph stages (diagnostics).
 #ifdef FP_STAGE_TIMING
 __global__ void fp_stamp_kernel(unsigned long long* t);
-#define FP_STAMP(ctx, strm, slot) fp_stamp_kernel<<<1, 1, 0, (strm)>>>(&(ctx)->d_sc->plan_prof[slot])
+#define FP_STAMP(ctx, strm, slot) fp_launch(fp_stamp_kernel, 1, 1, 0, (strm), &(ctx)->d_sc->plan_prof[slot])
 #else
 #define FP_STAMP(ctx, strm, slot) ((void)0)
 #endif

@@ -1100,6 +1100,7 @@ __device__ __forceinline__ bool classify(const MoveArgs& a, uint4& rec, const si
 
 template <int PART>
 __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     cg::grid_group grid = cg::this_grid();
     __shared__ signed char s_bp[121][5][2];
     extern __shared__ __align__(16) unsigned char s_dyn[];  // TailSmem (block 0's tail) / seed windows
@@ -1342,6 +1343,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
 #define SEED_MARK_MINB 3
 #endif
 __global__ void __launch_bounds__(MOVE_THREADS, SEED_MARK_MINB) seed_mark_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     __shared__ signed char s_bp[121][5][2];
     extern __shared__ __align__(16) unsigned char s_dyn[];
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
@@ -1355,6 +1357,7 @@ __global__ void __launch_bounds__(MOVE_THREADS, SEED_MARK_MINB) seed_mark_kernel
 #define SEED_CLASSIFY_MINB 2
 #endif
 __global__ void __launch_bounds__(MOVE_THREADS, SEED_CLASSIFY_MINB) seed_classify_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     __shared__ signed char s_bp[121][5][2];
     extern __shared__ __align__(16) unsigned char s_dyn[];
     __shared__ unsigned int s_app[2 + 2 * SEED_GROUPS];
@@ -1374,11 +1377,13 @@ __global__ void __launch_bounds__(MOVE_THREADS, SEED_CLASSIFY_MINB) seed_classif
 }
 
 __global__ void __launch_bounds__(MOVE_THREADS) p2_count_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     __shared__ unsigned s_red[32];
     p2_count(a, s_red);
 }
 
 __global__ void __launch_bounds__(MOVE_THREADS) p2_number_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     __shared__ unsigned s_red[32];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         a.sc->t_motion[1] = globaltimer();
@@ -1394,6 +1399,7 @@ __global__ void __launch_bounds__(MOVE_THREADS) p2_number_kernel(MoveArgs a) {
 // Each returns at once when the phase has too few contended agents for the rounds.
 #define PREP_THREADS 256
 __global__ void __launch_bounds__(PREP_THREADS) bk_count_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     __shared__ signed char s_bp[121][5][2];
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
     const unsigned nc = cta_load(&a.pcount[1]);  // (its barriers also publish s_bp)
@@ -1420,18 +1426,21 @@ __global__ void __launch_bounds__(PREP_THREADS) bk_count_kernel(MoveArgs a) {
 // bbase = exclusive prefix of the bucket sizes: per-CTA sums, then each CTA's slice (both
 // launched with the same grid).
 __global__ void __launch_bounds__(MOVE_THREADS) bk_scan_count_kernel(MoveArgs a, unsigned g1) {
+    FP_PDL_WAIT();
     __shared__ unsigned s_red[32];
     if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
     bk_scan_count(a, cta_load(&a.scan[g1]), s_red);
 }
 
 __global__ void __launch_bounds__(MOVE_THREADS) bk_scan_base_kernel(MoveArgs a, unsigned g1) {
+    FP_PDL_WAIT();
     __shared__ unsigned s_red[32];
     if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
     bk_scan_base(a, cta_load(&a.scan[g1]), s_red);
 }
 
 __global__ void __launch_bounds__(PREP_THREADS) bk_place_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     const unsigned nc = cta_load(&a.pcount[1]);
     if (nc <= TAIL_MAX) return;
     const unsigned nthreads = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1448,11 +1457,13 @@ __global__ void __launch_bounds__(PREP_THREADS) bk_place_kernel(MoveArgs a) {
 }
 
 __global__ void __launch_bounds__(PREP_THREADS) bk_sort_kernel(MoveArgs a, unsigned g1) {
+    FP_PDL_WAIT();
     if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
     bk_sort(a, cta_load(&a.scan[g1]), blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 __global__ void __launch_bounds__(PREP_THREADS) bk_sort_long_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     __shared__ unsigned s_rank[(PREP_THREADS / 32) * BK_SORT_MAX];
     if (cta_load(&a.pcount[1]) <= TAIL_MAX) return;
     bk_sort_long(a, s_rank);
@@ -1460,6 +1471,7 @@ __global__ void __launch_bounds__(PREP_THREADS) bk_sort_long_kernel(MoveArgs a) 
 
 // Per contended agent, once every bucket is sorted: its check record (see bk_check).
 __global__ void __launch_bounds__(PREP_THREADS) bk_final_kernel(MoveArgs a) {
+    FP_PDL_WAIT();
     __shared__ signed char s_bp[121][5][2];
     for (int k = threadIdx.x; k < 121 * 10; k += blockDim.x) (&s_bp[0][0][0])[k] = (&c_bpath[0][0][0])[k];
     const unsigned nc = cta_load(&a.pcount[1]);  // (its barriers also publish s_bp)
@@ -1515,6 +1527,7 @@ __global__ void __launch_bounds__(PREP_THREADS) bk_final_kernel(MoveArgs a) {
 // few (the usual case: a handful per step); more than EXITS_SMEM are left to the host's radix sort.
 #define EXITS_SMEM 4096
 __global__ void __launch_bounds__(1024) exits_sort_kernel(unsigned long long* exits, DevScalars* sc) {
+    FP_PDL_WAIT();
     __shared__ unsigned long long key[EXITS_SMEM];
     const unsigned n = (unsigned)sc->n_exits;
     if (n > EXITS_SMEM) {
@@ -1533,6 +1546,7 @@ __global__ void __launch_bounds__(1024) exits_sort_kernel(unsigned long long* ex
 }
 
 __global__ void move_begin_kernel(DevScalars* sc) {
+    FP_PDL_WAIT();
     for (int r = threadIdx.x; r < 64; r += blockDim.x) sc->chk_max[r] = sc->chk_cnt[r] = sc->p1_max[r] = 0;
     if (threadIdx.x) return;
     sc->t_motion[0] = globaltimer();  // (the marking pass, when it runs, restamps its start)
@@ -1599,7 +1613,7 @@ static int ensure_buckets(fp_ctx* ctx) {
 // Mode B: records are built here from the plan-tile buckets when current, else the order list.
 int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     cudaStream_t s = ctx->stream;
-    move_begin_kernel<<<1, 64, 0, s>>>(ctx->d_sc);
+    fp_launch(move_begin_kernel, 1, 64, 0, s, ctx->d_sc);
     FP_LAUNCHED(ctx);
     if (ctx->n == 0) return FP_OK;
     if (int rc = ensure_buckets(ctx)) return rc;
@@ -1713,39 +1727,39 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
     if (premade && !tiny) {  // steps 1 and 2 over the plan's records: two plain launches
         const unsigned sb = std::min(seed_blocks, std::max(1u, (unsigned)fp_blocks(ctx->n, SEED_ITEM)));
         if (!ctx->plan_marked) {  // (else the plan kernels marked the footprints as they emitted them)
-            seed_mark_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
+            fp_launch(seed_mark_kernel, sb, MOVE_THREADS, seed_smem, s, a);
             FP_LAUNCHED(ctx);
         }
-        seed_classify_kernel<<<sb, MOVE_THREADS, seed_smem, s>>>(a);
+        fp_launch(seed_classify_kernel, sb, MOVE_THREADS, seed_smem, s, a);
         FP_LAUNCHED(ctx);
     } else {
         FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<1>, a));
         ctx->ctr.kernel_launches++;
     }
     if (!tiny) {
-        p2_count_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a);
+        fp_launch(p2_count_kernel, a.p2g, MOVE_THREADS, 0, s, a);
         FP_LAUNCHED(ctx);
-        p2_number_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a);
+        fp_launch(p2_number_kernel, a.p2g, MOVE_THREADS, 0, s, a);
         FP_LAUNCHED(ctx);
         const unsigned pg = prep_blocks;
-        bk_count_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        fp_launch(bk_count_kernel, pg, PREP_THREADS, 0, s, a);
         FP_LAUNCHED(ctx);
-        bk_scan_count_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a, a.p2g);
+        fp_launch(bk_scan_count_kernel, a.p2g, MOVE_THREADS, 0, s, a, a.p2g);
         FP_LAUNCHED(ctx);
-        bk_scan_base_kernel<<<a.p2g, MOVE_THREADS, 0, s>>>(a, a.p2g);
+        fp_launch(bk_scan_base_kernel, a.p2g, MOVE_THREADS, 0, s, a, a.p2g);
         FP_LAUNCHED(ctx);
-        bk_place_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        fp_launch(bk_place_kernel, pg, PREP_THREADS, 0, s, a);
         FP_LAUNCHED(ctx);
-        bk_sort_kernel<<<pg, PREP_THREADS, 0, s>>>(a, a.p2g);
+        fp_launch(bk_sort_kernel, pg, PREP_THREADS, 0, s, a, a.p2g);
         FP_LAUNCHED(ctx);
-        bk_sort_long_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        fp_launch(bk_sort_long_kernel, pg, PREP_THREADS, 0, s, a);
         FP_LAUNCHED(ctx);
-        bk_final_kernel<<<pg, PREP_THREADS, 0, s>>>(a);
+        fp_launch(bk_final_kernel, pg, PREP_THREADS, 0, s, a);
         FP_LAUNCHED(ctx);
     }
     FP_CUDA(ctx, cudaLaunchKernelEx(&cfg, move_rounds_kernel<2>, a));
     ctx->ctr.kernel_launches++;
-    exits_sort_kernel<<<1, 1024, 0, s>>>(ctx->d_exits, ctx->d_sc);
+    fp_launch(exits_sort_kernel, 1, 1024, 0, s, ctx->d_exits, ctx->d_sc);
     FP_LAUNCHED(ctx);
     ctx->rec_fresh = false;
     ctx->marks_dirty = false;
@@ -1754,7 +1768,7 @@ int fp_motion_launch(fp_ctx* ctx, bool spatial) {
 }
 
 int fp_exits_sort_launch(fp_ctx* ctx) {
-    exits_sort_kernel<<<1, 1024, 0, ctx->stream>>>(ctx->d_exits, ctx->d_sc);
+    fp_launch(exits_sort_kernel, 1, 1024, 0, ctx->stream, ctx->d_exits, ctx->d_sc);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -1762,12 +1776,14 @@ int fp_exits_sort_launch(fp_ctx* ctx) {
 // Exit records are (rank << 32 | id) with distinct ranks in [0, n_alive): a rank flag array,
 // its exclusive scan, and a scatter put them in processing order.
 __global__ void exits_flag_kernel(const unsigned long long* exits, uint32_t ne, uint32_t* flag) {
+    FP_PDL_WAIT();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < ne) flag[(uint32_t)(exits[i] >> 32)] = 1u;
 }
 
 __global__ void exits_place_kernel(const unsigned long long* exits, uint32_t ne, const uint32_t* pos,
                                    unsigned long long* out) {
+    FP_PDL_WAIT();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < ne) out[pos[(uint32_t)(exits[i] >> 32)]] = exits[i];
 }
@@ -1781,10 +1797,10 @@ int fp_exits_finish(fp_ctx* ctx) {
     const uint32_t na = std::max<uint32_t>(ctx->n_order, 1);
     if (!ctx->d_scan_sums2) FP_CUDA(ctx, cudaMalloc(&ctx->d_scan_sums2, FP_SCAN_SUMS * 4));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_cnt, 0, (size_t)na * 4, ctx->stream));
-    exits_flag_kernel<<<fp_blocks(ne, 256), 256, 0, ctx->stream>>>(ctx->d_exits, ne, ctx->d_cnt);
+    fp_launch(exits_flag_kernel, fp_blocks(ne, 256), 256, 0, ctx->stream, ctx->d_exits, ne, ctx->d_cnt);
     FP_LAUNCHED(ctx);
     if (int rc = fp_scan_u32(ctx, ctx->d_cnt, ctx->d_off, na, ctx->d_scan_sums2, ctx->stream)) return rc;
-    exits_place_kernel<<<fp_blocks(ne, 256), 256, 0, ctx->stream>>>(ctx->d_exits, ne, ctx->d_off, ctx->d_exits_sorted);
+    fp_launch(exits_place_kernel, fp_blocks(ne, 256), 256, 0, ctx->stream, ctx->d_exits, ne, ctx->d_off, ctx->d_exits_sorted);
     FP_LAUNCHED(ctx);
     FP_CUDA(ctx, cudaMemcpyAsync(ctx->d_exits, ctx->d_exits_sorted, ne * sizeof(unsigned long long),
                                  cudaMemcpyDeviceToDevice, ctx->stream));

@@ -27,6 +27,7 @@
 
 __global__ void fy_targets_kernel(const unsigned long long* pn, uint64_t seed, const long long* pstep, uint32_t* j,
                                   uint32_t* cnt) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)*pn;
     const uint64_t step = (uint64_t)*pstep;
     GS_LOOP(i, n) {
@@ -40,6 +41,7 @@ __global__ void fy_targets_kernel(const unsigned long long* pn, uint64_t seed, c
 
 __global__ void fy_scatter_kernel(const unsigned long long* pn, const uint32_t* j, uint32_t* cursor,
                                   const uint32_t* off, uint32_t* bucket) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)*pn;
     GS_LOOP(i, n) {
         if (i == 0) continue;
@@ -52,6 +54,7 @@ __global__ void fy_scatter_kernel(const unsigned long long* pn, const uint32_t* 
 // One thread per target slot q: sort L_q (tiny), link succ, record nxt(q).
 __global__ void fy_link_kernel(const unsigned long long* pn, const uint32_t* off, const uint32_t* cnt,
                                uint32_t* bucket, uint32_t* succ, uint32_t* nxt) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)*pn;
     GS_LOOP(q, n) {
         const uint32_t o = off[q], c = cnt[q];
@@ -76,6 +79,7 @@ __global__ void fy_link_kernel(const unsigned long long* pn, const uint32_t* off
 }
 
 __global__ void fy_chain_kernel(const unsigned long long* pn, const uint32_t* nxt, uint32_t* V) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)*pn;
     GS_LOOP(s, n) {
         uint32_t t = s;
@@ -94,6 +98,7 @@ __global__ void fy_chain_kernel(const unsigned long long* pn, const uint32_t* nx
 __global__ void fy_final_kernel(const unsigned long long* pn, const uint32_t* j, const uint32_t* succ,
                                 const uint32_t* V, const uint32_t* ids, uint32_t* out, uint32_t* rank,
                                 uint32_t* cnt, uint32_t* cursor) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)*pn;
     GS_LOOP(p, n) {
         cnt[p] = 0;
@@ -139,17 +144,17 @@ static int fy_run(fp_ctx* ctx, cudaStream_t s, const unsigned long long* n_dev, 
     const unsigned G = (unsigned)std::min<size_t>(fp_blocks(cap, 256), (size_t)ctx->sm_count * FP_ORDER_CTAS_PER_SM);
     // d_cnt / d_cursor are zero here: zeroed at allocation, re-zeroed by fy_final_kernel and by
     // the exits sort that borrows d_cnt (move.cu fp_exits_finish)
-    fy_targets_kernel<<<G, 256, 0, s>>>(n_dev, seed, step_dev, ctx->d_j, ctx->d_cnt);
+    fp_launch(fy_targets_kernel, G, 256, 0, s, n_dev, seed, step_dev, ctx->d_j, ctx->d_cnt);
     FP_LAUNCHED(ctx);
     if (int rc = fp_scan_u32(ctx, ctx->d_cnt, ctx->d_off, cap, ctx->d_scan_sums2, s)) return rc;
-    fy_scatter_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_j, ctx->d_cursor, ctx->d_off, ctx->d_fy_bucket);
+    fp_launch(fy_scatter_kernel, G, 256, 0, s, n_dev, ctx->d_j, ctx->d_cursor, ctx->d_off, ctx->d_fy_bucket);
     FP_LAUNCHED(ctx);
-    fy_link_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_off, ctx->d_cnt, ctx->d_fy_bucket, ctx->d_succ, ctx->d_nxt);
+    fp_launch(fy_link_kernel, G, 256, 0, s, n_dev, ctx->d_off, ctx->d_cnt, ctx->d_fy_bucket, ctx->d_succ, ctx->d_nxt);
     FP_LAUNCHED(ctx);
-    fy_chain_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_nxt, ctx->d_V);
+    fp_launch(fy_chain_kernel, G, 256, 0, s, n_dev, ctx->d_nxt, ctx->d_V);
     FP_LAUNCHED(ctx);
     if (wait_before_final) FP_CUDA(ctx, cudaStreamWaitEvent(s, wait_before_final, 0));  // ids ready
-    fy_final_kernel<<<G, 256, 0, s>>>(n_dev, ctx->d_j, ctx->d_succ, ctx->d_V, ids, out, rank, ctx->d_cnt,
+    fp_launch(fy_final_kernel, G, 256, 0, s, n_dev, ctx->d_j, ctx->d_succ, ctx->d_V, ids, out, rank, ctx->d_cnt,
                                       ctx->d_cursor);
     FP_LAUNCHED(ctx);
     return FP_OK;

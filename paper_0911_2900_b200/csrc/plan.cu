@@ -228,6 +228,7 @@ __device__ __forceinline__ void choose_exact(const PlanCommon& a, uint32_t i, ui
 // Host-API single-agent entry points (fp_choose_desired / fp_enumerate_candidates): an agent
 // given by value against the context's occupancy snapshot (the reference's const SimState&).
 __global__ void choose_one_kernel(PlanCommon a, uint32_t id, int px, int py, int v, long long step, int32_t* out) {
+    FP_PDL_WAIT();
     int cx, cy;
     choose_exact_at(a, id, a.g.wrap(px), py, v, (uint64_t)step, &cx, &cy);
     out[0] = cx;
@@ -235,6 +236,7 @@ __global__ void choose_one_kernel(PlanCommon a, uint32_t id, int px, int py, int
 }
 
 __global__ void candidates_one_kernel(PlanCommon a, int px, int py, int v, int32_t* cx, int32_t* cy, uint32_t* n_out) {
+    FP_PDL_WAIT();
     uint32_t n = 0;
     for_each_candidate(a, a.g.wrap(px), py, v, [&](int x, int y) {
         cx[n] = x;
@@ -246,6 +248,7 @@ __global__ void candidates_one_kernel(PlanCommon a, int px, int py, int v, int32
 }
 
 __global__ void plan_exact_kernel(PlanCommon a) {
+    FP_PDL_WAIT();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.n || !a.alive[i]) return;
     int cx, cy;
@@ -655,6 +658,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) plan_stream_kernel(const __gr
                                                                       const __grid_constant__ CUtensorMap tmap_o,
                                                                       const __grid_constant__ CUtensorMap tmap_l,
                                                                       StreamArgs A) {
+    FP_PDL_WAIT();
     extern __shared__ __align__(128) uint32_t smem_raw[];
     uint32_t* ringw = smem_raw + (((128u - (smem_u32(smem_raw) & 127u)) & 127u) >> 2);
     uint32_t* ringo = ringw + RING_SLOTS * CHUNK_ROWS * A.boxw;
@@ -946,6 +950,7 @@ __device__ __forceinline__ uint32_t bits11(const uint32_t* plane, const Geo& g, 
 
 __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanCommon a, const uint2* list,
                                                                         EmitArgs E) {
+    FP_PDL_WAIT();
     __shared__ double s_w[EXACT_THREADS];
     __shared__ int s_c[EXACT_THREADS];
     __shared__ uint32_t s_wr[11], s_er[11];  // the ball's wall / exit bits (frame rows and columns -5..5)
@@ -1080,6 +1085,7 @@ __global__ void __launch_bounds__(EXACT_THREADS) plan_exact_list_kernel(PlanComm
 // path's choice probabilities (fast weights / fast total, fp32).
 __global__ void choice_kernel(PlanCommon a, const uint32_t* plane, int PW, uint32_t i, int32_t* cx, int32_t* cy,
                               double* w, float* p, uint32_t* n_out) {
+    FP_PDL_WAIT();
     const int px = a.g.wrap(a.x[i]);
     const int py = a.y[i];
     const ExactWeight wf = make_weight(a, px, py);
@@ -1142,7 +1148,7 @@ bool fp_plan_tiled(const fp_ctx* ctx) { return tiled_ok(ctx); }
 int fp_plan_exact_launch(fp_ctx* ctx, double k_s, uint64_t seed) {
     if (ctx->n == 0) return FP_OK;
     PlanCommon a = make_common(ctx, k_s, seed);
-    plan_exact_kernel<<<fp_blocks(ctx->n, 128), 128, 0, ctx->stream>>>(a);
+    fp_launch(plan_exact_kernel, fp_blocks(ctx->n, 128), 128, 0, ctx->stream, a);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -1207,13 +1213,13 @@ static void launch_stream_kernel(fp_ctx* ctx, const StreamArgs& A) {
     const bool mixed = ctx->mixed_v;
 #define FP_SK(V, D, M)                                                                                         \
     if (V > 0 && v == V && drive == D && mixed == M) {                                                         \
-        plan_stream_kernel<V, D, M><<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(           \
+        fp_launch(plan_stream_kernel<V, D, M>, ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream,            \
             ctx->tmap_plane, ctx->tmap_occ, ctx->tmap_wall, A);                                                \
         return;                                                                                                \
     }
     FP_STREAM_VARIANTS(FP_SK)
 #undef FP_SK
-    plan_stream_kernel<0, false, false><<<ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream>>>(
+    fp_launch(plan_stream_kernel<0, false, false>, ctx->sm_count, PLAN_THREADS, stream_smem(ctx), ctx->stream,
         ctx->tmap_plane, ctx->tmap_occ, ctx->tmap_wall, A);
 }
 
@@ -1248,6 +1254,7 @@ static int launch_stream(fp_ctx* ctx, const StreamArgs& A) {
 
 #ifdef FP_STAGE_TIMING
 __global__ void fp_stamp_kernel(unsigned long long* t) {
+    FP_PDL_WAIT();
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
     *t = v;
@@ -1279,7 +1286,7 @@ int fp_plan_launch(fp_ctx* ctx, double k_s, uint64_t seed, cudaEvent_t wait_befo
     if (wait_before_kernel) FP_CUDA(ctx, cudaStreamWaitEvent(ctx->stream, wait_before_kernel, 0));
     if (int rc = launch_stream(ctx, A)) return rc;
     FP_STAMP(ctx, ctx->stream, 2);
-    plan_exact_list_kernel<<<ctx->sm_count * 4, EXACT_THREADS, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
+    fp_launch(plan_exact_list_kernel, ctx->sm_count * 4, EXACT_THREADS, 0, ctx->stream, A.c, ctx->d_fallback, emit_args(ctx));
     FP_LAUNCHED(ctx);
     FP_STAMP(ctx, ctx->stream, 3);
     return FP_OK;
@@ -1320,7 +1327,7 @@ int fp_plan_kernel_time(fp_ctx* ctx, double k_s, uint64_t seed, int iters, doubl
     ctx->rec_fresh = false;
     ctx->marks_dirty = true;
     // leave the state planned (the fallbacks of the last launch decided exactly)
-    plan_exact_list_kernel<<<ctx->sm_count * 4, EXACT_THREADS, 0, ctx->stream>>>(A.c, ctx->d_fallback, emit_args(ctx));
+    fp_launch(plan_exact_list_kernel, ctx->sm_count * 4, EXACT_THREADS, 0, ctx->stream, A.c, ctx->d_fallback, emit_args(ctx));
     FP_LAUNCHED(ctx);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1336,7 +1343,7 @@ int fp_choice_launch(fp_ctx* ctx, uint32_t agent, double k_s, int32_t* d_cx, int
         if (int rc = fp_plan_prepare(ctx, k_s)) return rc;
         plane = ctx->d_plane;
     }
-    choice_kernel<<<1, 1, 0, ctx->stream>>>(a, plane, ctx->PW, agent, d_cx, d_cy, d_w, d_p, d_n);
+    fp_launch(choice_kernel, 1, 1, 0, ctx->stream, a, plane, ctx->PW, agent, d_cx, d_cy, d_w, d_p, d_n);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -1346,7 +1353,7 @@ int fp_choose_one_launch(fp_ctx* ctx, uint32_t id, int px, int py, int v, int64_
                          int32_t* d_out) {
     if (int rc = ensure_pathmasks(ctx)) return rc;
     PlanCommon a = make_common(ctx, k_s, seed);
-    choose_one_kernel<<<1, 1, 0, ctx->stream>>>(a, id, px, py, v, (long long)step, d_out);
+    fp_launch(choose_one_kernel, 1, 1, 0, ctx->stream, a, id, px, py, v, (long long)step, d_out);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -1354,7 +1361,7 @@ int fp_choose_one_launch(fp_ctx* ctx, uint32_t id, int px, int py, int v, int64_
 // enumerate_candidates(st, agent) for one agent given by value (planning.hpp:23-57).
 int fp_candidates_one_launch(fp_ctx* ctx, int px, int py, int v, int32_t* d_cx, int32_t* d_cy, uint32_t* d_n) {
     PlanCommon a = make_common(ctx, 0.0, 0);
-    candidates_one_kernel<<<1, 1, 0, ctx->stream>>>(a, px, py, v, d_cx, d_cy, d_n);
+    fp_launch(candidates_one_kernel, 1, 1, 0, ctx->stream, a, px, py, v, d_cx, d_cy, d_n);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }

@@ -24,6 +24,7 @@
 
 __global__ void plane_build_kernel(Geo g, int PW, const double* field, int potential, double K,
                                    uint32_t* plane, int* cval) {
+    FP_PDL_WAIT();
     const size_t total = (size_t)PW * g.H;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int y = (int)(i / PW);
@@ -74,6 +75,7 @@ __global__ void plane_build_kernel(Geo g, int PW, const double* field, int poten
 // Words outside the plane (rows >= H, columns past the pitch) read as Wall.
 __global__ void plane_tile_kernel(const uint32_t* plane, int PW, int H, int tile_w, int boxw, int rows_chunks,
                                   size_t total, uint32_t* out) {
+    FP_PDL_WAIT();
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int c = (int)(i % boxw);
         const size_t rb = i / boxw;  // (stripe * rows_chunks + chunk) * 8 + row
@@ -89,6 +91,7 @@ __global__ void plane_tile_kernel(const uint32_t* plane, int PW, int H, int tile
 // Row pass of the radius-5 min/max of C (cval: INT_MIN wall / outside, INT_MIN + 1 unreachable
 // free cell; a window holding an unreachable cell gets rmin = INT_MIN).
 __global__ void plane_rowminmax_kernel(int PW, int H, const int* cval, int* rmin, int* rmax) {
+    FP_PDL_WAIT();
     const size_t total = (size_t)PW * H;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int xp = (int)(i % PW);
@@ -113,6 +116,7 @@ __global__ void plane_rowminmax_kernel(int PW, int H, const int* cval, int* rmin
 
 __global__ void plane_unsafe_kernel(int PW, int H, const int* cval, const int* rmin, const int* rmax,
                                     uint32_t* plane, unsigned long long* n_unsafe) {
+    FP_PDL_WAIT();
     const size_t total = (size_t)PW * H;
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         const int c = cval[i];
@@ -134,6 +138,7 @@ __global__ void plane_unsafe_kernel(int PW, int H, const int* cval, const int* r
 
 // Ghost bits of a bitplane for periodic-x grids: bits at x outside [0, W) mirror wrap(x).
 __global__ void ghost_bits_kernel(Geo g, uint32_t* plane) {
+    FP_PDL_WAIT();
     // words that hold any x outside [0, W): word 0 (x in [-32,0)) and words from (W+32)/32 on
     const int first_right = (g.W + FP_XPAD_BITS) >> 5;
     const int per_row = 1 + (g.P - first_right);
@@ -162,16 +167,16 @@ __global__ void ghost_bits_kernel(Geo g, uint32_t* plane) {
 
 int fp_ghost_occ(fp_ctx* ctx) {
     if (ctx->boundary != FP_BOUNDARY_PERIODIC_X) return FP_OK;
-    ghost_bits_kernel<<<fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream>>>(fp_geo(ctx), ctx->d_occ);
+    fp_launch(ghost_bits_kernel, fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream, fp_geo(ctx), ctx->d_occ);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
 
 int fp_ghost_static(fp_ctx* ctx) {
     if (ctx->boundary != FP_BOUNDARY_PERIODIC_X) return FP_OK;
-    ghost_bits_kernel<<<fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream>>>(fp_geo(ctx), ctx->d_wall);
+    fp_launch(ghost_bits_kernel, fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream, fp_geo(ctx), ctx->d_wall);
     FP_LAUNCHED(ctx);
-    ghost_bits_kernel<<<fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream>>>(fp_geo(ctx), ctx->d_exit);
+    fp_launch(ghost_bits_kernel, fp_blocks((size_t)ctx->H * 4, 256), 256, 0, ctx->stream, fp_geo(ctx), ctx->d_exit);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -196,6 +201,7 @@ static PFN_encodeTiled get_encode() {
 
 // Marks every tile whose window (tile + FP_HALO cells, wrapped at a periodic seam) holds an Exit.
 __global__ void tile_exit_kernel(Geo g, int tile_w, int tile_h, int tiles_x, int tiles_y, uint8_t* flag) {
+    FP_PDL_WAIT();
     const size_t nwords = (size_t)g.P * g.H;
     for (size_t w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < nwords; w += (size_t)gridDim.x * blockDim.x) {
         uint32_t bits = g.exitb[w];
@@ -269,8 +275,7 @@ static int make_tmap(fp_ctx* ctx) {
     FP_CUDA(ctx, cudaMalloc(&ctx->d_tile_exit, nt));
     FP_CUDA(ctx, cudaMemsetAsync(ctx->d_tile_exit, 0, nt, ctx->stream));
     const size_t nwords = (size_t)ctx->P * ctx->H;
-    tile_exit_kernel<<<(unsigned)std::min<size_t>(fp_blocks(nwords, 256), (size_t)ctx->sm_count * 16), 256, 0,
-                       ctx->stream>>>(fp_geo(ctx), ctx->tile_w, ctx->tile_h, ctx->tiles_x, ctx->tiles_y,
+    fp_launch(tile_exit_kernel, (unsigned)std::min<size_t>(fp_blocks(nwords, 256), (size_t)ctx->sm_count * 16), 256, 0, ctx->stream, fp_geo(ctx), ctx->tile_w, ctx->tile_h, ctx->tiles_x, ctx->tiles_y,
                                       ctx->d_tile_exit);
     FP_LAUNCHED(ctx);
     return FP_OK;
@@ -291,20 +296,20 @@ int fp_plane_ensure(fp_ctx* ctx, double k_s) {
     FP_CUDA(ctx, cudaMallocAsync(&rmax, total * 4, s));
     const double K = k_s * 1.4426950408889634;  // k_s * log2(e)
     const unsigned G = (unsigned)ctx->sm_count * 8;
-    plane_build_kernel<<<G, 256, 0, s>>>(fp_geo(ctx), ctx->PW, ctx->d_field, ctx->potential, K, ctx->d_plane, cval);
+    fp_launch(plane_build_kernel, G, 256, 0, s, fp_geo(ctx), ctx->PW, ctx->d_field, ctx->potential, K, ctx->d_plane, cval);
     FP_LAUNCHED(ctx);
     if (ctx->potential == FP_POTENTIAL_EXIT_DISTANCE) {
-        plane_rowminmax_kernel<<<G, 256, 0, s>>>(ctx->PW, ctx->H, cval, rmin, rmax);
+        fp_launch(plane_rowminmax_kernel, G, 256, 0, s, ctx->PW, ctx->H, cval, rmin, rmax);
         FP_LAUNCHED(ctx);
         FP_CUDA(ctx, cudaMemsetAsync(&ctx->d_sc->pad[0], 0, 8, s));
-        plane_unsafe_kernel<<<G, 256, 0, s>>>(ctx->PW, ctx->H, cval, rmin, rmax, ctx->d_plane, &ctx->d_sc->pad[0]);
+        fp_launch(plane_unsafe_kernel, G, 256, 0, s, ctx->PW, ctx->H, cval, rmin, rmax, ctx->d_plane, &ctx->d_sc->pad[0]);
         FP_LAUNCHED(ctx);
     }
     {
         const int boxw = ctx->tile_w + 16, rc = (ctx->H + 7) / 8;
         const size_t tot = (size_t)ctx->tiles_x * rc * 8 * boxw;
         if (!ctx->d_plane_t) FP_CUDA(ctx, cudaMalloc(&ctx->d_plane_t, tot * 4));
-        plane_tile_kernel<<<G, 256, 0, s>>>(ctx->d_plane, ctx->PW, ctx->H, ctx->tile_w, boxw, rc, tot, ctx->d_plane_t);
+        fp_launch(plane_tile_kernel, G, 256, 0, s, ctx->d_plane, ctx->PW, ctx->H, ctx->tile_w, boxw, rc, tot, ctx->d_plane_t);
         FP_LAUNCHED(ctx);
     }
     FP_CUDA(ctx, cudaFreeAsync(cval, s));

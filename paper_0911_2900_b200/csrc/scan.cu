@@ -38,6 +38,7 @@ __device__ __forceinline__ uint32_t load_flags(const uint8_t* alive, uint32_t n,
 }
 
 __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_sums_kernel(const uint32_t* in, uint32_t n, uint32_t* sums) {
+    FP_PDL_WAIT();
     __shared__ uint32_t s_warp[33];
     uint32_t v[FP_SCAN_PER], t = 0;
     load_run(in, n, blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER, v);
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_sums_kernel(const uint32_t
 // per thread); the grand total to *total_out (when given).
 __global__ void __launch_bounds__(FP_SCAN_TOP) scan_top_kernel(uint32_t* sums, uint32_t nb,
                                                                unsigned long long* total_out) {
+    FP_PDL_WAIT();
     __shared__ uint32_t s_warp[33];
     constexpr int PER = FP_SCAN_SUMS / FP_SCAN_TOP;
     const uint32_t per = (nb + FP_SCAN_TOP - 1) / FP_SCAN_TOP;  // <= PER
@@ -76,6 +78,7 @@ __global__ void __launch_bounds__(FP_SCAN_TOP) scan_top_kernel(uint32_t* sums, u
 
 __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_apply_kernel(const uint32_t* in, uint32_t n, const uint32_t* sums,
                                                                    uint32_t* out) {
+    FP_PDL_WAIT();
     __shared__ uint32_t s_warp[33];
     const uint32_t base = blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER;
     uint32_t v[FP_SCAN_PER], t = 0;
@@ -103,6 +106,7 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) scan_apply_kernel(const uint32_
 
 // Compaction of the alive flags: per-tile counts, then ascending ids written from the offsets.
 __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_sums_kernel(const uint8_t* alive, uint32_t n, uint32_t* sums) {
+    FP_PDL_WAIT();
     __shared__ uint32_t s_warp[33];
     const uint32_t v = __popc(load_flags(alive, n, blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER));
     uint32_t total;
@@ -112,6 +116,7 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_sums_kernel(const uint8_
 
 __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_scatter_kernel(const uint8_t* alive, uint32_t n,
                                                                        const uint32_t* sums, uint32_t* ids) {
+    FP_PDL_WAIT();
     __shared__ uint32_t s_warp[33];
     const uint32_t base = blockIdx.x * FP_SCAN_TILE + threadIdx.x * FP_SCAN_PER;
     uint32_t f = load_flags(alive, n, base);
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(FP_SCAN_BLOCK) select_scatter_kernel(const uin
 #define FP_SCAN_USE_SMALL 0
 #endif
 __global__ void __launch_bounds__(FP_SCAN_TOP) scan_small_kernel(const uint32_t* in, uint32_t n, uint32_t* out) {
+    FP_PDL_WAIT();
     __shared__ uint32_t s_warp[33];
     uint32_t carry = 0;
     for (uint32_t r0 = 0; r0 < n; r0 += FP_SCAN_SMALL_ROUND) {
@@ -163,17 +169,17 @@ __global__ void __launch_bounds__(FP_SCAN_TOP) scan_small_kernel(const uint32_t*
 
 int fp_scan_u32(fp_ctx* ctx, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* sums, cudaStream_t s) {
     if (FP_SCAN_USE_SMALL && n <= FP_SCAN_SMALL_MAX) {  // measured slower than the 3-pass scan
-        scan_small_kernel<<<1, FP_SCAN_TOP, 0, s>>>(in, n, out);
+        fp_launch(scan_small_kernel, 1, FP_SCAN_TOP, 0, s, in, n, out);
         FP_LAUNCHED(ctx);
         return FP_OK;
     }
     const uint32_t nb = std::max<uint32_t>(1, (n + FP_SCAN_TILE - 1) / FP_SCAN_TILE);
     if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "scan: more than 134M elements");
-    scan_sums_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(in, n, sums);
+    fp_launch(scan_sums_kernel, nb, FP_SCAN_BLOCK, 0, s, in, n, sums);
     FP_LAUNCHED(ctx);
-    scan_top_kernel<<<1, FP_SCAN_TOP, 0, s>>>(sums, nb, nullptr);
+    fp_launch(scan_top_kernel, 1, FP_SCAN_TOP, 0, s, sums, nb, nullptr);
     FP_LAUNCHED(ctx);
-    scan_apply_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(in, n, sums, out);
+    fp_launch(scan_apply_kernel, nb, FP_SCAN_BLOCK, 0, s, in, n, sums, out);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }
@@ -182,11 +188,11 @@ int fp_select_alive(fp_ctx* ctx, const uint8_t* alive, uint32_t n, uint32_t* ids
                     uint32_t* sums, cudaStream_t s) {
     const uint32_t nb = std::max<uint32_t>(1, (n + FP_SCAN_TILE - 1) / FP_SCAN_TILE);
     if (nb > FP_SCAN_SUMS) return fp_fail(ctx, FP_ERUNTIME, "select: more than 134M agents");
-    select_sums_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(alive, n, sums);
+    fp_launch(select_sums_kernel, nb, FP_SCAN_BLOCK, 0, s, alive, n, sums);
     FP_LAUNCHED(ctx);
-    scan_top_kernel<<<1, FP_SCAN_TOP, 0, s>>>(sums, nb, count);
+    fp_launch(scan_top_kernel, 1, FP_SCAN_TOP, 0, s, sums, nb, count);
     FP_LAUNCHED(ctx);
-    select_scatter_kernel<<<nb, FP_SCAN_BLOCK, 0, s>>>(alive, n, sums, ids);
+    fp_launch(select_scatter_kernel, nb, FP_SCAN_BLOCK, 0, s, alive, n, sums, ids);
     FP_LAUNCHED(ctx);
     return FP_OK;
 }

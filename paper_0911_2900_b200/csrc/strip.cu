@@ -117,6 +117,7 @@ __device__ __forceinline__ bool bit_at(const uint32_t* plane, const Geo& g, int 
 
 // 2a. contention marks of every planned walk (P1: in a footprint, P2: in two or more).
 __global__ void strip_mark_kernel(StripArgs s) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)s.sc->n_planned;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const uint4 r = s.rec0[k];
@@ -132,6 +133,7 @@ __global__ void strip_mark_kernel(StripArgs s) {
 
 // 2b. seeds: walks whose footprint touches a band; contended walks listed for the closure.
 __global__ void strip_seed_kernel(StripArgs s) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)s.sc->n_planned;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         const uint4 r = s.rec0[k];
@@ -161,6 +163,7 @@ __global__ void strip_seed_kernel(StripArgs s) {
 // 2c. closure (one CTA): a contended walk sharing a footprint cell with a deferred one is
 // deferred, until nothing changes.  Monotone, so the fixed point does not depend on timing.
 __global__ void __launch_bounds__(1024) strip_closure_kernel(StripArgs s) {
+    FP_PDL_WAIT();
     __shared__ int s_changed;
     const uint32_t n = (uint32_t)s.sc->strip_nc;
     for (int it = 0;; ++it) {
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(1024) strip_closure_kernel(StripArgs s) {
 // 2d. deferred walks into the send buffer (rank, desired cell, snapshot occupancy of the footprint)
 // and out of the local motion (m = 0).
 __global__ void strip_export_kernel(StripArgs s, DefRec* out, uint32_t cap, unsigned long long* hdr) {
+    FP_PDL_WAIT();
     const uint32_t n = (uint32_t)s.sc->n_planned;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         if (!s.dflag[k]) continue;
@@ -225,6 +229,7 @@ __global__ void strip_export_kernel(StripArgs s, DefRec* out, uint32_t cap, unsi
 // 3. after the local motion: header + local exits into the send buffer.
 __global__ void strip_pack_kernel(DevScalars* sc, const unsigned long long* exits, unsigned long long* hdr,
                                   unsigned long long* xout, uint32_t cap) {
+    FP_PDL_WAIT();
     const unsigned long long ne = sc->n_exits;
     for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < ne && i < cap; i += gridDim.x * blockDim.x)
         xout[i] = exits[i];
@@ -281,6 +286,7 @@ __device__ __forceinline__ uint32_t res_insert(const ResolveArgs& a, int x, int 
 }
 
 __global__ void __launch_bounds__(RES_TAIL_THREADS) strip_resolve_kernel(ResolveArgs a) {
+    FP_PDL_WAIT();
     __shared__ uint32_t cum[65];
     __shared__ uint32_t cnt[2];
     __shared__ uint32_t s_ns;
@@ -412,6 +418,7 @@ __global__ void __launch_bounds__(1024) strip_finish_kernel(const unsigned char*
                                                             const unsigned long long* rexits, uint8_t* alive,
                                                             unsigned long long* exits, uint32_t exits_cap,
                                                             DevScalars* sc) {
+    FP_PDL_WAIT();
     __shared__ unsigned long long s_base;
     if (threadIdx.x == 0) s_base = 0;
     __syncthreads();
@@ -458,6 +465,7 @@ __global__ void __launch_bounds__(1024) strip_finish_kernel(const unsigned char*
 }
 
 __global__ void strip_reset_kernel(DevScalars* sc, unsigned long long* hdr) {
+    FP_PDL_WAIT();
     sc->n_planned = 0;
     sc->strip_nc = 0;
     sc->strip_rexits = 0;
@@ -466,6 +474,7 @@ __global__ void strip_reset_kernel(DevScalars* sc, unsigned long long* hdr) {
 
 __global__ void owned_init_kernel(const int32_t* x, const uint8_t* alive, uint32_t n, Geo g, int lo, int hi,
                                   uint8_t* owned) {
+    FP_PDL_WAIT();
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int px = g.wrap(x[i]);
@@ -570,13 +579,13 @@ int fp_strip_defer_launch(fp_ctx* c) {
     const StripArgs s = strip_args(c);
     const unsigned G = (unsigned)std::min<size_t>(fp_blocks(c->n, 256), (size_t)c->sm_count * 8);
     unsigned long long* hdr = reinterpret_cast<unsigned long long*>(S.d_send);
-    strip_mark_kernel<<<G, 256, 0, c->stream>>>(s);
+    fp_launch(strip_mark_kernel, G, 256, 0, c->stream, s);
     FP_LAUNCHED(c);
-    strip_seed_kernel<<<G, 256, 0, c->stream>>>(s);
+    fp_launch(strip_seed_kernel, G, 256, 0, c->stream, s);
     FP_LAUNCHED(c);
-    strip_closure_kernel<<<1, 1024, 0, c->stream>>>(s);
+    fp_launch(strip_closure_kernel, 1, 1024, 0, c->stream, s);
     FP_LAUNCHED(c);
-    strip_export_kernel<<<G, 256, 0, c->stream>>>(
+    fp_launch(strip_export_kernel, G, 256, 0, c->stream,
         s, reinterpret_cast<DefRec*>(reinterpret_cast<unsigned char*>(S.d_send) + XH_WORDS * 8), S.cap_def, hdr);
     FP_LAUNCHED(c);
     const size_t nwords = (size_t)c->P * c->H;
@@ -588,7 +597,7 @@ int fp_strip_defer_launch(fp_ctx* c) {
 
 // Start of a strip step (before the plan): counters and the send header.
 int fp_strip_begin_launch(fp_ctx* c) {
-    strip_reset_kernel<<<1, 1, 0, c->stream>>>(c->d_sc, reinterpret_cast<unsigned long long*>(c->st.d_send));
+    fp_launch(strip_reset_kernel, 1, 1, 0, c->stream, c->d_sc, reinterpret_cast<unsigned long long*>(c->st.d_send));
     FP_LAUNCHED(c);
     return FP_OK;
 }
@@ -597,7 +606,7 @@ int fp_strip_begin_launch(fp_ctx* c) {
 int fp_strip_pack_launch(fp_ctx* c) {
     StripCtx& S = c->st;
     unsigned char* base = reinterpret_cast<unsigned char*>(S.d_send);
-    strip_pack_kernel<<<8, 256, 0, c->stream>>>(
+    fp_launch(strip_pack_kernel, 8, 256, 0, c->stream,
         c->d_sc, c->d_exits, reinterpret_cast<unsigned long long*>(base),
         reinterpret_cast<unsigned long long*>(base + XH_WORDS * 8 + (size_t)S.cap_def * sizeof(DefRec)), S.cap_exit);
     FP_LAUNCHED(c);
@@ -629,9 +638,9 @@ int fp_strip_resolve_launch(fp_ctx* c) {
     a.rexits = S.d_rexits;
     a.sc = c->d_sc;
     a.s = strip_args(c);
-    strip_resolve_kernel<<<1, RES_TAIL_THREADS, 0, c->stream>>>(a);
+    fp_launch(strip_resolve_kernel, 1, RES_TAIL_THREADS, 0, c->stream, a);
     FP_LAUNCHED(c);
-    strip_finish_kernel<<<1, 1024, 0, c->stream>>>(a.recv, S.d_rhdr, S.xbytes, S.nranks, S.cap_def, S.cap_exit, S.rank,
+    fp_launch(strip_finish_kernel, 1, 1024, 0, c->stream, a.recv, S.d_rhdr, S.xbytes, S.nranks, S.cap_def, S.cap_exit, S.rank,
                                                     S.d_rexits, c->d_alive, c->d_exits, c->cap, c->d_sc);
     FP_LAUNCHED(c);
     return FP_OK;
@@ -639,7 +648,7 @@ int fp_strip_resolve_launch(fp_ctx* c) {
 
 int fp_strip_owned_init(fp_ctx* c) {
     if (!c->st.on || c->n == 0) return FP_OK;
-    owned_init_kernel<<<fp_blocks(c->n, 256), 256, 0, c->stream>>>(c->d_x, c->d_alive, c->n, fp_geo(c), c->st.x_lo,
+    fp_launch(owned_init_kernel, fp_blocks(c->n, 256), 256, 0, c->stream, c->d_x, c->d_alive, c->n, fp_geo(c), c->st.x_lo,
                                                                    c->st.x_hi, c->st.d_owned);
     FP_LAUNCHED(c);
     return FP_OK;
