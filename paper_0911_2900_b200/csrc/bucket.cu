@@ -40,15 +40,12 @@ __global__ void bucket_count_kernel(Geo g, const int32_t* x, const int32_t* y, c
         const bool take = i < n && alive[i] && (!owned || owned[i]);
         const unsigned b = __ballot_sync(0xffffffffu, take);
         if ((threadIdx.x & 31) == 0 && b) atomicAdd(&s_taken, (unsigned)__popc(b));
+        // agents of one warp in the same chunk (dense exit queues) share one counter atomic
+        const uint32_t c = take ? (uint32_t)(g.wrap(x[i]) / tile_w) * cps + (uint32_t)(y[i] >> 3) : FP_NONE;
+        const uint32_t sl = fp_warp_slot(cnt, c, FP_NONE);
         if (i >= n) continue;
-        if (!take) {
-            chunk_of[i] = FP_NONE;
-            continue;
-        }
-        const int px = g.wrap(x[i]), py = y[i];
-        const uint32_t c = (uint32_t)(px / tile_w) * cps + (uint32_t)(py >> 3);
         chunk_of[i] = c;
-        slot[i] = atomicAdd(&cnt[c], 1u);
+        if (take) slot[i] = sl;
     }
     __syncthreads();
     if (threadIdx.x == 0 && s_taken) atomicAdd(n_planned, (unsigned long long)s_taken);

@@ -361,6 +361,17 @@ int fp_fail(fp_ctx* ctx, int code, const std::string& msg);
         if (e__ != cudaSuccess) return fp_cuda_fail((ctx), e__, "launch");   \
     } while (0)
 
+// Warp-aggregated counter reservation: the lanes of a warp holding the same key take
+// consecutive slots of ctr[key] with one atomic per distinct key (lane order inside a key).
+// Every lane of the warp must call it; `skip` keys reserve nothing (returns garbage).
+__device__ __forceinline__ uint32_t fp_warp_slot(uint32_t* ctr, uint32_t key, uint32_t skip) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader && key != skip) base = atomicAdd(&ctr[key], (uint32_t)__popc(peers));
+    return __shfl_sync(0xffffffffu, base, leader) + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+}
+
 inline unsigned fp_blocks(size_t n, unsigned tpb) {
     size_t b = (n + tpb - 1) / tpb;
     return (unsigned)(b == 0 ? 1 : b);
