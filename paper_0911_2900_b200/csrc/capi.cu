@@ -15,6 +15,10 @@
 
 static thread_local std::string g_error;
 
+#ifndef FP_RUN_UNROLL
+#define FP_RUN_UNROLL 8  // steps per run() graph launch (FASTPED_RUN_UNROLL overrides)
+#endif
+
 bool fp_pdl_enabled() {
     static const bool on = [] {
         const char* e = getenv("FASTPED_PDL");
@@ -117,7 +121,12 @@ __global__ void sc_set_kernel(DevScalars* sc, long long step, unsigned long long
 }
 
 __global__ void sc_step_kernel(DevScalars* sc) {
-    FP_PDL_WAIT(); sc->step += 1; }
+    FP_PDL_WAIT();
+    const unsigned long long t = fp_globaltimer();
+    sc->move_ns += t - sc->t_plan_end;
+    sc->t_step0 = t;
+    sc->step += 1;
+}
 
 // occupancy from alive positions + make_state checks (state.hpp:46-70)
 __global__ void build_occ_kernel(const int32_t* x, const int32_t* y, const uint8_t* alive, uint32_t n,
@@ -303,6 +312,7 @@ extern "C" void fp_destroy(fp_ctx* c) {
     if (c->stream4) cudaStreamSynchronize(c->stream4);
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
+    if (c->graph_multi) cudaGraphExecDestroy(c->graph_multi);
     if (c->st.graph_fin) cudaGraphExecDestroy(c->st.graph_fin);
     fp_strip_nccl_destroy(c);
     {
@@ -632,11 +642,45 @@ extern "C" int fp_step(fp_ctx* c, double k_s, uint64_t seed, fp_step_stats* out)
 // Captures the two per-step graphs: plan phase = bucketing + plan kernel, with the movement
 // order (alive compaction + parallel Fisher-Yates) on a forked branch; move phase = motion
 // rounds + ghost refresh + step advance.
+// run() replays FP_RUN_UNROLL steps per graph launch: the plan and move graphs as alternating
+// child-graph nodes of one graph, so consecutive phases meet at a graph edge instead of a host
+// graph launch.  The plan/move split then comes from the device clock (move_begin_kernel and
+// sc_step_kernel stamp the phase boundaries).  FASTPED_RUN_UNROLL=1 keeps one launch per phase.
+static int run_unroll() {
+    static const int u = [] {
+        const char* e = getenv("FASTPED_RUN_UNROLL");
+        const int v = e ? atoi(e) : FP_RUN_UNROLL;
+        return std::max(1, std::min(64, v));
+    }();
+    return u;
+}
+
+static cudaError_t build_multi(fp_ctx* c, cudaGraph_t gp, cudaGraph_t gm) {
+    const int u = run_unroll();
+    if (u < 2) return cudaSuccess;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaGraphCreate(&g, 0);
+    cudaGraphNode_t prev = nullptr;
+    for (int k = 0; k < u && e == cudaSuccess; ++k)
+        for (cudaGraph_t child : {gp, gm}) {
+            cudaGraphNode_t nd = nullptr;
+            e = cudaGraphAddChildGraphNode(&nd, g, prev ? &prev : nullptr, prev ? 1 : 0, child);
+            if (e != cudaSuccess) break;
+            prev = nd;
+        }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->graph_multi, g, 0);
+    if (g) cudaGraphDestroy(g);
+    if (e == cudaSuccess) c->run_unroll = u;
+    return e;
+}
+
 static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     if (c->graph_plan) cudaGraphExecDestroy(c->graph_plan);
     if (c->graph_move) cudaGraphExecDestroy(c->graph_move);
     if (c->st.graph_fin) cudaGraphExecDestroy(c->st.graph_fin);
-    c->graph_plan = c->graph_move = c->st.graph_fin = nullptr;
+    if (c->graph_multi) cudaGraphExecDestroy(c->graph_multi);
+    c->graph_plan = c->graph_move = c->st.graph_fin = c->graph_multi = nullptr;
+    c->run_unroll = 0;
     const bool strip = c->st.on;
     cudaGraph_t g = nullptr;
     const int64_t k0 = c->ctr.kernel_launches;
@@ -668,8 +712,11 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     }
     if (e != cudaSuccess) return fp_cuda_fail(c, e, "capture(plan)");
     e = cudaGraphInstantiate(&c->graph_plan, g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(plan)");
+    cudaGraph_t g_plan = g;  // kept for the unrolled run graph
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g_plan);
+        return fp_cuda_fail(c, e, "instantiate(plan)");
+    }
     g = nullptr;
     FP_CUDA(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     if (strip) rc = fp_strip_defer_launch(c);  // band-connected walks leave the local motion
@@ -683,11 +730,17 @@ static int capture(fp_ctx* c, double k_s, uint64_t seed) {
     e = cudaStreamEndCapture(c->stream, &g);
     if (rc != FP_OK) {
         if (g) cudaGraphDestroy(g);
+        cudaGraphDestroy(g_plan);
         return rc;
     }
-    if (e != cudaSuccess) return fp_cuda_fail(c, e, "capture(move)");
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g_plan);
+        return fp_cuda_fail(c, e, "capture(move)");
+    }
     e = cudaGraphInstantiate(&c->graph_move, g, 0);
+    if (e == cudaSuccess && !strip) e = build_multi(c, g_plan, g);
     cudaGraphDestroy(g);
+    cudaGraphDestroy(g_plan);
     if (e != cudaSuccess) return fp_cuda_fail(c, e, "instantiate(move)");
     if (strip) {  // after the exchange: resolve the deferred walks, global exits, ++step
         g = nullptr;
@@ -723,6 +776,48 @@ __global__ void run_begin_kernel(DevScalars* sc) {
     sc->tot_disp = 0;
     sc->tot_dx = 0;
     sc->tot_updates = 0;
+    sc->plan_ns = sc->move_ns = 0;
+    sc->t_step0 = fp_globaltimer();
+}
+
+static int run_finish(fp_ctx* c, int32_t steps, double wall_s, double plan_s, double move_s, fp_run_stats* out) {
+    if (int rc = read_scalars(c)) return rc;
+    fp_run_stats rs{};
+    rs.wall_time_s = wall_s;
+    rs.plan_time_s = plan_s >= 0 ? plan_s : (double)c->h_sc->plan_ns * 1e-9;
+    rs.move_time_s = move_s >= 0 ? move_s : (double)c->h_sc->move_ns * 1e-9;
+    rs.steps = steps;
+    rs.exited = (int64_t)c->h_sc->tot_exits;
+    rs.displacement_cells = (int64_t)c->h_sc->tot_disp;
+    rs.agent_updates = (int64_t)c->h_sc->tot_updates;
+    rs.alive = c->alive;
+    c->n_order = (uint32_t)c->h_sc->n_alive;
+    c->n_exits = 0;  // the per-phase exit list is only kept by fp_move / fp_step
+    c->ctr.planned_agents += rs.agent_updates;
+    if (out) *out = rs;
+    return FP_OK;
+}
+
+// run() over the unrolled graph: events around the whole loop only.
+static int run_unrolled(fp_ctx* c, int32_t steps, fp_run_stats* out) {
+    cudaEvent_t e0, e1;
+    FP_CUDA(c, cudaEventCreate(&e0));
+    FP_CUDA(c, cudaEventCreate(&e1));
+    cudaEventRecord(e0, c->stream);
+    int s = 0;
+    for (; s + c->run_unroll <= steps; s += c->run_unroll) FP_CUDA(c, cudaGraphLaunch(c->graph_multi, c->stream));
+    for (; s < steps; ++s) {
+        FP_CUDA(c, cudaGraphLaunch(c->graph_plan, c->stream));
+        FP_CUDA(c, cudaGraphLaunch(c->graph_move, c->stream));
+    }
+    cudaEventRecord(e1, c->stream);
+    FP_CUDA(c, cudaEventSynchronize(e1));
+    c->ctr.kernel_launches += (int64_t)steps * c->launches_per_step;
+    float tot = 0;
+    cudaEventElapsedTime(&tot, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return run_finish(c, steps, tot * 1e-3, -1.0, -1.0, out);
 }
 
 // run(): `steps` steps as graph replays, CUDA events between phases; one host sync at the end.
@@ -740,6 +835,7 @@ extern "C" int fp_run(fp_ctx* c, double k_s, uint64_t seed, int32_t steps, fp_ru
     FP_LAUNCHED(c);
     const int64_t launches_per_step = 0;  // counted at capture; see fp_counters note
     (void)launches_per_step;
+    if (c->graph_multi && c->run_unroll > 1) return run_unrolled(c, steps, out);
     std::vector<cudaEvent_t> ev((size_t)2 * steps + 1);
     for (auto& e : ev) FP_CUDA(c, cudaEventCreate(&e));
     const int64_t k0 = c->ctr.kernel_launches;

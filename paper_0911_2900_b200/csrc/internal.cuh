@@ -180,6 +180,10 @@ struct DevScalars {
     unsigned long long strip_rhops;  // strip mode: hops | dx << 32 of the resolved walks
     unsigned long long plan_prof[8]; // FP_PLAN_PROF builds: plan-kernel wait / work cycle counters
     unsigned long long n_plan_items; // plan items this step (bucket.cu)
+    unsigned long long t_step0;      // globaltimer: start of this step's plan phase (run/step kernels)
+    unsigned long long t_plan_end;   // globaltimer: start of this step's motion phase
+    unsigned long long plan_ns;      // plan / motion phase time summed over a run (device clock)
+    unsigned long long move_ns;
 };
 
 // x-strip decomposition of one simulation over several GPUs (strip.cu).
@@ -333,6 +337,8 @@ struct fp_ctx {
     // captured step graphs (fp_run): plan phase (bucketing + plan || order) and move phase
     cudaGraphExec_t graph_plan = nullptr;
     cudaGraphExec_t graph_move = nullptr;
+    cudaGraphExec_t graph_multi = nullptr;  // run(): FP_RUN_UNROLL steps (plan, move child graphs) in one graph
+    int run_unroll = 0;
     double graph_ks = 0.0;
     uint64_t graph_seed = 0;
     bool graph_valid = false;
@@ -370,6 +376,12 @@ __device__ __forceinline__ uint32_t fp_warp_slot(uint32_t* ctr, uint32_t key, ui
     uint32_t base = 0;
     if (lane == leader && key != skip) base = atomicAdd(&ctr[key], (uint32_t)__popc(peers));
     return __shfl_sync(0xffffffffu, base, leader) + (uint32_t)__popc(peers & ((1u << lane) - 1u));
+}
+
+__device__ __forceinline__ unsigned long long fp_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 inline unsigned fp_blocks(size_t n, unsigned tpb) {

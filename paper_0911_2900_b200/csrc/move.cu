@@ -1549,7 +1549,10 @@ __global__ void move_begin_kernel(DevScalars* sc) {
     FP_PDL_WAIT();
     for (int r = threadIdx.x; r < 64; r += blockDim.x) sc->chk_max[r] = sc->chk_cnt[r] = sc->p1_max[r] = 0;
     if (threadIdx.x) return;
-    sc->t_motion[0] = globaltimer();  // (the marking pass, when it runs, restamps its start)
+    const unsigned long long t = globaltimer();
+    sc->t_motion[0] = t;  // (the marking pass, when it runs, restamps its start)
+    sc->t_plan_end = t;
+    sc->plan_ns += t - sc->t_step0;
     sc->n_exits = 0;
     sc->exits_sorted = 0;
     sc->disp = 0;
