@@ -229,6 +229,38 @@ def test_run_matches_stepping():
     assert rs.plan_time_s + rs.move_time_s <= rs.wall_time_s + 1e-3
 
 
+@pytest.mark.parametrize("wide", [False, True])
+def test_potential_change_between_graph_steps(wide):
+    """state.hpp: potential / drive_gradient are mutable fields of SimState.  step() and run()
+    replay captured graphs that hold the plan kernel's parameters by value, so a change of the
+    gradient (DriveX -> DriveX) or of the potential kind between steps must re-capture them:
+    the trajectory follows the oracle stepped with the same changes.  The narrow ring plans
+    through the untiled variant, the wide one through the tiled weight plane."""
+    r = np.random.default_rng(0x9AD1 + wide)
+    cells = random_periodic(r, 300 if wide else 40, 24, 0.04)
+    for _ in range(3):
+        cells[int(r.integers(1, 23)), int(r.integers(0, cells.shape[1]))] = EXIT
+    nfree = int((cells == FREE).sum())
+    x, y = O.spawn_agents(cells, nfree // 4, 77)
+    dev, orc = pair(cells, x, y, 3, 1, 1, 8.0)
+    p = fp.SimParams(k_s=1.2, seed=4242)
+    schedule = [(1, 8.0), (1, 2.5), (1, -6.0), (0, 0.0), (1, 11.0)]
+    for i, (kind, g) in enumerate(schedule):
+        dev.set_potential(kind, g)
+        orc.s.potential, orc.s.drive_gradient = kind, g
+        if i % 2 == 0:
+            for s in range(3):
+                fp.step(dev, p)
+                orc.step_once(p.k_s, p.seed)
+                assert fp.state_hash(dev) == orc.hash(), f"phase {i} step {s}"
+        else:
+            fp.run(dev, fp.SimParams(k_s=1.2, seed=4242, steps=3))
+            for s in range(3):
+                orc.step_once(p.k_s, p.seed)
+            assert fp.state_hash(dev) == orc.hash(), f"phase {i} run"
+        assert_same_state(dev, orc, f"phase {i}")
+
+
 @pytest.mark.parametrize("name", ["corridor", "ring"])
 def test_config_trajectories(name):
     """Configs 1 and 3 at full size (config 3: 182,000 agents, DriveX on the ring)."""

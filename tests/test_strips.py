@@ -133,6 +133,36 @@ def test_full_size_configs_on_virtual_strips(config, world, steps):
     _compare(fp, single, strips, steps, wl.k_s, wl.seed)
 
 
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_nccl_transport_single_rank_communicator():
+    """The library's own NCCL transport on hardware, as far as one GPU allows: a one-rank
+    communicator (fp_nccl_unique_id -> fp_strip_set_nccl -> ncclCommInitRank) whose every step
+    runs the real exchange on the context's stream -- ncclAllGather of the headers, the read
+    back, ncclGroupStart/End around the (empty) peer loop and the self copy -- and must equal
+    the plain single-context run, exits in processing order included.  Two NCCL ranks cannot share
+    one device, so the peer sends stay covered by the host and in-process transports."""
+    from paper_0911_2900_b200 import fastped as fp
+    rng = np.random.default_rng(1234)
+    cells = random_grid(rng, 160, 70, 0.05, 5)
+    grid = fp.Grid(cells)
+    x, y = O.spawn_agents(cells, 2500, 21)
+    v = np.full(len(x), 4)
+    single = fp.SimState(grid, None, _roster(fp, x, y, v))
+    rank = fp.StripRank(grid, None, _roster(fp, x, y, v), 0, 1, 0, nccl_id=fp.nccl_unique_id())
+    assert (rank.x_lo, rank.x_hi) == (0, 160) and rank.owned().all()
+    p = fp.SimParams(k_s=1.2, seed=29, steps=1)
+    for s in range(40):
+        a = fp.step(single, p)
+        b = fp.step(rank, p)
+        assert (b.alive, b.exited, b.displacement_cells) == (a.alive, a.exited, a.displacement_cells), s
+        assert fp.state_hash(rank) == fp.state_hash(single), s
+    rs_a = fp.run(single, fp.SimParams(k_s=1.2, seed=29, steps=20))
+    rs_b = fp.run(rank, fp.SimParams(k_s=1.2, seed=29, steps=20))
+    assert (rs_b.alive, rs_b.exited, rs_b.displacement_cells) == (rs_a.alive, rs_a.exited, rs_a.displacement_cells)
+    assert fp.state_hash(rank) == fp.state_hash(single)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
