@@ -43,7 +43,7 @@ CASES = {
     "corridor": ("corridor", {}, 396),
     "ring": ("ring", {}, 396),
     "plaza": ("plaza", {}, 396),
-    "obstacles": ("obstacles", {}, 20),
+    "obstacles": ("obstacles", {}, int(os.environ.get("FASTPED_OBSTACLES_STEPS", "100"))),
 }
 
 
@@ -68,6 +68,8 @@ def make(name: str, cores: int) -> None:
         disp.append(d)
         ex_all.append(np.asarray(ex, np.uint32))
         ex_off.append(ex_off[-1] + len(ex))
+        if cfg.n >= 1_000_000 and s % 10 == 9:
+            print(f"  {name}: step {s + 1}/{steps}, {time.time() - t1:.0f} s", file=sys.stderr, flush=True)
     t2 = time.time()
     np.savez_compressed(
         os.path.join(HERE, f"full_{name}.npz"), config=cfg_name, kwargs=repr(kw), steps=steps, k_s=cfg.k_s,
