@@ -664,12 +664,14 @@ struct TailSmem {
 #endif
 #define MOVE_LOCAL_MAX 4096    // ... while the CTA holds at most this many pending agents
 #define QC_CAP 8192
+#define MOVE_SEG 8192          // list entries a CTA takes per pass-1/pass-2 segment (<= both queue sizes)
 // The kernel's dynamic shared memory serves, one after another, the seed windows, the long-bucket
 // ranking, the round queues and the tail.
 #define MOVE_DYN_SMEM (sizeof(TailSmem) > QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned) \
                            ? sizeof(TailSmem) : QP_CAP * sizeof(uint2) + QC_CAP * sizeof(unsigned))
 static_assert((MOVE_THREADS / 32) * BK_SORT_MAX * sizeof(unsigned) <= MOVE_DYN_SMEM, "long-bucket ranking");
 static_assert(MOVE_ASYNC_K * MOVE_THREADS * sizeof(uint2) <= MOVE_DYN_SMEM, "async entries");
+static_assert(MOVE_SEG <= QC_CAP && MOVE_SEG <= QP_CAP && MOVE_SEG % (4 * MOVE_THREADS) == 0, "segment size");
 static_assert(MOVE_ASYNC_K >= 1 && MOVE_ASYNC_K <= 32, "async entries per thread");
 
 __device__ __forceinline__ unsigned tail_insert(TailSmem& T, const MoveArgs& a, int x, int y) {
@@ -1204,10 +1206,32 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
             if (gtid == 0) a.pcount[4 + (r + 2) % 3] = 0;
             uint2* next = a.alist[(r + 1) & 1];
             unsigned int* ncount = &a.pcount[4 + (r + 1) % 3];
-            // pass 1: watch tests, four list entries per thread in flight; entry k goes to CTA
-            // k mod G, so a short list (late rounds) still spreads over every CTA
+            // The CTA takes its share of the list (entry k goes to CTA k mod G, so a short list
+            // in a late round still spreads over every CTA) in segments of MOVE_SEG entries: no
+            // segment can overflow the two shared-memory queues, and the agents a segment leaves
+            // pending go to the next list in one bulk flush before the following segment (one
+            // global atomic per CTA and segment).  Lists of up to G * MOVE_SEG entries are one
+            // segment; config 5's 6-7 million contended agents take five or six.
+            unsigned long long hops = 0;
+            long long p1_clk = 0, c_p2 = clock64();
+            for (unsigned seg0 = 0; blockIdx.x + (size_t)gridDim.x * seg0 < np; seg0 += MOVE_SEG) {
+            if (seg0) {
+                __syncthreads();
+                const unsigned nqf = min(*qpn, (unsigned)QP_CAP);
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    s_q[2] = nqf ? atomicAdd(ncount, nqf) : 0u;
+                    *qpn = 0;
+                    *qcn = 0;
+                }
+                __syncthreads();
+                for (unsigned i = threadIdx.x; i < nqf; i += blockDim.x) next[s_q[2] + i] = qp[i];
+                __syncthreads();
+            }
+            // pass 1: watch tests, four list entries per thread in flight
             const long long c_p1 = clock64();
-            for (unsigned base = threadIdx.x; blockIdx.x + (size_t)gridDim.x * base < np; base += 4 * blockDim.x) {
+            for (unsigned base = seg0 + threadIdx.x;
+                 base < seg0 + MOVE_SEG && blockIdx.x + (size_t)gridDim.x * base < np; base += 4 * blockDim.x) {
                 uint2 e[4];
                 unsigned v[4];
 #pragma unroll
@@ -1233,10 +1257,9 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                 }
             }
             __syncthreads();
-            const long long c_p2 = clock64();
-            if (threadIdx.x == 0 && r < 64) atomicMax(&a.sc->p1_max[r], (unsigned long long)(c_p2 - c_p1));
+            c_p2 = clock64();
+            p1_clk += c_p2 - c_p1;
             // pass 2: full checks of this CTA's woken agents
-            unsigned long long hops = 0;
             const unsigned nchk = min(*qcn, (unsigned)QC_CAP);
             if (threadIdx.x == 0 && r < 64 && nchk) atomicAdd(&a.sc->chk_cnt[r], (unsigned long long)nchk);
             for (unsigned i = threadIdx.x; i < nchk; i += blockDim.x) {
@@ -1248,6 +1271,8 @@ __global__ void __launch_bounds__(MOVE_THREADS, 1) move_rounds_kernel(MoveArgs a
                     else next[atomicAdd(ncount, 1u)] = make_uint2(ci, w);
                 }
             }
+            }  // segments
+            if (threadIdx.x == 0 && r < 64) atomicMax(&a.sc->p1_max[r], (unsigned long long)p1_clk);
             // local iterations: this CTA's still-pending agents whose watched blocker walked
             // during this round (in any CTA) are checked again at once, so a chain of agents can
             // advance several links per grid round.  Each pending agent lives in one CTA's
