@@ -6,9 +6,9 @@ on BASELINE.json's configurations at their full sizes:
     corridor 250x50      2,000 agents        396 steps
     ring 4000x200      182,000 agents        396 steps (DriveX, g = 1)
     plaza 20000x5000 1,000,000 agents        396 steps
-    obstacles 40000x10000 10,000,000 agents   20 steps (mixed v_max 2..5)
+    obstacles 40000x10000 10,000,000 agents  100 steps (mixed v_max 2..5; FASTPED_OBSTACLES_STEPS)
 
-    python tests/golden/make_fullsize.py [name ...]     # ~12 min on 8 cores
+    python tests/golden/make_fullsize.py [name ...]     # ~30 min on 8 cores (obstacles: ~12 s per step)
 
 Geometry and roster come from oracle/configs.py (the checker-side generators; the roster is the
 reference's own spawn_agents), the static field from the reference's compute_static_field,
