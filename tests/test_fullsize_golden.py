@@ -123,7 +123,7 @@ def test_run_matches_reference(name):
 
 @pytest.mark.gpu
 @pytest.mark.timeout(1800)
-@pytest.mark.parametrize("name", ["room_v5", "plaza"])
+@pytest.mark.parametrize("name", ["room_v5", "plaza", "obstacles"])
 def test_repeated_runs_are_identical(name):
     """Race probe for the lock-free motion and plan pipelines: the same run repeated on fresh
     contexts always ends on the reference's final state (a lost occupancy update or a stale ring
